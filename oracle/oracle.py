@@ -1,0 +1,574 @@
+"""TEST INFRASTRUCTURE ONLY (see oracle/README.md).
+
+ctypes bindings for the two CPU checkers with one Python surface:
+
+* ``Port`` — ``_build/libvipkit_port.so``, the plain-C restatement
+  (``vipkit_port.c``), always available after ``make -C oracle``.
+* ``Ref``  — ``_ref/libvipkit_ref.so``, the UNMODIFIED reference library
+  (``/root/reference/proj/src``) behind ``ref_shim.cpp``. Present wherever it
+  was built (it travels to the GPU box as a build product).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
+legs import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_SO = os.path.join(HERE, "_build", "libvipkit_port.so")
+REF_SO = os.path.join(HERE, "_ref", "libvipkit_ref.so")
+
+KINDS = {"path": 0, "star": 1, "tree": 2, "grid": 3, "pa": 4, "uniform": 5}
+PARTITION_METHODS = {"random": 0, "bfs_greedy": 1}
+
+u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+c_u64, c_u32, c_int, c_double, c_vp = C.c_uint64, C.c_uint32, C.c_int, C.c_double, C.c_void_p
+
+ERROR_NAMES = {1: "parse_error", 2: "range_error", 3: "parameter_error", 4: "format_error",
+               5: "partition_error", 6: "sampling_error", 7: "config_error", 8: "shape_error",
+               9: "io_error", 23: "error"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERROR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = ERROR_NAMES.get(code, "error")
+
+
+def _a32(x):
+    return np.ascontiguousarray(x, dtype=np.uint32)
+
+
+def _a64(x):
+    return np.ascontiguousarray(x, dtype=np.uint64)
+
+
+@dataclass
+class CSR:
+    """Host CSR with the reference layout (graph.hpp:20-46)."""
+    n: int
+    off: np.ndarray            # u64 [n+1]
+    tgt: np.ndarray            # u32 [m]
+    rev_off: np.ndarray = None  # u64 [n+1]
+    rev_tgt: np.ndarray = None  # u32 [m]
+
+    @property
+    def m(self) -> int:
+        return int(self.tgt.shape[0])
+
+    def ensure_reverse(self):
+        if self.rev_off is None:
+            self.rev_off, self.rev_tgt = transpose(self.n, self.off, self.tgt)
+        return self
+
+    def out_degree(self) -> np.ndarray:
+        return np.diff(self.off)
+
+
+def transpose(n, off, tgt):
+    """Reverse CSR by counting transpose (same as graph.cpp:587-595)."""
+    m = tgt.shape[0]
+    src = np.repeat(np.arange(n, dtype=np.uint32), np.diff(off).astype(np.int64))
+    order = np.lexsort((src, tgt))
+    rev_tgt = src[order].astype(np.uint32)
+    cnt = np.bincount(tgt, minlength=n).astype(np.uint64)
+    rev_off = np.zeros(n + 1, dtype=np.uint64)
+    np.cumsum(cnt, out=rev_off[1:])
+    assert rev_off[-1] == m
+    return rev_off, rev_tgt
+
+
+@dataclass
+class Expansion:
+    batch: np.ndarray
+    frontier: list = field(default_factory=list)
+    all_vertices: np.ndarray = None
+    indptr: list = field(default_factory=list)
+    edges: list = field(default_factory=list)
+
+
+class Port:
+    """The C restatement (vipkit_port.c)."""
+
+    name = "port"
+
+    def __init__(self, path: str = PORT_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+        L = self.lib = C.CDLL(path)
+        L.vp_last_error.restype = C.c_char_p
+        L.vp_mix64.restype = c_u64
+        L.vp_mix64.argtypes = [c_u64]
+        L.vp_seed_key.restype = c_u64
+        L.vp_seed_key.argtypes = [c_u64, u64p, c_u32]
+        L.vp_generate.argtypes = [c_int, c_u64, c_u64, c_u64, C.POINTER(c_vp), C.POINTER(c_vp),
+                                  C.POINTER(c_u64)]
+        L.vp_graph_from_edges.argtypes = [c_u64, u32p, u32p, c_u64, c_int, C.POINTER(c_vp),
+                                          C.POINTER(c_vp), C.POINTER(c_u64)]
+        L.vp_free.argtypes = [c_vp]
+        L.vp_make_roles.argtypes = [c_u64, c_double, c_double, c_double, c_u64, u8p]
+        L.vp_epoch_minibatches.argtypes = [u8p, c_u64, u32p, c_u32, c_u64, c_u64, c_u64, u32p,
+                                           C.POINTER(c_u64)]
+        L.vp_expand.restype = c_vp
+        L.vp_expand.argtypes = [u64p, u32p, c_u64, u32p, c_u64, u32p, c_u32, c_u64, c_u64, c_u32,
+                                c_u64]
+        L.vp_expansion_free.argtypes = [c_vp]
+        L.vp_initial_probs.argtypes = [u8p, c_u64, u32p, c_u32, c_u64, f64p]
+        L.vp_propagate.argtypes = [u64p, u64p, u32p, c_u64, u32p, c_u32, f64p, f64p, f64p]
+        L.vp_rank_by_scores.argtypes = [u32p, c_u64, c_u32, f64p, u32p, f64p, C.POINTER(c_u64)]
+        L.vp_cache_capacity.argtypes = [c_double, c_u64, c_u32, C.POINTER(c_u64)]
+        L.vp_classify.argtypes = [u32p, c_u64, u32p, c_u32, c_vp, u64p]
+        L.vp_build_reorder.argtypes = [u32p, c_u64, c_u32, f64p, u32p, u64p]
+        L.vp_features.argtypes = [c_u64, c_u32, c_int, u32p, c_u64, c_vp]
+
+    def _check(self, rc):
+        if rc != 0:
+            raise OracleError(rc, self.lib.vp_last_error().decode())
+
+    # ---- rng ----
+    def mix64(self, x):
+        return self.lib.vp_mix64(x)
+
+    def seed_key(self, seed, parts):
+        p = _a64(parts)
+        return self.lib.vp_seed_key(seed, p, len(p))
+
+    # ---- graph ----
+    def _take_csr(self, n, po, pt, m):
+        off = np.ctypeslib.as_array(C.cast(po, C.POINTER(c_u64)), shape=(n + 1,)).copy()
+        tgt = (np.ctypeslib.as_array(C.cast(pt, C.POINTER(C.c_uint32)), shape=(m,)).copy()
+               if m else np.zeros(0, np.uint32))
+        self.lib.vp_free(po)
+        self.lib.vp_free(pt)
+        return CSR(n, off, tgt)
+
+    def generate(self, kind, n, d=2, seed=0) -> CSR:
+        po, pt, m = c_vp(), c_vp(), c_u64()
+        self._check(self.lib.vp_generate(KINDS[kind], n, d, seed, C.byref(po), C.byref(pt),
+                                         C.byref(m)))
+        return self._take_csr(n, po, pt, m.value)
+
+    def from_edges(self, n, edges, undirected) -> CSR:
+        e = np.asarray(edges, dtype=np.uint32).reshape(-1, 2)
+        po, pt, m = c_vp(), c_vp(), c_u64()
+        self._check(self.lib.vp_graph_from_edges(n, _a32(e[:, 0]), _a32(e[:, 1]), len(e),
+                                                 int(undirected), C.byref(po), C.byref(pt),
+                                                 C.byref(m)))
+        return self._take_csr(n, po, pt, m.value)
+
+    def make_roles(self, n, train, valid=0.0, test=0.0, seed=0):
+        out = np.zeros(n, np.uint8)
+        self._check(self.lib.vp_make_roles(n, train, valid, test, seed, out))
+        return out
+
+    # ---- sampling ----
+    def epoch_permutation(self, roles, labels, k, b, epoch, seed):
+        n = len(roles)
+        out = np.zeros(n, np.uint32)
+        cnt = c_u64()
+        self._check(self.lib.vp_epoch_minibatches(np.ascontiguousarray(roles, np.uint8), n,
+                                                  _a32(labels), k, b, epoch, seed, out,
+                                                  C.byref(cnt)))
+        return out[:cnt.value]
+
+    def epoch_minibatches(self, roles, labels, k, b, epoch, seed):
+        perm = self.epoch_permutation(roles, labels, k, b, epoch, seed)
+        return [perm[i:i + b] for i in range(0, len(perm), b)]
+
+    def expand(self, g: CSR, batch, fanouts, seed, epoch=0, part=0, batch_index=0) -> Expansion:
+        class _X(C.Structure):
+            _fields_ = [("L", c_u32), ("nb", c_u64), ("batch", C.POINTER(C.c_uint32)),
+                        ("fsize", C.POINTER(c_u64)), ("frontier", C.POINTER(C.POINTER(C.c_uint32))),
+                        ("indptr", C.POINTER(C.POINTER(c_u64))),
+                        ("edges", C.POINTER(C.POINTER(C.c_uint32))), ("nall", c_u64),
+                        ("all", C.POINTER(C.c_uint32))]
+        b = _a32(batch)
+        f = _a32(fanouts)
+        p = self.lib.vp_expand(g.off, g.tgt, g.n, b, len(b), f, len(f), seed, epoch, part,
+                               batch_index)
+        if not p:
+            msg = self.lib.vp_last_error().decode()
+            raise OracleError(6 if "empty batch" in msg else 3, msg)
+        x = C.cast(p, C.POINTER(_X)).contents
+        out = Expansion(batch=b.copy())
+        prev = len(b)
+        for h in range(x.L):
+            fs = x.fsize[h]
+            out.frontier.append(np.ctypeslib.as_array(x.frontier[h], shape=(fs,)).copy()
+                                if fs else np.zeros(0, np.uint32))
+            ip = np.ctypeslib.as_array(x.indptr[h], shape=(prev + 1,)).copy()
+            out.indptr.append(ip)
+            ne = int(ip[-1])
+            out.edges.append(np.ctypeslib.as_array(x.edges[h], shape=(ne,)).copy()
+                             if ne else np.zeros(0, np.uint32))
+            prev = fs
+        out.all_vertices = np.ctypeslib.as_array(x.all, shape=(x.nall,)).copy()
+        self.lib.vp_expansion_free(p)
+        return out
+
+    # ---- vip ----
+    def initial_probs(self, roles, labels, K, k, b):
+        n = len(roles)
+        out = np.zeros(n, np.float64)
+        self._check(self.lib.vp_initial_probs(np.ascontiguousarray(roles, np.uint8), n,
+                                              _a32(labels), k, b, out))
+        return out
+
+    def propagate(self, g: CSR, fanouts, p0):
+        g.ensure_reverse()
+        f = _a32(fanouts)
+        hop = np.zeros((len(f), g.n), np.float64)
+        total = np.zeros(g.n, np.float64)
+        p0 = np.ascontiguousarray(p0, np.float64)
+        if p0.shape[0] != g.n:
+            raise OracleError(8, "p0 length does not match vertex count")
+        self._check(self.lib.vp_propagate(g.off, g.rev_off, g.rev_tgt, g.n, f, len(f), p0, hop,
+                                          total))
+        return hop, total
+
+    # ---- policies ----
+    def rank_by_scores(self, labels, K, k, scores):
+        labels = _a32(labels)
+        scores = np.ascontiguousarray(scores, np.float64)
+        if scores.shape[0] != labels.shape[0]:
+            raise OracleError(8, "score vector length does not match vertex count")
+        n = len(labels)
+        order = np.zeros(n, np.uint32)
+        sc = np.zeros(n, np.float64)
+        cnt = c_u64()
+        self._check(self.lib.vp_rank_by_scores(labels, n, k, scores, order, sc, C.byref(cnt)))
+        return order[:cnt.value], sc[:cnt.value]
+
+    def cache_capacity(self, alpha, n, K):
+        cap = c_u64()
+        self._check(self.lib.vp_cache_capacity(alpha, n, K, C.byref(cap)))
+        return cap.value
+
+    def build_cache(self, orders, alpha, n):
+        cap = self.cache_capacity(alpha, n, len(orders))
+        cached = [np.asarray(o[:cap], np.uint32) for o in orders]
+        return cached, bitsets(cached, n)
+
+    def classify(self, all_vertices, labels, k, bits=None):
+        out = np.zeros(3, np.uint64)
+        a = _a32(all_vertices)
+        bp = None if bits is None else _a64(bits).ctypes.data
+        keep = None if bits is None else _a64(bits)
+        if keep is not None:
+            bp = keep.ctypes.data
+        self.lib.vp_classify(a, len(a), _a32(labels), k, bp, out)
+        return tuple(int(x) for x in out)
+
+    def build_reorder(self, labels, K, scores):
+        labels = _a32(labels)
+        n = len(labels)
+        s = np.ascontiguousarray(np.asarray(scores, np.float64).reshape(K, n))
+        oon = np.zeros(n, np.uint32)
+        ranges = np.zeros(2 * K, np.uint64)
+        self._check(self.lib.vp_build_reorder(labels, n, K, s, oon, ranges))
+        return oon, ranges.reshape(K, 2)
+
+    def features(self, seed, D, ids, fp16=False):
+        ids = _a32(ids)
+        out = np.zeros((len(ids), D), np.float16 if fp16 else np.float32)
+        self.lib.vp_features(seed, D, int(fp16), ids, len(ids), out.ctypes.data)
+        return out
+
+
+def bitsets(cached, n):
+    """CachePlan::member_bits layout (policies.hpp:55-60): K x ceil(n/64) u64."""
+    W = (n + 63) // 64
+    bits = np.zeros((len(cached), W), np.uint64)
+    for k, c in enumerate(cached):
+        c = np.asarray(c, np.uint64)
+        np.bitwise_or.at(bits[k], (c >> np.uint64(6)).astype(np.int64),
+                         np.left_shift(np.uint64(1), c & np.uint64(63)))
+    return bits
+
+
+class Ref:
+    """The unmodified reference library behind ref_shim.cpp."""
+
+    name = "reference"
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle` where /root/reference exists")
+        L = self.lib = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_set_threads.argtypes = [C.c_uint]
+        L.ref_mix64.restype = c_u64
+        L.ref_mix64.argtypes = [c_u64]
+        L.ref_seed_key.restype = c_u64
+        L.ref_seed_key.argtypes = [c_u64, u64p, c_u32]
+        L.ref_stream_draws.argtypes = [c_u64, c_u64, c_u64, u64p]
+        for fn in ("ref_graph_generate", "ref_graph_from_edges", "ref_graph_from_csr",
+                   "ref_graph_load_vcsr", "ref_expand"):
+            getattr(L, fn).restype = c_vp
+        L.ref_graph_generate.argtypes = [c_int, c_u64, c_u64, c_u64]
+        L.ref_graph_from_edges.argtypes = [c_u64, u32p, u32p, c_u64, c_int]
+        L.ref_graph_from_csr.argtypes = [c_u64, c_u64, u64p, u32p]
+        L.ref_graph_load_vcsr.argtypes = [C.c_char_p]
+        L.ref_graph_write_vcsr.argtypes = [c_vp, C.c_char_p]
+        L.ref_graph_n.restype = c_u64
+        L.ref_graph_n.argtypes = [c_vp]
+        L.ref_graph_m.restype = c_u64
+        L.ref_graph_m.argtypes = [c_vp]
+        L.ref_graph_copy.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp]
+        L.ref_graph_free.argtypes = [c_vp]
+        L.ref_make_roles.argtypes = [c_u64, c_double, c_double, c_double, c_u64, u8p]
+        L.ref_partition_graph.argtypes = [c_vp, u8p, c_u64, c_u32, c_int, c_u64, u32p]
+        L.ref_epoch_minibatches.argtypes = [u8p, c_u64, u32p, c_u32, c_u32, c_u64, c_u64, c_u64,
+                                            c_vp, u32p, C.POINTER(c_u64)]
+        L.ref_expand.argtypes = [c_vp, u32p, c_u64, u32p, c_u32, c_u64, c_u64, c_u32, c_u64, c_int]
+        for fn in ("ref_exp_frontier_size", "ref_exp_edges_size"):
+            getattr(L, fn).restype = c_u64
+            getattr(L, fn).argtypes = [c_vp, c_u32]
+        L.ref_exp_all_size.restype = c_u64
+        L.ref_exp_all_size.argtypes = [c_vp]
+        for fn in ("ref_exp_frontier", "ref_exp_edges"):
+            getattr(L, fn).restype = C.POINTER(C.c_uint32)
+            getattr(L, fn).argtypes = [c_vp, c_u32]
+        L.ref_exp_all.restype = C.POINTER(C.c_uint32)
+        L.ref_exp_all.argtypes = [c_vp]
+        L.ref_exp_indptr.restype = C.POINTER(c_u64)
+        L.ref_exp_indptr.argtypes = [c_vp, c_u32]
+        L.ref_exp_free.argtypes = [c_vp]
+        L.ref_expand_classify_range.argtypes = [c_vp, u32p, c_u64, c_u64, u32p, c_u32, c_u64,
+                                                c_u64, c_u32, c_u64, c_u64, u32p, c_vp, C.c_uint,
+                                                u64p]
+        L.ref_initial_probs.argtypes = [u8p, c_u64, u32p, c_u32, c_u32, c_u64, f64p]
+        L.ref_propagate.argtypes = [c_vp, u32p, c_u32, f64p, c_vp, f64p]
+        L.ref_empirical_vip.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u64, u32p, c_u32, c_u64,
+                                        c_u64, f64p]
+        L.ref_rank_by_scores.argtypes = [u32p, c_u64, c_u32, c_u32, f64p, c_u64, u32p, f64p,
+                                         C.POINTER(c_u64)]
+        L.ref_build_cache.argtypes = [u32p, u64p, c_u32, c_double, c_u64, u64p, u64p]
+        L.ref_simulate.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, u32p,
+                                   u64p, u64p]
+        L.ref_build_reorder.argtypes = [u32p, c_u64, c_u32, f64p, u32p, u64p]
+        self._handles = {}
+
+    def _check(self, rc):
+        if rc != 0:
+            raise OracleError(rc, self.lib.ref_last_error().decode())
+
+    def _ptr(self, p):
+        if not p:
+            msg = self.lib.ref_last_error().decode()
+            code = 3
+            for c, nm in ((6, "empty"), (6, "no train"), (8, "length"), (2, "out of range"),
+                          (4, "offsets"), (4, "target")):
+                if nm in msg:
+                    code = c
+                    break
+            raise OracleError(code, msg)
+        return p
+
+    def set_threads(self, n):
+        self.lib.ref_set_threads(n)
+
+    # ---- rng ----
+    def mix64(self, x):
+        return self.lib.ref_mix64(x)
+
+    def seed_key(self, seed, parts):
+        p = _a64(parts)
+        return self.lib.ref_seed_key(seed, p, len(p))
+
+    def stream_draws(self, key, bound, count):
+        out = np.zeros(count, np.uint64)
+        self.lib.ref_stream_draws(key, bound, count, out)
+        return out
+
+    # ---- graph: a reference Graph lives as long as the CSR that names it ----
+    def _graph(self, g: CSR):
+        h = self._handles.get(id(g))
+        if h is None or h[0] is not g:
+            p = self._ptr(self.lib.ref_graph_from_csr(g.n, g.m, _a64(g.off), _a32(g.tgt)))
+            h = (g, p)
+            self._handles[id(g)] = h
+        return h[1]
+
+    def release(self, g: CSR):
+        h = self._handles.pop(id(g), None)
+        if h is not None:
+            self.lib.ref_graph_free(h[1])
+
+    def _copy_graph(self, p) -> CSR:
+        n, m = self.lib.ref_graph_n(p), self.lib.ref_graph_m(p)
+        off = np.zeros(n + 1, np.uint64)
+        tgt = np.zeros(m, np.uint32)
+        roff = np.zeros(n + 1, np.uint64)
+        rtgt = np.zeros(m, np.uint32)
+        self.lib.ref_graph_copy(p, off.ctypes.data, tgt.ctypes.data, roff.ctypes.data,
+                                rtgt.ctypes.data)
+        g = CSR(n, off, tgt, roff, rtgt)
+        self._handles[id(g)] = (g, p)
+        return g
+
+    def generate(self, kind, n, d=2, seed=0) -> CSR:
+        return self._copy_graph(self._ptr(self.lib.ref_graph_generate(KINDS[kind], n, d, seed)))
+
+    def from_edges(self, n, edges, undirected) -> CSR:
+        e = np.asarray(edges, dtype=np.uint32).reshape(-1, 2)
+        return self._copy_graph(self._ptr(self.lib.ref_graph_from_edges(
+            n, _a32(e[:, 0]), _a32(e[:, 1]), len(e), int(undirected))))
+
+    def load_vcsr(self, path) -> CSR:
+        return self._copy_graph(self._ptr(self.lib.ref_graph_load_vcsr(path.encode())))
+
+    def write_vcsr(self, g: CSR, path):
+        self._check(self.lib.ref_graph_write_vcsr(self._graph(g), path.encode()))
+
+    def make_roles(self, n, train, valid=0.0, test=0.0, seed=0):
+        out = np.zeros(n, np.uint8)
+        self._check(self.lib.ref_make_roles(n, train, valid, test, seed, out))
+        return out
+
+    def partition(self, g: CSR, roles, K, method="bfs_greedy", seed=1):
+        out = np.zeros(g.n, np.uint32)
+        self._check(self.lib.ref_partition_graph(self._graph(g), np.ascontiguousarray(roles, np.uint8),
+                                                 g.n, K, PARTITION_METHODS[method], seed, out))
+        return out
+
+    # ---- sampling ----
+    def epoch_permutation(self, roles, labels, k, b, epoch, seed, K=None, seed_keys=None):
+        n = len(roles)
+        labels = _a32(labels)
+        K = int(labels.max()) + 1 if K is None else K
+        out = np.zeros(n, np.uint32)
+        cnt = c_u64()
+        sk = None if seed_keys is None else _a32(seed_keys)
+        self._check(self.lib.ref_epoch_minibatches(np.ascontiguousarray(roles, np.uint8), n,
+                                                   labels, K, k, b, epoch, seed,
+                                                   None if sk is None else sk.ctypes.data, out,
+                                                   C.byref(cnt)))
+        return out[:cnt.value]
+
+    def epoch_minibatches(self, roles, labels, k, b, epoch, seed, K=None):
+        perm = self.epoch_permutation(roles, labels, k, b, epoch, seed, K)
+        return [perm[i:i + b] for i in range(0, len(perm), b)]
+
+    def expand(self, g: CSR, batch, fanouts, seed, epoch=0, part=0, batch_index=0,
+               with_mfg=True) -> Expansion:
+        b = _a32(batch)
+        f = _a32(fanouts)
+        p = self._ptr(self.lib.ref_expand(self._graph(g), b, len(b), f, len(f), seed, epoch, part,
+                                          batch_index, int(with_mfg)))
+        L = self.lib
+        out = Expansion(batch=b.copy())
+        for h in range(len(f)):
+            fs = L.ref_exp_frontier_size(p, h)
+            out.frontier.append(np.ctypeslib.as_array(L.ref_exp_frontier(p, h), shape=(fs,)).copy()
+                                if fs else np.zeros(0, np.uint32))
+            if with_mfg:
+                prev = len(b) if h == 0 else len(out.frontier[h - 1])
+                out.indptr.append(np.ctypeslib.as_array(L.ref_exp_indptr(p, h),
+                                                        shape=(prev + 1,)).copy())
+                ne = L.ref_exp_edges_size(p, h)
+                out.edges.append(np.ctypeslib.as_array(L.ref_exp_edges(p, h), shape=(ne,)).copy()
+                                 if ne else np.zeros(0, np.uint32))
+        na = L.ref_exp_all_size(p)
+        out.all_vertices = np.ctypeslib.as_array(L.ref_exp_all(p), shape=(na,)).copy()
+        L.ref_exp_free(p)
+        return out
+
+    def expand_classify_range(self, g: CSR, perm, b, fanouts, seed, epoch, k, i0, i1, labels,
+                              cache_bits=None, threads=1):
+        t = np.zeros(4, np.uint64)
+        bits = None if cache_bits is None else _a64(cache_bits)
+        self._check(self.lib.ref_expand_classify_range(
+            self._graph(g), _a32(perm), len(perm), b, _a32(fanouts), len(fanouts), seed, epoch, k,
+            i0, i1, _a32(labels), None if bits is None else bits.ctypes.data, threads, t))
+        return tuple(int(x) for x in t)
+
+    # ---- vip ----
+    def initial_probs(self, roles, labels, K, k, b):
+        n = len(roles)
+        out = np.zeros(n, np.float64)
+        self._check(self.lib.ref_initial_probs(np.ascontiguousarray(roles, np.uint8), n,
+                                               _a32(labels), K, k, b, out))
+        return out
+
+    def propagate(self, g: CSR, fanouts, p0):
+        f = _a32(fanouts)
+        p0 = np.ascontiguousarray(p0, np.float64)
+        if p0.shape[0] != g.n:
+            raise OracleError(8, "p0 length does not match vertex count")
+        hop = np.zeros((len(f), g.n), np.float64)
+        total = np.zeros(g.n, np.float64)
+        self._check(self.lib.ref_propagate(self._graph(g), f, len(f), p0, hop.ctypes.data, total))
+        return hop, total
+
+    def empirical_vip(self, g: CSR, roles, labels, K, k, b, fanouts, S, seed):
+        out = np.zeros(g.n, np.float64)
+        f = _a32(fanouts)
+        self._check(self.lib.ref_empirical_vip(self._graph(g), np.ascontiguousarray(roles, np.uint8),
+                                               _a32(labels), K, k, b, f, len(f), S, seed, out))
+        return out
+
+    # ---- policies ----
+    def rank_by_scores(self, labels, K, k, scores):
+        labels = _a32(labels)
+        n = len(labels)
+        scores = np.ascontiguousarray(scores, np.float64)
+        order = np.zeros(n, np.uint32)
+        sc = np.zeros(n, np.float64)
+        cnt = c_u64()
+        self._check(self.lib.ref_rank_by_scores(labels, n, K, k, scores, len(scores), order, sc,
+                                                C.byref(cnt)))
+        return order[:cnt.value], sc[:cnt.value]
+
+    def build_cache(self, orders, alpha, n):
+        K = len(orders)
+        offs = np.zeros(K + 1, np.uint64)
+        offs[1:] = np.cumsum([len(o) for o in orders])
+        cat = _a32(np.concatenate([np.asarray(o, np.uint32) for o in orders])
+                   if K else np.zeros(0, np.uint32))
+        take = np.zeros(max(K, 1), np.uint64)
+        W = (n + 63) // 64
+        bits = np.zeros(max(K, 1) * W, np.uint64)
+        self._check(self.lib.ref_build_cache(cat, offs, K, alpha, n, take, bits))
+        cached = [np.asarray(orders[k][:int(take[k])], np.uint32) for k in range(K)]
+        return cached, bits.reshape(max(K, 1), W)[:K]
+
+    def simulate(self, g: CSR, roles, labels, K, fanouts, b, E, seed, cached):
+        offs = np.zeros(K + 1, np.uint64)
+        offs[1:] = np.cumsum([len(c) for c in cached])
+        cat = _a32(np.concatenate([np.asarray(c, np.uint32) for c in cached]) if K else [])
+        cells = np.zeros(E * K * 3, np.uint64)
+        f = _a32(fanouts)
+        self._check(self.lib.ref_simulate(self._graph(g), np.ascontiguousarray(roles, np.uint8),
+                                          _a32(labels), K, f, len(f), b, E, seed, cat, offs, cells))
+        return cells.reshape(E, K, 3)
+
+    def build_reorder(self, labels, K, scores):
+        labels = _a32(labels)
+        n = len(labels)
+        s = np.ascontiguousarray(np.asarray(scores, np.float64).reshape(K, n))
+        oon = np.zeros(n, np.uint32)
+        ranges = np.zeros(2 * K, np.uint64)
+        self._check(self.lib.ref_build_reorder(labels, n, K, s, oon, ranges))
+        return oon, ranges.reshape(K, 2)
+
+
+def port() -> Port:
+    return Port()
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref() -> Ref:
+    return Ref()
