@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Sample+gather minibatches/s (+ VIP edges/s) on B200, BASELINE.json metric.
+
+One process per GPU (torchrun for N > 1). Workload (default `c3`, the
+ogbn-products-shaped config of BASELINE.json configs[2], the largest that
+fits one GPU): community power-law graph n=2,449,029, d=25 (m ~ 122.4M CSR
+slots), K=8 partitions (communities), 8% train, 100-dim fp32 features, VIP
+cache alpha=0.20, fanouts (15,10,5), batch 1024, SeedSpec{42}.
+
+A "step" is one wave of `--wave` minibatches per GPU through the whole hot
+path: sampler (K5/K6 + MFG + relabel) then classify+gather (K9/K10). GPU g
+owns partitions k = g (mod N) and processes their minibatches; rows of
+partitions owned by other GPUs are read over NVLink by the gather kernel
+(CUDA IPC mappings). Per-GPU work is fixed as N grows -> "scaling": "weak".
+
+`value`: inputs (seed ids) already resident in HBM. `e2e`: the same waves
+through the C ABI from pinned HOST seed buffers (H2D inside the timed region)
+with the per-minibatch tallies read back to the host. Both timed with CUDA
+events on the launching stream, max over ranks.
+
+`--impl reference` times the reference's own CPU implementation (the
+unmodified vipkit library compiled in oracle/_ref) on the same minibatches
+with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[0]: synthetic power-law 100K / 2M edges, 64-d fp32, 1 partition
+    "c1": dict(workload="C1 synthetic power-law 100K nodes / 2M edges, 64-d fp32, 1 partition",
+               n=100_000, d=10, K=1, p_in=1.0, train=0.10, dim=64, dtype=0, alpha=0.0,
+               fanouts=(15, 10, 5), b=1024),
+    # configs[1]: ogbn-arxiv-shaped, 169K nodes, ~1.2M edges (x2 slots), 128-d, 2 partitions, cache 10%
+    "c2": dict(workload="C2 ogbn-arxiv-shaped 169K nodes, 128-d fp32, 2 partitions, VIP cache 10%",
+               n=169_343, d=7, K=2, p_in=0.8, train=0.537, dim=128, dtype=0, alpha=0.10,
+               fanouts=(15, 10, 5), b=1024),
+    # configs[2]: ogbn-products-shaped, 2.45M nodes, 62M edges (x2 slots), 100-d, 8 partitions, cache 20%
+    "c3": dict(workload="C3 ogbn-products-shaped 2.45M nodes / 122M CSR slots, 100-d fp32, "
+                        "8 partitions, fanout (15,10,5), batch 1024, VIP cache 20%",
+               n=2_449_029, d=25, K=8, p_in=0.8, train=0.08, dim=100, dtype=0, alpha=0.20,
+               fanouts=(15, 10, 5), b=1024),
+}
+GRAPH_SEED, ROLES_SEED, SAMPLE_SEED, FEATURE_SEED = 7, 3, 42, 1234
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_data(cfg, threads):
+    from paper_2305_03152_b200 import vipkit as vk
+    t = time.time()
+    off, tgt, labels = vk.synth_community_powerlaw(cfg["n"], cfg["d"], cfg["K"], cfg["p_in"], GRAPH_SEED,
+                                                   threads)
+    roles = vk.synth_roles(cfg["n"], cfg["train"], 0.0, 0.0, ROLES_SEED)
+    log(f"[bench] graph n={cfg['n']} m={len(tgt)} generated in {time.time() - t:.1f}s")
+    return off, tgt, labels, roles
+
+
+def schedule(vk, cfg, roles, labels, parts, count):
+    """(epoch, partition, batch_index, seeds) in round-robin over `parts`,
+    epochs advancing as partitions run out (commsim.cpp:45-52 order per cell)."""
+    out, e = [], 0
+    b = cfg["b"]
+    while len(out) < count:
+        per = {k: vk.epoch_permutation(roles, labels, k, b, e, SAMPLE_SEED) for k in parts}
+        nb = {k: (len(per[k]) + b - 1) // b for k in parts}
+        for i in range(max(nb.values())):
+            for k in parts:
+                if i < nb[k]:
+                    out.append((e, k, i, per[k][i * b:(i + 1) * b]))
+        e += 1
+    return out[:count]
+
+
+# ------------------------------------------------------------------ b200 arm
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_03152_b200 import vipkit as vk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    K, M, L = cfg["K"], args.wave, len(cfg["fanouts"])
+    nthreads = max(1, (os.cpu_count() or 8) // world)
+    off, tgt, labels, roles = make_data(cfg, nthreads)
+    n, m = cfg["n"], len(tgt)
+    g = vk.Graph.from_csr(off, tgt, undirected=True, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    sh = stream.cuda_stream
+
+    # ---- VIP analysis for all K partitions in one multi-column pass (timed)
+    p0 = np.stack([vk.initial_probs(roles, labels, k, cfg["b"]) for k in range(K)])
+    p0_d = torch.from_numpy(p0).to(f"cuda:{dev}")
+    tot_d = torch.empty((K, n), dtype=torch.float64, device=f"cuda:{dev}")
+    with torch.cuda.stream(stream):
+        vk.propagate_device(g, cfg["fanouts"], K, p0_d.data_ptr(), None, tot_d.data_ptr(), sh)  # warm
+        torch.cuda.synchronize(dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        reps = 3
+        ev[0].record(stream)
+        for _ in range(reps):
+            vk.propagate_device(g, cfg["fanouts"], K, p0_d.data_ptr(), None, tot_d.data_ptr(), sh)
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
+    vip_ms = ev[0].elapsed_time(ev[1]) / reps
+    totals = tot_d.cpu().numpy()
+    vip_bytes = L * (8 * n + 4 * m + 8 * K * m + 32 * K * n)
+    vip = {"edges_per_s": L * m * K / (vip_ms / 1e3), "ms": vip_ms, "partitions": K, "hops": L,
+           "m": m, "achieved_gbs": vip_bytes / (vip_ms / 1e3) / 1e9}
+
+    # ---- ranking, cache plan, VIP-ordered feature plane
+    orders = [vk.rank_by_scores(labels, k, totals[k], device=dev)[0] for k in range(K)]
+    plan = vk.build_cache(orders, cfg["alpha"], n)
+    oon, ranges = vk.build_reorder(labels, K, totals, device=dev)
+    plane = vk.FeaturePlane(n, K, cfg["dim"], labels, oon, ranges, dtype=cfg["dtype"], device=dev)
+    mine = [k for k in range(K) if k % world == rank]
+    for k in mine:
+        plane.load_partition(k, plan.cached[k], feature_seed=FEATURE_SEED)
+    if world > 1:
+        handles = {k: plane.export(k) for k in mine}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, handles)
+        for r, hs in enumerate(gathered):
+            if r != rank:
+                for k, (h, rows) in hs.items():
+                    plane.attach(k, h, rows)
+        dist.barrier()
+
+    # ---- minibatch schedule + device-resident seeds
+    W, S = args.warmup, args.steps
+    sched = schedule(vk, cfg, roles, labels, mine, (W + 2 * S) * M)
+    waves = [sched[i * M:(i + 1) * M] for i in range(W + 2 * S)]
+    sampler = vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED)
+    view = sampler.view()
+    cap_all = view.all_stride
+    rb = plane.row_bytes
+    out = torch.empty(M * cap_all * rb, dtype=torch.uint8, device=f"cuda:{dev}")
+    seeds_all = np.concatenate([w[3] for wv in waves for w in wv]).astype(np.uint32)
+    seeds_d = torch.from_numpy(seeds_all.view(np.int32)).to(f"cuda:{dev}")
+    wave_offsets, pos = [], 0
+    for wv in waves:
+        o = np.zeros(len(wv) + 1, np.uint64)
+        o[1:] = np.cumsum([len(w[3]) for w in wv])
+        wave_offsets.append(o + pos)
+        pos += int(o[-1])
+    cw = sampler.count_words()
+    hist_counts = torch.zeros((W + 2 * S, cw), dtype=torch.int32, device=f"cuda:{dev}")
+    hist_tally = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64, device=f"cuda:{dev}")
+
+    def wave(i, host=False, pinned=None):
+        wv = waves[i]
+        refs = [(e, k, bi) for (e, k, bi, _) in wv]
+        if host:
+            sampler.run([w[3] for w in wv], refs, stream=sh)
+        else:
+            sampler.run(wave_offsets[i], refs, stream=sh, seeds_device_ptr=seeds_d.data_ptr())
+        evs[i][1].record(stream)
+        plane.gather(sampler, out.data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh)
+        evs[i][2].record(stream)
+        sampler.snapshot_counts(hist_counts[i].data_ptr(), stream=sh)
+        if pinned is not None:
+            pinned[i].copy_(hist_tally[i], non_blocking=True)
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(W + 2 * S)]
+    with torch.cuda.stream(stream):
+        for i in range(W):
+            evs[i][0].record(stream)
+            wave(i)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        clocks = Clocks(dev)
+        clocks.start()
+        l0 = vk.launch_count()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(W, W + S):
+            evs[i][0].record(stream)
+            wave(i)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        launches = vk.launch_count() - l0
+        clk = clocks.stop()
+        # e2e: host seeds (H2D inside the region) + tallies read back to the host
+        pinned = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64).pin_memory()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(W + S, W + 2 * S):
+            evs[i][0].record(stream)
+            wave(i, host=True, pinned=pinned)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    e2e_ms = e0.elapsed_time(e1)
+    tl = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        dist.all_reduce(tl, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(tl[0]), float(tl[1])
+
+    # ---- roofline of the dominant kernel (gather) and of the sampler, from the timed waves
+    tally = hist_tally.cpu().numpy()
+    cnts = hist_counts.cpu().numpy().view(np.uint32)
+    gather_ms = [evs[i][1].elapsed_time(evs[i][2]) for i in range(W, W + S)]
+    sample_ms = [evs[i][0].elapsed_time(evs[i][1]) for i in range(W, W + S)]
+    g_bytes, s_bytes, rows, misses, peer = 0, 0, 0, 0, 0
+    for i in range(W, W + S):
+        nmb = len(waves[i])
+        allc = tally[i, :nmb, :3].sum(axis=1)
+        rows += int(allc.sum())
+        misses += int(tally[i, :nmb, 2].sum())
+        peer += int(tally[i, :nmb, 3].sum())
+        g_bytes += int(allc.sum()) * (2 * rb + 8)
+        fc = cnts[i, :(L + 1) * M].reshape(L + 1, M)[:, :nmb].astype(np.int64)
+        ec = cnts[i, (L + 1) * M:2 * (L + 1) * M].reshape(L + 1, M)[:, :nmb].astype(np.int64)
+        ac = cnts[i, 2 * (L + 1) * M:2 * (L + 1) * M + M][:nmb].astype(np.int64)
+        s_bytes += int(sum(16 * fc[h - 1].sum() + 8 * ec[h].sum() for h in range(1, L + 1))
+                       + 8 * (fc[1:].sum() + ac.sum()))
+    hbm, peak_kind = peaks()
+    g_ach = g_bytes / S / (statistics.mean(gather_ms) / 1e3) / 1e9
+    s_ach = s_bytes / S / (statistics.mean(sample_ms) / 1e3) / 1e9
+    total_mb = sum(len(waves[i]) for i in range(W, W + S)) * world
+    value = total_mb / (ms / 1e3)
+    e2e_val = total_mb / (e2e_ms / 1e3)
+    h2d = int(sum(len(w[3]) * 4 for i in range(W + S, W + 2 * S) for w in waves[i]) / S)
+    result = {
+        "metric": "sample+gather minibatches/s", "value": value, "unit": "minibatches/s",
+        "n_gpus": world, "steps": S, "warmup": W, "ms_per_step": ms / S, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 ids / fp32 rows / fp64 VIP",
+        "data": "synthetic (community power-law graph, counter-hashed feature rows)",
+        "config": {"workload": cfg["workload"], "n": n, "m_slots": m, "partitions": K,
+                   "fanouts": list(cfg["fanouts"]), "batch": cfg["b"], "minibatches_per_step_per_gpu": M,
+                   "feature_dim": cfg["dim"], "row_bytes": rb, "alpha": cfg["alpha"],
+                   "partitions_per_gpu": len(mine), "l2": "inputs larger than L2 (graph "
+                   f"{(8 * n + 4 * m) / 1e9:.2f} GB, features {n * rb / 1e9:.2f} GB); no flush"},
+        "e2e": {"value": e2e_val, "unit": "minibatches/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": M * 4 * 8},
+        "roofline": {"bound": "hbm", "kernel": "k_gather (classify+gather)", "achieved": g_ach,
+                     "peak": hbm, "unit": "GB/s", "frac": g_ach / hbm, "traffic": None,
+                     "peak_kind": peak_kind, "bytes_per_launch": g_bytes / S,
+                     "ms_per_launch": statistics.mean(gather_ms)},
+        "sampler": {"ms_per_wave": statistics.mean(sample_ms), "achieved_gbs": s_ach,
+                    "frac": s_ach / hbm, "bytes_per_wave": s_bytes / S},
+        "vip": {**vip, "unit": "edges/s", "frac": vip["achieved_gbs"] / hbm},
+        "tallies": {"rows": rows, "miss_rows": misses, "miss_rows_over_nvlink": peer,
+                    "miss_fraction": misses / max(rows, 1)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(cfg, off, tgt, labels, roles, plan, waves[W:W + S])
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# -------------------------------------------------------------- CPU baseline
+def cpu_baseline(cfg, off, tgt, labels, roles, plan, waves, budget_s=12.0):
+    """The reference's own CPU path (oracle/_ref, unmodified vipkit) on a
+    bounded sample of the same minibatches: epoch_minibatches + expand +
+    classify (commsim.cpp:41-73), all host threads over independent
+    minibatches. Gather is not included (the reference has none)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return {"value": None, "unit": "minibatches/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    R = O.ref()
+    threads = os.cpu_count() or 1
+    t = time.time()
+    from oracle.oracle import CSR
+    G = CSR(cfg["n"], off, tgt)
+    R._graph(G)
+    log(f"[bench] reference graph built in {time.time() - t:.1f}s")
+    mbs = [w for wv in waves for w in wv]
+    done, t0 = 0, time.time()
+    for (e, k, i, seeds) in mbs:
+        R.expand_classify_range(G, seeds, len(seeds), cfg["fanouts"], SAMPLE_SEED, e, k, 0, 1, labels,
+                                plan.member_bits[k], 1)
+        done += 1
+        if time.time() - t0 > budget_s / 4:
+            break
+    single = done / (time.time() - t0)
+    # threaded: independent minibatches of one partition-epoch cell
+    e, k = mbs[0][0], mbs[0][1]
+    perm = R.epoch_permutation(roles, labels, k, cfg["b"], e, SAMPLE_SEED, K=cfg["K"])
+    nb = (len(perm) + cfg["b"] - 1) // cfg["b"]
+    take = max(1, min(nb, int(single * threads * budget_s / 2)))
+    t0 = time.time()
+    R.expand_classify_range(G, perm, cfg["b"], cfg["fanouts"], SAMPLE_SEED, e, k, 0, take, labels,
+                            plan.member_bits[k], threads)
+    multi = take / (time.time() - t0)
+    R.release(G)
+    return {"value": multi, "unit": "minibatches/s", "cores": threads, "kind": "reference",
+            "single_thread_value": single,
+            "sample": f"{take} minibatches of (epoch {e}, partition {k}) expand+classify with {threads} "
+                      f"threads; {done} minibatches single-threaded; gather excluded (not in reference)"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the unmodified reference CPU path on the same config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2305_03152_b200 import vipkit as vk
+    K, M = cfg["K"], args.wave
+    threads = os.cpu_count() or 1
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    off, tgt, labels, roles = make_data(cfg, threads)
+    R = O.ref()
+    G = O.CSR(cfg["n"], off, tgt)
+    R._graph(G)
+    W, S = args.warmup, args.steps
+    n = cfg["n"]
+    # the reference's VIP for the cache plan (propagate, rank, build_cache)
+    R.set_threads(threads)
+    orders = []
+    for k in range(K):
+        _, tot = R.propagate(G, cfg["fanouts"], R.initial_probs(roles, labels, K, k, cfg["b"]))
+        orders.append(R.rank_by_scores(labels, K, k, tot)[0])
+    _, bits = R.build_cache(orders, cfg["alpha"], n)
+    # per-step minibatch count bounded so the whole run stays within minutes
+    per_step = max(1, min(M, int(os.environ.get("VIPKIT_REF_MB_PER_STEP", "4"))))
+    sched = schedule(vk, cfg, roles, labels, list(range(K)), (W + S) * per_step)
+    t_all = 0.0
+    for i in range(W + S):
+        t0 = time.time()
+        chunk = sched[i * per_step:(i + 1) * per_step]
+        import concurrent.futures as cf
+        with cf.ThreadPoolExecutor(max_workers=min(threads, len(chunk))) as ex:
+            list(ex.map(lambda w: R.expand_classify_range(
+                G, w[3], len(w[3]), cfg["fanouts"], SAMPLE_SEED, w[0], w[1], 0, 1, labels,
+                bits[w[1]], max(1, threads // len(chunk))), chunk))
+        if i >= W:
+            t_all += time.time() - t0
+    value = S * per_step / t_all
+    print(json.dumps({
+        "impl": "reference", "metric": "sample+gather minibatches/s", "value": value,
+        "unit": "minibatches/s", "n_gpus": args.gpus, "steps": S, "warmup": W,
+        "ms_per_step": t_all / S * 1e3, "higher_is_better": True, "scaling": "weak",
+        "config": {"workload": cfg["workload"], "minibatches_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": "minibatches/s", "cores": threads, "kind": "reference",
+                         "sample": f"{per_step} minibatches per step (expand+classify, unmodified vipkit), "
+                                   f"{threads} host threads; gather not in the reference"},
+        "e2e": {"value": value, "unit": "minibatches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--wave", type=int, default=32, help="minibatches per step per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

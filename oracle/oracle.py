@@ -115,6 +115,7 @@ class Port:
         L.vp_graph_from_edges.argtypes = [c_u64, u32p, u32p, c_u64, c_int, C.POINTER(c_vp),
                                           C.POINTER(c_vp), C.POINTER(c_u64)]
         L.vp_free.argtypes = [c_vp]
+        L.vp_stream_draws.argtypes = [c_u64, c_u64, c_u64, u64p]
         L.vp_make_roles.argtypes = [c_u64, c_double, c_double, c_double, c_u64, u8p]
         L.vp_epoch_minibatches.argtypes = [u8p, c_u64, u32p, c_u32, c_u64, c_u64, c_u64, u32p,
                                            C.POINTER(c_u64)]
@@ -141,6 +142,11 @@ class Port:
     def seed_key(self, seed, parts):
         p = _a64(parts)
         return self.lib.vp_seed_key(seed, p, len(p))
+
+    def stream_draws(self, key, bound, count):
+        out = np.zeros(count, np.uint64)
+        self.lib.vp_stream_draws(key, bound, count, out)
+        return out
 
     # ---- graph ----
     def _take_csr(self, n, po, pt, m):

@@ -58,6 +58,13 @@ uint64_t vp_seed_derived(uint64_t seed, uint64_t tag) { return vp_mix64(seed ^ v
 
 void vp_free(void* p) { free(p); }
 
+/* `count` draws of one stream: next_below(bound), or next_u64 when bound == 0 */
+void vp_stream_draws(uint64_t key, uint64_t bound, uint64_t count, uint64_t* out) {
+  vp_stream s;
+  vp_stream_init(&s, key);
+  for (uint64_t i = 0; i < count; ++i) out[i] = bound ? vp_next_below(&s, bound) : vp_next_u64(&s);
+}
+
 /* ---------------------------------------------------------------- graph */
 typedef struct { uint32_t u, v; } edge_t;
 static int cmp_edge(const void* a, const void* b) {

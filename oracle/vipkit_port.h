@@ -26,6 +26,7 @@ double vp_next_double(vp_stream* s);
 uint64_t vp_next_below(vp_stream* s, uint64_t bound);
 uint64_t vp_seed_key(uint64_t seed, const uint64_t* parts, uint32_t np);
 uint64_t vp_seed_derived(uint64_t seed, uint64_t tag);
+void vp_stream_draws(uint64_t key, uint64_t bound, uint64_t count, uint64_t* out);
 
 /* ---- graph (graph.cpp) ---- kinds follow SynthKind order (graph.hpp:80) */
 enum { VP_PATH = 0, VP_STAR = 1, VP_TREE = 2, VP_GRID = 3, VP_PA = 4, VP_UNIFORM = 5 };

@@ -1,0 +1,579 @@
+// Ranking, cache plan and the VIP-ordered feature plane with the fused
+// classify + gather kernel.
+//
+//  * vk_rank_by_scores   = order_remotes (/root/reference/proj/src/policies.cpp:
+//    20-34, 134-138) as a stable device radix sort on an order-preserving key
+//    of (score desc) over ids in ascending order -> ties by ascending id.
+//  * vk_build_reorder    = build_reorder (reorder.cpp:11-34): two stable sorts
+//    (score desc within partition, then partition id).
+//  * feature plane       = the north-star's VIP-ordered store: per resident
+//    partition k, local rows in build_reorder order then cache rows in ranking
+//    order (CachePlan prefix, policies.cpp:149-163), plus slot map u32[n].
+//  * vk_plane_gather     = classify (commsim.cpp:61-73) + row gather for a
+//    whole wave: 128-bit loads/stores, flattened over (row, 16-byte chunk) so
+//    every lane moves data and writes are fully coalesced; misses read the
+//    owner partition's rows from local HBM or, multi-GPU, a peer's HBM over
+//    NVLink (CUDA IPC mapping) inside the same kernel.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+#include "rng.cuh"
+
+struct vk_sampler_s;
+namespace vk {
+void sampler_internal(vk_sampler_s* s, const std::uint32_t** all, std::uint64_t* all_stride,
+                      const std::uint32_t** all_count, std::uint32_t* nmb, const std::uint32_t** partitions,
+                      vk_graph_s** g, cudaStream_t* last_stream);
+std::uint64_t sampler_desc_stride();
+void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out);
+cudaEvent_t sampler_done_event(vk_sampler_s* s);
+}  // namespace vk
+
+struct vk_plane_s {
+  int device = 0;
+  std::uint64_t n = 0;
+  std::uint32_t K = 0, dim = 0;
+  int dtype = VK_F32;
+  std::uint64_t row_bytes = 0;
+  vk::DevBuf part_of, owner_row;  // u32 [n] each
+  std::vector<std::uint64_t> rstart, rend;
+  std::vector<std::uint32_t> old_of_new;  // host copy (local row order)
+  struct Part {
+    bool resident = false, attached = false;
+    vk::DevBuf store;  // (n_local + n_cache) rows
+    vk::DevBuf slot;   // u32 [n]
+    std::uint64_t n_local = 0, n_cache = 0;
+    std::vector<std::uint64_t> cache_bits;  // CachePlan::member_bits[k]
+    void* peer = nullptr;                   // IPC-mapped local rows of a remote partition
+  };
+  std::vector<Part> parts;
+  vk::DevBuf d_base, d_slot, d_nlocal;  // K-entry tables for the gather kernel
+  cudaStream_t stream = nullptr;
+};
+
+namespace vk {
+namespace {
+
+// Order-preserving u64 key of a double, descending: -0.0 == +0.0 as in the
+// reference comparator (policies.cpp:28).
+__device__ __forceinline__ std::uint64_t desc_key(double x) {
+  std::uint64_t b = (x == 0.0) ? 0ull : (std::uint64_t)__double_as_longlong(x);
+  const std::uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  return ~asc;
+}
+
+__global__ void k_rank_keys(const double* __restrict__ scores, const std::uint32_t* __restrict__ part_of,
+                            std::uint64_t n, std::uint32_t k, std::uint64_t* __restrict__ keys,
+                            std::uint32_t* __restrict__ ids, unsigned long long* __restrict__ nremote) {
+  std::uint64_t cnt = 0;
+  for (std::uint64_t v = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (std::uint64_t)gridDim.x * blockDim.x) {
+    const bool remote = part_of[v] != k;
+    keys[v] = remote ? desc_key(scores[v]) : ~0ull;  // locals sort to the tail
+    ids[v] = (std::uint32_t)v;
+    cnt += remote;
+  }
+  atomicAdd(nremote, (unsigned long long)cnt);
+}
+
+__global__ void k_gather_scores(const double* __restrict__ scores, const std::uint32_t* __restrict__ order,
+                                std::uint64_t cnt, double* __restrict__ out) {
+  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (std::uint64_t)gridDim.x * blockDim.x)
+    out[i] = scores[order[i]];
+}
+
+__global__ void k_reorder_keys(const double* __restrict__ scores, const std::uint32_t* __restrict__ part_of,
+                               std::uint64_t n, std::uint64_t* __restrict__ keys, std::uint32_t* __restrict__ ids) {
+  for (std::uint64_t v = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (std::uint64_t)gridDim.x * blockDim.x) {
+    keys[v] = desc_key(scores[(std::uint64_t)part_of[v] * n + v]);
+    ids[v] = (std::uint32_t)v;
+  }
+}
+
+__global__ void k_part_keys(const std::uint32_t* __restrict__ part_of, const std::uint32_t* __restrict__ ids,
+                            std::uint64_t n, std::uint32_t* __restrict__ keys) {
+  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (std::uint64_t)gridDim.x * blockDim.x)
+    keys[i] = part_of[ids[i]];
+}
+
+unsigned grid_for(std::uint64_t work, int device) {
+  const std::uint64_t g = (work + 255) / 256;
+  const std::uint64_t cap = (std::uint64_t)sm_count(device) * 16;
+  return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+template <class K, class V>
+void radix_sort_pairs(DevBuf& k_in, DevBuf& k_out, DevBuf& v_in, DevBuf& v_out, std::uint64_t n, int end_bit,
+                      cudaStream_t st) {
+  std::size_t tmp = 0;
+  VK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k_in.as<K>(), k_out.as<K>(), v_in.as<V>(),
+                                          v_out.as<V>(), (std::int64_t)n, 0, end_bit, st));
+  DevBuf t(tmp);
+  VK_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, k_in.as<K>(), k_out.as<K>(), v_in.as<V>(), v_out.as<V>(),
+                                          (std::int64_t)n, 0, end_bit, st));
+  count_launch(4);
+}
+
+// ---- synthetic feature rows (identical to oracle vp_feature_*) ----
+__device__ __forceinline__ std::uint64_t feat_bits(std::uint64_t seed, std::uint64_t v, std::uint32_t j,
+                                                   std::uint32_t D) {
+  return mix64(seed ^ mix64(v * (std::uint64_t)D + j));
+}
+
+__global__ void k_synth_rows(const std::uint32_t* __restrict__ ids, std::uint64_t rows, std::uint32_t D,
+                             int fp16, std::uint64_t seed, void* __restrict__ out) {
+  const std::uint64_t total = rows * D;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t r = e / D;
+    const std::uint32_t j = (std::uint32_t)(e - r * D);
+    const std::uint64_t x = feat_bits(seed, ids[r], j, D);
+    if (fp16)
+      static_cast<__half*>(out)[e] = __float2half_rn((float)(x >> 53) * 0x1.0p-10f - 1.0f);
+    else
+      static_cast<float*>(out)[e] = (float)(x >> 40) * 0x1.0p-23f - 1.0f;
+  }
+}
+
+__global__ void k_fill_slots(const std::uint32_t* __restrict__ ids, std::uint64_t count, std::uint32_t base,
+                             std::uint32_t* __restrict__ slot) {
+  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (std::uint64_t)gridDim.x * blockDim.x)
+    slot[ids[i]] = base + (std::uint32_t)i;
+}
+
+// ---- classify + gather ----
+struct GatherParams {
+  const std::uint32_t* all;
+  std::uint64_t all_stride;
+  const std::uint32_t* all_count;
+  const char* desc;          // WaveDesc array; partition at desc + mb*desc_stride
+  std::uint64_t desc_stride;
+  const char* const* base;   // [K] local-row base of each partition (local or peer)
+  const std::uint32_t* const* slot;  // [K] slot map (resident partitions)
+  const std::uint32_t* nlocal;       // [K]
+  const std::uint32_t* part_of;
+  const std::uint32_t* owner_row;
+  const unsigned char* peer_mask;    // [K] 1 if the partition's rows live on another GPU
+  char* out;
+  std::uint64_t out_stride_bytes;
+  std::uint64_t row_bytes;
+  std::uint32_t V;                   // vector elements per row
+  std::uint64_t magic;               // ceil(2^64 / V)
+  unsigned long long* counts;        // [nmb][4]
+};
+
+template <class T>
+__global__ void __launch_bounds__(256) k_gather(GatherParams p) {
+  const std::uint32_t mb = blockIdx.y;
+  const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
+  const std::uint32_t cnt = p.all_count[mb];
+  const std::uint32_t* all = p.all + mb * p.all_stride;
+  const std::uint32_t* slot = p.slot[k];
+  const std::uint32_t nl = p.nlocal[k];
+  const T* store = reinterpret_cast<const T*>(p.base[k]);
+  T* out = reinterpret_cast<T*>(p.out + mb * p.out_stride_bytes);
+  const std::uint32_t V = p.V;
+  const std::uint64_t rowv = p.row_bytes / sizeof(T);
+  const std::uint32_t total = cnt * V;
+  unsigned c_local = 0, c_cache = 0, c_miss = 0, c_peer = 0;
+  for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const std::uint32_t r = V == 1 ? e : (std::uint32_t)__umul64hi((std::uint64_t)e, p.magic);
+    const std::uint32_t c = e - r * V;
+    const std::uint32_t v = __ldg(all + r);
+    const std::uint32_t s = __ldg(slot + v);
+    const T* src;
+    if (s != VK_MISS) {
+      src = store + (std::uint64_t)s * rowv;
+      if (c == 0) (s < nl ? c_local : c_cache)++;
+    } else {
+      const std::uint32_t o = __ldg(p.part_of + v);
+      src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
+      if (c == 0) {
+        ++c_miss;
+        c_peer += p.peer_mask[o];
+      }
+    }
+    out[e] = src[c];
+  }
+  // block-reduce the class counts, one atomic per class per CTA
+  __shared__ unsigned sh[4][8];
+  unsigned vals[4] = {c_local, c_cache, c_miss, c_peer};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    unsigned x = __reduce_add_sync(0xffffffffu, vals[q]);
+    if ((threadIdx.x & 31) == 0) sh[q][threadIdx.x >> 5] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[threadIdx.x][w];
+    if (t) atomicAdd(p.counts + mb * 4 + threadIdx.x, t);
+  }
+}
+
+}  // namespace
+}  // namespace vk
+
+using namespace vk;
+
+extern "C" {
+
+int vk_rank_by_scores(int device, uint64_t n, const uint32_t* part_of, uint32_t k, const double* scores,
+                      uint64_t n_scores, uint32_t* order_out, double* score_out, uint64_t* count_out) {
+  return guard([&] {
+    if (!part_of || !scores || !order_out || !count_out) raise(VK_ERR_PARAMETER, "null argument");
+    if (n_scores != n) raise(VK_ERR_SHAPE, "score vector length does not match vertex count");  // policies.cpp:135-136
+    DeviceGuard dg(device);
+    cudaStream_t st;
+    VK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+      DevBuf dsc(n * 8), dpart(n * 4), k0(n * 8), k1(n * 8), i0(n * 4), i1(n * 4), cnt(8);
+      VK_CUDA(cudaMemcpyAsync(dsc.p, scores, n * 8, cudaMemcpyHostToDevice, st));
+      VK_CUDA(cudaMemcpyAsync(dpart.p, part_of, n * 4, cudaMemcpyHostToDevice, st));
+      VK_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+      k_rank_keys<<<grid_for(n, device), 256, 0, st>>>(dsc.as<double>(), dpart.as<std::uint32_t>(), n, k,
+                                                       k0.as<std::uint64_t>(), i0.as<std::uint32_t>(),
+                                                       cnt.as<unsigned long long>());
+      count_launch();
+      VK_LAUNCH_CHECK();
+      radix_sort_pairs<std::uint64_t, std::uint32_t>(k0, k1, i0, i1, n, 64, st);
+      unsigned long long c = 0;
+      VK_CUDA(cudaMemcpyAsync(&c, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+      VK_CUDA(cudaStreamSynchronize(st));
+      if (c) {
+        VK_CUDA(cudaMemcpyAsync(order_out, i1.p, c * 4, cudaMemcpyDeviceToHost, st));
+        if (score_out) {
+          k_gather_scores<<<grid_for(c, device), 256, 0, st>>>(dsc.as<double>(), i1.as<std::uint32_t>(), c,
+                                                               k0.as<double>());
+          count_launch();
+          VK_LAUNCH_CHECK();
+          VK_CUDA(cudaMemcpyAsync(score_out, k0.p, c * 8, cudaMemcpyDeviceToHost, st));
+        }
+      }
+      VK_CUDA(cudaStreamSynchronize(st));
+      *count_out = c;
+    } catch (...) {
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaStreamDestroy(st);
+  });
+}
+
+int vk_build_reorder(int device, uint64_t n, uint32_t K, const uint32_t* part_of, const double* scores,
+                     uint32_t* old_of_new, uint64_t* ranges) {
+  return guard([&] {
+    if (!part_of || !scores || !old_of_new || !ranges) raise(VK_ERR_PARAMETER, "null argument");
+    if (K == 0) raise(VK_ERR_PARAMETER, "partition count must be >= 1");
+    std::vector<std::uint64_t> cnt(K, 0);
+    for (std::uint64_t v = 0; v < n; ++v) {
+      if (part_of[v] >= K) raise(VK_ERR_FORMAT, "partition label out of range");
+      cnt[part_of[v]]++;
+    }
+    DeviceGuard dg(device);
+    cudaStream_t st;
+    VK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+      DevBuf dsc(n * 8 * K), dpart(n * 4), k0(n * 8), k1(n * 8), i0(n * 4), i1(n * 4), p0(n * 4), p1(n * 4);
+      VK_CUDA(cudaMemcpyAsync(dsc.p, scores, n * 8 * K, cudaMemcpyHostToDevice, st));
+      VK_CUDA(cudaMemcpyAsync(dpart.p, part_of, n * 4, cudaMemcpyHostToDevice, st));
+      k_reorder_keys<<<grid_for(n, device), 256, 0, st>>>(dsc.as<double>(), dpart.as<std::uint32_t>(), n,
+                                                          k0.as<std::uint64_t>(), i0.as<std::uint32_t>());
+      count_launch();
+      VK_LAUNCH_CHECK();
+      radix_sort_pairs<std::uint64_t, std::uint32_t>(k0, k1, i0, i1, n, 64, st);
+      k_part_keys<<<grid_for(n, device), 256, 0, st>>>(dpart.as<std::uint32_t>(), i1.as<std::uint32_t>(), n,
+                                                       p0.as<std::uint32_t>());
+      count_launch();
+      VK_LAUNCH_CHECK();
+      int bits = 1;
+      while ((1ull << bits) < K) ++bits;
+      radix_sort_pairs<std::uint32_t, std::uint32_t>(p0, p1, i1, i0, n, bits, st);
+      VK_CUDA(cudaMemcpyAsync(old_of_new, i0.p, n * 4, cudaMemcpyDeviceToHost, st));
+      VK_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaStreamDestroy(st);
+    std::uint64_t pos = 0;
+    for (std::uint32_t k = 0; k < K; ++k) {
+      ranges[2 * k] = pos;
+      pos += cnt[k];
+      ranges[2 * k + 1] = pos;
+    }
+  });
+}
+
+int vk_plane_create(int device, uint64_t n, uint32_t K, uint32_t dim, int dtype, const uint32_t* part_of,
+                    const uint32_t* old_of_new, const uint64_t* ranges, vk_plane* out) {
+  return guard([&] {
+    if (!part_of || !old_of_new || !ranges || !out) raise(VK_ERR_PARAMETER, "null argument");
+    if (K == 0 || dim == 0 || n == 0) raise(VK_ERR_PARAMETER, "n, K and dim must be >= 1");
+    if (dtype != VK_F32 && dtype != VK_F16) raise(VK_ERR_PARAMETER, "dtype must be VK_F32 or VK_F16");
+    // owner_row[v] = position of v inside its partition's range (reorder map)
+    std::vector<std::uint32_t> owner(n, VK_MISS);
+    std::vector<std::uint64_t> rs(K), re(K);
+    std::uint64_t prev = 0;
+    for (std::uint32_t k = 0; k < K; ++k) {
+      rs[k] = ranges[2 * k];
+      re[k] = ranges[2 * k + 1];
+      if (rs[k] != prev || re[k] < rs[k] || re[k] > n) raise(VK_ERR_SHAPE, "reorder ranges malformed");
+      prev = re[k];
+      for (std::uint64_t i = rs[k]; i < re[k]; ++i) {
+        const std::uint32_t v = old_of_new[i];
+        if (v >= n || owner[v] != VK_MISS) raise(VK_ERR_SHAPE, "old_of_new is not a permutation");
+        if (part_of[v] != k) raise(VK_ERR_SHAPE, "reorder range does not match partition labels");
+        owner[v] = (std::uint32_t)(i - rs[k]);
+      }
+    }
+    if (prev != n) raise(VK_ERR_SHAPE, "reorder map size does not match vertex count");
+    DeviceGuard dg(device);
+    auto* p = new vk_plane_s();
+    try {
+      p->device = device;
+      p->n = n;
+      p->K = K;
+      p->dim = dim;
+      p->dtype = dtype;
+      p->row_bytes = (std::uint64_t)dim * (dtype == VK_F16 ? 2 : 4);
+      p->rstart = rs;
+      p->rend = re;
+      p->old_of_new.assign(old_of_new, old_of_new + n);
+      p->parts.resize(K);
+      VK_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+      p->part_of.alloc(n * 4);
+      p->owner_row.alloc(n * 4);
+      VK_CUDA(cudaMemcpyAsync(p->part_of.p, part_of, n * 4, cudaMemcpyHostToDevice, p->stream));
+      VK_CUDA(cudaMemcpyAsync(p->owner_row.p, owner.data(), n * 4, cudaMemcpyHostToDevice, p->stream));
+      p->d_base.alloc(K * sizeof(void*));
+      p->d_slot.alloc(K * sizeof(void*));
+      p->d_nlocal.alloc(K * 4 + K);  // u32 nlocal[K] then u8 peer_mask[K]
+      VK_CUDA(cudaMemsetAsync(p->d_base.p, 0, p->d_base.bytes, p->stream));
+      VK_CUDA(cudaMemsetAsync(p->d_slot.p, 0, p->d_slot.bytes, p->stream));
+      VK_CUDA(cudaMemsetAsync(p->d_nlocal.p, 0, p->d_nlocal.bytes, p->stream));
+      VK_CUDA(cudaStreamSynchronize(p->stream));
+    } catch (...) {
+      vk_plane_destroy(p);
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int vk_plane_destroy(vk_plane p) {
+  return guard([&] {
+    if (!p) return;
+    DeviceGuard dg(p->device);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    for (auto& part : p->parts)
+      if (part.peer) cudaIpcCloseMemHandle(part.peer);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+  });
+}
+
+namespace {
+
+void publish_tables(vk_plane_s& p) {
+  std::vector<const void*> base(p.K, nullptr), slot(p.K, nullptr);
+  std::vector<unsigned char> nl(p.K * 4 + p.K, 0);
+  for (std::uint32_t k = 0; k < p.K; ++k) {
+    const auto& q = p.parts[k];
+    if (q.resident) {
+      base[k] = q.store.p;
+      slot[k] = q.slot.p;
+      const std::uint32_t x = (std::uint32_t)q.n_local;
+      std::memcpy(nl.data() + 4 * k, &x, 4);
+    } else if (q.attached) {
+      base[k] = q.peer;
+      nl[p.K * 4 + k] = 1;
+    }
+  }
+  VK_CUDA(cudaMemcpyAsync(p.d_base.p, base.data(), p.K * sizeof(void*), cudaMemcpyHostToDevice, p.stream));
+  VK_CUDA(cudaMemcpyAsync(p.d_slot.p, slot.data(), p.K * sizeof(void*), cudaMemcpyHostToDevice, p.stream));
+  VK_CUDA(cudaMemcpyAsync(p.d_nlocal.p, nl.data(), nl.size(), cudaMemcpyHostToDevice, p.stream));
+  VK_CUDA(cudaStreamSynchronize(p.stream));
+}
+
+}  // namespace
+
+int vk_plane_load_partition(vk_plane p, uint32_t k, const uint32_t* cache_ids, uint64_t n_cache,
+                            const void* features, uint64_t feature_seed) {
+  return guard([&] {
+    if (!p) raise(VK_ERR_PARAMETER, "null plane");
+    if (k >= p->K) raise(VK_ERR_CONFIG, "partition index out of range");
+    if (n_cache && !cache_ids) raise(VK_ERR_PARAMETER, "null cache ids");
+    auto& q = p->parts[k];
+    const std::uint64_t n = p->n;
+    const std::uint64_t nl = p->rend[k] - p->rstart[k];
+    // cache ids: remote, distinct, in range (a ranking prefix always is)
+    std::vector<std::uint64_t> bits((n + 63) / 64, 0);
+    std::vector<std::uint32_t> part_host(n);
+    DeviceGuard dg(p->device);
+    VK_CUDA(cudaMemcpy(part_host.data(), p->part_of.p, n * 4, cudaMemcpyDeviceToHost));
+    for (std::uint64_t i = 0; i < n_cache; ++i) {
+      const std::uint32_t v = cache_ids[i];
+      if (v >= n) raise(VK_ERR_FORMAT, "cached vertex id out of range");  // policies.cpp:191
+      if (part_host[v] == k) raise(VK_ERR_PARAMETER, "cache holds a vertex local to its partition");
+      if ((bits[v >> 6] >> (v & 63)) & 1u) raise(VK_ERR_PARAMETER, "duplicate cached vertex");
+      bits[v >> 6] |= 1ull << (v & 63);
+    }
+    const std::uint64_t rows = nl + n_cache;
+    if (rows >= VK_MISS) raise(VK_ERR_UNSUPPORTED, "too many rows in one partition store");
+    std::vector<std::uint32_t> ids(rows);
+    std::memcpy(ids.data(), p->old_of_new.data() + p->rstart[k], nl * 4);
+    if (n_cache) std::memcpy(ids.data() + nl, cache_ids, n_cache * 4);
+    q.store.alloc(std::max<std::uint64_t>(rows, 1) * p->row_bytes);
+    q.slot.alloc(n * 4);
+    DevBuf dids(std::max<std::uint64_t>(rows, 1) * 4);
+    cudaStream_t st = p->stream;
+    VK_CUDA(cudaMemcpyAsync(dids.p, ids.data(), rows * 4, cudaMemcpyHostToDevice, st));
+    VK_CUDA(cudaMemsetAsync(q.slot.p, 0xFF, n * 4, st));
+    if (rows) {
+      k_fill_slots<<<grid_for(rows, p->device), 256, 0, st>>>(dids.as<std::uint32_t>(), rows, 0,
+                                                             q.slot.as<std::uint32_t>());
+      count_launch();
+      VK_LAUNCH_CHECK();
+    }
+    if (features) {
+      // stage the selected rows on the host, one H2D copy
+      std::vector<unsigned char> rowsbuf(rows * p->row_bytes);
+      const unsigned char* src = static_cast<const unsigned char*>(features);
+      for (std::uint64_t r = 0; r < rows; ++r)
+        std::memcpy(rowsbuf.data() + r * p->row_bytes, src + (std::uint64_t)ids[r] * p->row_bytes, p->row_bytes);
+      VK_CUDA(cudaMemcpyAsync(q.store.p, rowsbuf.data(), rowsbuf.size(), cudaMemcpyHostToDevice, st));
+      VK_CUDA(cudaStreamSynchronize(st));
+    } else if (rows) {
+      k_synth_rows<<<grid_for(rows * p->dim, p->device), 256, 0, st>>>(dids.as<std::uint32_t>(), rows, p->dim,
+                                                                      p->dtype == VK_F16, feature_seed, q.store.p);
+      count_launch();
+      VK_LAUNCH_CHECK();
+    }
+    VK_CUDA(cudaStreamSynchronize(st));
+    q.resident = true;
+    q.attached = false;
+    q.n_local = nl;
+    q.n_cache = n_cache;
+    q.cache_bits = std::move(bits);
+    publish_tables(*p);
+  });
+}
+
+int vk_plane_is_cached(vk_plane p, uint32_t k, uint32_t v, int* out) {
+  return guard([&] {
+    if (!p || !out) raise(VK_ERR_PARAMETER, "null argument");
+    if (k >= p->K || !p->parts[k].resident) raise(VK_ERR_CONFIG, "partition not resident on this plane");
+    if (v >= p->n) raise(VK_ERR_RANGE, "vertex id out of range");
+    *out = (int)((p->parts[k].cache_bits[v >> 6] >> (v & 63)) & 1u);  // policies.hpp:58-60
+  });
+}
+
+int vk_plane_export(vk_plane p, uint32_t k, void* handle64, uint64_t* rows) {
+  return guard([&] {
+    if (!p || !handle64) raise(VK_ERR_PARAMETER, "null argument");
+    if (k >= p->K || !p->parts[k].resident) raise(VK_ERR_CONFIG, "partition not resident on this plane");
+    DeviceGuard dg(p->device);
+    cudaIpcMemHandle_t h;
+    VK_CUDA(cudaIpcGetMemHandle(&h, p->parts[k].store.p));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, 64);
+    if (rows) *rows = p->parts[k].n_local;
+  });
+}
+
+int vk_plane_attach(vk_plane p, uint32_t k, const void* handle64, uint64_t rows) {
+  return guard([&] {
+    if (!p || !handle64) raise(VK_ERR_PARAMETER, "null argument");
+    if (k >= p->K) raise(VK_ERR_CONFIG, "partition index out of range");
+    if (p->parts[k].resident) raise(VK_ERR_CONFIG, "partition already resident on this plane");
+    if (rows != p->rend[k] - p->rstart[k]) raise(VK_ERR_SHAPE, "peer partition row count mismatch");
+    DeviceGuard dg(p->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    void* ptr = nullptr;
+    VK_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    auto& q = p->parts[k];
+    if (q.peer) cudaIpcCloseMemHandle(q.peer);
+    q.peer = ptr;
+    q.attached = true;
+    publish_tables(*p);
+  });
+}
+
+int vk_plane_row_bytes(vk_plane p, uint64_t* row_bytes) {
+  return guard([&] {
+    if (!p || !row_bytes) raise(VK_ERR_PARAMETER, "null argument");
+    *row_bytes = p->row_bytes;
+  });
+}
+
+int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_rows, uint64_t* counts_dev,
+                    vk_stream_t stream) {
+  return guard([&] {
+    if (!p || !s || !out_dev || !counts_dev) raise(VK_ERR_PARAMETER, "null argument");
+    GatherParams gp{};
+    std::uint32_t nmb = 0;
+    vk_graph_s* g = nullptr;
+    cudaStream_t last = nullptr;
+    const std::uint32_t* parts = nullptr;
+    sampler_internal(s, &gp.all, &gp.all_stride, &gp.all_count, &nmb, &parts, &g, &last);
+    if (nmb == 0) raise(VK_ERR_PARAMETER, "sampler has not run");
+    if (g->device != p->device) raise(VK_ERR_CONFIG, "sampler and plane live on different devices");
+    if (g->n != p->n) raise(VK_ERR_SHAPE, "sampler graph and plane vertex counts differ");
+    std::vector<std::uint32_t> hp;
+    sampler_host_partitions(s, hp);
+    for (std::uint32_t k : hp) {
+      if (k >= p->K || !p->parts[k].resident)
+        raise(VK_ERR_CONFIG, "minibatch partition " + std::to_string(k) + " is not resident on this plane");
+    }
+    for (std::uint32_t k = 0; k < p->K; ++k)
+      if (!p->parts[k].resident && !p->parts[k].attached)
+        raise(VK_ERR_CONFIG, "partition " + std::to_string(k) + " is neither resident nor attached");
+    DeviceGuard dg(p->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : (last ? last : p->stream);
+    if (st != last) VK_CUDA(cudaStreamWaitEvent(st, sampler_done_event(s), 0));
+    VK_CUDA(cudaMemsetAsync(counts_dev, 0, (std::uint64_t)nmb * 4 * 8, st));
+    gp.desc = reinterpret_cast<const char*>(parts);
+    gp.desc_stride = sampler_desc_stride();
+    gp.base = reinterpret_cast<const char* const*>(p->d_base.p);
+    gp.slot = reinterpret_cast<const std::uint32_t* const*>(p->d_slot.p);
+    gp.nlocal = p->d_nlocal.as<std::uint32_t>();
+    gp.peer_mask = p->d_nlocal.as<unsigned char>() + 4 * p->K;
+    gp.part_of = p->part_of.as<std::uint32_t>();
+    gp.owner_row = p->owner_row.as<std::uint32_t>();
+    gp.out = static_cast<char*>(out_dev);
+    gp.out_stride_bytes = out_stride_rows * p->row_bytes;
+    gp.row_bytes = p->row_bytes;
+    gp.counts = reinterpret_cast<unsigned long long*>(counts_dev);
+    const bool v16 = (p->row_bytes % 16 == 0) && ((std::uintptr_t)out_dev % 16 == 0);
+    const bool v4 = (p->row_bytes % 4 == 0) && ((std::uintptr_t)out_dev % 4 == 0);
+    const std::uint64_t esz = v16 ? 16 : (v4 ? 4 : 2);
+    gp.V = (std::uint32_t)(p->row_bytes / esz);
+    gp.magic = gp.V == 1 ? 0 : (~0ull / gp.V) + 1;  // ceil(2^64 / V)
+    if ((std::uint64_t)gp.all_stride * gp.V >= (1ull << 32))
+      raise(VK_ERR_UNSUPPORTED, "rows x vector width exceeds 2^32 per minibatch");
+    const unsigned gx = (unsigned)std::max<std::uint64_t>(
+        1, std::min<std::uint64_t>((std::uint64_t)sm_count(p->device) * 8 / nmb + 1,
+                                   ceil_div(gp.all_stride * gp.V, 256)));
+    dim3 grid(gx, nmb);
+    if (v16)
+      k_gather<uint4><<<grid, 256, 0, st>>>(gp);
+    else if (v4)
+      k_gather<std::uint32_t><<<grid, 256, 0, st>>>(gp);
+    else
+      k_gather<std::uint16_t><<<grid, 256, 0, st>>>(gp);
+    count_launch();
+    VK_LAUNCH_CHECK();
+  });
+}
+
+}  // extern "C"

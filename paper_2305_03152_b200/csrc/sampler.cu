@@ -1,0 +1,712 @@
+// Node-wise fanout sampler on the device, bit-identical to vipkit::expand
+// (/root/reference/proj/src/sampling.cpp:72-128), batched over a "wave" of
+// minibatches so one launch keeps the whole GPU busy.
+//
+// Per hop h = 1..L, for every minibatch of the wave:
+//   k_sample   one thread per vertex v of F_{h-1}: stream key =
+//              key_step(prefix(e,k,i,h), v) (sampling.cpp:110-112); deg <= f
+//              copies the CSR slice, else a *sparse* partial Fisher-Yates over
+//              the neighbour list (positions < f tracked in a small array,
+//              displaced positions >= f in a <= f-entry map) -- the same draw
+//              sequence as the reference's full scratch copy (sampling.cpp:
+//              82-91), verified in tests. Draws land at the source's MFG row
+//              (indptr) and set bits in the hop bitmap and the all bitmap.
+//   k_compact  single-pass decoupled look-back over the hop bitmap:
+//              F_h = sorted distinct ids (sort+unique of sampling.cpp:115-116
+//              for free), per-word rank prefix, and -- fused -- the next hop's
+//              MFG indptr = exclusive scan of min(f_{h+1}, deg(v)).
+//   k_relabel  MFG dst = rank of each drawn id in F_h (bitmap rank: prefix
+//              word + popc).
+// Then all_vertices = compaction of the all bitmap (sampling.cpp:121-126) and
+// the relabel map F_h -> index in all_vertices.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+#include "rng.cuh"
+#include "scan.cuh"
+
+namespace vk {
+
+constexpr int kCompactThreads = 256;
+constexpr int kWordsPerThread = 2;
+constexpr int kTileWords = kCompactThreads * kWordsPerThread;
+
+// Per-minibatch wave descriptor (uploaded once per run).
+struct WaveDesc {
+  std::uint64_t key_prefix[VK_MAX_HOPS];
+  std::uint64_t seed_begin;
+  std::uint32_t seed_count;
+  std::uint32_t partition;
+};
+
+}  // namespace vk
+using vk::WaveDesc;
+using vk::kCompactThreads;
+using vk::kTileWords;
+using vk::kWordsPerThread;
+
+struct vk_sampler_s {
+  vk_graph_s* g = nullptr;
+  vk_sampler_config cfg{};
+  std::uint32_t L = 0, M = 0;
+  std::uint64_t n = 0, W = 0, tiles = 0;
+  std::uint64_t capF[VK_MAX_HOPS + 1]{};  // [0] = batch size
+  std::uint64_t capS[VK_MAX_HOPS + 1]{};  // [h] edges of hop h
+  std::uint64_t capS_max = 0, capAll = 0;
+  vk::DevBuf F[VK_MAX_HOPS + 1], allidx[VK_MAX_HOPS + 1], indptr[VK_MAX_HOPS + 1], dst[VK_MAX_HOPS + 1];
+  vk::DevBuf counts;  // u32: fcount[(L+1)*M] | ecount[(L+1)*M] | allcount[M] | err[1]
+  vk::DevBuf edges_tmp, all, hopbits, allbits, hopprefix, allprefix, status, tickets, desc, seed_stage;
+  vk::PinnedBuf desc_host[2], seed_host[2];
+  cudaEvent_t staged[2] = {nullptr, nullptr};
+  bool staged_used[2] = {false, false};
+  int slot = 0;
+  std::uint32_t last_nmb = 0;
+  std::vector<std::uint32_t> last_parts;
+  cudaEvent_t done = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaStream_t last_stream = nullptr;
+
+  std::uint32_t* fcount(std::uint32_t h) const { return counts.as<std::uint32_t>() + (std::uint64_t)h * M; }
+  std::uint32_t* ecount(std::uint32_t h) const {
+    return counts.as<std::uint32_t>() + (std::uint64_t)(L + 1) * M + (std::uint64_t)h * M;
+  }
+  std::uint32_t* allcount() const { return counts.as<std::uint32_t>() + 2ull * (L + 1) * M; }
+  std::uint32_t* err() const { return allcount() + M; }
+  std::size_t counts_words() const { return 2ull * (L + 1) * M + M + 1; }
+};
+
+namespace vk {
+namespace {
+
+// ------------------------------------------------------------- kernels
+
+// Hop-1 preparation, one CTA per minibatch: copy the seeds into F_0, mark
+// them in the all bitmap, and scan min(f_1, deg) into the hop-1 indptr.
+__global__ void __launch_bounds__(1024) k_prepare(const WaveDesc* __restrict__ desc,
+                                                  const std::uint32_t* __restrict__ seeds,
+                                                  const std::uint32_t* __restrict__ outdeg, std::uint64_t n,
+                                                  std::uint32_t f1, std::uint32_t* __restrict__ F0,
+                                                  std::uint64_t capF0, std::uint32_t* __restrict__ fcount0,
+                                                  std::uint32_t* __restrict__ indptr1,
+                                                  std::uint32_t* __restrict__ ecount1,
+                                                  unsigned long long* __restrict__ allbits, std::uint64_t W,
+                                                  std::uint32_t* __restrict__ err) {
+  __shared__ unsigned long long sm[32];
+  const std::uint32_t mb = blockIdx.x;
+  const WaveDesc d = desc[mb];
+  std::uint32_t* f0 = F0 + mb * capF0;
+  std::uint32_t* ip = indptr1 + mb * (capF0 + 1);
+  unsigned long long* ab = allbits + mb * W;
+  unsigned long long carry = 0;
+  for (std::uint32_t base = 0; base < d.seed_count; base += blockDim.x) {
+    const std::uint32_t i = base + threadIdx.x;
+    unsigned long long c = 0;
+    if (i < d.seed_count) {
+      std::uint32_t v = seeds[d.seed_begin + i];
+      if (v >= n) {
+        atomicOr(err, 1u);
+        v = 0;
+      }
+      f0[i] = v;
+      atomicOr(ab + (v >> 6), 1ull << (v & 63));
+      c = min(f1, outdeg[v]);
+    }
+    unsigned long long tot;
+    const unsigned long long inc = block_inclusive_scan<1024>(c, sm, &tot);
+    if (i < d.seed_count) ip[i] = (std::uint32_t)(carry + inc - c);
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    ip[d.seed_count] = (std::uint32_t)carry;
+    ecount1[mb] = (std::uint32_t)carry;
+    fcount0[mb] = d.seed_count;
+  }
+}
+
+// Sparse partial Fisher-Yates, same draws as sampling.cpp:87-91.
+template <int MAXF>
+__device__ __forceinline__ void sample_one(const std::uint32_t* __restrict__ nbrs, std::uint32_t deg,
+                                           std::uint32_t f, Stream& s, std::uint32_t* __restrict__ out,
+                                           unsigned long long* __restrict__ hb, unsigned long long* __restrict__ ab) {
+  if (deg <= f) {  // sampling.cpp:76-78: all neighbours, CSR order
+    for (std::uint32_t i = 0; i < deg; ++i) {
+      const std::uint32_t u = __ldg(nbrs + i);
+      out[i] = u;
+      atomicOr(hb + (u >> 6), 1ull << (u & 63));
+      atomicOr(ab + (u >> 6), 1ull << (u & 63));
+    }
+    return;
+  }
+  std::uint32_t lo[MAXF];           // current value at positions [0, f)
+  std::uint32_t hpos[MAXF], hval[MAXF];  // displaced positions >= f
+  std::uint32_t nh = 0;
+  for (std::uint32_t i = 0; i < f; ++i) lo[i] = __ldg(nbrs + i);
+  for (std::uint32_t i = 0; i < f; ++i) {
+    const std::uint32_t j = i + (std::uint32_t)s.next_below((std::uint64_t)(deg - i));
+    const std::uint32_t vi = lo[i];
+    std::uint32_t vj;
+    if (j < f) {
+      vj = lo[j];
+      lo[j] = vi;
+    } else {
+      std::uint32_t c = 0;
+      while (c < nh && hpos[c] != j) ++c;
+      if (c < nh) {
+        vj = hval[c];
+        hval[c] = vi;
+      } else {
+        vj = __ldg(nbrs + j);
+        hpos[nh] = j;
+        hval[nh] = vi;
+        ++nh;
+      }
+    }
+    out[i] = vj;  // scratch[i] after the swap
+    atomicOr(hb + (vj >> 6), 1ull << (vj & 63));
+    atomicOr(ab + (vj >> 6), 1ull << (vj & 63));
+  }
+}
+
+template <int MAXF>
+__global__ void __launch_bounds__(256) k_sample(const WaveDesc* __restrict__ desc, std::uint32_t h,
+                                                std::uint32_t f, const std::uint64_t* __restrict__ off,
+                                                const std::uint32_t* __restrict__ tgt,
+                                                const std::uint32_t* __restrict__ outdeg,
+                                                const std::uint32_t* __restrict__ Fprev, std::uint64_t capFprev,
+                                                const std::uint32_t* __restrict__ fcount_prev,
+                                                const std::uint32_t* __restrict__ indptr,
+                                                std::uint32_t* __restrict__ edges, std::uint64_t capS,
+                                                unsigned long long* __restrict__ hopbits,
+                                                unsigned long long* __restrict__ allbits, std::uint64_t W) {
+  const std::uint32_t mb = blockIdx.y;
+  const std::uint32_t cnt = fcount_prev[mb];
+  const std::uint64_t prefix = desc[mb].key_prefix[h - 1];
+  const std::uint32_t* fp = Fprev + mb * capFprev;
+  const std::uint32_t* ip = indptr + mb * (capFprev + 1);
+  std::uint32_t* ed = edges + mb * capS;
+  unsigned long long* hb = hopbits + mb * W;
+  unsigned long long* ab = allbits + mb * W;
+  for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x) {
+    const std::uint32_t v = fp[j];
+    Stream s(key_step(prefix, v));
+    sample_one<MAXF>(tgt + off[v], outdeg[v], f, s, ed + ip[j], hb, ab);
+  }
+}
+
+struct CompactParams {
+  const unsigned long long* bits;  // [M][W]
+  std::uint32_t* list;             // [M][cap_list]
+  std::uint64_t cap_list;
+  std::uint32_t* prefix;           // [M][W] rank prefix per word
+  std::uint32_t* count;            // [M]
+  // fused next-hop indptr (has_next)
+  const std::uint32_t* outdeg;
+  std::uint32_t f_next;
+  std::uint32_t* indptr_next;      // [M][cap_list + 1]
+  std::uint32_t* ecount_next;      // [M]
+  unsigned long long* status;      // [M][tiles]
+  unsigned* ticket;
+  std::uint64_t W, tiles;
+  std::uint32_t nmb;
+};
+
+template <bool HAS_NEXT>
+__global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
+  __shared__ unsigned s_ticket;
+  __shared__ unsigned long long s_sm[kCompactThreads / 32];
+  __shared__ unsigned long long s_excl;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1u);
+  __syncthreads();
+  const unsigned ticket = s_ticket;
+  const std::uint32_t mb = ticket / (unsigned)p.tiles;
+  const std::uint32_t tile = ticket % (unsigned)p.tiles;
+  if (mb >= p.nmb) return;
+  const unsigned long long* bits = p.bits + mb * p.W;
+  const std::uint64_t w0 = (std::uint64_t)tile * kTileWords + (std::uint64_t)threadIdx.x * kWordsPerThread;
+  unsigned long long wd[kWordsPerThread];
+  unsigned long long vc = 0, dc = 0;
+#pragma unroll
+  for (int k = 0; k < kWordsPerThread; ++k) {
+    wd[k] = (w0 + k < p.W) ? bits[w0 + k] : 0ull;
+    vc += __popcll(wd[k]);
+    if (HAS_NEXT) {
+      unsigned long long x = wd[k];
+      while (x) {
+        const int b = __ffsll(x) - 1;
+        x &= x - 1;
+        const std::uint32_t v = (std::uint32_t)((w0 + k) * 64 + b);
+        dc += min(p.f_next, __ldg(p.outdeg + v));
+      }
+    }
+  }
+  const unsigned long long mine = pack_vd(vc, dc);
+  unsigned long long total;
+  const unsigned long long inc = block_inclusive_scan<kCompactThreads>(mine, s_sm, &total);
+  if (threadIdx.x == 0) s_excl = lookback(p.status + mb * p.tiles, tile, total);
+  __syncthreads();
+  const unsigned long long ex = s_excl + inc - mine;
+  std::uint32_t pos = (std::uint32_t)unpack_v(ex);
+  std::uint32_t dpos = (std::uint32_t)unpack_d(ex);
+  std::uint32_t* list = p.list + mb * p.cap_list;
+  std::uint32_t* pre = p.prefix + mb * p.W;
+  std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
+#pragma unroll
+  for (int k = 0; k < kWordsPerThread; ++k) {
+    if (w0 + k >= p.W) break;
+    pre[w0 + k] = pos;
+    unsigned long long x = wd[k];
+    while (x) {
+      const int b = __ffsll(x) - 1;
+      x &= x - 1;
+      const std::uint32_t v = (std::uint32_t)((w0 + k) * 64 + b);
+      list[pos] = v;
+      if (HAS_NEXT) {
+        ipn[pos] = dpos;
+        dpos += min(p.f_next, __ldg(p.outdeg + v));
+      }
+      ++pos;
+    }
+  }
+  if (tile == p.tiles - 1 && threadIdx.x == kCompactThreads - 1) {
+    const unsigned long long all = s_excl + total;
+    const std::uint32_t tv = (std::uint32_t)unpack_v(all), td = (std::uint32_t)unpack_d(all);
+    p.count[mb] = tv;
+    if (HAS_NEXT) {
+      ipn[tv] = td;
+      p.ecount_next[mb] = td;
+    }
+  }
+}
+
+__device__ __forceinline__ std::uint32_t bit_rank(const unsigned long long* __restrict__ bits,
+                                                  const std::uint32_t* __restrict__ prefix, std::uint32_t v) {
+  const std::uint32_t w = v >> 6;
+  return __ldg(prefix + w) + (std::uint32_t)__popcll(__ldg(bits + w) & ((1ull << (v & 63)) - 1ull));
+}
+
+// MFG dst: rank of every drawn id in F_h.
+__global__ void k_relabel(const std::uint32_t* __restrict__ edges, std::uint64_t in_stride,
+                          const std::uint32_t* __restrict__ ecount, const unsigned long long* __restrict__ bits,
+                          const std::uint32_t* __restrict__ prefix, std::uint64_t W, std::uint32_t* __restrict__ dst,
+                          std::uint64_t out_stride) {
+  const std::uint32_t mb = blockIdx.y;
+  const std::uint32_t cnt = ecount[mb];
+  const std::uint32_t* e = edges + mb * in_stride;
+  std::uint32_t* o = dst + mb * out_stride;
+  const unsigned long long* b = bits + mb * W;
+  const std::uint32_t* pr = prefix + mb * W;
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    o[i] = bit_rank(b, pr, e[i]);
+}
+
+struct AllIdxParams {
+  const std::uint32_t* F[VK_MAX_HOPS + 1];
+  std::uint32_t* idx[VK_MAX_HOPS + 1];
+  std::uint64_t cap[VK_MAX_HOPS + 1];
+  const std::uint32_t* count[VK_MAX_HOPS + 1];
+};
+
+// Relabel map: position of every F_h vertex (h = 0..L) in all_vertices.
+__global__ void k_allidx(AllIdxParams p, const unsigned long long* __restrict__ bits,
+                         const std::uint32_t* __restrict__ prefix, std::uint64_t W) {
+  const std::uint32_t mb = blockIdx.y, h = blockIdx.z;
+  const std::uint32_t cnt = p.count[h][mb];
+  const std::uint32_t* f = p.F[h] + mb * p.cap[h];
+  std::uint32_t* o = p.idx[h] + mb * p.cap[h];
+  const unsigned long long* b = bits + mb * W;
+  const std::uint32_t* pr = prefix + mb * W;
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    o[i] = bit_rank(b, pr, f[i]);
+}
+
+template <int MAXF>
+void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStream_t st) {
+  vk_graph_s& g = *s.g;
+  const std::uint64_t capPrev = s.capF[h - 1];
+  const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(capPrev, 256), 4096);
+  k_sample<MAXF><<<dim3(gx, nmb), 256, 0, st>>>(
+      s.desc.as<WaveDesc>(), h, s.cfg.fanouts[h - 1], g.d_off(), g.d_tgt(), g.out_deg.as<std::uint32_t>(),
+      s.F[h - 1].as<std::uint32_t>(), capPrev, s.fcount(h - 1), s.indptr[h].as<std::uint32_t>(),
+      s.edges_tmp.as<std::uint32_t>(), s.capS_max, s.hopbits.as<unsigned long long>(),
+      s.allbits.as<unsigned long long>(), s.W);
+}
+
+void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, std::uint32_t slot,
+                 cudaStream_t st) {
+  CompactParams p{};
+  p.bits = (hop ? s.hopbits : s.allbits).as<unsigned long long>();
+  p.list = hop ? s.F[h].as<std::uint32_t>() : s.all.as<std::uint32_t>();
+  p.cap_list = hop ? s.capF[h] : s.capAll;
+  p.prefix = (hop ? s.hopprefix : s.allprefix).as<std::uint32_t>();
+  p.count = hop ? s.fcount(h) : s.allcount();
+  const bool has_next = hop && h < s.L;
+  p.outdeg = s.g->out_deg.as<std::uint32_t>();
+  if (has_next) {
+    p.f_next = s.cfg.fanouts[h];
+    p.indptr_next = s.indptr[h + 1].as<std::uint32_t>();
+    p.ecount_next = s.ecount(h + 1);
+  }
+  p.status = s.status.as<unsigned long long>() + (std::uint64_t)slot * s.M * s.tiles;
+  p.ticket = s.tickets.as<unsigned>() + slot;
+  p.W = s.W;
+  p.tiles = s.tiles;
+  p.nmb = nmb;
+  const unsigned grid = (unsigned)(nmb * s.tiles);
+  if (has_next)
+    k_compact<true><<<grid, kCompactThreads, 0, st>>>(p);
+  else
+    k_compact<false><<<grid, kCompactThreads, 0, st>>>(p);
+}
+
+}  // namespace
+}  // namespace vk
+
+using namespace vk;
+
+extern "C" {
+
+int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out) {
+  return guard([&] {
+    if (!g || !cfg || !out) raise(VK_ERR_PARAMETER, "null argument");
+    const std::uint32_t L = cfg->num_hops;
+    if (L == 0) raise(VK_ERR_PARAMETER, "fanout list must have at least one hop");
+    if (L > VK_MAX_HOPS) raise(VK_ERR_UNSUPPORTED, "at most 8 hops are supported");
+    for (std::uint32_t h = 0; h < L; ++h)
+      if (cfg->fanouts[h] < 1) raise(VK_ERR_PARAMETER, "each fanout must be >= 1");
+    if (cfg->batch_size == 0) raise(VK_ERR_PARAMETER, "batch size must be >= 1");
+    if (cfg->max_minibatches == 0) raise(VK_ERR_PARAMETER, "max_minibatches must be >= 1");
+    DeviceGuard dg(g->device);
+    auto* s = new vk_sampler_s();
+    try {
+      s->g = g;
+      s->cfg = *cfg;
+      s->L = L;
+      s->M = cfg->max_minibatches;
+      s->n = g->n;
+      s->W = (g->n + 63) / 64;
+      s->tiles = (s->W + kTileWords - 1) / kTileWords;
+      const std::uint64_t dmax = std::max<std::uint64_t>(1, g->max_out_degree);
+      s->capF[0] = cfg->batch_size;
+      std::uint64_t all = cfg->batch_size;
+      for (std::uint32_t h = 1; h <= L; ++h) {
+        const std::uint64_t f = std::min<std::uint64_t>(cfg->fanouts[h - 1], dmax);
+        s->capS[h] = s->capF[h - 1] * f;
+        s->capF[h] = std::min<std::uint64_t>(s->n, s->capS[h]);
+        s->capS_max = std::max(s->capS_max, s->capS[h]);
+        all += s->capF[h];
+      }
+      s->capAll = std::min<std::uint64_t>(s->n, all);
+      for (std::uint32_t h = 1; h <= L; ++h)
+        if (s->capS[h] >= (1ull << 31))
+          raise(VK_ERR_UNSUPPORTED, "per-minibatch edge capacity exceeds 2^31; lower batch size or fanouts");
+      if (s->n >= (1ull << 31) && s->capAll >= (1ull << 31))
+        raise(VK_ERR_UNSUPPORTED, "per-minibatch vertex capacity exceeds 2^31");
+      const std::uint64_t M = s->M;
+      for (std::uint32_t h = 0; h <= L; ++h) {
+        s->F[h].alloc(M * s->capF[h] * 4);
+        s->allidx[h].alloc(M * s->capF[h] * 4);
+        if (h >= 1) {
+          s->dst[h].alloc(M * s->capS[h] * 4);
+          // MFG row pointer of hop h: |F_{h-1}|+1 entries per minibatch
+          s->indptr[h].alloc(M * (s->capF[h - 1] + 1) * 4);
+        }
+      }
+      s->edges_tmp.alloc(M * s->capS_max * 4);
+      s->all.alloc(M * s->capAll * 4);
+      s->hopbits.alloc(M * s->W * 8);
+      s->allbits.alloc(M * s->W * 8);
+      s->hopprefix.alloc(M * s->W * 4);
+      s->allprefix.alloc(M * s->W * 4);
+      s->status.alloc((std::uint64_t)(L + 1) * M * s->tiles * 8);
+      s->tickets.alloc((L + 1) * 4);
+      s->counts.alloc(s->counts_words() * 4);
+      s->desc.alloc(M * sizeof(WaveDesc));
+      s->seed_stage.alloc(M * cfg->batch_size * 4);
+      for (int k = 0; k < 2; ++k) {
+        s->desc_host[k].ensure(M * sizeof(WaveDesc));
+        s->seed_host[k].ensure(M * cfg->batch_size * 4);
+        VK_CUDA(cudaEventCreateWithFlags(&s->staged[k], cudaEventDisableTiming));
+      }
+      VK_CUDA(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
+      VK_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+      VK_CUDA(cudaMemsetAsync(s->hopbits.p, 0, s->hopbits.bytes, s->stream));
+      VK_CUDA(cudaMemsetAsync(s->allbits.p, 0, s->allbits.bytes, s->stream));
+      VK_CUDA(cudaMemsetAsync(s->counts.p, 0, s->counts.bytes, s->stream));
+      VK_CUDA(cudaStreamSynchronize(s->stream));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int vk_sampler_destroy(vk_sampler s) {
+  return guard([&] {
+    if (!s) return;
+    DeviceGuard dg(s->g->device);
+    if (s->last_stream) cudaStreamSynchronize(s->last_stream);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    for (int k = 0; k < 2; ++k)
+      if (s->staged[k]) cudaEventDestroy(s->staged[k]);
+    if (s->done) cudaEventDestroy(s->done);
+    delete s;
+  });
+}
+
+int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const uint32_t* seeds,
+                   const uint64_t* seed_offsets, int seeds_on_device, vk_stream_t stream) {
+  return guard([&] {
+    if (!s || !refs || !seeds || !seed_offsets) raise(VK_ERR_PARAMETER, "null argument");
+    if (nmb == 0) raise(VK_ERR_PARAMETER, "empty wave");
+    if (nmb > s->M) raise(VK_ERR_PARAMETER, "wave exceeds max_minibatches");
+    vk_graph_s& g = *s->g;
+    DeviceGuard dg(g.device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+    // make sure the previous run on another stream has finished with the
+    // shared workspace before it is rewritten
+    if (s->last_stream && s->last_stream != st) VK_CUDA(cudaStreamSynchronize(s->last_stream));
+    const std::uint64_t b = s->cfg.batch_size;
+    const std::uint64_t total = seed_offsets[nmb] - seed_offsets[0];
+    for (std::uint32_t i = 0; i < nmb; ++i) {
+      const std::uint64_t c = seed_offsets[i + 1] - seed_offsets[i];
+      if (c == 0) raise(VK_ERR_SAMPLING, "cannot expand an empty batch");  // sampling.cpp:97
+      if (c > b) raise(VK_ERR_PARAMETER, "minibatch larger than the sampler's batch_size");
+    }
+    // double-buffered pinned staging: only wait for the H2D copy issued two
+    // waves ago, so the host can queue the next wave while this one runs
+    const int slot = s->slot;
+    s->slot ^= 1;
+    if (s->staged_used[slot]) VK_CUDA(cudaEventSynchronize(s->staged[slot]));
+    WaveDesc* d = s->desc_host[slot].as<WaveDesc>();
+    for (std::uint32_t i = 0; i < nmb; ++i) {
+      std::memset(&d[i], 0, sizeof(WaveDesc));
+      for (std::uint32_t h = 1; h <= s->L; ++h)
+        d[i].key_prefix[h - 1] = sample_key_prefix(s->cfg.global_seed, refs[i].epoch, refs[i].partition,
+                                                   refs[i].batch_index, h);
+      d[i].seed_begin = seed_offsets[i] - seed_offsets[0];
+      d[i].seed_count = (std::uint32_t)(seed_offsets[i + 1] - seed_offsets[i]);
+      d[i].partition = refs[i].partition;
+    }
+    VK_CUDA(cudaMemcpyAsync(s->desc.p, d, nmb * sizeof(WaveDesc), cudaMemcpyHostToDevice, st));
+    const std::uint32_t* dseeds;
+    if (seeds_on_device) {
+      dseeds = seeds + seed_offsets[0];
+    } else {
+      for (std::uint64_t i = 0; i < total; ++i)
+        if (seeds[seed_offsets[0] + i] >= s->n)
+          raise(VK_ERR_RANGE, "seed vertex id out of range: " + std::to_string(seeds[seed_offsets[0] + i]));
+      std::memcpy(s->seed_host[slot].p, seeds + seed_offsets[0], total * 4);
+      VK_CUDA(cudaMemcpyAsync(s->seed_stage.p, s->seed_host[slot].p, total * 4, cudaMemcpyHostToDevice, st));
+      dseeds = s->seed_stage.as<std::uint32_t>();
+    }
+    VK_CUDA(cudaEventRecord(s->staged[slot], st));
+    s->staged_used[slot] = true;
+    VK_CUDA(cudaMemsetAsync(s->status.p, 0, s->status.bytes, st));
+    VK_CUDA(cudaMemsetAsync(s->tickets.p, 0, s->tickets.bytes, st));
+    VK_CUDA(cudaMemsetAsync(s->err(), 0, 4, st));
+    const std::uint32_t* outdeg = g.out_deg.as<std::uint32_t>();
+    k_prepare<<<nmb, 1024, 0, st>>>(s->desc.as<WaveDesc>(), dseeds, outdeg, s->n, s->cfg.fanouts[0],
+                                    s->F[0].as<std::uint32_t>(), s->capF[0], s->fcount(0),
+                                    s->indptr[1].as<std::uint32_t>(), s->ecount(1),
+                                    s->allbits.as<unsigned long long>(), s->W, s->err());
+    count_launch();
+    VK_LAUNCH_CHECK();
+    for (std::uint32_t h = 1; h <= s->L; ++h) {
+      const std::uint32_t f = s->cfg.fanouts[h - 1];
+      if (f <= 32 || g.max_out_degree <= f)
+        launch_sample<32>(*s, h, nmb, st);
+      else if (f <= 128)
+        launch_sample<128>(*s, h, nmb, st);
+      else if (f <= 1024)
+        launch_sample<1024>(*s, h, nmb, st);
+      else
+        raise(VK_ERR_UNSUPPORTED, "fanouts above 1024 with higher-degree vertices are not supported");
+      count_launch();
+      VK_LAUNCH_CHECK();
+      run_compact(*s, true, h, nmb, h - 1, st);
+      count_launch();
+      VK_LAUNCH_CHECK();
+      const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(s->capS[h], 256), 4096);
+      k_relabel<<<dim3(gx, nmb), 256, 0, st>>>(s->edges_tmp.as<std::uint32_t>(), s->capS_max, s->ecount(h),
+                                               s->hopbits.as<unsigned long long>(),
+                                               s->hopprefix.as<std::uint32_t>(), s->W,
+                                               s->dst[h].as<std::uint32_t>(), s->capS[h]);
+      count_launch();
+      VK_LAUNCH_CHECK();
+      VK_CUDA(cudaMemsetAsync(s->hopbits.p, 0, (std::uint64_t)nmb * s->W * 8, st));
+    }
+    run_compact(*s, false, 0, nmb, s->L, st);
+    count_launch();
+    VK_LAUNCH_CHECK();
+    AllIdxParams ap{};
+    std::uint64_t capmax = 0;
+    for (std::uint32_t h = 0; h <= s->L; ++h) {
+      ap.F[h] = s->F[h].as<std::uint32_t>();
+      ap.idx[h] = s->allidx[h].as<std::uint32_t>();
+      ap.cap[h] = s->capF[h];
+      ap.count[h] = s->fcount(h);
+      capmax = std::max(capmax, s->capF[h]);
+    }
+    const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(capmax, 256), 1024);
+    k_allidx<<<dim3(gx, nmb, s->L + 1), 256, 0, st>>>(ap, s->allbits.as<unsigned long long>(),
+                                                       s->allprefix.as<std::uint32_t>(), s->W);
+    count_launch();
+    VK_LAUNCH_CHECK();
+    VK_CUDA(cudaMemsetAsync(s->allbits.p, 0, (std::uint64_t)nmb * s->W * 8, st));
+    VK_CUDA(cudaEventRecord(s->done, st));
+    s->last_nmb = nmb;
+    s->last_stream = st;
+    s->last_parts.resize(nmb);
+    for (std::uint32_t i = 0; i < nmb; ++i) s->last_parts[i] = refs[i].partition;
+  });
+}
+
+namespace {
+
+void sync_last(vk_sampler_s& s) {
+  if (s.last_nmb == 0) raise(VK_ERR_PARAMETER, "sampler has not run");
+  VK_CUDA(cudaStreamSynchronize(s.last_stream ? s.last_stream : s.stream));
+}
+
+std::vector<std::uint32_t> host_counts(vk_sampler_s& s) {
+  sync_last(s);
+  std::vector<std::uint32_t> c(s.counts_words());
+  VK_CUDA(cudaMemcpy(c.data(), s.counts.p, c.size() * 4, cudaMemcpyDeviceToHost));
+  if (c.back()) raise(VK_ERR_RANGE, "seed vertex id out of range");
+  return c;
+}
+
+void check_mb_hop(vk_sampler_s& s, std::uint32_t mb, std::uint32_t hop, std::uint32_t lo) {
+  if (mb >= s.last_nmb) raise(VK_ERR_PARAMETER, "minibatch index out of range");
+  if (hop < lo || hop > s.L) raise(VK_ERR_PARAMETER, "hop out of range");
+}
+
+}  // namespace
+
+int vk_sampler_sizes(vk_sampler s, uint64_t* frontier_sizes, uint64_t* edge_counts, uint64_t* all_sizes) {
+  return guard([&] {
+    if (!s) raise(VK_ERR_PARAMETER, "null sampler");
+    DeviceGuard dg(s->g->device);
+    const auto c = host_counts(*s);
+    const std::uint32_t M = s->M, L = s->L;
+    for (std::uint32_t i = 0; i < s->last_nmb; ++i) {
+      for (std::uint32_t h = 1; h <= L; ++h) {
+        if (frontier_sizes) frontier_sizes[i * L + h - 1] = c[(std::uint64_t)h * M + i];
+        if (edge_counts) edge_counts[i * L + h - 1] = c[(std::uint64_t)(L + 1) * M + (std::uint64_t)h * M + i];
+      }
+      if (all_sizes) all_sizes[i] = c[2ull * (L + 1) * M + i];
+    }
+  });
+}
+
+int vk_sampler_copy_frontier(vk_sampler s, uint32_t mb, uint32_t hop, uint32_t* out) {
+  return guard([&] {
+    if (!s || !out) raise(VK_ERR_PARAMETER, "null argument");
+    DeviceGuard dg(s->g->device);
+    check_mb_hop(*s, mb, hop, 0);
+    const auto c = host_counts(*s);
+    const std::uint64_t cnt = c[(std::uint64_t)hop * s->M + mb];
+    VK_CUDA(cudaMemcpy(out, s->F[hop].as<std::uint32_t>() + mb * s->capF[hop], cnt * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int vk_sampler_copy_all(vk_sampler s, uint32_t mb, uint32_t* out) {
+  return guard([&] {
+    if (!s || !out) raise(VK_ERR_PARAMETER, "null argument");
+    DeviceGuard dg(s->g->device);
+    check_mb_hop(*s, mb, 0, 0);
+    const auto c = host_counts(*s);
+    const std::uint64_t cnt = c[2ull * (s->L + 1) * s->M + mb];
+    VK_CUDA(cudaMemcpy(out, s->all.as<std::uint32_t>() + mb * s->capAll, cnt * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int vk_sampler_copy_mfg(vk_sampler s, uint32_t mb, uint32_t hop, uint64_t* indptr, uint32_t* dst) {
+  return guard([&] {
+    if (!s) raise(VK_ERR_PARAMETER, "null sampler");
+    DeviceGuard dg(s->g->device);
+    check_mb_hop(*s, mb, hop, 1);
+    const auto c = host_counts(*s);
+    const std::uint64_t nsrc = c[(std::uint64_t)(hop - 1) * s->M + mb];
+    const std::uint64_t ne = c[(std::uint64_t)(s->L + 1) * s->M + (std::uint64_t)hop * s->M + mb];
+    if (indptr) {
+      std::vector<std::uint32_t> ip(nsrc + 1);
+      VK_CUDA(cudaMemcpy(ip.data(), s->indptr[hop].as<std::uint32_t>() + mb * (s->capF[hop - 1] + 1),
+                         (nsrc + 1) * 4, cudaMemcpyDeviceToHost));
+      for (std::uint64_t i = 0; i <= nsrc; ++i) indptr[i] = ip[i];
+    }
+    if (dst && ne)
+      VK_CUDA(cudaMemcpy(dst, s->dst[hop].as<std::uint32_t>() + mb * s->capS[hop], ne * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int vk_sampler_copy_relabel(vk_sampler s, uint32_t mb, uint32_t hop, uint32_t* all_index) {
+  return guard([&] {
+    if (!s || !all_index) raise(VK_ERR_PARAMETER, "null argument");
+    DeviceGuard dg(s->g->device);
+    check_mb_hop(*s, mb, hop, 0);
+    const auto c = host_counts(*s);
+    const std::uint64_t cnt = c[(std::uint64_t)hop * s->M + mb];
+    VK_CUDA(cudaMemcpy(all_index, s->allidx[hop].as<std::uint32_t>() + mb * s->capF[hop], cnt * 4,
+                       cudaMemcpyDeviceToHost));
+  });
+}
+
+int vk_sampler_snapshot_counts(vk_sampler s, uint32_t* dst_dev, uint64_t* words, vk_stream_t stream) {
+  return guard([&] {
+    if (!s) raise(VK_ERR_PARAMETER, "null sampler");
+    if (words) *words = s->counts_words();
+    if (!dst_dev) return;
+    DeviceGuard dg(s->g->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : (s->last_stream ? s->last_stream : s->stream);
+    if (s->last_stream && st != s->last_stream) VK_CUDA(cudaStreamWaitEvent(st, s->done, 0));
+    VK_CUDA(cudaMemcpyAsync(dst_dev, s->counts.p, s->counts_words() * 4, cudaMemcpyDeviceToDevice, st));
+  });
+}
+
+int vk_sampler_get_view(vk_sampler s, vk_sampler_view* v) {
+  return guard([&] {
+    if (!s || !v) raise(VK_ERR_PARAMETER, "null argument");
+    std::memset(v, 0, sizeof *v);
+    v->nmb = s->last_nmb;
+    v->num_hops = s->L;
+    v->all = s->all.as<std::uint32_t>();
+    v->all_stride = s->capAll;
+    v->all_count = s->allcount();
+    for (std::uint32_t h = 0; h <= s->L; ++h) {
+      v->frontier[h] = s->F[h].as<std::uint32_t>();
+      v->frontier_stride[h] = s->capF[h];
+      v->frontier_count[h] = s->fcount(h);
+      v->all_index[h] = s->allidx[h].as<std::uint32_t>();
+      if (h >= 1) {
+        v->mfg_indptr[h] = s->indptr[h].as<std::uint32_t>();
+        v->mfg_dst[h] = s->dst[h].as<std::uint32_t>();
+        v->mfg_stride[h] = s->capS[h];
+      }
+    }
+  });
+}
+
+}  // extern "C"
+
+// internal accessors for the feature plane (plane.cu)
+namespace vk {
+void sampler_internal(vk_sampler_s* s, const std::uint32_t** all, std::uint64_t* all_stride,
+                      const std::uint32_t** all_count, std::uint32_t* nmb, const std::uint32_t** partitions,
+                      vk_graph_s** g, cudaStream_t* last_stream) {
+  *all = s->all.as<std::uint32_t>();
+  *all_stride = s->capAll;
+  *all_count = s->allcount();
+  *nmb = s->last_nmb;
+  *partitions = reinterpret_cast<const std::uint32_t*>(s->desc.as<char>() + offsetof(WaveDesc, partition));
+  *g = s->g;
+  *last_stream = s->last_stream;
+}
+std::uint64_t sampler_desc_stride() { return sizeof(WaveDesc); }
+void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out) { out = s->last_parts; }
+cudaEvent_t sampler_done_event(vk_sampler_s* s) { return s->done; }
+std::uint64_t sampler_capacity_all(vk_sampler_s* s) { return s->capAll; }
+}  // namespace vk

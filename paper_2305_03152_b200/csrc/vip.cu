@@ -1,0 +1,487 @@
+// VIP analysis on the device: hop-wise vertex-inclusion-probability
+// propagation in the log(1-p) domain (replaces vipkit::propagate,
+// /root/reference/proj/src/vip.cpp:37-83).
+//
+// Formulation (verified bitwise-equal on CPU):
+//   lm_h[v]  = log1p(-w_h(outdeg v) * p_{h-1}[v])        (one value per sampler;
+//              the reference evaluates log1p per edge, vip.cpp:66-70)
+//   hop_h[u] = clamp(-expm1( sum_{v in in(u)} lm_h[v] ))  (pull over reverse CSR)
+//   total[u] = clamp(-expm1( sum_h log1p(-hop_h[u]) ))    (vip.cpp:76-81; the
+//              running sum is carried in hop order so it is bit-identical to
+//              the reference given the same hop values)
+// Only the summation order of the pull differs from the reference, hence the
+// 1e-5 relative tolerance of the north-star (exact for the 0/1 special cases).
+//
+// Kernel shape: rows are grouped by in-degree class; a class is processed by
+// G-lane groups (G = 4 .. 32) or whole CTAs; rows above kSplitDeg are cut into
+// edge chunks reduced by separate CTAs and finished in fixed chunk order
+// (deterministic). The hoist of the next hop, the running total and the hop
+// output are fused into the pull's epilogue, so each hop is one pass over the
+// reverse CSR. `C` columns (partitions) are propagated together: one index
+// stream serves C probability vectors (the lm gather fetches C contiguous
+// doubles).
+#include <cmath>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace vk {
+namespace {
+
+constexpr double kFlushBelow = 1e-300;  // vip.cpp:16
+constexpr int kMaxHops = VK_MAX_HOPS;
+
+// In-degree classes: [0] G=4 deg<=12, [1] G=8 <=48, [2] G=16 <=160,
+// [3] G=32 <=1536, [4] CTA <=kSplitDeg, [5] split rows (chunked).
+constexpr std::uint64_t kClassMax[5] = {12, 48, 160, 1536, 32768};
+constexpr std::uint64_t kSplitDeg = 32768;
+constexpr std::uint64_t kChunk = 16384;
+constexpr int kCtaThreads = 256;
+
+__device__ __forceinline__ double clamp_prob(double x) {  // vip.cpp:18-21
+  if (!(x > kFlushBelow)) return 0.0;
+  return x < 1.0 ? x : 1.0;
+}
+
+struct HopParams {
+  const std::uint64_t* off;   // reverse offsets
+  const std::uint32_t* tgt;   // reverse targets
+  const std::uint32_t* outdeg;
+  const double* lm;           // [n][C] current hop
+  double* lm_next;            // [n][C] next hop (unused on last hop)
+  double* hop_out;            // base for column c: hop_out + c*hop_col_stride + (h-1)*n
+  double* total;              // [c*n + u] running log-sum, final total on the last hop
+  std::uint64_t n;
+  std::uint64_t hop_col_stride;  // L*n (0 if hop_out null)
+  std::uint32_t h;               // 1-based hop
+  std::uint32_t L;
+  double f_next;                 // fanout of hop h+1 (as double)
+  int write_hop;
+};
+
+template <int C>
+__device__ __forceinline__ void epilogue(const HopParams& p, std::uint64_t u, int c, double s) {
+  const double cur = clamp_prob(-expm1(s));
+  if (p.write_hop) p.hop_out[c * p.hop_col_stride + (std::uint64_t)(p.h - 1) * p.n + u] = cur;
+  double* acc = p.total + (std::uint64_t)c * p.n + u;
+  const double term = log1p(-cur);
+  const double a = p.h == 1 ? term : (*acc + term);
+  if (p.h == p.L) {
+    *acc = clamp_prob(-expm1(a));
+  } else {
+    *acc = a;
+    // hoist for hop h+1: TransitionModel::weight (vip.hpp:22-26) of sampler u
+    const double d = (double)p.outdeg[u];
+    const double w = d <= p.f_next ? 1.0 : p.f_next / d;
+    const double wp = cur == 0.0 ? 0.0 : w * cur;  // vip.cpp:58-60
+    p.lm_next[u * C + c] = log1p(-wp);
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void load_lm(const double* __restrict__ lm, std::uint32_t v, double* out) {
+  if constexpr (C == 1) {
+    out[0] = __ldg(lm + v);
+  } else {
+    const double2* q = reinterpret_cast<const double2*>(lm + (std::uint64_t)v * C);
+#pragma unroll
+    for (int k = 0; k < C / 2; ++k) {
+      const double2 x = __ldg(q + k);
+      out[2 * k] = x.x;
+      out[2 * k + 1] = x.y;
+    }
+  }
+}
+
+// Sum of lm over tgt[a..b) for one lane of a G-lane group (stride G, 4 in
+// flight).
+template <int C, int G>
+__device__ __forceinline__ void lane_sum(const HopParams& p, std::uint64_t a, std::uint64_t b, int lane,
+                                         double* s) {
+  std::uint64_t i = a + lane;
+  for (; i + 3 * G < b; i += 4 * G) {
+    const std::uint32_t v0 = __ldg(p.tgt + i), v1 = __ldg(p.tgt + i + G), v2 = __ldg(p.tgt + i + 2 * G),
+                        v3 = __ldg(p.tgt + i + 3 * G);
+    double x0[C], x1[C], x2[C], x3[C];
+    load_lm<C>(p.lm, v0, x0);
+    load_lm<C>(p.lm, v1, x1);
+    load_lm<C>(p.lm, v2, x2);
+    load_lm<C>(p.lm, v3, x3);
+#pragma unroll
+    for (int c = 0; c < C; ++c) s[c] += (x0[c] + x1[c]) + (x2[c] + x3[c]);
+  }
+  for (; i < b; i += G) {
+    double x[C];
+    load_lm<C>(p.lm, __ldg(p.tgt + i), x);
+#pragma unroll
+    for (int c = 0; c < C; ++c) s[c] += x[c];
+  }
+}
+
+// G-lane groups, one row per group; warp-uniform outer loop so the shuffle
+// reduction always runs with the full warp.
+template <int C, int G>
+__global__ void __launch_bounds__(256) k_pull_group(HopParams p, const std::uint32_t* __restrict__ rows,
+                                                    std::uint64_t nrows) {
+  constexpr int kGroupsPerWarp = 32 / G;
+  const int lane = threadIdx.x % G;
+  const std::uint64_t warp = (blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x) / 32;
+  const std::uint64_t nwarps = ((std::uint64_t)gridDim.x * blockDim.x) / 32;
+  const int gw = (threadIdx.x % 32) / G;
+  for (std::uint64_t r0 = warp * kGroupsPerWarp; r0 < nrows; r0 += nwarps * kGroupsPerWarp) {
+    const std::uint64_t r = r0 + gw;
+    double s[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) s[c] = 0.0;
+    std::uint32_t u = 0;
+    if (r < nrows) {
+      u = rows[r];
+      lane_sum<C, G>(p, p.off[u], p.off[u + 1], lane, s);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < C; ++c) s[c] += __shfl_xor_sync(0xffffffffu, s[c], o, G);
+    if (r < nrows) {
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (c % G == lane) epilogue<C>(p, u, c, s[c]);
+    }
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void block_reduce(double* s, double (*sh)[C]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < C; ++c) s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < C; ++c) sh[w][c] = s[c];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      double t = 0.0;
+      for (int k = 0; k < kCtaThreads / 32; ++k) t += sh[k][c];
+      s[c] = t;
+    }
+  }
+  __syncthreads();
+}
+
+// One CTA per row (heavy rows).
+template <int C>
+__global__ void __launch_bounds__(kCtaThreads) k_pull_cta(HopParams p, const std::uint32_t* __restrict__ rows,
+                                                          std::uint64_t nrows) {
+  __shared__ double sh[kCtaThreads / 32][C];
+  for (std::uint64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const std::uint32_t u = rows[r];
+    double s[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) s[c] = 0.0;
+    lane_sum<C, kCtaThreads>(p, p.off[u], p.off[u + 1], threadIdx.x, s);
+    block_reduce<C>(s, sh);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int c = 0; c < C; ++c) epilogue<C>(p, u, c, s[c]);
+  }
+}
+
+// Split rows: chunk j covers [chunk_lo[j], chunk_hi[j]) of one row; partial
+// sums are reduced in chunk order by k_split_finish.
+template <int C>
+__global__ void __launch_bounds__(kCtaThreads) k_pull_chunk(HopParams p, const std::uint64_t* __restrict__ lo,
+                                                            const std::uint64_t* __restrict__ hi,
+                                                            std::uint64_t nchunks, double* __restrict__ partial) {
+  __shared__ double sh[kCtaThreads / 32][C];
+  for (std::uint64_t j = blockIdx.x; j < nchunks; j += gridDim.x) {
+    double s[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) s[c] = 0.0;
+    lane_sum<C, kCtaThreads>(p, lo[j], hi[j], threadIdx.x, s);
+    block_reduce<C>(s, sh);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int c = 0; c < C; ++c) partial[j * C + c] = s[c];
+  }
+}
+
+template <int C>
+__global__ void k_split_finish(HopParams p, const std::uint32_t* __restrict__ rows,
+                               const std::uint64_t* __restrict__ first_chunk, std::uint64_t nrows,
+                               const double* __restrict__ partial) {
+  const std::uint64_t r = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  for (int c = 0; c < C; ++c) {
+    double s = 0.0;
+    for (std::uint64_t j = first_chunk[r]; j < first_chunk[r + 1]; ++j) s += partial[j * C + c];
+    epilogue<C>(p, rows[r], c, s);
+  }
+}
+
+// Hop-1 hoist from p0 (vip.cpp:57-61 with log1p moved here) + p0 range check
+// (vip.cpp:41-43).
+template <int C>
+__global__ void k_hoist_p0(const double* __restrict__ p0, std::uint64_t n, std::uint64_t col0,
+                           const std::uint32_t* __restrict__ outdeg, double f1, double* __restrict__ lm,
+                           unsigned* __restrict__ bad) {
+  for (std::uint64_t v = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (std::uint64_t)gridDim.x * blockDim.x) {
+    const double d = (double)outdeg[v];
+    const double w = d <= f1 ? 1.0 : f1 / d;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const double pv = p0[(col0 + c) * n + v];
+      if (!(pv >= 0.0 && pv <= 1.0)) *bad = 1u;
+      const double wp = pv == 0.0 ? 0.0 : w * pv;
+      lm[v * C + c] = log1p(-wp);
+    }
+  }
+}
+
+unsigned grid_cap(int device, std::uint64_t work, unsigned block) {
+  const std::uint64_t g = (work + block - 1) / block;
+  const std::uint64_t cap = (std::uint64_t)sm_count(device) * (2048 / block) * 4;
+  return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+template <int C>
+void run_columns(vk_graph_s& g, const std::uint32_t* fan, std::uint32_t L, const double* p0_dev,
+                 std::uint64_t col0, double* hop_dev, double* total_dev, cudaStream_t st, DevBuf& lm_a,
+                 DevBuf& lm_b, DevBuf& partial, const DevBuf& bad) {
+  const std::uint64_t n = g.n;
+  double* lm = lm_a.as<double>();
+  double* lmn = lm_b.as<double>();
+  k_hoist_p0<C><<<grid_cap(g.device, n, 256), 256, 0, st>>>(p0_dev, n, col0, g.out_deg.as<std::uint32_t>(),
+                                                             (double)fan[0], lm, bad.as<unsigned>());
+  count_launch();
+  VK_LAUNCH_CHECK();
+  const auto& so = g.sched_offsets;  // [6 classes + split-rows meta]
+  const std::uint32_t* rows = g.sched_rows.as<std::uint32_t>();
+  for (std::uint32_t h = 1; h <= L; ++h) {
+    HopParams p;
+    p.off = g.rev_off;
+    p.tgt = g.rev_tgt;
+    p.outdeg = g.out_deg.as<std::uint32_t>();
+    p.lm = lm;
+    p.lm_next = lmn;
+    p.hop_out = hop_dev ? hop_dev + col0 * (std::uint64_t)L * n : nullptr;
+    p.total = total_dev + col0 * n;
+    p.n = n;
+    p.hop_col_stride = (std::uint64_t)L * n;
+    p.h = h;
+    p.L = L;
+    p.f_next = h < L ? (double)fan[h] : 1.0;
+    p.write_hop = hop_dev != nullptr;
+    auto cls = [&](int c) { return std::pair<const std::uint32_t*, std::uint64_t>(rows + so[c], so[c + 1] - so[c]); };
+    {
+      auto [r, k] = cls(0);
+      if (k) k_pull_group<C, 4><<<grid_cap(g.device, k * 4, 256), 256, 0, st>>>(p, r, k), count_launch();
+    }
+    {
+      auto [r, k] = cls(1);
+      if (k) k_pull_group<C, 8><<<grid_cap(g.device, k * 8, 256), 256, 0, st>>>(p, r, k), count_launch();
+    }
+    {
+      auto [r, k] = cls(2);
+      if (k) k_pull_group<C, 16><<<grid_cap(g.device, k * 16, 256), 256, 0, st>>>(p, r, k), count_launch();
+    }
+    {
+      auto [r, k] = cls(3);
+      if (k) k_pull_group<C, 32><<<grid_cap(g.device, k * 32, 256), 256, 0, st>>>(p, r, k), count_launch();
+    }
+    {
+      auto [r, k] = cls(4);
+      if (k) {
+        const unsigned grid = (unsigned)std::min<std::uint64_t>(k, (std::uint64_t)sm_count(g.device) * 8);
+        k_pull_cta<C><<<grid, kCtaThreads, 0, st>>>(p, r, k);
+        count_launch();
+      }
+    }
+    {
+      auto [r, k] = cls(5);
+      if (k) {
+        const std::uint64_t nch = so[7];
+        const std::uint64_t* meta = reinterpret_cast<const std::uint64_t*>(rows + so[6]);
+        // meta layout: lo[nch], hi[nch], first_chunk[k+1]
+        const unsigned grid = (unsigned)std::min<std::uint64_t>(nch, (std::uint64_t)sm_count(g.device) * 8);
+        k_pull_chunk<C><<<grid, kCtaThreads, 0, st>>>(p, meta, meta + nch, nch, partial.as<double>());
+        k_split_finish<C><<<ceil_div(k, 128), 128, 0, st>>>(p, r, meta + 2 * nch, k, partial.as<double>());
+        count_launch(2);
+      }
+    }
+    VK_LAUNCH_CHECK();
+    std::swap(lm, lmn);
+  }
+}
+
+}  // namespace
+
+// Build the in-degree class schedule once per graph (host-side bucketing of
+// the reverse offsets; one-time cost like the reference's CSR rebuild).
+void build_vip_schedule(vk_graph_s& g) {
+  if (g.sched_ready) return;
+  const std::uint64_t n = g.n;
+  std::vector<std::uint64_t> off(n + 1);
+  VK_CUDA(cudaMemcpy(off.data(), g.rev_off, (n + 1) * 8, cudaMemcpyDeviceToHost));
+  std::vector<std::uint64_t> cnt(6, 0);
+  std::vector<std::uint8_t> cls(n);
+  std::uint64_t nchunks = 0;
+  for (std::uint64_t u = 0; u < n; ++u) {
+    const std::uint64_t d = off[u + 1] - off[u];
+    int c = 5;
+    for (int k = 0; k < 5; ++k)
+      if (d <= kClassMax[k]) {
+        c = k;
+        break;
+      }
+    cls[u] = (std::uint8_t)c;
+    cnt[c]++;
+    if (c == 5) nchunks += (d + kChunk - 1) / kChunk;
+  }
+  // rows (u32) for classes 0..5, then an 8-byte aligned meta block for the
+  // split rows: lo[nchunks], hi[nchunks], first_chunk[nsplit+1] (u64).
+  std::vector<std::uint64_t> so(8, 0);
+  for (int c = 0; c < 6; ++c) so[c + 1] = so[c] + cnt[c];
+  std::uint64_t meta_start = (so[6] + 1) & ~1ull;  // u64 alignment in u32 units
+  const std::uint64_t nsplit = cnt[5];
+  const std::uint64_t meta_words = 2 * nchunks + nsplit + 1;
+  std::vector<std::uint32_t> host(meta_start + 2 * meta_words, 0);
+  std::vector<std::uint64_t> pos(so.begin(), so.begin() + 6);
+  std::vector<std::uint64_t> lo, hi, first{0};
+  for (std::uint64_t u = 0; u < n; ++u) {
+    host[pos[cls[u]]++] = (std::uint32_t)u;
+    if (cls[u] == 5) {
+      for (std::uint64_t a = off[u]; a < off[u + 1]; a += kChunk) {
+        lo.push_back(a);
+        hi.push_back(std::min(off[u + 1], a + kChunk));
+      }
+      first.push_back(lo.size());
+    }
+  }
+  std::uint64_t* meta = reinterpret_cast<std::uint64_t*>(host.data() + meta_start);
+  for (std::uint64_t j = 0; j < nchunks; ++j) {
+    meta[j] = lo[j];
+    meta[nchunks + j] = hi[j];
+  }
+  for (std::uint64_t r = 0; r <= nsplit; ++r) meta[2 * nchunks + r] = first[r];
+  g.sched_rows.alloc(host.size() * 4);
+  VK_CUDA(cudaMemcpy(g.sched_rows.p, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
+  so[6] = meta_start;
+  so[7] = nchunks;
+  g.sched_offsets = so;
+  g.sched_ready = true;
+}
+
+}  // namespace vk
+
+using namespace vk;
+
+namespace {
+
+void validate_fanouts(const std::uint32_t* fanouts, std::uint32_t L) {
+  // FanoutSpec::validate (sampling.cpp:11-15)
+  if (L == 0) raise(VK_ERR_PARAMETER, "fanout list must have at least one hop");
+  if (L > VK_MAX_HOPS) raise(VK_ERR_UNSUPPORTED, "at most 8 hops are supported");
+  if (!fanouts) raise(VK_ERR_PARAMETER, "null fanouts");
+  for (std::uint32_t h = 0; h < L; ++h)
+    if (fanouts[h] < 1) raise(VK_ERR_PARAMETER, "each fanout must be >= 1");
+}
+
+void propagate_device(vk_graph_s& g, const std::uint32_t* fanouts, std::uint32_t L, std::uint32_t ncols,
+                      const double* p0, double* hop, double* total, cudaStream_t st) {
+  validate_fanouts(fanouts, L);
+  if (ncols == 0) return;
+  build_vip_schedule(g);
+  const std::uint64_t n = g.n;
+  const std::uint32_t cmax = ncols >= 8 ? 8 : (ncols >= 4 ? 4 : (ncols >= 2 ? 2 : 1));
+  auto ensure = [](DevBuf& b, std::size_t bytes) {
+    if (b.bytes < bytes) b.alloc(bytes);
+  };
+  const std::uint64_t nch = g.sched_offsets[7];
+  ensure(g.vip_lm_a, n * 8 * cmax);
+  ensure(g.vip_lm_b, n * 8 * cmax);
+  ensure(g.vip_partial, std::max<std::uint64_t>(1, nch) * 8 * cmax);
+  ensure(g.vip_flag, sizeof(unsigned));
+  DevBuf& lm_a = g.vip_lm_a;
+  DevBuf& lm_b = g.vip_lm_b;
+  DevBuf& partial = g.vip_partial;
+  DevBuf& bad = g.vip_flag;
+  VK_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned), st));
+  std::uint32_t c0 = 0;
+  while (c0 < ncols) {
+    const std::uint32_t rem = ncols - c0;
+    if (rem >= 8) {
+      run_columns<8>(g, fanouts, L, p0, c0, hop, total, st, lm_a, lm_b, partial, bad);
+      c0 += 8;
+    } else if (rem >= 4) {
+      run_columns<4>(g, fanouts, L, p0, c0, hop, total, st, lm_a, lm_b, partial, bad);
+      c0 += 4;
+    } else if (rem >= 2) {
+      run_columns<2>(g, fanouts, L, p0, c0, hop, total, st, lm_a, lm_b, partial, bad);
+      c0 += 2;
+    } else {
+      run_columns<1>(g, fanouts, L, p0, c0, hop, total, st, lm_a, lm_b, partial, bad);
+      c0 += 1;
+    }
+  }
+  unsigned h = 0;
+  VK_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof h, cudaMemcpyDeviceToHost, st));
+  VK_CUDA(cudaStreamSynchronize(st));  // surfaces the p0 range error synchronously
+  if (h) raise(VK_ERR_PARAMETER, "p0 entries must lie in [0,1]");
+}
+
+}  // namespace
+
+extern "C" {
+
+int vk_initial_probs(uint64_t n, const uint8_t* roles, const uint32_t* part_of, uint32_t k,
+                     uint64_t batch_size, double* p0_out) {
+  return guard([&] {
+    // vip.cpp:25-35
+    if (batch_size == 0) raise(VK_ERR_PARAMETER, "batch size must be >= 1");
+    if (!roles || !part_of || !p0_out) raise(VK_ERR_PARAMETER, "null argument");
+    std::uint64_t T = 0;
+    for (std::uint64_t v = 0; v < n; ++v) T += (part_of[v] == k && roles[v] == 0);
+    if (T == 0) raise(VK_ERR_SAMPLING, "partition " + std::to_string(k) + " has no train vertices");
+    const double p = std::min(1.0, (double)batch_size / (double)T);
+    for (std::uint64_t v = 0; v < n; ++v) p0_out[v] = (part_of[v] == k && roles[v] == 0) ? p : 0.0;
+  });
+}
+
+int vk_vip_propagate(vk_graph g, const uint32_t* fanouts, uint32_t num_hops, uint32_t ncols,
+                     const double* p0, double* hop_out, double* total_out) {
+  return guard([&] {
+    if (!g || !p0 || !total_out) raise(VK_ERR_PARAMETER, "null argument");
+    DeviceGuard dg(g->device);
+    validate_fanouts(fanouts, num_hops);
+    const std::uint64_t n = g->n;
+    // vip.cpp:41-43 (host-side check keeps the error synchronous and exact)
+    for (std::uint64_t i = 0; i < n * (std::uint64_t)ncols; ++i)
+      if (!(p0[i] >= 0.0 && p0[i] <= 1.0)) raise(VK_ERR_PARAMETER, "p0 entries must lie in [0,1]");
+    DevBuf dp0(n * 8 * ncols), dtot(n * 8 * ncols);
+    DevBuf dhop(hop_out ? n * 8 * ncols * num_hops : 0);
+    VK_CUDA(cudaMemcpyAsync(dp0.p, p0, n * 8 * ncols, cudaMemcpyHostToDevice, g->stream));
+    propagate_device(*g, fanouts, num_hops, ncols, dp0.as<double>(), hop_out ? dhop.as<double>() : nullptr,
+                     dtot.as<double>(), g->stream);
+    VK_CUDA(cudaMemcpyAsync(total_out, dtot.p, n * 8 * ncols, cudaMemcpyDeviceToHost, g->stream));
+    if (hop_out)
+      VK_CUDA(cudaMemcpyAsync(hop_out, dhop.p, n * 8 * ncols * num_hops, cudaMemcpyDeviceToHost, g->stream));
+    VK_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+int vk_vip_propagate_device(vk_graph g, const uint32_t* fanouts, uint32_t num_hops, uint32_t ncols,
+                            const double* p0_dev, double* hop_dev, double* total_dev, vk_stream_t stream) {
+  return guard([&] {
+    if (!g || !p0_dev || !total_dev) raise(VK_ERR_PARAMETER, "null argument");
+    DeviceGuard dg(g->device);
+    propagate_device(*g, fanouts, num_hops, ncols, p0_dev, hop_dev, total_dev,
+                     stream ? static_cast<cudaStream_t>(stream) : g->stream);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+"""GPU: ranking, reorder, cache membership and the classify+gather kernel vs
+the oracle. Bit-exact rows (fp32 and fp16) and exact local/cache/miss tallies."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import csr_from
+
+pytestmark = pytest.mark.gpu
+
+
+def test_rank_by_scores_bit_exact(vk, port, golden):
+    pol = golden("policy.npz")
+    for k in range(4):
+        o, s = vk.rank_by_scores(pol["labels"], k, pol[f"total_{k}"])
+        np.testing.assert_array_equal(o, pol[f"order_{k}"])
+        np.testing.assert_array_equal(s, pol[f"score_{k}"])
+    o, _ = vk.rank_by_scores(np.array([0, 1, 1, 1], np.uint32), 0, np.full(4, 5.0))
+    np.testing.assert_array_equal(o, pol["tie_order"])
+    rng = np.random.default_rng(3)
+    n = 200000
+    labels = rng.integers(0, 5, n).astype(np.uint32)
+    scores = np.round(rng.random(n), 3)           # many ties
+    scores[rng.integers(0, n, 5000)] = 0.0
+    scores[rng.integers(0, n, 5000)] = -0.0        # -0.0 ties +0.0 (policies.cpp:28)
+    scores[rng.integers(0, n, 100)] = 1.0
+    for k in (0, 4):
+        o1, s1 = vk.rank_by_scores(labels, k, scores)
+        o2, s2 = port.rank_by_scores(labels, 5, k, scores)
+        np.testing.assert_array_equal(o1, o2)
+    with pytest.raises(vk.ShapeError):
+        vk.rank_by_scores(labels, 0, scores[:-1])
+
+
+def test_build_reorder_bit_exact(vk, golden):
+    pol = golden("policy.npz")
+    oon, ranges = vk.build_reorder(pol["labels"], 4, np.stack([pol[f"total_{k}"] for k in range(4)]))
+    np.testing.assert_array_equal(oon, pol["old_of_new"])
+    np.testing.assert_array_equal(ranges, pol["ranges"])
+
+
+def _pipeline(vk, port, csr, roles, labels, K, fan, b, alpha, seed, dim, dtype, feature_seed, nmb):
+    """VIP -> rank -> cache -> reorder -> plane(all K resident) -> sample -> gather."""
+    n = csr.n
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    p0 = np.stack([vk.initial_probs(roles, labels, k, b) for k in range(K)])
+    scores = vk.propagate(g, fan, p0, with_hops=False)
+    totals = np.stack([s.total for s in scores])
+    orders = [vk.rank_by_scores(labels, k, totals[k])[0] for k in range(K)]
+    plan = vk.build_cache(orders, alpha, n)
+    oon, ranges = vk.build_reorder(labels, K, totals)
+    plane = vk.FeaturePlane(n, K, dim, labels, oon, ranges, dtype=dtype)
+    for k in range(K):
+        plane.load_partition(k, plan.cached[k], feature_seed=feature_seed)
+    batches, refs = [], []
+    for k in range(K):
+        perm = vk.epoch_permutation(roles, labels, k, b, 0, seed)
+        for i in range(min(nmb, (len(perm) + b - 1) // b)):
+            batches.append(perm[i * b:(i + 1) * b])
+            refs.append((0, k, i))
+    s = vk.Sampler(g, fan, b, len(batches), seed)
+    s.run(batches, refs)
+    view = s.view()
+    rb = plane.row_bytes
+    out_ptr = C.c_void_p()
+    vk.check(vk.lib().vk_device_alloc(0, len(batches) * view.all_stride * rb, C.byref(out_ptr)))
+    cnt_ptr = C.c_void_p()
+    vk.check(vk.lib().vk_device_alloc(0, len(batches) * 32, C.byref(cnt_ptr)))
+    plane.gather(s, out_ptr.value, view.all_stride, cnt_ptr.value)
+    counts = np.zeros(len(batches) * 4, np.uint64)
+    vk.check(vk.lib().vk_memcpy(counts.ctypes.data, cnt_ptr, counts.nbytes, 2))
+    counts = counts.reshape(-1, 4)
+    _, _, al = s.sizes()
+    rows = []
+    for i in range(len(batches)):
+        buf = np.zeros(int(al[i]) * rb, np.uint8)
+        vk.check(vk.lib().vk_memcpy(buf.ctypes.data, out_ptr.value + i * view.all_stride * rb, buf.nbytes, 2))
+        rows.append(buf)
+    vk.lib().vk_device_free(out_ptr)
+    vk.lib().vk_device_free(cnt_ptr)
+    return dict(plan=plan, plane=plane, sampler=s, batches=batches, refs=refs, counts=counts,
+                rows=rows, totals=totals, g=g)
+
+
+@pytest.mark.parametrize("dtype,dim", [(0, 64), (1, 128), (0, 100), (0, 3)])
+def test_gather_rows_and_tallies(vk, port, golden, dtype, dim):
+    fx = golden("expand_grid.npz")
+    csr = csr_from(golden("graphs.npz"), "pa5000")
+    roles, labels = fx["roles"], fx["labels"]
+    r = _pipeline(vk, port, csr, roles, labels, 4, [15, 10, 5], 64, 0.2, 42, dim, dtype, 1234, 3)
+    plan = r["plan"]
+    for i, (e, k, bi) in enumerate(r["refs"]):
+        x = port.expand(csr, r["batches"][i], [15, 10, 5], 42, e, k, bi)
+        exp = port.features(1234, dim, x.all_vertices, fp16=dtype == 1)
+        got = r["rows"][i].view(np.float16 if dtype == 1 else np.float32).reshape(-1, dim)
+        np.testing.assert_array_equal(got.view(np.uint16 if dtype == 1 else np.uint32),
+                                      exp.view(np.uint16 if dtype == 1 else np.uint32))
+        loc, hit, miss = port.classify(x.all_vertices, labels, k, plan.member_bits[k])
+        assert tuple(int(c) for c in r["counts"][i][:3]) == (loc, hit, miss)
+        assert r["counts"][i][3] == 0  # single GPU: no miss crosses NVLink
+    # cache membership == CachePlan::is_cached
+    for k in range(4):
+        for v in list(plan.cached[k][:20]) + [0, 1, 2, 3]:
+            assert r["plane"].is_cached(k, int(v)) == plan.is_cached(k, int(v))
+
+
+def test_cache_reduces_misses(vk, port):
+    """Miss rows fall as alpha grows (nested prefix caches), alpha = 0 has no hits."""
+    csr = port.generate("pa", 20000, 6, 9)
+    roles = port.make_roles(csr.n, 0.1, 0, 0, 3)
+    labels = (np.arange(csr.n) % 4).astype(np.uint32)
+    prev = None
+    for alpha in (0.0, 0.1, 0.3, 3.0):
+        r = _pipeline(vk, port, csr, roles, labels, 4, [10, 5], 128, alpha, 7, 16, 0, 5, 2)
+        miss = int(r["counts"][:, 2].sum())
+        hits = int(r["counts"][:, 1].sum())
+        if alpha == 0.0:
+            assert hits == 0
+        if alpha == 3.0:
+            assert miss == 0
+        if prev is not None:
+            assert miss <= prev
+        prev = miss

@@ -1,0 +1,117 @@
+"""GPU: the batched sampler (K5/K6 + MFG + relabel) vs the oracle. Bit-exact:
+frontiers, all_vertices, MFG row pointers, MFG edges (global id = F_h[dst]) and
+the relabel maps."""
+import numpy as np
+import pytest
+
+from conftest import csr_from
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_graph(vk, csr):
+    return vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+
+
+def assert_same(gpu, L, frontiers, all_vertices, indptr=None, edges=None):
+    np.testing.assert_array_equal(gpu.all_vertices, all_vertices)
+    for h in range(L):
+        np.testing.assert_array_equal(gpu.frontier[h], frontiers[h])
+        if indptr is not None:
+            np.testing.assert_array_equal(gpu.mfg_indptr[h], indptr[h])
+            np.testing.assert_array_equal(gpu.frontier[h][gpu.mfg_dst[h]], edges[h])
+    # relabel maps: all_vertices[all_index[h]] == F_h (h = 0 is the batch)
+    np.testing.assert_array_equal(gpu.all_vertices[gpu.all_index[0]], gpu.batch)
+    for h in range(L):
+        np.testing.assert_array_equal(gpu.all_vertices[gpu.all_index[h + 1]], gpu.frontier[h])
+
+
+@pytest.mark.parametrize("fixture,graph", [("expand_small.npz", "pa400"), ("expand_grid.npz", "pa5000")])
+def test_wave_vs_golden(vk, golden, fixture, graph):
+    fx = golden(fixture)
+    csr = csr_from(golden("graphs.npz"), graph)
+    g = dev_graph(vk, csr)
+    L = len(fx["fanouts"])
+    nmb = int(fx["nmb"])
+    s = vk.Sampler(g, fx["fanouts"], int(fx["b"]), nmb, int(fx["seed"]))
+    batches = [fx[f"mb{i}_batch"] for i in range(nmb)]
+    refs = [tuple(int(x) for x in fx[f"mb{i}_ref"]) for i in range(nmb)]
+    s.run(batches, refs)
+    for i in range(nmb):
+        p = f"mb{i}"
+        r = s.result(i)
+        np.testing.assert_array_equal(r.batch, batches[i])
+        assert_same(r, L, [fx[f"{p}_f{h + 1}"] for h in range(L)], fx[p + "_all"],
+                    [fx[f"{p}_ip{h + 1}"] for h in range(L)], [fx[f"{p}_ed{h + 1}"] for h in range(L)])
+
+
+def test_c1_epoch_slice_vs_oracle(vk, port):
+    """C1 (BASELINE configs[0]): PA 1e5/d=10, roles 0.1, K=1, b=1024,
+    (15,10,5), SeedSpec{42}: the first 8 minibatches of epoch 0 in one wave."""
+    csr = port.generate("pa", 100000, 10, 7)
+    roles = port.make_roles(csr.n, 0.1, 0, 0, 3)
+    labels = np.zeros(csr.n, np.uint32)
+    perm = port.epoch_permutation(roles, labels, 0, 1024, 0, 42)
+    np.testing.assert_array_equal(perm, vk.epoch_permutation(roles, labels, 0, 1024, 0, 42))
+    batches = [perm[i * 1024:(i + 1) * 1024] for i in range(8)]
+    g = dev_graph(vk, csr)
+    s = vk.Sampler(g, [15, 10, 5], 1024, 8, 42)
+    s.run(batches, [(0, 0, i) for i in range(8)])
+    for i in range(8):
+        x = port.expand(csr, batches[i], [15, 10, 5], 42, 0, 0, i)
+        assert_same(s.result(i), 3, x.frontier, x.all_vertices, x.indptr, x.edges)
+
+
+def test_ragged_last_batch_and_reuse(vk, port):
+    csr = port.generate("pa", 30000, 5, 11)
+    roles = port.make_roles(csr.n, 0.2, 0, 0, 2)
+    labels = (np.arange(csr.n) % 3).astype(np.uint32)
+    g = dev_graph(vk, csr)
+    s = vk.Sampler(g, [10, 5], 300, 6, 9)
+    for e in range(2):  # the second run reuses (and must fully reset) the workspace
+        perm = port.epoch_permutation(roles, labels, 1, 300, e, 9)
+        nb = (len(perm) + 299) // 300
+        assert nb >= 6
+        idx = list(range(nb - 6, nb))  # ends with the ragged batch
+        batches = [perm[i * 300:(i + 1) * 300] for i in idx]
+        assert len(batches[-1]) < 300
+        s.run(batches, [(e, 1, i) for i in idx])
+        for j, i in enumerate(idx):
+            x = port.expand(csr, batches[j], [10, 5], 9, e, 1, i)
+            assert_same(s.result(j), 2, x.frontier, x.all_vertices, x.indptr, x.edges)
+
+
+def test_large_fanout_path(vk, port):
+    """fanout > 32 with hub vertices of higher degree (128-entry FY state)."""
+    csr = port.generate("pa", 20000, 8, 4)
+    batch = np.argsort(-np.diff(csr.off).astype(np.int64))[:64].astype(np.uint32)  # hubs
+    g = dev_graph(vk, csr)
+    s = vk.Sampler(g, [40, 3], 64, 1, 5)
+    s.run([batch], [(1, 0, 2)])
+    x = port.expand(csr, batch, [40, 3], 5, 1, 0, 2)
+    assert_same(s.result(0), 2, x.frontier, x.all_vertices, x.indptr, x.edges)
+
+
+def test_saturating_and_duplicates(vk, port, golden):
+    csr = csr_from(golden("graphs.npz"), "pa120")
+    g = dev_graph(vk, csr)
+    x = vk.expand(g, [3, 17, 3], [1000, 1000], 1, (0, 0, 0))  # duplicate seed
+    y = port.expand(csr, [3, 17, 3], [1000, 1000], 1, 0, 0, 0)
+    assert_same(x, 2, y.frontier, y.all_vertices, y.indptr, y.edges)
+
+
+def test_expand_single_and_errors(vk, port, golden):
+    csr = csr_from(golden("graphs.npz"), "uni200")
+    g = dev_graph(vk, csr)
+    x = vk.expand(g, [1, 2, 3, 50, 51], [3, 2, 2], 5, (7, 0, 3))
+    y = port.expand(csr, [1, 2, 3, 50, 51], [3, 2, 2], 5, 7, 0, 3)
+    assert_same(x, 3, y.frontier, y.all_vertices, y.indptr, y.edges)
+    with pytest.raises(vk.SamplingError):
+        vk.expand(g, [], [3, 2], 5)
+    with pytest.raises(vk.ParameterError):
+        vk.expand(g, [1], [3, 0], 5)
+    s = vk.Sampler(g, [3, 2], 8, 2, 5)
+    with pytest.raises(vk.RangeError):
+        s.run([[1, 999]], [(0, 0, 0)])
+    with pytest.raises(vk.SamplingError):
+        s.run([[1], []], [(0, 0, 0), (0, 0, 1)])

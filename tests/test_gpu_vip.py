@@ -1,0 +1,127 @@
+"""GPU: VIP propagation (K1-K3) through the C ABI vs the oracle.
+
+Tolerance (north-star): 1e-5 relative, with an absolute floor at the
+reference's flush threshold kFlushBelow = 1e-300 (vip.cpp:16). The exact
+special cases (0/1 indicators, zero preservation) must be bit-exact."""
+import numpy as np
+import pytest
+
+from conftest import csr_from
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+def dev_graph(vk, csr, directed=False):
+    if directed:
+        return vk.Graph.from_csr(csr.off, csr.tgt, validate=True)
+    return vk.Graph.from_csr(csr.off, csr.tgt, undirected=True, validate=True)
+
+
+def close(a, b):
+    np.testing.assert_allclose(a, b, rtol=RTOL, atol=1e-300)
+
+
+def test_three_path_hand_values(vk, golden):
+    v = golden("vip.npz")
+    g = dev_graph(vk, csr_from(golden("graphs.npz"), "path3"))
+    s = vk.propagate(g, [1, 1], [1.0, 0.0, 0.0])
+    assert list(s.hop[0]) == [0.0, 1.0, 0.0]
+    assert s.hop[1][1] == 0.0
+    np.testing.assert_allclose(s.hop, v["path3_hop"], rtol=1e-15)
+    np.testing.assert_allclose(s.total, [0.5, 1.0, 0.5], rtol=1e-15)
+
+
+def test_saturating_fanouts_bit_exact(vk, golden):
+    v = golden("vip.npz")
+    g = dev_graph(vk, csr_from(golden("graphs.npz"), "pa150"))
+    p0 = np.zeros(150)
+    p0[5] = 1.0
+    s = vk.propagate(g, [1000] * 3, p0)
+    np.testing.assert_array_equal(s.hop, v["sat_hop"])
+    np.testing.assert_array_equal(s.total, v["sat_total"])
+
+
+def test_directed_tree_reverse_built_on_device(vk, golden):
+    gg = golden("graphs.npz")
+    v = golden("vip.npz")
+    csr = csr_from(gg, "dtree13")
+    g = dev_graph(vk, csr, directed=True)
+    assert not g.symmetric
+    roff, rtgt = g.reverse()
+    np.testing.assert_array_equal(roff, csr.rev_off)
+    np.testing.assert_array_equal(rtgt, csr.rev_tgt)
+    p0 = np.zeros(13)
+    p0[0] = 1.0
+    s = vk.propagate(g, [2, 2], p0)
+    np.testing.assert_allclose(s.hop, v["dtree_hop"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(s.total, v["dtree_total"], rtol=1e-12, atol=0)
+
+
+def test_grid_partitions_vs_golden_and_multicolumn(vk, golden):
+    v = golden("vip.npz")
+    fx = golden("expand_grid.npz")
+    g = dev_graph(vk, csr_from(golden("graphs.npz"), "pa5000"))
+    p0 = np.stack([vk.initial_probs(fx["roles"], fx["labels"], k, 64) for k in range(4)])
+    singles = [vk.propagate(g, [15, 10, 5], p0[k]) for k in range(4)]
+    multi = vk.propagate(g, [15, 10, 5], p0)  # 4 columns in one pass
+    for k in range(4):
+        np.testing.assert_array_equal(p0[k], v[f"grid_p0_{k}"])
+        close(singles[k].hop, v[f"grid_hop_{k}"])
+        close(singles[k].total, v[f"grid_total_{k}"])
+        # the column batch computes each column with the same arithmetic order
+        np.testing.assert_array_equal(multi[k].hop, singles[k].hop)
+        np.testing.assert_array_equal(multi[k].total, singles[k].total)
+
+
+def test_c1_vs_oracle(vk, port):
+    """C1: PA n=1e5, d=10 (m=1,999,890), roles 0.1, K=1, b=1024, (15,10,5)."""
+    csr = port.generate("pa", 100000, 10, 7)
+    assert csr.m == 1999890
+    roles = port.make_roles(csr.n, 0.1, 0, 0, 3)
+    labels = np.zeros(csr.n, np.uint32)
+    p0 = port.initial_probs(roles, labels, 1, 0, 1024)
+    hop, tot = port.propagate(csr, [15, 10, 5], p0)
+    g = dev_graph(vk, csr)
+    s = vk.propagate(g, [15, 10, 5], p0)
+    close(s.hop, hop)
+    close(s.total, tot)
+    assert np.all((tot == 0) == (s.total == 0))  # zero pattern exact
+
+
+@pytest.mark.parametrize("L,fan", [(2, [5, 5]), (4, [25, 25, 25, 25]), (2, [25, 15])])
+def test_hop_sweep_vs_oracle(vk, port, L, fan):
+    csr = port.generate("pa", 20000, 6, 3)
+    roles = port.make_roles(csr.n, 0.05, 0, 0, 1)
+    labels = (np.arange(csr.n) % 2).astype(np.uint32)
+    p0 = np.stack([port.initial_probs(roles, labels, 2, k, 256) for k in range(2)])
+    g = dev_graph(vk, csr)
+    res = vk.propagate(g, fan, p0)
+    for k in range(2):
+        hop, tot = port.propagate(csr, fan, p0[k])
+        close(res[k].hop, hop)
+        close(res[k].total, tot)
+
+
+def test_heavy_rows_split_path(vk, port):
+    """A star with 100k leaves exercises the chunked (split-row) reduction."""
+    n = 100001
+    csr = port.generate("star", n)
+    p0 = np.full(n, 0.3)
+    hop, tot = port.propagate(csr, [3, 2], p0)
+    g = dev_graph(vk, csr)
+    s = vk.propagate(g, [3, 2], p0)
+    close(s.hop, hop)
+    close(s.total, tot)
+
+
+def test_errors(vk, golden):
+    g = dev_graph(vk, csr_from(golden("graphs.npz"), "path3"))
+    with pytest.raises(vk.ParameterError):
+        vk.propagate(g, [1, 1], [1.5, 0.0, 0.0])
+    with pytest.raises(vk.ShapeError):
+        vk.propagate(g, [1, 1], [1.0, 0.0])
+    with pytest.raises(vk.ParameterError):
+        vk.propagate(g, [1, 0], [1.0, 0.0, 0.0])
+    with pytest.raises(vk.FormatError):
+        vk.Graph.from_csr(np.array([0, 1, 1], np.uint64), np.array([0], np.uint32), validate=True)
