@@ -304,8 +304,8 @@ void run_columns(vk_graph_s& g, const std::uint32_t* fan, std::uint32_t L, const
     {
       auto [r, k] = cls(5);
       if (k) {
-        const std::uint64_t nch = so[7];
-        const std::uint64_t* meta = reinterpret_cast<const std::uint64_t*>(rows + so[6]);
+        const std::uint64_t nch = so[8];
+        const std::uint64_t* meta = reinterpret_cast<const std::uint64_t*>(rows + so[7]);
         // meta layout: lo[nch], hi[nch], first_chunk[k+1]
         const unsigned grid = (unsigned)std::min<std::uint64_t>(nch, (std::uint64_t)sm_count(g.device) * 8);
         k_pull_chunk<C><<<grid, kCtaThreads, 0, st>>>(p, meta, meta + nch, nch, partial.as<double>());
@@ -344,7 +344,7 @@ void build_vip_schedule(vk_graph_s& g) {
   }
   // rows (u32) for classes 0..5, then an 8-byte aligned meta block for the
   // split rows: lo[nchunks], hi[nchunks], first_chunk[nsplit+1] (u64).
-  std::vector<std::uint64_t> so(8, 0);
+  std::vector<std::uint64_t> so(9, 0);
   for (int c = 0; c < 6; ++c) so[c + 1] = so[c] + cnt[c];
   std::uint64_t meta_start = (so[6] + 1) & ~1ull;  // u64 alignment in u32 units
   const std::uint64_t nsplit = cnt[5];
@@ -370,8 +370,8 @@ void build_vip_schedule(vk_graph_s& g) {
   for (std::uint64_t r = 0; r <= nsplit; ++r) meta[2 * nchunks + r] = first[r];
   g.sched_rows.alloc(host.size() * 4);
   VK_CUDA(cudaMemcpy(g.sched_rows.p, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
-  so[6] = meta_start;
-  so[7] = nchunks;
+  so[7] = meta_start;
+  so[8] = nchunks;
   g.sched_offsets = so;
   g.sched_ready = true;
 }
@@ -401,7 +401,7 @@ void propagate_device(vk_graph_s& g, const std::uint32_t* fanouts, std::uint32_t
   auto ensure = [](DevBuf& b, std::size_t bytes) {
     if (b.bytes < bytes) b.alloc(bytes);
   };
-  const std::uint64_t nch = g.sched_offsets[7];
+  const std::uint64_t nch = g.sched_offsets[8];
   ensure(g.vip_lm_a, n * 8 * cmax);
   ensure(g.vip_lm_b, n * 8 * cmax);
   ensure(g.vip_partial, std::max<std::uint64_t>(1, nch) * 8 * cmax);
