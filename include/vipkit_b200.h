@@ -189,6 +189,11 @@ VK_API int vk_sampler_get_view(vk_sampler s, vk_sampler_view* view);
 VK_API int vk_sampler_snapshot_counts(vk_sampler s, uint32_t* dst_dev, uint64_t* words,
                                       vk_stream_t stream);
 
+/* Device-side RngStream draws (rng.hpp:19-44) for conformance tests:
+ * `count` values of next_below(bound) (next_u64 when bound == 0). */
+VK_API int vk_debug_stream_draws(int device, uint64_t key, uint64_t bound, uint64_t count,
+                                 uint64_t* out);
+
 /* --------------------------------------------------- ranking / cache plan
  * vipkit::rank_by_scores -> order_remotes (policies.hpp:48, policies.cpp:
  * 20-34, 134-138): vertices with part_of != k ordered by (score desc, id asc),

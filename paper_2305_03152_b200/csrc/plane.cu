@@ -166,12 +166,43 @@ struct GatherParams {
   std::uint64_t out_stride_bytes;
   std::uint64_t row_bytes;
   std::uint32_t V;                   // vector elements per row
-  std::uint64_t magic;               // ceil(2^64 / V)
+  std::uint32_t magic32;             // ceil(2^32 / V): row = umulhi(e, magic32) for e < 32*V
   unsigned long long* counts;        // [nmb][4]
 };
 
+// Streaming 16/4/2-byte copies: the feature table is read through L1
+// (no_allocate) and the gathered rows are written evict-first so neither
+// evicts the graph / slot maps from L2.
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+  if constexpr (sizeof(T) == 16) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+  } else {
+    return __ldg(p);
+  }
+}
+template <class T>
+__device__ __forceinline__ void st_stream(T* p, const T& v) {
+  if constexpr (sizeof(T) == 16) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+  } else {
+    __stcs(p, v);
+  }
+}
+
+// One warp per group of 32 consecutive output rows: lanes first resolve the
+// 32 source rows in parallel (classify: slot map -> local / cache row, or the
+// owner partition's row, local HBM or a peer GPU over NVLink), then the warp
+// copies the group as one flat, fully coalesced range of 32*V vectors with
+// kUnroll independent loads in flight per lane.
 template <class T>
 __global__ void __launch_bounds__(256) k_gather(GatherParams p) {
+  constexpr int kUnroll = 8;
+  __shared__ const T* s_src[8][32];
   const std::uint32_t mb = blockIdx.y;
   const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
   const std::uint32_t cnt = p.all_count[mb];
@@ -181,27 +212,50 @@ __global__ void __launch_bounds__(256) k_gather(GatherParams p) {
   const T* store = reinterpret_cast<const T*>(p.base[k]);
   T* out = reinterpret_cast<T*>(p.out + mb * p.out_stride_bytes);
   const std::uint32_t V = p.V;
+  const std::uint32_t magic = p.magic32;
   const std::uint64_t rowv = p.row_bytes / sizeof(T);
-  const std::uint32_t total = cnt * V;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const std::uint32_t gw = blockIdx.x * (blockDim.x >> 5) + w;
+  const std::uint32_t nw = gridDim.x * (blockDim.x >> 5);
   unsigned c_local = 0, c_cache = 0, c_miss = 0, c_peer = 0;
-  for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const std::uint32_t r = V == 1 ? e : (std::uint32_t)__umul64hi((std::uint64_t)e, p.magic);
-    const std::uint32_t c = e - r * V;
-    const std::uint32_t v = __ldg(all + r);
-    const std::uint32_t s = __ldg(slot + v);
-    const T* src;
-    if (s != VK_MISS) {
-      src = store + (std::uint64_t)s * rowv;
-      if (c == 0) (s < nl ? c_local : c_cache)++;
-    } else {
-      const std::uint32_t o = __ldg(p.part_of + v);
-      src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
-      if (c == 0) {
+  for (std::uint32_t r0 = gw * 32; r0 < cnt; r0 += nw * 32) {
+    const std::uint32_t r = r0 + lane;
+    const T* src = nullptr;
+    if (r < cnt) {
+      const std::uint32_t v = __ldg(all + r);
+      const std::uint32_t s = __ldg(slot + v);
+      if (s != VK_MISS) {
+        src = store + (std::uint64_t)s * rowv;
+        (s < nl ? c_local : c_cache)++;
+      } else {
+        const std::uint32_t o = __ldg(p.part_of + v);
+        src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
         ++c_miss;
         c_peer += p.peer_mask[o];
       }
     }
-    out[e] = src[c];
+    s_src[w][lane] = src;
+    __syncwarp();
+    const std::uint32_t rows = min(32u, cnt - r0);
+    const std::uint32_t total = rows * V;
+    T* dst = out + (std::uint64_t)r0 * V;
+    for (std::uint32_t e0 = lane; e0 < total; e0 += 32 * kUnroll) {
+      T val[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const std::uint32_t e = e0 + 32 * u;
+        if (e < total) {
+          const std::uint32_t row = V == 1 ? e : __umulhi(e, magic);
+          val[u] = ld_stream(s_src[w][row] + (e - row * V));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const std::uint32_t e = e0 + 32 * u;
+        if (e < total) st_stream(dst + e, val[u]);
+      }
+    }
+    __syncwarp();
   }
   // block-reduce the class counts, one atomic per class per CTA
   __shared__ unsigned sh[4][8];
@@ -558,12 +612,12 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     const bool v4 = (p->row_bytes % 4 == 0) && ((std::uintptr_t)out_dev % 4 == 0);
     const std::uint64_t esz = v16 ? 16 : (v4 ? 4 : 2);
     gp.V = (std::uint32_t)(p->row_bytes / esz);
-    gp.magic = gp.V == 1 ? 0 : (~0ull / gp.V) + 1;  // ceil(2^64 / V)
-    if ((std::uint64_t)gp.all_stride * gp.V >= (1ull << 32))
-      raise(VK_ERR_UNSUPPORTED, "rows x vector width exceeds 2^32 per minibatch");
+    if (gp.V >= (1u << 15)) raise(VK_ERR_UNSUPPORTED, "feature rows above 512 KiB are not supported");
+    gp.magic32 = gp.V == 1 ? 0u : (std::uint32_t)((0xffffffffull / gp.V) + 1);  // ceil(2^32 / V)
+    // enough warps in flight to saturate HBM: ~16 resident warps per SM
+    const std::uint64_t want = (std::uint64_t)sm_count(p->device) * 8;  // CTAs of 8 warps
     const unsigned gx = (unsigned)std::max<std::uint64_t>(
-        1, std::min<std::uint64_t>((std::uint64_t)sm_count(p->device) * 8 / nmb + 1,
-                                   ceil_div(gp.all_stride * gp.V, 256)));
+        1, std::min<std::uint64_t>((want + nmb - 1) / nmb, ceil_div(gp.all_stride, 256)));
     dim3 grid(gx, nmb);
     if (v16)
       k_gather<uint4><<<grid, 256, 0, st>>>(gp);

@@ -46,16 +46,46 @@ struct Stream {
     x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
     return x ^ (x >> 31);
   }
-  // rng.hpp:35-40. bound < 2^32 on every sampler path (degrees are u32
-  // counts of a u32-id graph); the 64-bit division is kept for exactness and
-  // the power-of-two bound (which rejects the top `bound` values) falls out
-  // of the same formula.
+  // rng.hpp:35-40: limit = ~0 - ~0 % bound, reject x >= limit, return
+  // x % bound (the power-of-two bound, which rejects the top `bound`
+  // values, falls out of the same formula). On the device both remainders
+  // use an exact FP64-reciprocal reduction (mod_u64) instead of the ~80
+  // instruction 64-bit division routine; results are identical.
   VK_HD std::uint64_t next_below(std::uint64_t bound) {
+#ifdef __CUDA_ARCH__
+    if (bound < (1ull << 40)) {
+      if (bound <= 1) {  // ~0 % 1 == 0: limit = ~0; x % 1 == 0
+        std::uint64_t x = next_u64();
+        while (x == ~0ull) x = next_u64();
+        return 0;
+      }
+      const double inv = __drcp_rn((double)bound);
+      const std::uint64_t limit = ~0ull - mod_u64(~0ull, bound, inv);
+      std::uint64_t x = next_u64();
+      while (x >= limit) x = next_u64();
+      return mod_u64(x, bound, inv);
+    }
+#endif
     const std::uint64_t limit = ~0ull - ~0ull % bound;
     std::uint64_t x = next_u64();
     while (x >= limit) x = next_u64();
     return x % bound;
   }
+
+#ifdef __CUDA_ARCH__
+  // Exact x % b for 2 <= b < 2^40, inv = RN(1/b). First estimate
+  // q = trunc(x*inv) is within ~2^13 of x/b, so r = x - q*b fits in an int64;
+  // a second FP64 step brings r into (-b, 2b), then one correction each way.
+  __device__ __forceinline__ static std::uint64_t mod_u64(std::uint64_t x, std::uint64_t b, double inv) {
+    const std::uint64_t q = (std::uint64_t)(__ull2double_rz(x) * inv);
+    long long r = (long long)(x - q * b);
+    const long long q2 = __double2ll_rn((double)r * inv);
+    r -= q2 * (long long)b;
+    if (r < 0) r += (long long)b;
+    if (r >= (long long)b) r -= (long long)b;
+    return (std::uint64_t)r;
+  }
+#endif
 };
 
 // Key prefix of the neighbour-sample stream (sampling.cpp:110-112):

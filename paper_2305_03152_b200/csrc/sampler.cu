@@ -30,8 +30,7 @@
 namespace vk {
 
 constexpr int kCompactThreads = 256;
-constexpr int kWordsPerThread = 2;
-constexpr int kTileWords = kCompactThreads * kWordsPerThread;
+constexpr int kTileWords = kCompactThreads;  // one 64-bit word per thread
 
 // Per-minibatch wave descriptor (uploaded once per run).
 struct WaveDesc {
@@ -45,7 +44,6 @@ struct WaveDesc {
 using vk::WaveDesc;
 using vk::kCompactThreads;
 using vk::kTileWords;
-using vk::kWordsPerThread;
 
 struct vk_sampler_s {
   vk_graph_s* g = nullptr;
@@ -125,78 +123,96 @@ __global__ void __launch_bounds__(1024) k_prepare(const WaveDesc* __restrict__ d
   }
 }
 
-// Sparse partial Fisher-Yates, same draws as sampling.cpp:87-91.
-template <int MAXF>
+// Sparse partial Fisher-Yates, same draws as sampling.cpp:87-91: the value
+// at positions [0, f) lives in lo[], positions >= f displaced by a swap in the
+// (hp, hv) map (at most f entries); untouched positions read the CSR slice.
+// `S` is the slot stride of the per-thread arrays (blockDim for the shared-
+// memory layout, where thread t's slot i is at i*S + t, bank-conflict free;
+// 1 for the local-memory fallback used for fanouts > 32).
 __device__ __forceinline__ void sample_one(const std::uint32_t* __restrict__ nbrs, std::uint32_t deg,
                                            std::uint32_t f, Stream& s, std::uint32_t* __restrict__ out,
-                                           unsigned long long* __restrict__ hb, unsigned long long* __restrict__ ab) {
+                                           unsigned long long* __restrict__ hb, std::uint32_t* lo,
+                                           std::uint32_t* hp, std::uint32_t* hv, unsigned S) {
   if (deg <= f) {  // sampling.cpp:76-78: all neighbours, CSR order
     for (std::uint32_t i = 0; i < deg; ++i) {
       const std::uint32_t u = __ldg(nbrs + i);
       out[i] = u;
       atomicOr(hb + (u >> 6), 1ull << (u & 63));
-      atomicOr(ab + (u >> 6), 1ull << (u & 63));
     }
     return;
   }
-  std::uint32_t lo[MAXF];           // current value at positions [0, f)
-  std::uint32_t hpos[MAXF], hval[MAXF];  // displaced positions >= f
+  for (std::uint32_t i = 0; i < f; ++i) lo[i * S] = __ldg(nbrs + i);
   std::uint32_t nh = 0;
-  for (std::uint32_t i = 0; i < f; ++i) lo[i] = __ldg(nbrs + i);
   for (std::uint32_t i = 0; i < f; ++i) {
     const std::uint32_t j = i + (std::uint32_t)s.next_below((std::uint64_t)(deg - i));
-    const std::uint32_t vi = lo[i];
+    const std::uint32_t vi = lo[i * S];
     std::uint32_t vj;
     if (j < f) {
-      vj = lo[j];
-      lo[j] = vi;
+      vj = lo[j * S];
+      lo[j * S] = vi;
     } else {
       std::uint32_t c = 0;
-      while (c < nh && hpos[c] != j) ++c;
+      while (c < nh && hp[c * S] != j) ++c;
       if (c < nh) {
-        vj = hval[c];
-        hval[c] = vi;
+        vj = hv[c * S];
+        hv[c * S] = vi;
       } else {
         vj = __ldg(nbrs + j);
-        hpos[nh] = j;
-        hval[nh] = vi;
+        hp[nh * S] = j;
+        hv[nh * S] = vi;
         ++nh;
       }
     }
     out[i] = vj;  // scratch[i] after the swap
     atomicOr(hb + (vj >> 6), 1ull << (vj & 63));
-    atomicOr(ab + (vj >> 6), 1ull << (vj & 63));
   }
 }
 
+struct SampleParams {
+  const WaveDesc* desc;
+  std::uint32_t h, f;
+  const std::uint64_t* off;
+  const std::uint32_t* tgt;
+  const std::uint32_t* outdeg;
+  const std::uint32_t* Fprev;
+  std::uint64_t capFprev;
+  const std::uint32_t* fcount_prev;
+  const std::uint32_t* indptr;
+  std::uint32_t* edges;
+  std::uint64_t capS;
+  unsigned long long* hopbits;
+  std::uint64_t W;
+};
+
+// One thread per frontier vertex; FY state in shared memory (f <= 32) or in
+// local memory (MAXF > 0, large fanouts).
 template <int MAXF>
-__global__ void __launch_bounds__(256) k_sample(const WaveDesc* __restrict__ desc, std::uint32_t h,
-                                                std::uint32_t f, const std::uint64_t* __restrict__ off,
-                                                const std::uint32_t* __restrict__ tgt,
-                                                const std::uint32_t* __restrict__ outdeg,
-                                                const std::uint32_t* __restrict__ Fprev, std::uint64_t capFprev,
-                                                const std::uint32_t* __restrict__ fcount_prev,
-                                                const std::uint32_t* __restrict__ indptr,
-                                                std::uint32_t* __restrict__ edges, std::uint64_t capS,
-                                                unsigned long long* __restrict__ hopbits,
-                                                unsigned long long* __restrict__ allbits, std::uint64_t W) {
+__global__ void __launch_bounds__(256) k_sample(SampleParams p) {
+  extern __shared__ std::uint32_t sm_fy[];
   const std::uint32_t mb = blockIdx.y;
-  const std::uint32_t cnt = fcount_prev[mb];
-  const std::uint64_t prefix = desc[mb].key_prefix[h - 1];
-  const std::uint32_t* fp = Fprev + mb * capFprev;
-  const std::uint32_t* ip = indptr + mb * (capFprev + 1);
-  std::uint32_t* ed = edges + mb * capS;
-  unsigned long long* hb = hopbits + mb * W;
-  unsigned long long* ab = allbits + mb * W;
+  const std::uint32_t cnt = p.fcount_prev[mb];
+  const std::uint64_t prefix = p.desc[mb].key_prefix[p.h - 1];
+  const std::uint32_t* fp = p.Fprev + mb * p.capFprev;
+  const std::uint32_t* ip = p.indptr + mb * (p.capFprev + 1);
+  std::uint32_t* ed = p.edges + mb * p.capS;
+  unsigned long long* hb = p.hopbits + mb * p.W;
   for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x) {
     const std::uint32_t v = fp[j];
     Stream s(key_step(prefix, v));
-    sample_one<MAXF>(tgt + off[v], outdeg[v], f, s, ed + ip[j], hb, ab);
+    if constexpr (MAXF == 0) {
+      const unsigned S = blockDim.x;
+      std::uint32_t* lo = sm_fy + threadIdx.x;
+      sample_one(p.tgt + p.off[v], p.outdeg[v], p.f, s, ed + ip[j], hb, lo, lo + p.f * S, lo + 2 * p.f * S, S);
+    } else {
+      std::uint32_t lo[MAXF], hp[MAXF], hv[MAXF];
+      sample_one(p.tgt + p.off[v], p.outdeg[v], p.f, s, ed + ip[j], hb, lo, hp, hv, 1);
+    }
   }
 }
 
 struct CompactParams {
   const unsigned long long* bits;  // [M][W]
+  unsigned long long* allbits;     // hop compactions OR their words into the all bitmap
   std::uint32_t* list;             // [M][cap_list]
   std::uint64_t cap_list;
   std::uint32_t* prefix;           // [M][W] rank prefix per word
@@ -212,11 +228,19 @@ struct CompactParams {
   std::uint32_t nmb;
 };
 
-template <bool HAS_NEXT>
+constexpr int kStage = 5120;  // ids staged in shared memory per tile (else direct writes)
+
+// One word (64 vertices) per thread, one tile of kTileWords words per CTA.
+// Tile ids are emitted into shared memory at their scanned positions and
+// copied out with coalesced stores (direct scattered stores only for the rare
+// tile denser than kStage).
+template <bool HAS_NEXT, bool OR_ALL>
 __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   __shared__ unsigned s_ticket;
   __shared__ unsigned long long s_sm[kCompactThreads / 32];
   __shared__ unsigned long long s_excl;
+  __shared__ std::uint32_t s_ids[kStage];
+  __shared__ std::uint32_t s_ip[HAS_NEXT ? kStage : 1];
   if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1u);
   __syncthreads();
   const unsigned ticket = s_ticket;
@@ -224,21 +248,16 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const std::uint32_t tile = ticket % (unsigned)p.tiles;
   if (mb >= p.nmb) return;
   const unsigned long long* bits = p.bits + mb * p.W;
-  const std::uint64_t w0 = (std::uint64_t)tile * kTileWords + (std::uint64_t)threadIdx.x * kWordsPerThread;
-  unsigned long long wd[kWordsPerThread];
-  unsigned long long vc = 0, dc = 0;
-#pragma unroll
-  for (int k = 0; k < kWordsPerThread; ++k) {
-    wd[k] = (w0 + k < p.W) ? bits[w0 + k] : 0ull;
-    vc += __popcll(wd[k]);
-    if (HAS_NEXT) {
-      unsigned long long x = wd[k];
-      while (x) {
-        const int b = __ffsll(x) - 1;
-        x &= x - 1;
-        const std::uint32_t v = (std::uint32_t)((w0 + k) * 64 + b);
-        dc += min(p.f_next, __ldg(p.outdeg + v));
-      }
+  const std::uint64_t w = (std::uint64_t)tile * kTileWords + threadIdx.x;
+  const unsigned long long wd = w < p.W ? bits[w] : 0ull;
+  if (OR_ALL && wd) p.allbits[mb * p.W + w] |= wd;
+  unsigned long long vc = __popcll(wd), dc = 0;
+  if (HAS_NEXT) {
+    unsigned long long x = wd;
+    while (x) {
+      const int b = __ffsll(x) - 1;
+      x &= x - 1;
+      dc += min(p.f_next, __ldg(p.outdeg + (std::uint32_t)(w * 64 + b)));
     }
   }
   const unsigned long long mine = pack_vd(vc, dc);
@@ -246,31 +265,44 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const unsigned long long inc = block_inclusive_scan<kCompactThreads>(mine, s_sm, &total);
   if (threadIdx.x == 0) s_excl = lookback(p.status + mb * p.tiles, tile, total);
   __syncthreads();
-  const unsigned long long ex = s_excl + inc - mine;
-  std::uint32_t pos = (std::uint32_t)unpack_v(ex);
-  std::uint32_t dpos = (std::uint32_t)unpack_d(ex);
+  const unsigned long long base = s_excl;
+  const unsigned long long lex = inc - mine;  // tile-local exclusive prefix
+  std::uint32_t lpos = (std::uint32_t)unpack_v(lex);
+  std::uint32_t dpos = (std::uint32_t)(unpack_d(base) + unpack_d(lex));
+  const std::uint32_t gbase = (std::uint32_t)unpack_v(base);
+  const std::uint32_t tcount = (std::uint32_t)unpack_v(total);
   std::uint32_t* list = p.list + mb * p.cap_list;
-  std::uint32_t* pre = p.prefix + mb * p.W;
   std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
-#pragma unroll
-  for (int k = 0; k < kWordsPerThread; ++k) {
-    if (w0 + k >= p.W) break;
-    pre[w0 + k] = pos;
-    unsigned long long x = wd[k];
-    while (x) {
-      const int b = __ffsll(x) - 1;
-      x &= x - 1;
-      const std::uint32_t v = (std::uint32_t)((w0 + k) * 64 + b);
-      list[pos] = v;
-      if (HAS_NEXT) {
-        ipn[pos] = dpos;
-        dpos += min(p.f_next, __ldg(p.outdeg + v));
-      }
-      ++pos;
+  if (w < p.W) p.prefix[mb * p.W + w] = gbase + lpos;
+  const bool staged = tcount <= (std::uint32_t)kStage;
+  unsigned long long x = wd;
+  while (x) {
+    const int b = __ffsll(x) - 1;
+    x &= x - 1;
+    const std::uint32_t v = (std::uint32_t)(w * 64 + b);
+    std::uint32_t d = 0;
+    if (HAS_NEXT) {
+      d = dpos;
+      dpos += min(p.f_next, __ldg(p.outdeg + v));
+    }
+    if (staged) {
+      s_ids[lpos] = v;
+      if (HAS_NEXT) s_ip[lpos] = d;
+    } else {
+      list[gbase + lpos] = v;
+      if (HAS_NEXT) ipn[gbase + lpos] = d;
+    }
+    ++lpos;
+  }
+  if (staged) {
+    __syncthreads();
+    for (std::uint32_t i = threadIdx.x; i < tcount; i += kCompactThreads) {
+      list[gbase + i] = s_ids[i];
+      if (HAS_NEXT) ipn[gbase + i] = s_ip[i];
     }
   }
   if (tile == p.tiles - 1 && threadIdx.x == kCompactThreads - 1) {
-    const unsigned long long all = s_excl + total;
+    const unsigned long long all = base + total;
     const std::uint32_t tv = (std::uint32_t)unpack_v(all), td = (std::uint32_t)unpack_d(all);
     p.count[mb] = tv;
     if (HAS_NEXT) {
@@ -286,19 +318,40 @@ __device__ __forceinline__ std::uint32_t bit_rank(const unsigned long long* __re
   return __ldg(prefix + w) + (std::uint32_t)__popcll(__ldg(bits + w) & ((1ull << (v & 63)) - 1ull));
 }
 
+// Rank lookups with kIlp independent elements in flight per thread.
+constexpr int kIlp = 4;
+
+template <class Src>
+__device__ __forceinline__ void rank_range(const std::uint32_t* __restrict__ in, std::uint32_t* __restrict__ out,
+                                           std::uint32_t cnt, const unsigned long long* __restrict__ b,
+                                           const std::uint32_t* __restrict__ pr) {
+  const std::uint32_t stride = gridDim.x * blockDim.x;
+  for (std::uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < cnt; i0 += kIlp * stride) {
+    std::uint32_t v[kIlp];
+#pragma unroll
+    for (int u = 0; u < kIlp; ++u) {
+      const std::uint32_t i = i0 + u * stride;
+      v[u] = i < cnt ? __ldg(in + i) : 0u;
+    }
+    std::uint32_t r[kIlp];
+#pragma unroll
+    for (int u = 0; u < kIlp; ++u) r[u] = bit_rank(b, pr, v[u]);
+#pragma unroll
+    for (int u = 0; u < kIlp; ++u) {
+      const std::uint32_t i = i0 + u * stride;
+      if (i < cnt) out[i] = r[u];
+    }
+  }
+}
+
 // MFG dst: rank of every drawn id in F_h.
-__global__ void k_relabel(const std::uint32_t* __restrict__ edges, std::uint64_t in_stride,
-                          const std::uint32_t* __restrict__ ecount, const unsigned long long* __restrict__ bits,
-                          const std::uint32_t* __restrict__ prefix, std::uint64_t W, std::uint32_t* __restrict__ dst,
-                          std::uint64_t out_stride) {
+__global__ void __launch_bounds__(256) k_relabel(const std::uint32_t* __restrict__ edges, std::uint64_t in_stride,
+                                                 const std::uint32_t* __restrict__ ecount,
+                                                 const unsigned long long* __restrict__ bits,
+                                                 const std::uint32_t* __restrict__ prefix, std::uint64_t W,
+                                                 std::uint32_t* __restrict__ dst, std::uint64_t out_stride) {
   const std::uint32_t mb = blockIdx.y;
-  const std::uint32_t cnt = ecount[mb];
-  const std::uint32_t* e = edges + mb * in_stride;
-  std::uint32_t* o = dst + mb * out_stride;
-  const unsigned long long* b = bits + mb * W;
-  const std::uint32_t* pr = prefix + mb * W;
-  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
-    o[i] = bit_rank(b, pr, e[i]);
+  rank_range<int>(edges + mb * in_stride, dst + mb * out_stride, ecount[mb], bits + mb * W, prefix + mb * W);
 }
 
 struct AllIdxParams {
@@ -309,34 +362,48 @@ struct AllIdxParams {
 };
 
 // Relabel map: position of every F_h vertex (h = 0..L) in all_vertices.
-__global__ void k_allidx(AllIdxParams p, const unsigned long long* __restrict__ bits,
-                         const std::uint32_t* __restrict__ prefix, std::uint64_t W) {
+__global__ void __launch_bounds__(256) k_allidx(AllIdxParams p, const unsigned long long* __restrict__ bits,
+                                                const std::uint32_t* __restrict__ prefix, std::uint64_t W) {
   const std::uint32_t mb = blockIdx.y, h = blockIdx.z;
-  const std::uint32_t cnt = p.count[h][mb];
-  const std::uint32_t* f = p.F[h] + mb * p.cap[h];
-  std::uint32_t* o = p.idx[h] + mb * p.cap[h];
-  const unsigned long long* b = bits + mb * W;
-  const std::uint32_t* pr = prefix + mb * W;
-  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
-    o[i] = bit_rank(b, pr, f[i]);
+  rank_range<int>(p.F[h] + mb * p.cap[h], p.idx[h] + mb * p.cap[h], p.count[h][mb], bits + mb * W,
+                  prefix + mb * W);
+}
+
+__global__ void k_stream_draws(std::uint64_t key, std::uint64_t bound, std::uint64_t count,
+                               std::uint64_t* __restrict__ out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  Stream s(key);
+  for (std::uint64_t i = 0; i < count; ++i) out[i] = bound ? s.next_below(bound) : s.next_u64();
 }
 
 template <int MAXF>
 void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStream_t st) {
   vk_graph_s& g = *s.g;
-  const std::uint64_t capPrev = s.capF[h - 1];
-  const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(capPrev, 256), 4096);
-  k_sample<MAXF><<<dim3(gx, nmb), 256, 0, st>>>(
-      s.desc.as<WaveDesc>(), h, s.cfg.fanouts[h - 1], g.d_off(), g.d_tgt(), g.out_deg.as<std::uint32_t>(),
-      s.F[h - 1].as<std::uint32_t>(), capPrev, s.fcount(h - 1), s.indptr[h].as<std::uint32_t>(),
-      s.edges_tmp.as<std::uint32_t>(), s.capS_max, s.hopbits.as<unsigned long long>(),
-      s.allbits.as<unsigned long long>(), s.W);
+  SampleParams p;
+  p.desc = s.desc.as<WaveDesc>();
+  p.h = h;
+  p.f = s.cfg.fanouts[h - 1];
+  p.off = g.d_off();
+  p.tgt = g.d_tgt();
+  p.outdeg = g.out_deg.as<std::uint32_t>();
+  p.Fprev = s.F[h - 1].as<std::uint32_t>();
+  p.capFprev = s.capF[h - 1];
+  p.fcount_prev = s.fcount(h - 1);
+  p.indptr = s.indptr[h].as<std::uint32_t>();
+  p.edges = s.edges_tmp.as<std::uint32_t>();
+  p.capS = s.capS_max;
+  p.hopbits = s.hopbits.as<unsigned long long>();
+  p.W = s.W;
+  const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, 256), 4096);
+  const std::size_t smem = MAXF == 0 ? (std::size_t)3 * p.f * 256 * 4 : 0;
+  k_sample<MAXF><<<dim3(gx, nmb), 256, smem, st>>>(p);
 }
 
 void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, std::uint32_t slot,
                  cudaStream_t st) {
   CompactParams p{};
   p.bits = (hop ? s.hopbits : s.allbits).as<unsigned long long>();
+  p.allbits = s.allbits.as<unsigned long long>();
   p.list = hop ? s.F[h].as<std::uint32_t>() : s.all.as<std::uint32_t>();
   p.cap_list = hop ? s.capF[h] : s.capAll;
   p.prefix = (hop ? s.hopprefix : s.allprefix).as<std::uint32_t>();
@@ -355,9 +422,11 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   p.nmb = nmb;
   const unsigned grid = (unsigned)(nmb * s.tiles);
   if (has_next)
-    k_compact<true><<<grid, kCompactThreads, 0, st>>>(p);
+    k_compact<true, true><<<grid, kCompactThreads, 0, st>>>(p);
+  else if (hop)
+    k_compact<false, true><<<grid, kCompactThreads, 0, st>>>(p);
   else
-    k_compact<false><<<grid, kCompactThreads, 0, st>>>(p);
+    k_compact<false, false><<<grid, kCompactThreads, 0, st>>>(p);
 }
 
 }  // namespace
@@ -424,6 +493,7 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       s->counts.alloc(s->counts_words() * 4);
       s->desc.alloc(M * sizeof(WaveDesc));
       s->seed_stage.alloc(M * cfg->batch_size * 4);
+      VK_CUDA(cudaFuncSetAttribute(k_sample<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32 * 256 * 4));
       for (int k = 0; k < 2; ++k) {
         s->desc_host[k].ensure(M * sizeof(WaveDesc));
         s->seed_host[k].ensure(M * cfg->batch_size * 4);
@@ -517,7 +587,7 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
     for (std::uint32_t h = 1; h <= s->L; ++h) {
       const std::uint32_t f = s->cfg.fanouts[h - 1];
       if (f <= 32 || g.max_out_degree <= f)
-        launch_sample<32>(*s, h, nmb, st);
+        launch_sample<0>(*s, h, nmb, st);
       else if (f <= 128)
         launch_sample<128>(*s, h, nmb, st);
       else if (f <= 1024)
@@ -652,6 +722,18 @@ int vk_sampler_copy_relabel(vk_sampler s, uint32_t mb, uint32_t hop, uint32_t* a
     const std::uint64_t cnt = c[(std::uint64_t)hop * s->M + mb];
     VK_CUDA(cudaMemcpy(all_index, s->allidx[hop].as<std::uint32_t>() + mb * s->capF[hop], cnt * 4,
                        cudaMemcpyDeviceToHost));
+  });
+}
+
+int vk_debug_stream_draws(int device, uint64_t key, uint64_t bound, uint64_t count, uint64_t* out) {
+  return guard([&] {
+    if (!out) raise(VK_ERR_PARAMETER, "null argument");
+    DeviceGuard dg(device);
+    DevBuf d(std::max<std::uint64_t>(count, 1) * 8);
+    k_stream_draws<<<1, 32>>>(key, bound, count, d.as<std::uint64_t>());
+    count_launch();
+    VK_LAUNCH_CHECK();
+    VK_CUDA(cudaMemcpy(out, d.p, count * 8, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -131,6 +131,7 @@ def lib():
     L.vk_plane_row_bytes.argtypes = [c_vp, C.POINTER(c_u64)]
     L.vk_synth_community_powerlaw.argtypes = [c_u64, c_u64, c_u32, c_double, c_u64, C.c_uint,
                                               C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), u32p]
+    L.vk_debug_stream_draws.argtypes = [c_int, c_u64, c_u64, c_u64, u64p]
     L.vk_synth_roles.argtypes = [c_u64, c_double, c_double, c_double, c_u64, u8p]
     _lib = L
     return L
@@ -146,6 +147,13 @@ def device_count() -> int:
     c = c_int()
     check(lib().vk_device_count(C.byref(c)))
     return c.value
+
+
+def stream_draws(key, bound, count, device=0) -> np.ndarray:
+    """RngStream draws computed on the device (conformance testing)."""
+    out = np.zeros(count, np.uint64)
+    check(lib().vk_debug_stream_draws(device, key, bound, count, out))
+    return out
 
 
 def launch_count() -> int:

@@ -115,3 +115,15 @@ def test_expand_single_and_errors(vk, port, golden):
         s.run([[1, 999]], [(0, 0, 0)])
     with pytest.raises(vk.SamplingError):
         s.run([[1], []], [(0, 0, 0), (0, 0, 1)])
+
+
+def test_device_rng_matches_reference_draws(vk, golden, port):
+    """RngStream on the device (FP64-reciprocal modulo) == reference draws,
+    including bound 1, powers of two, 2^32, >= 2^40 (slow path) and 2^63."""
+    g = golden("rng.npz")
+    for i, b in enumerate(g["bounds"]):
+        np.testing.assert_array_equal(vk.stream_draws(12345 + i, int(b), 64), g["draws"][i])
+    rng = np.random.default_rng(0)
+    for b in list(rng.integers(2, 1 << 32, 200)) + [(1 << 40) - 1, 3, 7, 1 << 31, (1 << 32) - 5]:
+        key = int(rng.integers(0, 1 << 62))
+        np.testing.assert_array_equal(vk.stream_draws(key, int(b), 300), port.stream_draws(key, int(b), 300))
