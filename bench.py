@@ -71,56 +71,49 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """NVML sampler (5 ms period) running during the timed region: median SM
+    clock under load, max SM clock, and any throttle reasons seen."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device):
-        self.device = device
-        self.proc = None
-        self.lines = []
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(device)
+            self.max_sm = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self.samples, self.mask = [], 0
+        self._stop = threading.Event()
+
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                self.mask |= N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable: {self.err}"]}
+        self._stop.set()
+        self.t.join()
+        reasons = sorted(v for k, v in self.REASONS.items() if self.mask & k)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_sm, "reasons": reasons, "samples": len(self.samples)}
 
 
 def make_data(cfg, threads):
@@ -215,11 +208,13 @@ def run_b200(args, cfg):
     W, S = args.warmup, args.steps
     sched = schedule(vk, cfg, roles, labels, mine, (W + 2 * S) * M)
     waves = [sched[i * M:(i + 1) * M] for i in range(W + 2 * S)]
-    sampler = vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED)
-    view = sampler.view()
+    P = args.pipes
+    samplers = [vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED) for _ in range(P)]
+    view = samplers[0].view()
     cap_all = view.all_stride
     rb = plane.row_bytes
-    out = torch.empty(M * cap_all * rb, dtype=torch.uint8, device=f"cuda:{dev}")
+    outs = [torch.empty(M * cap_all * rb, dtype=torch.uint8, device=f"cuda:{dev}") for _ in range(P)]
+    streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(P - 1)]
     seeds_all = np.concatenate([w[3] for wv in waves for w in wv]).astype(np.uint32)
     seeds_d = torch.from_numpy(seeds_all.view(np.int32)).to(f"cuda:{dev}")
     wave_offsets, pos = [], 0
@@ -228,57 +223,61 @@ def run_b200(args, cfg):
         o[1:] = np.cumsum([len(w[3]) for w in wv])
         wave_offsets.append(o + pos)
         pos += int(o[-1])
-    cw = sampler.count_words()
+    cw = samplers[0].count_words()
     hist_counts = torch.zeros((W + 2 * S, cw), dtype=torch.int32, device=f"cuda:{dev}")
     hist_tally = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64, device=f"cuda:{dev}")
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(W + 2 * S)]
 
     def wave(i, host=False, pinned=None):
+        # wave i runs on pipe i % P: sampler and gather of consecutive waves
+        # overlap on separate streams (sampler is L2-latency bound, gather HBM bound)
+        p = i % P
+        st, sp = streams[p], samplers[p]
+        sh_p = st.cuda_stream
         wv = waves[i]
         refs = [(e, k, bi) for (e, k, bi, _) in wv]
+        evs[i][0].record(st)
         if host:
-            sampler.run([w[3] for w in wv], refs, stream=sh)
+            sp.run([w[3] for w in wv], refs, stream=sh_p)
         else:
-            sampler.run(wave_offsets[i], refs, stream=sh, seeds_device_ptr=seeds_d.data_ptr())
-        evs[i][1].record(stream)
-        plane.gather(sampler, out.data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh)
-        evs[i][2].record(stream)
-        sampler.snapshot_counts(hist_counts[i].data_ptr(), stream=sh)
+            sp.run(wave_offsets[i], refs, stream=sh_p, seeds_device_ptr=seeds_d.data_ptr())
+        evs[i][1].record(st)
+        plane.gather(sp, outs[p].data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh_p)
+        evs[i][2].record(st)
+        sp.snapshot_counts(hist_counts[i].data_ptr(), stream=sh_p)
         if pinned is not None:
-            pinned[i].copy_(hist_tally[i], non_blocking=True)
+            with torch.cuda.stream(st):
+                pinned[i].copy_(hist_tally[i], non_blocking=True)
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(W + 2 * S)]
-    with torch.cuda.stream(stream):
-        for i in range(W):
-            evs[i][0].record(stream)
-            wave(i)
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        clocks = Clocks(dev)
-        clocks.start()
-        l0 = vk.launch_count()
+    def region(lo, hi, host=False, pinned=None):
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for i in range(W, W + S):
-            evs[i][0].record(stream)
-            wave(i)
+        for st in streams[1:]:
+            st.wait_event(t0)
+        for i in range(lo, hi):
+            wave(i, host, pinned)
+        for st in streams[1:]:
+            e = torch.cuda.Event()
+            e.record(st)
+            stream.wait_event(e)
         t1.record(stream)
         torch.cuda.synchronize(dev)
-        launches = vk.launch_count() - l0
-        clk = clocks.stop()
-        # e2e: host seeds (H2D inside the region) + tallies read back to the host
-        pinned = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64).pin_memory()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(W + S, W + 2 * S):
-            evs[i][0].record(stream)
-            wave(i, host=True, pinned=pinned)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-    ms = t0.elapsed_time(t1)
-    e2e_ms = e0.elapsed_time(e1)
+        return t0.elapsed_time(t1)
+
+    region(0, W)
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(dev)
+    clocks.start()
+    l0 = vk.launch_count()
+    ms = region(W, W + S)
+    launches = vk.launch_count() - l0
+    clk = clocks.stop()
+    # e2e: host seeds (H2D inside the region) + tallies read back to the host
+    pinned = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64).pin_memory()
+    if world > 1:
+        dist.barrier()
+    e2e_ms = region(W + S, W + 2 * S, host=True, pinned=pinned)
     tl = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=f"cuda:{dev}")
     if world > 1:
         dist.all_reduce(tl, op=dist.ReduceOp.MAX)
@@ -314,7 +313,7 @@ def run_b200(args, cfg):
         "n_gpus": world, "steps": S, "warmup": W, "ms_per_step": ms / S, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 ids / fp32 rows / fp64 VIP",
         "data": "synthetic (community power-law graph, counter-hashed feature rows)",
-        "config": {"workload": cfg["workload"], "n": n, "m_slots": m, "partitions": K,
+        "config": {"workload": cfg["workload"], "n": n, "m_slots": m, "partitions": K, "pipes": P,
                    "fanouts": list(cfg["fanouts"]), "batch": cfg["b"], "minibatches_per_step_per_gpu": M,
                    "feature_dim": cfg["dim"], "row_bytes": rb, "alpha": cfg["alpha"],
                    "partitions_per_gpu": len(mine), "l2": "inputs larger than L2 (graph "
@@ -444,6 +443,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--wave", type=int, default=32, help="minibatches per step per GPU")
+    ap.add_argument("--pipes", type=int, default=2, help="overlapped sampler+gather pipelines (streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

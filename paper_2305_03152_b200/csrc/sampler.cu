@@ -211,11 +211,11 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
 }
 
 struct CompactParams {
-  const unsigned long long* bits;  // [M][W]
+  unsigned long long* bits;        // [M][W]; zeroed as it is consumed (clean for the next hop/wave)
   unsigned long long* allbits;     // hop compactions OR their words into the all bitmap
   std::uint32_t* list;             // [M][cap_list]
   std::uint64_t cap_list;
-  std::uint32_t* prefix;           // [M][W] rank prefix per word
+  uint4* rank;                     // [M][W] {bits lo, bits hi, rank prefix, 0} per word
   std::uint32_t* count;            // [M]
   // fused next-hop indptr (has_next)
   const std::uint32_t* outdeg;
@@ -247,9 +247,10 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const std::uint32_t mb = ticket / (unsigned)p.tiles;
   const std::uint32_t tile = ticket % (unsigned)p.tiles;
   if (mb >= p.nmb) return;
-  const unsigned long long* bits = p.bits + mb * p.W;
+  unsigned long long* bits = p.bits + mb * p.W;
   const std::uint64_t w = (std::uint64_t)tile * kTileWords + threadIdx.x;
   const unsigned long long wd = w < p.W ? bits[w] : 0ull;
+  if (wd) bits[w] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
   if (OR_ALL && wd) p.allbits[mb * p.W + w] |= wd;
   unsigned long long vc = __popcll(wd), dc = 0;
   if (HAS_NEXT) {
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const std::uint32_t tcount = (std::uint32_t)unpack_v(total);
   std::uint32_t* list = p.list + mb * p.cap_list;
   std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
-  if (w < p.W) p.prefix[mb * p.W + w] = gbase + lpos;
+  if (w < p.W) p.rank[mb * p.W + w] = make_uint4((unsigned)wd, (unsigned)(wd >> 32), gbase + lpos, 0u);
   const bool staged = tcount <= (std::uint32_t)kStage;
   unsigned long long x = wd;
   while (x) {
@@ -312,19 +313,19 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   }
 }
 
-__device__ __forceinline__ std::uint32_t bit_rank(const unsigned long long* __restrict__ bits,
-                                                  const std::uint32_t* __restrict__ prefix, std::uint32_t v) {
-  const std::uint32_t w = v >> 6;
-  return __ldg(prefix + w) + (std::uint32_t)__popcll(__ldg(bits + w) & ((1ull << (v & 63)) - 1ull));
+// Rank of v in the compacted list: one 16-byte load of {bits, prefix} (one
+// L2 sector per lookup instead of two).
+__device__ __forceinline__ std::uint32_t bit_rank(const uint4* __restrict__ rank, std::uint32_t v) {
+  const uint4 r = __ldg(rank + (v >> 6));
+  const unsigned long long bits = (unsigned long long)r.x | ((unsigned long long)r.y << 32);
+  return r.z + (std::uint32_t)__popcll(bits & ((1ull << (v & 63)) - 1ull));
 }
 
 // Rank lookups with kIlp independent elements in flight per thread.
 constexpr int kIlp = 4;
 
-template <class Src>
 __device__ __forceinline__ void rank_range(const std::uint32_t* __restrict__ in, std::uint32_t* __restrict__ out,
-                                           std::uint32_t cnt, const unsigned long long* __restrict__ b,
-                                           const std::uint32_t* __restrict__ pr) {
+                                           std::uint32_t cnt, const uint4* __restrict__ rk) {
   const std::uint32_t stride = gridDim.x * blockDim.x;
   for (std::uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < cnt; i0 += kIlp * stride) {
     std::uint32_t v[kIlp];
@@ -335,7 +336,7 @@ __device__ __forceinline__ void rank_range(const std::uint32_t* __restrict__ in,
     }
     std::uint32_t r[kIlp];
 #pragma unroll
-    for (int u = 0; u < kIlp; ++u) r[u] = bit_rank(b, pr, v[u]);
+    for (int u = 0; u < kIlp; ++u) r[u] = bit_rank(rk, v[u]);
 #pragma unroll
     for (int u = 0; u < kIlp; ++u) {
       const std::uint32_t i = i0 + u * stride;
@@ -347,11 +348,10 @@ __device__ __forceinline__ void rank_range(const std::uint32_t* __restrict__ in,
 // MFG dst: rank of every drawn id in F_h.
 __global__ void __launch_bounds__(256) k_relabel(const std::uint32_t* __restrict__ edges, std::uint64_t in_stride,
                                                  const std::uint32_t* __restrict__ ecount,
-                                                 const unsigned long long* __restrict__ bits,
-                                                 const std::uint32_t* __restrict__ prefix, std::uint64_t W,
+                                                 const uint4* __restrict__ rank, std::uint64_t W,
                                                  std::uint32_t* __restrict__ dst, std::uint64_t out_stride) {
   const std::uint32_t mb = blockIdx.y;
-  rank_range<int>(edges + mb * in_stride, dst + mb * out_stride, ecount[mb], bits + mb * W, prefix + mb * W);
+  rank_range(edges + mb * in_stride, dst + mb * out_stride, ecount[mb], rank + mb * W);
 }
 
 struct AllIdxParams {
@@ -362,11 +362,9 @@ struct AllIdxParams {
 };
 
 // Relabel map: position of every F_h vertex (h = 0..L) in all_vertices.
-__global__ void __launch_bounds__(256) k_allidx(AllIdxParams p, const unsigned long long* __restrict__ bits,
-                                                const std::uint32_t* __restrict__ prefix, std::uint64_t W) {
+__global__ void __launch_bounds__(256) k_allidx(AllIdxParams p, const uint4* __restrict__ rank, std::uint64_t W) {
   const std::uint32_t mb = blockIdx.y, h = blockIdx.z;
-  rank_range<int>(p.F[h] + mb * p.cap[h], p.idx[h] + mb * p.cap[h], p.count[h][mb], bits + mb * W,
-                  prefix + mb * W);
+  rank_range(p.F[h] + mb * p.cap[h], p.idx[h] + mb * p.cap[h], p.count[h][mb], rank + mb * W);
 }
 
 __global__ void k_stream_draws(std::uint64_t key, std::uint64_t bound, std::uint64_t count,
@@ -395,7 +393,9 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
   p.hopbits = s.hopbits.as<unsigned long long>();
   p.W = s.W;
   const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, 256), 4096);
-  const std::size_t smem = MAXF == 0 ? (std::size_t)3 * p.f * 256 * 4 : 0;
+  // shared FY state only when some vertex can out-degree the fanout
+  const bool fy = g.max_out_degree > p.f;
+  const std::size_t smem = (MAXF == 0 && fy) ? (std::size_t)3 * p.f * 256 * 4 : 0;
   k_sample<MAXF><<<dim3(gx, nmb), 256, smem, st>>>(p);
 }
 
@@ -406,7 +406,7 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   p.allbits = s.allbits.as<unsigned long long>();
   p.list = hop ? s.F[h].as<std::uint32_t>() : s.all.as<std::uint32_t>();
   p.cap_list = hop ? s.capF[h] : s.capAll;
-  p.prefix = (hop ? s.hopprefix : s.allprefix).as<std::uint32_t>();
+  p.rank = (hop ? s.hopprefix : s.allprefix).as<uint4>();
   p.count = hop ? s.fcount(h) : s.allcount();
   const bool has_next = hop && h < s.L;
   p.outdeg = s.g->out_deg.as<std::uint32_t>();
@@ -486,8 +486,8 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       s->all.alloc(M * s->capAll * 4);
       s->hopbits.alloc(M * s->W * 8);
       s->allbits.alloc(M * s->W * 8);
-      s->hopprefix.alloc(M * s->W * 4);
-      s->allprefix.alloc(M * s->W * 4);
+      s->hopprefix.alloc(M * s->W * 16);  // RankWord {bits, prefix} per word
+      s->allprefix.alloc(M * s->W * 16);
       s->status.alloc((std::uint64_t)(L + 1) * M * s->tiles * 8);
       s->tickets.alloc((L + 1) * 4);
       s->counts.alloc(s->counts_words() * 4);
@@ -601,12 +601,10 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
       VK_LAUNCH_CHECK();
       const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(s->capS[h], 256), 4096);
       k_relabel<<<dim3(gx, nmb), 256, 0, st>>>(s->edges_tmp.as<std::uint32_t>(), s->capS_max, s->ecount(h),
-                                               s->hopbits.as<unsigned long long>(),
-                                               s->hopprefix.as<std::uint32_t>(), s->W,
-                                               s->dst[h].as<std::uint32_t>(), s->capS[h]);
+                                               s->hopprefix.as<uint4>(), s->W, s->dst[h].as<std::uint32_t>(),
+                                               s->capS[h]);
       count_launch();
       VK_LAUNCH_CHECK();
-      VK_CUDA(cudaMemsetAsync(s->hopbits.p, 0, (std::uint64_t)nmb * s->W * 8, st));
     }
     run_compact(*s, false, 0, nmb, s->L, st);
     count_launch();
@@ -621,11 +619,9 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
       capmax = std::max(capmax, s->capF[h]);
     }
     const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(capmax, 256), 1024);
-    k_allidx<<<dim3(gx, nmb, s->L + 1), 256, 0, st>>>(ap, s->allbits.as<unsigned long long>(),
-                                                       s->allprefix.as<std::uint32_t>(), s->W);
+    k_allidx<<<dim3(gx, nmb, s->L + 1), 256, 0, st>>>(ap, s->allprefix.as<uint4>(), s->W);
     count_launch();
     VK_LAUNCH_CHECK();
-    VK_CUDA(cudaMemsetAsync(s->allbits.p, 0, (std::uint64_t)nmb * s->W * 8, st));
     VK_CUDA(cudaEventRecord(s->done, st));
     s->last_nmb = nmb;
     s->last_stream = st;
