@@ -443,7 +443,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--wave", type=int, default=32, help="minibatches per step per GPU")
-    ap.add_argument("--pipes", type=int, default=2, help="overlapped sampler+gather pipelines (streams)")
+    ap.add_argument("--pipes", type=int, default=1, help="overlapped sampler+gather pipelines (streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -199,9 +200,8 @@ __device__ __forceinline__ void st_stream(T* p, const T& v) {
 // owner partition's row, local HBM or a peer GPU over NVLink), then the warp
 // copies the group as one flat, fully coalesced range of 32*V vectors with
 // kUnroll independent loads in flight per lane.
-template <class T>
-__global__ void __launch_bounds__(256) k_gather(GatherParams p) {
-  constexpr int kUnroll = 8;
+template <class T, int kUnroll, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   __shared__ const T* s_src[8][32];
   const std::uint32_t mb = blockIdx.y;
   const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
@@ -615,16 +615,29 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     if (gp.V >= (1u << 15)) raise(VK_ERR_UNSUPPORTED, "feature rows above 512 KiB are not supported");
     gp.magic32 = gp.V == 1 ? 0u : (std::uint32_t)((0xffffffffull / gp.V) + 1);  // ceil(2^32 / V)
     // enough warps in flight to saturate HBM: ~16 resident warps per SM
-    const std::uint64_t want = (std::uint64_t)sm_count(p->device) * 8;  // CTAs of 8 warps
+    const std::uint64_t want = (std::uint64_t)sm_count(p->device) * 8;  // CTAs of 8 warps (grid-stride)
     const unsigned gx = (unsigned)std::max<std::uint64_t>(
         1, std::min<std::uint64_t>((want + nmb - 1) / nmb, ceil_div(gp.all_stride, 256)));
     dim3 grid(gx, nmb);
-    if (v16)
-      k_gather<uint4><<<grid, 256, 0, st>>>(gp);
-    else if (v4)
-      k_gather<std::uint32_t><<<grid, 256, 0, st>>>(gp);
-    else
-      k_gather<std::uint16_t><<<grid, 256, 0, st>>>(gp);
+    // tuning knob (VK_GATHER_VARIANT): unroll depth vs occupancy
+    static const int variant = [] {
+      const char* e = std::getenv("VK_GATHER_VARIANT");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (v16) {
+      if (variant == 1)
+        k_gather<uint4, 4, 8><<<grid, 256, 0, st>>>(gp);
+      else if (variant == 2)
+        k_gather<uint4, 16, 2><<<grid, 256, 0, st>>>(gp);
+      else if (variant == 3)
+        k_gather<uint4, 8, 6><<<grid, 256, 0, st>>>(gp);
+      else
+        k_gather<uint4, 8, 4><<<grid, 256, 0, st>>>(gp);
+    } else if (v4) {
+      k_gather<std::uint32_t, 8, 1><<<grid, 256, 0, st>>>(gp);
+    } else {
+      k_gather<std::uint16_t, 8, 1><<<grid, 256, 0, st>>>(gp);
+    }
     count_launch();
     VK_LAUNCH_CHECK();
   });

@@ -186,9 +186,112 @@ struct SampleParams {
 
 // One thread per frontier vertex; FY state in shared memory (f <= 32) or in
 // local memory (MAXF > 0, large fanouts).
+constexpr int kSampleThreads = 128;
+
+// Shared-memory sampler (every fanout <= 32). Per thread, in slot-major
+// shared arrays (thread t's slot i at i*kSampleThreads + t, conflict free):
+//   lo[f] values at positions [0, f), hp/hv[f] the displaced-position map,
+//   jj[f] the draw targets, pv[f] the prefetched CSR values at jj.
+// The f draws depend only on the counter stream, so all of them are drawn
+// first and their neighbour loads issued in groups of 4 independent loads
+// (memory-level parallelism instead of one dependent load per draw); the
+// Fisher-Yates swaps are then replayed in order on shared memory. Outputs of a
+// warp's 32 consecutive sources are contiguous in the MFG edge array, so they
+// are staged per warp and written back with coalesced stores.
+__global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) {
+  extern __shared__ std::uint32_t sm_fy[];
+  constexpr unsigned S = kSampleThreads;
+  const unsigned f = p.f;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  std::uint32_t* lo = sm_fy + threadIdx.x;
+  std::uint32_t* hp = lo + f * S;
+  std::uint32_t* hv = hp + f * S;
+  std::uint32_t* jj = hv + f * S;
+  std::uint32_t* pv = jj + f * S;
+  std::uint32_t* stage = sm_fy + 5 * f * S + warp * 32 * f;
+  const std::uint32_t mb = blockIdx.y;
+  const std::uint32_t cnt = p.fcount_prev[mb];
+  const std::uint64_t prefix = p.desc[mb].key_prefix[p.h - 1];
+  const std::uint32_t* fp = p.Fprev + mb * p.capFprev;
+  const std::uint32_t* ip = p.indptr + mb * (p.capFprev + 1);
+  std::uint32_t* ed = p.edges + mb * p.capS;
+  unsigned long long* hb = p.hopbits + mb * p.W;
+  for (std::uint32_t j0 = (blockIdx.x * (S / 32) + warp) * 32; j0 < cnt; j0 += gridDim.x * S) {
+    const std::uint32_t j = j0 + lane;
+    const std::uint32_t base = ip[j0];
+    if (j < cnt) {
+      const std::uint32_t v = fp[j];
+      const std::uint32_t deg = p.outdeg[v];
+      const std::uint32_t* nbrs = p.tgt + p.off[v];
+      std::uint32_t* out = stage + (ip[j] - base);
+      if (deg <= f) {  // sampling.cpp:76-78: all neighbours, CSR order
+        for (std::uint32_t i0 = 0; i0 < deg; i0 += 4) {
+          std::uint32_t t[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) t[u] = i0 + u < deg ? __ldg(nbrs + i0 + u) : 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i0 + u < deg) {
+              out[i0 + u] = t[u];
+              atomicOr(hb + (t[u] >> 6), 1ull << (t[u] & 63));
+            }
+        }
+      } else {
+        Stream s(key_step(prefix, v));
+        for (std::uint32_t i = 0; i < f; ++i) jj[i * S] = i + (std::uint32_t)s.next_below((std::uint64_t)(deg - i));
+        for (std::uint32_t i0 = 0; i0 < f; i0 += 4) {
+          std::uint32_t a[4], b[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const std::uint32_t i = i0 + u;
+            const std::uint32_t ji = i < f ? jj[i * S] : 0u;
+            a[u] = i < f ? __ldg(nbrs + i) : 0u;
+            b[u] = (i < f && ji >= f) ? __ldg(nbrs + ji) : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i0 + u < f) {
+              lo[(i0 + u) * S] = a[u];
+              pv[(i0 + u) * S] = b[u];
+            }
+        }
+        std::uint32_t nh = 0;
+        for (std::uint32_t i = 0; i < f; ++i) {
+          const std::uint32_t ji = jj[i * S];
+          const std::uint32_t vi = lo[i * S];
+          std::uint32_t vj;
+          if (ji < f) {
+            vj = lo[ji * S];
+            lo[ji * S] = vi;
+          } else {
+            std::uint32_t c = 0;
+            while (c < nh && hp[c * S] != ji) ++c;
+            if (c < nh) {
+              vj = hv[c * S];
+              hv[c * S] = vi;
+            } else {
+              vj = pv[i * S];  // untouched position: the original CSR value
+              hp[nh * S] = ji;
+              hv[nh * S] = vi;
+              ++nh;
+            }
+          }
+          out[i] = vj;  // scratch[i] after the swap (sampling.cpp:87-91)
+          atomicOr(hb + (vj >> 6), 1ull << (vj & 63));
+        }
+      }
+    }
+    __syncwarp();
+    const std::uint32_t last = min(j0 + 32u, cnt);
+    const std::uint32_t total = ip[last] - base;
+    for (std::uint32_t i = lane; i < total; i += 32) ed[base + i] = stage[i];
+    __syncwarp();
+  }
+}
+
+// Local-memory fallback for fanouts > 32 (per-thread arrays, direct stores).
 template <int MAXF>
 __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
-  extern __shared__ std::uint32_t sm_fy[];
   const std::uint32_t mb = blockIdx.y;
   const std::uint32_t cnt = p.fcount_prev[mb];
   const std::uint64_t prefix = p.desc[mb].key_prefix[p.h - 1];
@@ -199,14 +302,8 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
   for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x) {
     const std::uint32_t v = fp[j];
     Stream s(key_step(prefix, v));
-    if constexpr (MAXF == 0) {
-      const unsigned S = blockDim.x;
-      std::uint32_t* lo = sm_fy + threadIdx.x;
-      sample_one(p.tgt + p.off[v], p.outdeg[v], p.f, s, ed + ip[j], hb, lo, lo + p.f * S, lo + 2 * p.f * S, S);
-    } else {
-      std::uint32_t lo[MAXF], hp[MAXF], hv[MAXF];
-      sample_one(p.tgt + p.off[v], p.outdeg[v], p.f, s, ed + ip[j], hb, lo, hp, hv, 1);
-    }
+    std::uint32_t lo[MAXF], hp[MAXF], hv[MAXF];
+    sample_one(p.tgt + p.off[v], p.outdeg[v], p.f, s, ed + ip[j], hb, lo, hp, hv, 1);
   }
 }
 
@@ -354,17 +451,12 @@ __global__ void __launch_bounds__(256) k_relabel(const std::uint32_t* __restrict
   rank_range(edges + mb * in_stride, dst + mb * out_stride, ecount[mb], rank + mb * W);
 }
 
-struct AllIdxParams {
-  const std::uint32_t* F[VK_MAX_HOPS + 1];
-  std::uint32_t* idx[VK_MAX_HOPS + 1];
-  std::uint64_t cap[VK_MAX_HOPS + 1];
-  const std::uint32_t* count[VK_MAX_HOPS + 1];
-};
-
-// Relabel map: position of every F_h vertex (h = 0..L) in all_vertices.
-__global__ void __launch_bounds__(256) k_allidx(AllIdxParams p, const uint4* __restrict__ rank, std::uint64_t W) {
-  const std::uint32_t mb = blockIdx.y, h = blockIdx.z;
-  rank_range(p.F[h] + mb * p.cap[h], p.idx[h] + mb * p.cap[h], p.count[h][mb], rank + mb * W);
+// Relabel map: position of every F_h vertex in all_vertices.
+__global__ void __launch_bounds__(256) k_allidx(const std::uint32_t* __restrict__ F, std::uint32_t* __restrict__ idx,
+                                                std::uint64_t cap, const std::uint32_t* __restrict__ count,
+                                                const uint4* __restrict__ rank, std::uint64_t W) {
+  const std::uint32_t mb = blockIdx.y;
+  rank_range(F + mb * cap, idx + mb * cap, count[mb], rank + mb * W);
 }
 
 __global__ void k_stream_draws(std::uint64_t key, std::uint64_t bound, std::uint64_t count,
@@ -392,11 +484,15 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
   p.capS = s.capS_max;
   p.hopbits = s.hopbits.as<unsigned long long>();
   p.W = s.W;
-  const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, 256), 4096);
-  // shared FY state only when some vertex can out-degree the fanout
-  const bool fy = g.max_out_degree > p.f;
-  const std::size_t smem = (MAXF == 0 && fy) ? (std::size_t)3 * p.f * 256 * 4 : 0;
-  k_sample<MAXF><<<dim3(gx, nmb), 256, smem, st>>>(p);
+  if (MAXF == 0) {
+    // 5 FY slots per thread + a 32*f staging row per warp
+    const std::size_t smem = (std::size_t)(5 * kSampleThreads + kSampleThreads) * p.f * 4;
+    const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, kSampleThreads), 8192);
+    k_sample_smem<<<dim3(gx, nmb), kSampleThreads, smem, st>>>(p);
+  } else {
+    const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, 256), 4096);
+    k_sample<MAXF><<<dim3(gx, nmb), 256, 0, st>>>(p);
+  }
 }
 
 void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, std::uint32_t slot,
@@ -493,7 +589,8 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       s->counts.alloc(s->counts_words() * 4);
       s->desc.alloc(M * sizeof(WaveDesc));
       s->seed_stage.alloc(M * cfg->batch_size * 4);
-      VK_CUDA(cudaFuncSetAttribute(k_sample<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32 * 256 * 4));
+      VK_CUDA(cudaFuncSetAttribute(k_sample_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   6 * 32 * kSampleThreads * 4));
       for (int k = 0; k < 2; ++k) {
         s->desc_host[k].ensure(M * sizeof(WaveDesc));
         s->seed_host[k].ensure(M * cfg->batch_size * 4);
@@ -586,9 +683,9 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
     VK_LAUNCH_CHECK();
     for (std::uint32_t h = 1; h <= s->L; ++h) {
       const std::uint32_t f = s->cfg.fanouts[h - 1];
-      if (f <= 32 || g.max_out_degree <= f)
+      if (f <= 32)
         launch_sample<0>(*s, h, nmb, st);
-      else if (f <= 128)
+      else if (g.max_out_degree <= f || f <= 128)
         launch_sample<128>(*s, h, nmb, st);
       else if (f <= 1024)
         launch_sample<1024>(*s, h, nmb, st);
@@ -599,7 +696,7 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
       run_compact(*s, true, h, nmb, h - 1, st);
       count_launch();
       VK_LAUNCH_CHECK();
-      const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(s->capS[h], 256), 4096);
+      const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(s->capS[h], 256 * kIlp), 4096);
       k_relabel<<<dim3(gx, nmb), 256, 0, st>>>(s->edges_tmp.as<std::uint32_t>(), s->capS_max, s->ecount(h),
                                                s->hopprefix.as<uint4>(), s->W, s->dst[h].as<std::uint32_t>(),
                                                s->capS[h]);
@@ -609,17 +706,13 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
     run_compact(*s, false, 0, nmb, s->L, st);
     count_launch();
     VK_LAUNCH_CHECK();
-    AllIdxParams ap{};
-    std::uint64_t capmax = 0;
+    // relabel map per hop (grids sized by each hop's capacity)
     for (std::uint32_t h = 0; h <= s->L; ++h) {
-      ap.F[h] = s->F[h].as<std::uint32_t>();
-      ap.idx[h] = s->allidx[h].as<std::uint32_t>();
-      ap.cap[h] = s->capF[h];
-      ap.count[h] = s->fcount(h);
-      capmax = std::max(capmax, s->capF[h]);
+      const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(s->capF[h], 256 * kIlp), 4096);
+      k_allidx<<<dim3(gx, nmb), 256, 0, st>>>(s->F[h].as<std::uint32_t>(), s->allidx[h].as<std::uint32_t>(),
+                                              s->capF[h], s->fcount(h), s->allprefix.as<uint4>(), s->W);
+      count_launch();
     }
-    const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(capmax, 256), 1024);
-    k_allidx<<<dim3(gx, nmb, s->L + 1), 256, 0, st>>>(ap, s->allprefix.as<uint4>(), s->W);
     count_launch();
     VK_LAUNCH_CHECK();
     VK_CUDA(cudaEventRecord(s->done, st));
