@@ -484,7 +484,7 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
   p.capS = s.capS_max;
   p.hopbits = s.hopbits.as<unsigned long long>();
   p.W = s.W;
-  if (MAXF == 0) {
+  if constexpr (MAXF == 0) {
     // 5 FY slots per thread + a 32*f staging row per warp
     const std::size_t smem = (std::size_t)(5 * kSampleThreads + kSampleThreads) * p.f * 4;
     const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, kSampleThreads), 8192);
