@@ -30,6 +30,7 @@ void sampler_internal(vk_sampler_s* s, const std::uint32_t** all, std::uint64_t*
                       const std::uint32_t** all_count, std::uint32_t* nmb, const std::uint32_t** partitions,
                       vk_graph_s** g, cudaStream_t* last_stream);
 std::uint64_t sampler_desc_stride();
+void sampler_all_rank(vk_sampler_s* s, const uint4** rank, std::uint64_t* W);
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out);
 cudaEvent_t sampler_done_event(vk_sampler_s* s);
 }  // namespace vk
@@ -151,6 +152,7 @@ __global__ void k_fill_slots(const std::uint32_t* __restrict__ ids, std::uint64_
 }
 
 // ---- classify + gather ----
+constexpr std::uint32_t kGatherTileWords = 64;  // 4096 vertices per (tile, minibatch) CTA
 struct GatherParams {
   const std::uint32_t* all;
   std::uint64_t all_stride;
@@ -169,6 +171,10 @@ struct GatherParams {
   std::uint32_t V;                   // vector elements per row
   std::uint32_t magic32;             // ceil(2^32 / V): row = umulhi(e, magic32) for e < 32*V
   unsigned long long* counts;        // [nmb][4]
+  // vertex-tile schedule: CTA b serves minibatch b % nmb, vertex tile b / nmb
+  const uint4* all_rank;             // [nmb][W] {bits, rank prefix} of all_vertices
+  std::uint64_t W;
+  std::uint32_t nmb, tiles, tile_words;
 };
 
 // Streaming 16/4/2-byte copies: the feature table is read through L1
@@ -203,9 +209,19 @@ __device__ __forceinline__ void st_stream(T* p, const T& v) {
 template <class T, int kUnroll, int kMinBlocks>
 __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   __shared__ const T* s_src[8][32];
-  const std::uint32_t mb = blockIdx.y;
+  // Vertex-tile-major schedule, minibatch fastest: the CTAs resident at any
+  // moment serve the same vertex range for every minibatch of the wave, so a
+  // feature row needed by several minibatches is read from HBM once and hit
+  // in L2 by the others (all_vertices is sorted: a vertex range is a
+  // contiguous run of output rows).
+  const std::uint32_t mb = blockIdx.x % p.nmb;
+  const std::uint32_t tile = blockIdx.x / p.nmb;
   const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
   const std::uint32_t cnt = p.all_count[mb];
+  const uint4* rk = p.all_rank + mb * p.W;
+  const std::uint64_t w0 = (std::uint64_t)tile * p.tile_words, w1 = w0 + p.tile_words;
+  const std::uint32_t lo = w0 < p.W ? rk[w0].z : cnt;
+  const std::uint32_t hi = w1 < p.W ? rk[w1].z : cnt;
   const std::uint32_t* all = p.all + mb * p.all_stride;
   const std::uint32_t* slot = p.slot[k];
   const std::uint32_t nl = p.nlocal[k];
@@ -215,13 +231,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   const std::uint32_t magic = p.magic32;
   const std::uint64_t rowv = p.row_bytes / sizeof(T);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const std::uint32_t gw = blockIdx.x * (blockDim.x >> 5) + w;
-  const std::uint32_t nw = gridDim.x * (blockDim.x >> 5);
   unsigned c_local = 0, c_cache = 0, c_miss = 0, c_peer = 0;
-  for (std::uint32_t r0 = gw * 32; r0 < cnt; r0 += nw * 32) {
+  for (std::uint32_t r0 = lo + w * 32; r0 < hi; r0 += (blockDim.x >> 5) * 32) {
     const std::uint32_t r = r0 + lane;
     const T* src = nullptr;
-    if (r < cnt) {
+    if (r < hi) {
       const std::uint32_t v = __ldg(all + r);
       const std::uint32_t s = __ldg(slot + v);
       if (s != VK_MISS) {
@@ -236,7 +250,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
     }
     s_src[w][lane] = src;
     __syncwarp();
-    const std::uint32_t rows = min(32u, cnt - r0);
+    const std::uint32_t rows = min(32u, hi - r0);
     const std::uint32_t total = rows * V;
     T* dst = out + (std::uint64_t)r0 * V;
     for (std::uint32_t e0 = lane; e0 < total; e0 += 32 * kUnroll) {
@@ -614,11 +628,11 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     gp.V = (std::uint32_t)(p->row_bytes / esz);
     if (gp.V >= (1u << 15)) raise(VK_ERR_UNSUPPORTED, "feature rows above 512 KiB are not supported");
     gp.magic32 = gp.V == 1 ? 0u : (std::uint32_t)((0xffffffffull / gp.V) + 1);  // ceil(2^32 / V)
-    // enough warps in flight to saturate HBM: ~16 resident warps per SM
-    const std::uint64_t want = (std::uint64_t)sm_count(p->device) * 8;  // CTAs of 8 warps (grid-stride)
-    const unsigned gx = (unsigned)std::max<std::uint64_t>(
-        1, std::min<std::uint64_t>((want + nmb - 1) / nmb, ceil_div(gp.all_stride, 256)));
-    dim3 grid(gx, nmb);
+    sampler_all_rank(s, &gp.all_rank, &gp.W);
+    gp.nmb = nmb;
+    gp.tile_words = kGatherTileWords;
+    gp.tiles = (std::uint32_t)((gp.W + kGatherTileWords - 1) / kGatherTileWords);
+    dim3 grid((unsigned)((std::uint64_t)gp.tiles * nmb));
     // tuning knob (VK_GATHER_VARIANT): unroll depth vs occupancy
     static const int variant = [] {
       const char* e = std::getenv("VK_GATHER_VARIANT");

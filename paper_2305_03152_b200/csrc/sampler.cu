@@ -182,11 +182,18 @@ struct SampleParams {
   std::uint64_t capS;
   unsigned long long* hopbits;
   std::uint64_t W;
+  // vertex-tile schedule (hops >= 2, sources sorted): CTA b serves minibatch
+  // b % nmb and the sources inside vertex tile b / nmb, found from the
+  // previous hop's rank words; minibatch-fastest order makes the CSR rows of a
+  // vertex range L2-resident for every minibatch that samples from them.
+  const uint4* rank_prev;
+  std::uint32_t nmb, tile_words;
 };
 
 // One thread per frontier vertex; FY state in shared memory (f <= 32) or in
 // local memory (MAXF > 0, large fanouts).
 constexpr int kSampleThreads = 128;
+constexpr std::uint32_t kSampleTileWords = 64;  // 4096 source vertices per (tile, minibatch) CTA
 
 // Shared-memory sampler (every fanout <= 32). Per thread, in slot-major
 // shared arrays (thread t's slot i at i*kSampleThreads + t, conflict free):
@@ -209,14 +216,30 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
   std::uint32_t* jj = hv + f * S;
   std::uint32_t* pv = jj + f * S;
   std::uint32_t* stage = sm_fy + 5 * f * S + warp * 32 * f;
-  const std::uint32_t mb = blockIdx.y;
-  const std::uint32_t cnt = p.fcount_prev[mb];
+  std::uint32_t mb, hi, jstart, jstride;
+  if (p.rank_prev) {
+    mb = blockIdx.x % p.nmb;
+    const std::uint32_t tile = blockIdx.x / p.nmb;
+    const std::uint32_t cnt = p.fcount_prev[mb];
+    const uint4* rk = p.rank_prev + mb * p.W;
+    const std::uint64_t w0 = (std::uint64_t)tile * p.tile_words, w1 = w0 + p.tile_words;
+    const std::uint32_t first = w0 < p.W ? rk[w0].z : cnt;
+    hi = w1 < p.W ? rk[w1].z : cnt;
+    jstart = first + warp * 32;
+    jstride = S;
+  } else {
+    mb = blockIdx.y;
+    hi = p.fcount_prev[mb];
+    jstart = (blockIdx.x * (S / 32) + warp) * 32;
+    jstride = gridDim.x * S;
+  }
+  const std::uint32_t cnt = hi;
   const std::uint64_t prefix = p.desc[mb].key_prefix[p.h - 1];
   const std::uint32_t* fp = p.Fprev + mb * p.capFprev;
   const std::uint32_t* ip = p.indptr + mb * (p.capFprev + 1);
   std::uint32_t* ed = p.edges + mb * p.capS;
   unsigned long long* hb = p.hopbits + mb * p.W;
-  for (std::uint32_t j0 = (blockIdx.x * (S / 32) + warp) * 32; j0 < cnt; j0 += gridDim.x * S) {
+  for (std::uint32_t j0 = jstart; j0 < cnt; j0 += jstride) {
     const std::uint32_t j = j0 + lane;
     const std::uint32_t base = ip[j0];
     if (j < cnt) {
@@ -487,8 +510,17 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
   if constexpr (MAXF == 0) {
     // 5 FY slots per thread + a 32*f staging row per warp
     const std::size_t smem = (std::size_t)(5 * kSampleThreads + kSampleThreads) * p.f * 4;
-    const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, kSampleThreads), 8192);
-    k_sample_smem<<<dim3(gx, nmb), kSampleThreads, smem, st>>>(p);
+    p.nmb = nmb;
+    p.tile_words = kSampleTileWords;
+    if (h >= 2) {
+      p.rank_prev = s.hopprefix.as<uint4>();
+      const std::uint64_t tiles = (s.W + kSampleTileWords - 1) / kSampleTileWords;
+      k_sample_smem<<<(unsigned)(tiles * nmb), kSampleThreads, smem, st>>>(p);
+    } else {
+      p.rank_prev = nullptr;
+      const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, kSampleThreads), 8192);
+      k_sample_smem<<<dim3(gx, nmb), kSampleThreads, smem, st>>>(p);
+    }
   } else {
     const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, 256), 4096);
     k_sample<MAXF><<<dim3(gx, nmb), 256, 0, st>>>(p);
@@ -877,6 +909,10 @@ void sampler_internal(vk_sampler_s* s, const std::uint32_t** all, std::uint64_t*
   *last_stream = s->last_stream;
 }
 std::uint64_t sampler_desc_stride() { return sizeof(WaveDesc); }
+void sampler_all_rank(vk_sampler_s* s, const uint4** rank, std::uint64_t* W) {
+  *rank = s->allprefix.as<uint4>();
+  *W = s->W;
+}
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out) { out = s->last_parts; }
 cudaEvent_t sampler_done_event(vk_sampler_s* s) { return s->done; }
 std::uint64_t sampler_capacity_all(vk_sampler_s* s) { return s->capAll; }
