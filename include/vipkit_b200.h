@@ -69,6 +69,7 @@ VK_API int vk_version(void);
 VK_API int vk_device_count(int* count);
 VK_API int vk_device_alloc(int device, size_t bytes, void** out);
 VK_API int vk_device_free(void* p);
+/* Synchronous copy after draining all device work (plumbing for ctypes callers). */
 VK_API int vk_memcpy(void* dst, const void* src, size_t bytes, int kind /*cudaMemcpyKind*/);
 VK_API int vk_stream_sync(vk_stream_t stream);
 /* Number of this library's kernels launched by the calling process so far

@@ -101,7 +101,12 @@ int vk_device_free(void* p) {
 }
 
 int vk_memcpy(void* dst, const void* src, size_t bytes, int kind) {
-  return guard([&] { VK_CUDA(cudaMemcpy(dst, src, bytes, static_cast<cudaMemcpyKind>(kind))); });
+  return guard([&] {
+    // the library works on non-blocking streams, which a legacy-stream
+    // cudaMemcpy does not order against: drain the device first
+    VK_CUDA(cudaDeviceSynchronize());
+    VK_CUDA(cudaMemcpy(dst, src, bytes, static_cast<cudaMemcpyKind>(kind)));
+  });
 }
 
 int vk_stream_sync(vk_stream_t stream) {

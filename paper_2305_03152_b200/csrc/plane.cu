@@ -630,8 +630,12 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     gp.magic32 = gp.V == 1 ? 0u : (std::uint32_t)((0xffffffffull / gp.V) + 1);  // ceil(2^32 / V)
     sampler_all_rank(s, &gp.all_rank, &gp.W);
     gp.nmb = nmb;
-    gp.tile_words = kGatherTileWords;
-    gp.tiles = (std::uint32_t)((gp.W + kGatherTileWords - 1) / kGatherTileWords);
+    static const std::uint32_t tile_words = [] {
+      const char* e = std::getenv("VK_GATHER_TILE_WORDS");
+      return e ? (std::uint32_t)std::atoi(e) : kGatherTileWords;
+    }();
+    gp.tile_words = tile_words;
+    gp.tiles = (std::uint32_t)((gp.W + tile_words - 1) / tile_words);
     dim3 grid((unsigned)((std::uint64_t)gp.tiles * nmb));
     // tuning knob (VK_GATHER_VARIANT): unroll depth vs occupancy
     static const int variant = [] {
