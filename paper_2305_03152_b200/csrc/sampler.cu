@@ -384,7 +384,10 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const unsigned long long mine = pack_vd(vc, dc);
   unsigned long long total;
   const unsigned long long inc = block_inclusive_scan<kCompactThreads>(mine, s_sm, &total);
-  if (threadIdx.x == 0) s_excl = lookback(p.status + mb * p.tiles, tile, total);
+  if (threadIdx.x < 32) {
+    const unsigned long long ex = lookback_warp(p.status + mb * p.tiles, tile, total);
+    if (threadIdx.x == 0) s_excl = ex;
+  }
   __syncthreads();
   const unsigned long long base = s_excl;
   const unsigned long long lex = inc - mine;  // tile-local exclusive prefix
@@ -514,7 +517,12 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
     p.tile_words = kSampleTileWords;
     if (h >= 2) {
       p.rank_prev = s.hopprefix.as<uint4>();
-      const std::uint64_t tiles = (s.W + kSampleTileWords - 1) / kSampleTileWords;
+      // ~512 sources per (tile, minibatch) CTA at full frontier capacity,
+      // at least kSampleTileWords words (4096 vertices) per tile
+      const std::uint64_t want_tiles = std::max<std::uint64_t>(1, p.capFprev / 512);
+      const std::uint64_t tw = std::max<std::uint64_t>(kSampleTileWords, (s.W + want_tiles - 1) / want_tiles);
+      p.tile_words = (std::uint32_t)tw;
+      const std::uint64_t tiles = (s.W + tw - 1) / tw;
       k_sample_smem<<<(unsigned)(tiles * nmb), kSampleThreads, smem, st>>>(p);
     } else {
       p.rank_prev = nullptr;

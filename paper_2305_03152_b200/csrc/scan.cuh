@@ -57,27 +57,48 @@ __device__ __forceinline__ unsigned long long peek(const unsigned long long* st)
   return v;
 }
 
-// Thread 0 only: publish this tile's aggregate, walk predecessors, publish
-// the inclusive prefix, return the exclusive prefix (packed v|d).
-__device__ __forceinline__ unsigned long long lookback(unsigned long long* status, unsigned tile,
-                                                       unsigned long long aggregate) {
+// Warp 0 only (all 32 lanes): publish this tile's aggregate, then look back
+// over a window of 32 predecessors at a time: the nearest inclusive prefix in
+// the window ends the walk, the aggregates after it are summed; lanes whose
+// predecessor has not published yet make the warp re-poll. Publishes the
+// inclusive prefix and returns the exclusive prefix (packed v|d) to all lanes.
+__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* status, unsigned tile,
+                                                            unsigned long long aggregate) {
+  const unsigned lane = threadIdx.x & 31;
   if (tile == 0) {
-    publish(status, kFlagInc | aggregate);
+    if (lane == 0) publish(status, kFlagInc | aggregate);
     return 0ull;
   }
-  publish(status + tile, kFlagAgg | aggregate);
+  if (lane == 0) publish(status + tile, kFlagAgg | aggregate);
   unsigned long long ex = 0;
-  int t = (int)tile - 1;
+  int top = (int)tile - 1;  // highest predecessor not yet accounted for
   while (true) {
-    unsigned long long s;
-    do {
-      s = peek(status + t);
-    } while ((s >> 62) == 0);
-    ex += s & kValueMask;
-    if ((s >> 62) == 2) break;
-    --t;
+    const int t = top - (int)lane;
+    unsigned long long s = t >= 0 ? peek(status + t) : (kFlagInc);  // t < 0: virtual zero prefix
+    unsigned flag = (unsigned)(s >> 62);
+    // wait until every lane's predecessor has published something
+    while (__any_sync(0xffffffffu, flag == 0)) {
+      if (flag == 0) {
+        s = peek(status + t);
+        flag = (unsigned)(s >> 62);
+      }
+    }
+    const unsigned inc_mask = __ballot_sync(0xffffffffu, flag == 2);
+    if (inc_mask) {
+      const unsigned first = __ffs(inc_mask) - 1;  // nearest inclusive predecessor
+      unsigned long long v = lane <= first ? (s & kValueMask) : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      ex += v;
+      break;
+    }
+    unsigned long long v = s & kValueMask;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    ex += v;
+    top -= 32;
   }
-  publish(status + tile, kFlagInc | (ex + aggregate));
+  if (lane == 0) publish(status + tile, kFlagInc | (ex + aggregate));
   return ex;
 }
 
