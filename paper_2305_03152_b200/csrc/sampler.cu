@@ -354,8 +354,9 @@ constexpr int kStage = 5120;  // ids staged in shared memory per tile (else dire
 // Tile ids are emitted into shared memory at their scanned positions and
 // copied out with coalesced stores (direct scattered stores only for the rare
 // tile denser than kStage).
-template <bool HAS_NEXT, bool OR_ALL>
+template <bool HAS_NEXT, bool OR_ALL, int WPT>
 __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
+  constexpr std::uint64_t TW = (std::uint64_t)kCompactThreads * WPT;  // words per tile
   __shared__ unsigned s_ticket;
   __shared__ unsigned long long s_sm[kCompactThreads / 32];
   __shared__ unsigned long long s_excl;
@@ -368,17 +369,25 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const std::uint32_t tile = ticket % (unsigned)p.tiles;
   if (mb >= p.nmb) return;
   unsigned long long* bits = p.bits + mb * p.W;
-  const std::uint64_t w = (std::uint64_t)tile * kTileWords + threadIdx.x;
-  const unsigned long long wd = w < p.W ? bits[w] : 0ull;
-  if (wd) bits[w] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
-  if (OR_ALL && wd) p.allbits[mb * p.W + w] |= wd;
-  unsigned long long vc = __popcll(wd), dc = 0;
-  if (HAS_NEXT) {
-    unsigned long long x = wd;
-    while (x) {
-      const int b = __ffsll(x) - 1;
-      x &= x - 1;
-      dc += min(p.f_next, __ldg(p.outdeg + (std::uint32_t)(w * 64 + b)));
+  const std::uint64_t w0 = (std::uint64_t)tile * TW + (std::uint64_t)threadIdx.x * WPT;
+  unsigned long long wd[WPT];
+#pragma unroll
+  for (int k = 0; k < WPT; ++k) wd[k] = w0 + k < p.W ? bits[w0 + k] : 0ull;
+  unsigned long long vc = 0, dc = 0;
+#pragma unroll
+  for (int k = 0; k < WPT; ++k) {
+    if (wd[k]) {
+      bits[w0 + k] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
+      if (OR_ALL) p.allbits[mb * p.W + w0 + k] |= wd[k];
+    }
+    vc += __popcll(wd[k]);
+    if (HAS_NEXT) {
+      unsigned long long x = wd[k];
+      while (x) {
+        const int b = __ffsll(x) - 1;
+        x &= x - 1;
+        dc += min(p.f_next, __ldg(p.outdeg + (std::uint32_t)((w0 + k) * 64 + b)));
+      }
     }
   }
   const unsigned long long mine = pack_vd(vc, dc);
@@ -397,26 +406,31 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const std::uint32_t tcount = (std::uint32_t)unpack_v(total);
   std::uint32_t* list = p.list + mb * p.cap_list;
   std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
-  if (w < p.W) p.rank[mb * p.W + w] = make_uint4((unsigned)wd, (unsigned)(wd >> 32), gbase + lpos, 0u);
   const bool staged = tcount <= (std::uint32_t)kStage;
-  unsigned long long x = wd;
-  while (x) {
-    const int b = __ffsll(x) - 1;
-    x &= x - 1;
-    const std::uint32_t v = (std::uint32_t)(w * 64 + b);
-    std::uint32_t d = 0;
-    if (HAS_NEXT) {
-      d = dpos;
-      dpos += min(p.f_next, __ldg(p.outdeg + v));
+#pragma unroll
+  for (int k = 0; k < WPT; ++k) {
+    const std::uint64_t w = w0 + k;
+    if (w < p.W)
+      p.rank[mb * p.W + w] = make_uint4((unsigned)wd[k], (unsigned)(wd[k] >> 32), gbase + lpos, 0u);
+    unsigned long long x = wd[k];
+    while (x) {
+      const int b = __ffsll(x) - 1;
+      x &= x - 1;
+      const std::uint32_t v = (std::uint32_t)(w * 64 + b);
+      std::uint32_t d = 0;
+      if (HAS_NEXT) {
+        d = dpos;
+        dpos += min(p.f_next, __ldg(p.outdeg + v));
+      }
+      if (staged) {
+        s_ids[lpos] = v;
+        if (HAS_NEXT) s_ip[lpos] = d;
+      } else {
+        list[gbase + lpos] = v;
+        if (HAS_NEXT) ipn[gbase + lpos] = d;
+      }
+      ++lpos;
     }
-    if (staged) {
-      s_ids[lpos] = v;
-      if (HAS_NEXT) s_ip[lpos] = d;
-    } else {
-      list[gbase + lpos] = v;
-      if (HAS_NEXT) ipn[gbase + lpos] = d;
-    }
-    ++lpos;
   }
   if (staged) {
     __syncthreads();
@@ -554,15 +568,20 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   p.status = s.status.as<unsigned long long>() + (std::uint64_t)slot * s.M * s.tiles;
   p.ticket = s.tickets.as<unsigned>() + slot;
   p.W = s.W;
-  p.tiles = s.tiles;
   p.nmb = nmb;
-  const unsigned grid = (unsigned)(nmb * s.tiles);
+  // sparse frontiers (every hop but the last) take 4 words per thread: fewer,
+  // fatter tiles; the dense last hop and all_vertices keep 1 word per thread so
+  // a tile's ids fit the shared staging buffer.
+  constexpr int kSparseWPT = 4;
+  const int wpt = has_next ? kSparseWPT : 1;
+  p.tiles = (s.W + (std::uint64_t)kCompactThreads * wpt - 1) / ((std::uint64_t)kCompactThreads * wpt);
+  const unsigned grid = (unsigned)(nmb * p.tiles);
   if (has_next)
-    k_compact<true, true><<<grid, kCompactThreads, 0, st>>>(p);
+    k_compact<true, true, kSparseWPT><<<grid, kCompactThreads, 0, st>>>(p);
   else if (hop)
-    k_compact<false, true><<<grid, kCompactThreads, 0, st>>>(p);
+    k_compact<false, true, 1><<<grid, kCompactThreads, 0, st>>>(p);
   else
-    k_compact<false, false><<<grid, kCompactThreads, 0, st>>>(p);
+    k_compact<false, false, 1><<<grid, kCompactThreads, 0, st>>>(p);
 }
 
 }  // namespace
