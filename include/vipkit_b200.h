@@ -95,6 +95,7 @@ VK_API int vk_graph_create(int device, uint64_t n, uint64_t m, const uint64_t* f
 VK_API int vk_graph_load_vcsr(int device, const char* path, uint32_t flags, vk_graph* out);
 VK_API int vk_graph_destroy(vk_graph g);
 VK_API int vk_graph_info(vk_graph g, uint64_t* n, uint64_t* m, int* symmetric, int* device);
+VK_API int vk_graph_copy_forward(vk_graph g, uint64_t* fwd_offsets, uint32_t* fwd_targets);
 VK_API int vk_graph_copy_reverse(vk_graph g, uint64_t* rev_offsets, uint32_t* rev_targets);
 
 /* ------------------------------------------------------------------- VIP

@@ -1,0 +1,500 @@
+// vipkit_b200 C++ mirror of the reference hot-path API.
+//
+// Drop-in for the reference's `namespace vipkit` declarations on this path
+// (/root/reference/proj/include/vipkit/{error,rng,graph,sampling,vip,
+// policies,reorder}.hpp): same type names, function names, argument meaning
+// and exception types, implemented by the B200 C ABI (include/vipkit_b200.h,
+// libvipkit_b200.so). Header-only; link with -lvipkit_b200.
+//
+//   #include <vipkit_b200/vipkit.hpp>     // instead of <vipkit/vip.hpp> ...
+//   vipkit::Graph g = vipkit::load_binary_csr("g.vcsr");
+//   auto scores = vipkit::propagate(g, tm, vipkit::initial_probs(roles, part, k, 1024), k);
+//
+// Differences (documented in INTEGRATION.md): the Graph keeps a device copy,
+// created on first use (the reference Graph is immutable, graph.hpp:17-19);
+// propagate_all() batches all partitions in one pass; expand_wave() and
+// FeatureStore are the batched / feature-gather entry points the reference
+// does not have.
+#pragma once
+
+#include <cstdint>
+#include <initializer_list>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../vipkit_b200.h"
+
+namespace vipkit {
+
+// ---- error.hpp:8-38 -------------------------------------------------------
+struct error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct parse_error : error { using error::error; };
+struct range_error : error { using error::error; };
+struct parameter_error : error { using error::error; };
+struct format_error : error { using error::error; };
+struct partition_error : error { using error::error; };
+struct sampling_error : error { using error::error; };
+struct config_error : error { using error::error; };
+struct shape_error : error { using error::error; };
+struct io_error : error { using error::error; };
+struct device_error : error { using error::error; };  // CUDA / NCCL / unsupported (no reference twin)
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == VK_OK) return;
+  const std::string msg = vk_last_error();
+  switch (rc) {
+    case VK_ERR_PARSE: throw parse_error(msg);
+    case VK_ERR_RANGE: throw range_error(msg);
+    case VK_ERR_PARAMETER: throw parameter_error(msg);
+    case VK_ERR_FORMAT: throw format_error(msg);
+    case VK_ERR_PARTITION: throw partition_error(msg);
+    case VK_ERR_SAMPLING: throw sampling_error(msg);
+    case VK_ERR_CONFIG: throw config_error(msg);
+    case VK_ERR_SHAPE: throw shape_error(msg);
+    case VK_ERR_IO: throw io_error(msg);
+    default: throw device_error(std::string(vk_status_name(rc)) + ": " + msg);
+  }
+}
+}  // namespace detail
+
+// ---- rng.hpp:9-74 (host side; the device twin is csrc/rng.cuh) -------------
+inline std::uint64_t mix64(std::uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+class RngStream {
+ public:
+  explicit RngStream(std::uint64_t key) : counter_(mix64(key)) {}
+  std::uint64_t next_u64() {
+    counter_ += 0x9e3779b97f4a7c15ull;
+    std::uint64_t x = counter_;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+  }
+  double next_double() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+  std::uint64_t next_below(std::uint64_t bound) {
+    const std::uint64_t limit = ~0ull - ~0ull % bound;
+    std::uint64_t x = next_u64();
+    while (x >= limit) x = next_u64();
+    return x % bound;
+  }
+
+ private:
+  std::uint64_t counter_;
+};
+namespace stream_tag {
+constexpr std::uint64_t synthesis = 0xA1, roles = 0xA2, partitioning = 0xA3, minibatch_perm = 0xB1,
+                        neighbor_sample = 0xB2, empirical_vip = 0xC1;
+}
+struct SeedSpec {
+  std::uint64_t global_seed = 0;
+  SeedSpec derived(std::uint64_t tag) const { return SeedSpec{mix64(global_seed ^ mix64(tag))}; }
+  std::uint64_t key(std::initializer_list<std::uint64_t> parts) const {
+    std::uint64_t h = global_seed;
+    for (std::uint64_t p : parts) h = mix64(h ^ mix64(p));
+    return h;
+  }
+  RngStream stream(std::initializer_list<std::uint64_t> parts) const { return RngStream(key(parts)); }
+};
+
+// ---- graph.hpp:14-69 --------------------------------------------------------
+using vertex_t = std::uint32_t;
+using offset_t = std::uint64_t;
+
+struct Graph {
+  std::vector<offset_t> fwd_offsets{0};
+  std::vector<vertex_t> fwd_targets;
+  std::vector<offset_t> rev_offsets{0};
+  std::vector<vertex_t> rev_targets;
+  int device = 0;  // CUDA device that holds the device copy
+
+  std::size_t num_vertices() const { return fwd_offsets.size() - 1; }
+  std::size_t num_edges() const { return fwd_targets.size(); }
+  std::uint64_t out_degree(vertex_t v) const { return fwd_offsets[v + 1] - fwd_offsets[v]; }
+  std::uint64_t in_degree(vertex_t v) const { return rev_offsets[v + 1] - rev_offsets[v]; }
+  std::span<const vertex_t> out_neighbors(vertex_t v) const {
+    return {fwd_targets.data() + fwd_offsets[v], fwd_targets.data() + fwd_offsets[v + 1]};
+  }
+  std::span<const vertex_t> in_neighbors(vertex_t v) const {
+    return {rev_targets.data() + rev_offsets[v], rev_targets.data() + rev_offsets[v + 1]};
+  }
+
+  /// Take ownership of an existing device copy of this graph.
+  void adopt(vk_graph h) { dev_ = std::shared_ptr<vk_graph_s>(h, [](vk_graph p) { vk_graph_destroy(p); }); }
+
+  /// Device copy (created on first use; the Graph is immutable by contract).
+  vk_graph handle() const {
+    if (!dev_) {
+      const bool have_rev = rev_offsets.size() == fwd_offsets.size() && rev_targets.size() == fwd_targets.size();
+      vk_graph h = nullptr;
+      detail::check(vk_graph_create(device, num_vertices(), num_edges(), fwd_offsets.data(),
+                                    fwd_targets.data(), have_rev ? rev_offsets.data() : nullptr,
+                                    have_rev ? rev_targets.data() : nullptr, 0, &h));
+      dev_ = std::shared_ptr<vk_graph_s>(h, [](vk_graph p) { vk_graph_destroy(p); });
+    }
+    return dev_.get();
+  }
+
+ private:
+  mutable std::shared_ptr<vk_graph_s> dev_;
+};
+
+enum class Role : std::uint8_t { train = 0, valid = 1, test = 2, none = 3 };
+
+struct VertexRoles {
+  std::vector<std::uint8_t> role;
+  std::size_t size() const { return role.size(); }
+  bool is_train(vertex_t v) const { return role[v] == static_cast<std::uint8_t>(Role::train); }
+};
+
+struct PartitionMap {
+  std::uint32_t K = 1;
+  std::vector<std::uint32_t> part_of;
+  std::vector<std::vector<vertex_t>> members;
+
+  static PartitionMap from_labels(std::vector<std::uint32_t> labels, std::uint32_t K) {  // graph.cpp:88-104
+    if (K == 0) throw parameter_error("partition count must be >= 1");
+    PartitionMap pm;
+    pm.K = K;
+    pm.part_of = std::move(labels);
+    pm.members.assign(K, {});
+    for (std::size_t v = 0; v < pm.part_of.size(); ++v) {
+      if (pm.part_of[v] >= K)
+        throw format_error("partition label " + std::to_string(pm.part_of[v]) + " out of range for K=" +
+                           std::to_string(K));
+      pm.members[pm.part_of[v]].push_back(static_cast<vertex_t>(v));
+    }
+    for (std::uint32_t k = 0; k < K; ++k)
+      if (pm.members[k].empty()) throw partition_error("partition " + std::to_string(k) + " is empty");
+    return pm;
+  }
+};
+
+/// load_binary_csr (graph.hpp:117): parsed on the host, validated and the
+/// reverse CSR rebuilt on the device (graph.cpp:587-596); the returned Graph
+/// holds host copies (as the reference's does) and keeps the device copy.
+inline Graph load_binary_csr(const std::string& path, int device = 0) {
+  vk_graph h = nullptr;
+  detail::check(vk_graph_load_vcsr(device, path.c_str(), 0, &h));
+  std::uint64_t n = 0, m = 0;
+  int sym = 0, dev = 0;
+  detail::check(vk_graph_info(h, &n, &m, &sym, &dev));
+  Graph g;
+  g.device = device;
+  g.fwd_offsets.resize(n + 1);
+  g.fwd_targets.resize(m);
+  g.rev_offsets.resize(n + 1);
+  g.rev_targets.resize(m);
+  detail::check(vk_graph_copy_forward(h, g.fwd_offsets.data(), g.fwd_targets.data()));
+  detail::check(vk_graph_copy_reverse(h, g.rev_offsets.data(), g.rev_targets.data()));
+  g.adopt(h);
+  return g;
+}
+
+// ---- sampling.hpp:14-64 ------------------------------------------------------
+struct FanoutSpec {
+  std::vector<std::uint32_t> fanouts;
+  std::size_t hops() const { return fanouts.size(); }
+  void validate() const {  // sampling.cpp:11-15
+    if (fanouts.empty()) throw parameter_error("fanout list must have at least one hop");
+    for (std::uint32_t f : fanouts)
+      if (f < 1) throw parameter_error("each fanout must be >= 1");
+  }
+  std::string label() const {
+    std::string s;
+    for (std::size_t i = 0; i < fanouts.size(); ++i) s += (i ? "-" : "") + std::to_string(fanouts[i]);
+    return s;
+  }
+};
+
+struct ExpandedNeighborhood {
+  std::vector<vertex_t> batch;
+  std::vector<std::vector<vertex_t>> frontier;
+  std::vector<vertex_t> all_vertices;
+  // MFG (builder contract): per hop h, row pointers over the
+  // sources of hop h and the index of each sampled vertex in frontier[h-1].
+  std::vector<std::vector<std::uint64_t>> mfg_indptr;
+  std::vector<std::vector<std::uint32_t>> mfg_dst;
+};
+
+struct BatchRef {
+  std::uint64_t epoch = 0;
+  std::uint32_t partition = 0;
+  std::uint64_t batch_index = 0;
+};
+
+inline std::vector<std::vector<vertex_t>> epoch_minibatches(const VertexRoles& roles, const PartitionMap& part,
+                                                            std::uint32_t k, std::uint64_t b, std::uint64_t epoch,
+                                                            const SeedSpec& seeds,
+                                                            const std::vector<vertex_t>* seed_keys = nullptr) {
+  std::vector<vertex_t> perm(roles.size());
+  std::uint64_t cnt = 0;
+  detail::check(vk_epoch_minibatches(roles.size(), roles.role.data(), part.part_of.data(), k, b, epoch,
+                                     seeds.global_seed, seed_keys ? seed_keys->data() : nullptr, perm.data(),
+                                     &cnt));
+  std::vector<std::vector<vertex_t>> out;
+  for (std::uint64_t pos = 0; pos < cnt; pos += b)
+    out.emplace_back(perm.begin() + pos, perm.begin() + std::min<std::uint64_t>(cnt, pos + b));
+  return out;
+}
+
+/// Batched expand: the device sampler for a wave of minibatches.
+class Sampler {
+ public:
+  Sampler(const Graph& g, const FanoutSpec& f, std::uint64_t batch_size, std::uint32_t max_minibatches,
+          const SeedSpec& seeds) {
+    f.validate();
+    if (f.hops() > VK_MAX_HOPS) throw device_error("at most 8 hops are supported");
+    vk_sampler_config cfg{};
+    cfg.num_hops = static_cast<std::uint32_t>(f.hops());
+    for (std::size_t h = 0; h < f.hops(); ++h) cfg.fanouts[h] = f.fanouts[h];
+    cfg.batch_size = batch_size;
+    cfg.max_minibatches = max_minibatches;
+    cfg.global_seed = seeds.global_seed;
+    vk_sampler s = nullptr;
+    detail::check(vk_sampler_create(g.handle(), &cfg, &s));
+    s_ = std::shared_ptr<vk_sampler_s>(s, [](vk_sampler p) { vk_sampler_destroy(p); });
+    L_ = cfg.num_hops;
+  }
+  void run(const std::vector<std::span<const vertex_t>>& batches, const std::vector<BatchRef>& refs) {
+    if (batches.size() != refs.size()) throw shape_error("one BatchRef per minibatch");
+    std::vector<std::uint32_t> cat;
+    std::vector<std::uint64_t> off{0};
+    std::vector<vk_batch_ref> r(refs.size());
+    for (std::size_t i = 0; i < batches.size(); ++i) {
+      cat.insert(cat.end(), batches[i].begin(), batches[i].end());
+      off.push_back(cat.size());
+      r[i] = vk_batch_ref{refs[i].epoch, refs[i].batch_index, refs[i].partition, 0};
+    }
+    detail::check(vk_sampler_run(s_.get(), static_cast<std::uint32_t>(refs.size()), r.data(), cat.data(),
+                                 off.data(), 0, nullptr));
+    nmb_ = static_cast<std::uint32_t>(refs.size());
+  }
+  ExpandedNeighborhood result(std::uint32_t mb) const {
+    std::vector<std::uint64_t> fs(nmb_ * L_), ec(nmb_ * L_), al(nmb_);
+    detail::check(vk_sampler_sizes(s_.get(), fs.data(), ec.data(), al.data()));
+    ExpandedNeighborhood nb;
+    vk_sampler_view v{};
+    detail::check(vk_sampler_get_view(s_.get(), &v));
+    std::uint32_t nbatch = 0;
+    detail::check(vk_memcpy(&nbatch, v.frontier_count[0] + mb, 4, 2 /*D2H*/));
+    nb.batch.resize(nbatch);
+    detail::check(vk_sampler_copy_frontier(s_.get(), mb, 0, nb.batch.data()));
+    for (std::uint32_t h = 1; h <= L_; ++h) {
+      nb.frontier.emplace_back(fs[mb * L_ + h - 1]);
+      detail::check(vk_sampler_copy_frontier(s_.get(), mb, h, nb.frontier.back().data()));
+      const std::uint64_t nsrc = h == 1 ? nbatch : fs[mb * L_ + h - 2];
+      nb.mfg_indptr.emplace_back(nsrc + 1);
+      nb.mfg_dst.emplace_back(ec[mb * L_ + h - 1]);
+      detail::check(vk_sampler_copy_mfg(s_.get(), mb, h, nb.mfg_indptr.back().data(), nb.mfg_dst.back().data()));
+    }
+    nb.all_vertices.resize(al[mb]);
+    detail::check(vk_sampler_copy_all(s_.get(), mb, nb.all_vertices.data()));
+    return nb;
+  }
+  vk_sampler handle() const { return s_.get(); }
+
+ private:
+  std::shared_ptr<vk_sampler_s> s_;
+  std::uint32_t L_ = 0, nmb_ = 0;
+};
+
+/// vipkit::expand (sampling.hpp:62-64) for one minibatch.
+inline ExpandedNeighborhood expand(const Graph& g, std::span<const vertex_t> batch, const FanoutSpec& fanouts,
+                                   const SeedSpec& seeds, const BatchRef& ref,
+                                   const std::vector<vertex_t>* seed_keys = nullptr) {
+  if (seed_keys) throw device_error("seed_keys replay is not supported on the device path");
+  if (batch.empty()) throw sampling_error("cannot expand an empty batch");  // sampling.cpp:97
+  Sampler s(g, fanouts, batch.size(), 1, seeds);
+  s.run({batch}, {ref});
+  return s.result(0);
+}
+
+// ---- vip.hpp:15-46 -----------------------------------------------------------
+struct TransitionModel {
+  enum class Kind { uniform_fanout };
+  Kind kind = Kind::uniform_fanout;
+  FanoutSpec fanouts;
+  double weight(std::size_t hop, std::uint64_t deg) const {
+    const double f = static_cast<double>(fanouts.fanouts[hop - 1]);
+    const double d = static_cast<double>(deg);
+    return d <= f ? 1.0 : f / d;
+  }
+};
+
+struct VipScores {
+  std::uint32_t partition = 0;
+  std::vector<double> p0;
+  std::vector<std::vector<double>> hop;
+  std::vector<double> total;
+};
+
+inline std::vector<double> initial_probs(const VertexRoles& roles, const PartitionMap& part, std::uint32_t k,
+                                         std::uint64_t b) {
+  std::vector<double> p0(roles.size());
+  detail::check(vk_initial_probs(roles.size(), roles.role.data(), part.part_of.data(), k, b, p0.data()));
+  return p0;
+}
+
+/// propagate for several p0 vectors in one pass over the reverse CSR.
+inline std::vector<VipScores> propagate_all(const Graph& g, const TransitionModel& tm,
+                                            std::vector<std::vector<double>> p0s, std::uint32_t first_partition = 0) {
+  tm.fanouts.validate();
+  const std::size_t n = g.num_vertices();
+  const std::size_t L = tm.fanouts.hops();
+  std::vector<double> cat;
+  for (auto& p : p0s) {
+    if (p.size() != n) throw shape_error("p0 length does not match vertex count");
+    cat.insert(cat.end(), p.begin(), p.end());
+  }
+  const auto C = static_cast<std::uint32_t>(p0s.size());
+  std::vector<double> hop(C * L * n), total(C * n);
+  detail::check(vk_vip_propagate(g.handle(), tm.fanouts.fanouts.data(), static_cast<std::uint32_t>(L), C,
+                                 cat.data(), hop.data(), total.data()));
+  std::vector<VipScores> out(C);
+  for (std::uint32_t c = 0; c < C; ++c) {
+    out[c].partition = first_partition + c;
+    out[c].p0 = std::move(p0s[c]);
+    for (std::size_t h = 0; h < L; ++h)
+      out[c].hop.emplace_back(hop.begin() + (c * L + h) * n, hop.begin() + (c * L + h + 1) * n);
+    out[c].total.assign(total.begin() + c * n, total.begin() + (c + 1) * n);
+  }
+  return out;
+}
+
+/// vipkit::propagate (vip.hpp:45-46).
+inline VipScores propagate(const Graph& g, const TransitionModel& tm, std::vector<double> p0,
+                           std::uint32_t partition = 0) {
+  std::vector<std::vector<double>> v;
+  v.push_back(std::move(p0));
+  return std::move(propagate_all(g, tm, std::move(v), partition)[0]);
+}
+
+// ---- policies.hpp:16-64 -------------------------------------------------------
+struct Ranking {
+  std::uint32_t partition = 0;
+  std::vector<vertex_t> order;
+  std::vector<double> score;
+  double effective_alpha = -1.0;
+};
+
+inline Ranking rank_by_scores(const PartitionMap& part, std::uint32_t k, std::span<const double> scores,
+                              int device = 0) {
+  Ranking r;
+  r.partition = k;
+  const std::size_t n = part.part_of.size();
+  r.order.resize(n);
+  r.score.resize(n);
+  std::uint64_t cnt = 0;
+  detail::check(vk_rank_by_scores(device, n, part.part_of.data(), k, scores.data(), scores.size(), r.order.data(),
+                                  r.score.data(), &cnt));
+  r.order.resize(cnt);
+  r.score.resize(cnt);
+  return r;
+}
+
+struct CachePlan {
+  std::uint32_t K = 1;
+  double alpha = 0.0;
+  std::vector<std::vector<vertex_t>> cached;
+  std::vector<std::vector<std::uint64_t>> member_bits;
+  bool is_cached(std::uint32_t k, vertex_t v) const { return (member_bits[k][v >> 6] >> (v & 63)) & 1u; }
+  static CachePlan empty(std::uint32_t K, std::size_t n) {
+    CachePlan plan;
+    plan.K = K;
+    plan.cached.assign(K, {});
+    plan.member_bits.assign(K, std::vector<std::uint64_t>((n + 63) / 64, 0));
+    return plan;
+  }
+};
+
+/// build_cache (policies.cpp:149-163): the ranking prefixes are the cache.
+inline CachePlan build_cache(const std::vector<Ranking>& rankings, double alpha, std::size_t n) {
+  const auto K = static_cast<std::uint32_t>(rankings.size());
+  if (K == 0) throw parameter_error("need at least one ranking");
+  std::uint64_t cap = 0;
+  detail::check(vk_cache_capacity(alpha, n, K, &cap));
+  CachePlan plan = CachePlan::empty(K, n);
+  plan.alpha = alpha;
+  for (std::uint32_t k = 0; k < K; ++k) {
+    const auto take = std::min<std::uint64_t>(cap, rankings[k].order.size());
+    plan.cached[k].assign(rankings[k].order.begin(), rankings[k].order.begin() + take);
+    for (vertex_t v : plan.cached[k]) plan.member_bits[k][v >> 6] |= 1ull << (v & 63);
+  }
+  return plan;
+}
+
+// ---- reorder.hpp:15-26 --------------------------------------------------------
+struct ReorderMap {
+  std::vector<vertex_t> new_of_old;
+  std::vector<vertex_t> old_of_new;
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> ranges;
+  std::size_t size() const { return new_of_old.size(); }
+};
+
+inline ReorderMap build_reorder(const PartitionMap& part, const std::vector<std::vector<double>>& scores,
+                                int device = 0) {
+  if (scores.size() != part.K) throw shape_error("need one score vector per partition");
+  const std::size_t n = part.part_of.size();
+  std::vector<double> cat;
+  for (const auto& s : scores) {
+    if (s.size() != n) throw shape_error("score vector length does not match vertex count");
+    cat.insert(cat.end(), s.begin(), s.end());
+  }
+  ReorderMap m;
+  m.old_of_new.resize(n);
+  std::vector<std::uint64_t> ranges(2 * part.K);
+  detail::check(vk_build_reorder(device, n, part.K, part.part_of.data(), cat.data(), m.old_of_new.data(),
+                                 ranges.data()));
+  m.new_of_old.resize(n);
+  for (std::size_t i = 0; i < n; ++i) m.new_of_old[m.old_of_new[i]] = static_cast<vertex_t>(i);
+  for (std::uint32_t k = 0; k < part.K; ++k) m.ranges.emplace_back(ranges[2 * k], ranges[2 * k + 1]);
+  return m;
+}
+
+// ---- feature gather (new: the reference never materialises features) -------
+class FeatureStore {
+ public:
+  FeatureStore(const PartitionMap& part, const ReorderMap& map, std::uint32_t dim, int dtype = VK_F32,
+               int device = 0) {
+    std::vector<std::uint64_t> r;
+    for (auto& [a, b] : map.ranges) {
+      r.push_back(a);
+      r.push_back(b);
+    }
+    vk_plane p = nullptr;
+    detail::check(vk_plane_create(device, part.part_of.size(), part.K, dim, dtype, part.part_of.data(),
+                                  map.old_of_new.data(), r.data(), &p));
+    p_ = std::shared_ptr<vk_plane_s>(p, [](vk_plane q) { vk_plane_destroy(q); });
+  }
+  void load_partition(std::uint32_t k, const std::vector<vertex_t>& cached, const void* features,
+                      std::uint64_t feature_seed = 0) {
+    detail::check(vk_plane_load_partition(p_.get(), k, cached.data(), cached.size(), features, feature_seed));
+  }
+  bool is_cached(std::uint32_t k, vertex_t v) const {
+    int out = 0;
+    detail::check(vk_plane_is_cached(p_.get(), k, v, &out));
+    return out != 0;
+  }
+  /// classify + gather for the sampler's last wave into device memory.
+  void gather(const Sampler& s, void* out_dev, std::uint64_t out_stride_rows, std::uint64_t* counts_dev,
+              vk_stream_t stream = nullptr) {
+    detail::check(vk_plane_gather(p_.get(), s.handle(), out_dev, out_stride_rows, counts_dev, stream));
+  }
+  vk_plane handle() const { return p_.get(); }
+
+ private:
+  std::shared_ptr<vk_plane_s> p_;
+};
+
+}  // namespace vipkit

@@ -338,6 +338,15 @@ int vk_graph_info(vk_graph g, uint64_t* n, uint64_t* m, int* symmetric, int* dev
   });
 }
 
+int vk_graph_copy_forward(vk_graph g, uint64_t* fwd_offsets, uint32_t* fwd_targets) {
+  return guard([&] {
+    if (!g) raise(VK_ERR_PARAMETER, "null graph");
+    DeviceGuard dg(g->device);
+    if (fwd_offsets) VK_CUDA(cudaMemcpy(fwd_offsets, g->d_off(), (g->n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (fwd_targets && g->m) VK_CUDA(cudaMemcpy(fwd_targets, g->d_tgt(), g->m * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
 int vk_graph_copy_reverse(vk_graph g, uint64_t* rev_offsets, uint32_t* rev_targets) {
   return guard([&] {
     if (!g) raise(VK_ERR_PARAMETER, "null graph");

