@@ -55,6 +55,8 @@ struct vk_plane_s {
   std::vector<Part> parts;
   vk::DevBuf d_base, d_slot, d_nlocal;  // K-entry tables for the gather kernel
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;  // remote-row gathers run here concurrently
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace vk {
@@ -206,9 +208,15 @@ __device__ __forceinline__ void st_stream(T* p, const T& v) {
 // owner partition's row, local HBM or a peer GPU over NVLink), then the warp
 // copies the group as one flat, fully coalesced range of 32*V vectors with
 // kUnroll independent loads in flight per lane.
-template <class T, int kUnroll, int kMinBlocks>
+// MODE 0: every row (no peer partitions). MODE 1: rows served from this GPU
+// (local rows, cache rows, misses owned by a co-resident partition). MODE 2:
+// rows owned by a partition on another GPU, read over NVLink. With peers the
+// two run concurrently on two streams so HBM-bound local copies are not held
+// back by NVLink-latency-bound remote ones inside the same warp.
+template <class T, int kUnroll, int kMinBlocks, int MODE>
 __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   __shared__ const T* s_src[8][32];
+  __shared__ std::uint32_t s_row[8][32];
   // Vertex-tile-major schedule, minibatch fastest: the CTAs resident at any
   // moment serve the same vertex range for every minibatch of the wave, so a
   // feature row needed by several minibatches is read from HBM once and hit
@@ -239,18 +247,35 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
       const std::uint32_t v = __ldg(all + r);
       const std::uint32_t s = __ldg(slot + v);
       if (s != VK_MISS) {
-        src = store + (std::uint64_t)s * rowv;
-        (s < nl ? c_local : c_cache)++;
+        if (MODE != 2) {
+          src = store + (std::uint64_t)s * rowv;
+          (s < nl ? c_local : c_cache)++;
+        }
       } else {
         const std::uint32_t o = __ldg(p.part_of + v);
-        src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
-        ++c_miss;
-        c_peer += p.peer_mask[o];
+        const bool remote = p.peer_mask[o] != 0;
+        if ((MODE == 0) || (MODE == 1 && !remote) || (MODE == 2 && remote)) {
+          src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
+          ++c_miss;
+          c_peer += remote;
+        }
       }
     }
-    s_src[w][lane] = src;
+    std::uint32_t rows;
+    if (MODE == 0) {
+      s_src[w][lane] = src;
+      s_row[w][lane] = lane;
+      rows = min(32u, hi - r0);
+    } else {  // compact this group's rows of the mode
+      const unsigned mask = __ballot_sync(0xffffffffu, src != nullptr);
+      const unsigned idx = __popc(mask & ((1u << lane) - 1u));
+      if (src) {
+        s_src[w][idx] = src;
+        s_row[w][idx] = lane;
+      }
+      rows = __popc(mask);
+    }
     __syncwarp();
-    const std::uint32_t rows = min(32u, hi - r0);
     const std::uint32_t total = rows * V;
     T* dst = out + (std::uint64_t)r0 * V;
     for (std::uint32_t e0 = lane; e0 < total; e0 += 32 * kUnroll) {
@@ -266,7 +291,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const std::uint32_t e = e0 + 32 * u;
-        if (e < total) st_stream(dst + e, val[u]);
+        if (e < total) {
+          const std::uint32_t row = V == 1 ? e : __umulhi(e, magic);
+          st_stream(dst + (std::uint64_t)s_row[w][row] * V + (e - row * V), val[u]);
+        }
       }
     }
     __syncwarp();
@@ -418,6 +446,9 @@ int vk_plane_create(int device, uint64_t n, uint32_t K, uint32_t dim, int dtype,
       p->old_of_new.assign(old_of_new, old_of_new + n);
       p->parts.resize(K);
       VK_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+      VK_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+      VK_CUDA(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
+      VK_CUDA(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
       p->part_of.alloc(n * 4);
       p->owner_row.alloc(n * 4);
       VK_CUDA(cudaMemcpyAsync(p->part_of.p, part_of, n * 4, cudaMemcpyHostToDevice, p->stream));
@@ -444,7 +475,11 @@ int vk_plane_destroy(vk_plane p) {
     if (p->stream) cudaStreamSynchronize(p->stream);
     for (auto& part : p->parts)
       if (part.peer) cudaIpcCloseMemHandle(part.peer);
+    if (p->aux) cudaStreamSynchronize(p->aux);
     if (p->stream) cudaStreamDestroy(p->stream);
+    if (p->aux) cudaStreamDestroy(p->aux);
+    if (p->fork) cudaEventDestroy(p->fork);
+    if (p->join) cudaEventDestroy(p->join);
     delete p;
   });
 }
@@ -637,27 +672,36 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     gp.tile_words = tile_words;
     gp.tiles = (std::uint32_t)((gp.W + tile_words - 1) / tile_words);
     dim3 grid((unsigned)((std::uint64_t)gp.tiles * nmb));
-    // tuning knob (VK_GATHER_VARIANT): unroll depth vs occupancy
-    static const int variant = [] {
-      const char* e = std::getenv("VK_GATHER_VARIANT");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (v16) {
-      if (variant == 1)
-        k_gather<uint4, 4, 8><<<grid, 256, 0, st>>>(gp);
-      else if (variant == 2)
-        k_gather<uint4, 16, 2><<<grid, 256, 0, st>>>(gp);
-      else if (variant == 3)
-        k_gather<uint4, 8, 6><<<grid, 256, 0, st>>>(gp);
-      else
-        k_gather<uint4, 8, 4><<<grid, 256, 0, st>>>(gp);
-    } else if (v4) {
-      k_gather<std::uint32_t, 8, 1><<<grid, 256, 0, st>>>(gp);
+    bool peers = false;
+    for (const auto& q : p->parts) peers |= q.attached;
+    auto launch = [&](int mode, cudaStream_t where) {
+      if (v16) {
+        if (mode == 0) k_gather<uint4, 8, 4, 0><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 1) k_gather<uint4, 8, 4, 1><<<grid, 256, 0, where>>>(gp);
+        else k_gather<uint4, 8, 4, 2><<<grid, 256, 0, where>>>(gp);
+      } else if (v4) {
+        if (mode == 0) k_gather<std::uint32_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 1) k_gather<std::uint32_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
+        else k_gather<std::uint32_t, 8, 1, 2><<<grid, 256, 0, where>>>(gp);
+      } else {
+        if (mode == 0) k_gather<std::uint16_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 1) k_gather<std::uint16_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
+        else k_gather<std::uint16_t, 8, 1, 2><<<grid, 256, 0, where>>>(gp);
+      }
+      count_launch();
+      VK_LAUNCH_CHECK();
+    };
+    if (!peers) {
+      launch(0, st);
     } else {
-      k_gather<std::uint16_t, 8, 1><<<grid, 256, 0, st>>>(gp);
+      // fork: remote (NVLink) rows on the plane's auxiliary stream, local rows on st
+      VK_CUDA(cudaEventRecord(p->fork, st));
+      VK_CUDA(cudaStreamWaitEvent(p->aux, p->fork, 0));
+      launch(2, p->aux);
+      launch(1, st);
+      VK_CUDA(cudaEventRecord(p->join, p->aux));
+      VK_CUDA(cudaStreamWaitEvent(st, p->join, 0));
     }
-    count_launch();
-    VK_LAUNCH_CHECK();
   });
 }
 
