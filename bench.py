@@ -156,7 +156,7 @@ def run_b200(args, cfg):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")  # host-side plumbing only (barriers, handle exchange, max)
     dev = local
     K, M, L = cfg["K"], args.wave, len(cfg["fanouts"])
     nthreads = max(1, (os.cpu_count() or 8) // world)
@@ -278,7 +278,7 @@ def run_b200(args, cfg):
     if world > 1:
         dist.barrier()
     e2e_ms = region(W + S, W + 2 * S, host=True, pinned=pinned)
-    tl = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=f"cuda:{dev}")
+    tl = torch.tensor([ms, e2e_ms], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(tl, op=dist.ReduceOp.MAX)
     ms, e2e_ms = float(tl[0]), float(tl[1])
