@@ -213,7 +213,7 @@ __device__ __forceinline__ void st_stream(T* p, const T& v) {
 // rows owned by a partition on another GPU, read over NVLink. With peers the
 // two run concurrently on two streams so HBM-bound local copies are not held
 // back by NVLink-latency-bound remote ones inside the same warp.
-template <class T, int kUnroll, int kMinBlocks, int MODE>
+template <class T, int kUnroll, int kMinBlocks, int MODE, bool STREAM_LD = true>
 __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   __shared__ const T* s_src[8][32];
   __shared__ std::uint32_t s_row[8][32];
@@ -285,7 +285,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
         const std::uint32_t e = e0 + 32 * u;
         if (e < total) {
           const std::uint32_t row = V == 1 ? e : __umulhi(e, magic);
-          val[u] = ld_stream(s_src[w][row] + (e - row * V));
+          const T* sp = s_src[w][row] + (e - row * V);
+          if constexpr (STREAM_LD)
+            val[u] = ld_stream(sp);
+          else
+            val[u] = *sp;
         }
       }
 #pragma unroll
@@ -672,13 +676,20 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     gp.tile_words = tile_words;
     gp.tiles = (std::uint32_t)((gp.W + tile_words - 1) / tile_words);
     dim3 grid((unsigned)((std::uint64_t)gp.tiles * nmb));
+    // split local / remote rows into concurrent kernels (VK_GATHER_SPLIT=1);
+    // default: one kernel, each warp mixes HBM and NVLink rows
+    static const bool split = [] {
+      const char* e = std::getenv("VK_GATHER_SPLIT");
+      return e && std::atoi(e) != 0;
+    }();
     bool peers = false;
     for (const auto& q : p->parts) peers |= q.attached;
+    peers = peers && split;
     auto launch = [&](int mode, cudaStream_t where) {
       if (v16) {
         if (mode == 0) k_gather<uint4, 8, 4, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<uint4, 8, 4, 1><<<grid, 256, 0, where>>>(gp);
-        else k_gather<uint4, 8, 4, 2><<<grid, 256, 0, where>>>(gp);
+        else k_gather<uint4, 16, 2, 2, false><<<grid, 256, 0, where>>>(gp);  // peer rows: plain LDG
       } else if (v4) {
         if (mode == 0) k_gather<std::uint32_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<std::uint32_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
