@@ -288,12 +288,13 @@ def run_b200(args, cfg):
     cnts = hist_counts.cpu().numpy().view(np.uint32)
     gather_ms = [evs[i][1].elapsed_time(evs[i][2]) for i in range(W, W + S)]
     sample_ms = [evs[i][0].elapsed_time(evs[i][1]) for i in range(W, W + S)]
-    g_bytes, s_bytes, rows, misses, peer = 0, 0, 0, 0, 0
+    g_bytes, s_bytes, rows, misses, peer, cache_hits = 0, 0, 0, 0, 0, 0
     for i in range(W, W + S):
         nmb = len(waves[i])
         allc = tally[i, :nmb, :3].sum(axis=1)
         rows += int(allc.sum())
         misses += int(tally[i, :nmb, 2].sum())
+        cache_hits += int(tally[i, :nmb, 1].sum())
         peer += int(tally[i, :nmb, 3].sum())
         g_bytes += int(allc.sum()) * (2 * rb + 8)
         fc = cnts[i, :(L + 1) * M].reshape(L + 1, M)[:, :nmb].astype(np.int64)
@@ -327,8 +328,9 @@ def run_b200(args, cfg):
         "sampler": {"ms_per_wave": statistics.mean(sample_ms), "achieved_gbs": s_ach,
                     "frac": s_ach / hbm, "bytes_per_wave": s_bytes / S},
         "vip": {**vip, "unit": "edges/s", "frac": vip["achieved_gbs"] / hbm},
-        "tallies": {"rows": rows, "miss_rows": misses, "miss_rows_over_nvlink": peer,
-                    "miss_fraction": misses / max(rows, 1)},
+        "tallies": {"rows": rows, "miss_rows": misses, "miss_rows_no_cache": misses + cache_hits,
+                    "miss_reduction_by_vip_cache": 1.0 - misses / max(misses + cache_hits, 1),
+                    "miss_rows_over_nvlink": peer, "miss_fraction": misses / max(rows, 1)},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
