@@ -34,6 +34,7 @@ struct vk_graph_s {
   // VIP workspace, grown on demand and kept across calls (no allocation on
   // the timed path).
   vk::DevBuf vip_lm_a, vip_lm_b, vip_partial, vip_flag;
+  bool vip_last_f32 = false;  // storage width used by the last propagate (diagnostics)
 
   const std::uint64_t* d_off() const { return fwd_off.as<std::uint64_t>(); }
   const std::uint32_t* d_tgt() const { return fwd_tgt.as<std::uint32_t>(); }

@@ -125,3 +125,36 @@ def test_errors(vk, golden):
         vk.propagate(g, [1, 0], [1.0, 0.0, 0.0])
     with pytest.raises(vk.FormatError):
         vk.Graph.from_csr(np.array([0, 1, 1], np.uint64), np.array([0], np.uint32), validate=True)
+
+
+def test_float_lm_storage_within_tolerance(vk, port, monkeypatch):
+    """Large graphs store the hoisted log terms in float; forced
+    here on C1: still within 1e-5 relative, 0/1 cases exact."""
+    monkeypatch.setenv("VK_VIP_LM", "32")
+    csr = port.generate("pa", 100000, 10, 7)
+    roles = port.make_roles(csr.n, 0.1, 0, 0, 3)
+    labels = (np.arange(csr.n) % 4).astype(np.uint32)
+    p0 = np.stack([port.initial_probs(roles, labels, 4, k, 1024) for k in range(4)])
+    g = dev_graph(vk, csr)
+    res = vk.propagate(g, [15, 10, 5], p0)
+    for k in range(4):
+        hop, tot = port.propagate(csr, [15, 10, 5], p0[k])
+        close(res[k].hop, hop)
+        close(res[k].total, tot)
+        assert np.all((tot == 0) == (res[k].total == 0))
+        assert np.all((tot == 1) == (res[k].total == 1))
+
+
+def test_float_lm_storage_falls_back_for_subnormal_terms(vk, port, monkeypatch):
+    """A nonzero w*p below FLT_MIN would lose relative accuracy in float
+    storage: the library detects it and redoes the pass in double."""
+    monkeypatch.setenv("VK_VIP_LM", "32")
+    csr = port.generate("pa", 2000, 4, 3)
+    p0 = np.zeros(csr.n)
+    p0[:50] = 1e-200
+    p0[50:60] = 0.5
+    g = dev_graph(vk, csr)
+    s = vk.propagate(g, [5, 5], p0)
+    hop, tot = port.propagate(csr, [5, 5], p0)
+    close(s.hop, hop)
+    close(s.total, tot)
