@@ -133,23 +133,24 @@ __device__ __forceinline__ void load_lm(const void* __restrict__ lmv, std::uint3
 template <int C, int G, class LM>
 __device__ __forceinline__ void lane_sum(const HopParams& p, std::uint64_t a, std::uint64_t b, int lane,
                                          double* s) {
-  std::uint64_t i = a + lane;
-  for (; i + 3 * G < b; i += 4 * G) {
-    const std::uint32_t v0 = __ldg(p.tgt + i), v1 = __ldg(p.tgt + i + G), v2 = __ldg(p.tgt + i + 2 * G),
-                        v3 = __ldg(p.tgt + i + 3 * G);
-    double x0[C], x1[C], x2[C], x3[C];
-    load_lm<C, LM>(p.lm, v0, x0);
-    load_lm<C, LM>(p.lm, v1, x1);
-    load_lm<C, LM>(p.lm, v2, x2);
-    load_lm<C, LM>(p.lm, v3, x3);
+  // batches of 4 predicated index loads, then 4 independent lm gathers: every
+  // batch costs two memory round trips, whatever the row's length
+  for (std::uint64_t i = a + lane; i < b; i += 4 * G) {
+    std::uint32_t v[4];
 #pragma unroll
-    for (int c = 0; c < C; ++c) s[c] += (x0[c] + x1[c]) + (x2[c] + x3[c]);
-  }
-  for (; i < b; i += G) {
-    double x[C];
-    load_lm<C, LM>(p.lm, __ldg(p.tgt + i), x);
+    for (int k = 0; k < 4; ++k) v[k] = i + k * G < b ? __ldg(p.tgt + i + k * G) : 0u;
+    double x[4][C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) s[c] += x[c];
+    for (int k = 0; k < 4; ++k) {
+      if (i + k * G < b) {
+        load_lm<C, LM>(p.lm, v[k], x[k]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) x[k][c] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) s[c] += (x[0][c] + x[1][c]) + (x[2][c] + x[3][c]);
   }
 }
 
@@ -163,16 +164,29 @@ __global__ void __launch_bounds__(256) k_pull_group(HopParams p, const std::uint
   const std::uint64_t warp = (blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x) / 32;
   const std::uint64_t nwarps = ((std::uint64_t)gridDim.x * blockDim.x) / 32;
   const int gw = (threadIdx.x % 32) / G;
-  for (std::uint64_t r0 = warp * kGroupsPerWarp; r0 < nrows; r0 += nwarps * kGroupsPerWarp) {
+  // the next row's id and offsets are fetched while this row is summed
+  std::uint64_t r0 = warp * kGroupsPerWarp;
+  std::uint32_t u = 0;
+  std::uint64_t ra = 0, rb = 0;
+  if (r0 + gw < nrows) {
+    u = rows[r0 + gw];
+    ra = p.off[u];
+    rb = p.off[u + 1];
+  }
+  for (; r0 < nrows; r0 += nwarps * kGroupsPerWarp) {
     const std::uint64_t r = r0 + gw;
+    const std::uint64_t rn = r + nwarps * kGroupsPerWarp;
+    std::uint32_t un = 0;
+    std::uint64_t na = 0, nb = 0;
+    if (rn < nrows) {
+      un = rows[rn];
+      na = p.off[un];
+      nb = p.off[un + 1];
+    }
     double s[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) s[c] = 0.0;
-    std::uint32_t u = 0;
-    if (r < nrows) {
-      u = rows[r];
-      lane_sum<C, G, LM>(p, p.off[u], p.off[u + 1], lane, s);
-    }
+    if (r < nrows) lane_sum<C, G, LM>(p, ra, rb, lane, s);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1)
 #pragma unroll
@@ -182,6 +196,9 @@ __global__ void __launch_bounds__(256) k_pull_group(HopParams p, const std::uint
       for (int c = 0; c < C; ++c)
         if (c % G == lane) epilogue<C, LM>(p, u, c, s[c]);
     }
+    u = un;
+    ra = na;
+    rb = nb;
   }
 }
 
