@@ -92,6 +92,27 @@ __device__ __forceinline__ void epilogue(const HopParams& p, std::uint64_t u, in
   }
 }
 
+template <int C>
+__device__ __forceinline__ void load_lm_f(const void* __restrict__ lmv, std::uint32_t v, float* out) {
+  const float* lm = static_cast<const float*>(lmv) + (std::uint64_t)v * C;
+  if constexpr (C == 1) {
+    out[0] = __ldg(lm);
+  } else if constexpr (C == 2) {
+    const float2 x = __ldg(reinterpret_cast<const float2*>(lm));
+    out[0] = x.x;
+    out[1] = x.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < C / 4; ++k) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(lm) + k);
+      out[4 * k] = x.x;
+      out[4 * k + 1] = x.y;
+      out[4 * k + 2] = x.z;
+      out[4 * k + 3] = x.w;
+    }
+  }
+}
+
 template <int C, class LM>
 __device__ __forceinline__ void load_lm(const void* __restrict__ lmv, std::uint32_t v, double* out) {
   if constexpr (sizeof(LM) == 4) {
@@ -139,18 +160,35 @@ __device__ __forceinline__ void lane_sum(const HopParams& p, std::uint64_t a, st
     std::uint32_t v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = i + k * G < b ? __ldg(p.tgt + i + k * G) : 0u;
-    double x[4][C];
+    if constexpr (sizeof(LM) == 4) {
+      // float storage: the 4 terms of a batch are added in float (error
+      // ~2e-7 relative, bounded whatever the degree) and converted once
+      float x[4][C];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (i + k * G < b) {
-        load_lm<C, LM>(p.lm, v[k], x[k]);
-      } else {
+      for (int k = 0; k < 4; ++k) {
+        if (i + k * G < b) {
+          load_lm_f<C>(p.lm, v[k], x[k]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < C; ++c) x[k][c] = 0.0;
+          for (int c = 0; c < C; ++c) x[k][c] = 0.0f;
+        }
       }
-    }
 #pragma unroll
-    for (int c = 0; c < C; ++c) s[c] += (x[0][c] + x[1][c]) + (x[2][c] + x[3][c]);
+      for (int c = 0; c < C; ++c) s[c] += (double)((x[0][c] + x[1][c]) + (x[2][c] + x[3][c]));
+    } else {
+      double x[4][C];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (i + k * G < b) {
+          load_lm<C, LM>(p.lm, v[k], x[k]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c) x[k][c] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) s[c] += (x[0][c] + x[1][c]) + (x[2][c] + x[3][c]);
+    }
   }
 }
 
