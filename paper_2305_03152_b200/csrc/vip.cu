@@ -22,6 +22,7 @@
 // doubles).
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "internal.cuh"
@@ -63,8 +64,12 @@ struct HopParams {
 };
 
 template <class LM>
+__device__ __forceinline__ void store_lm(const HopParams& p, void* dst, std::uint64_t i, double wp);
+__device__ __forceinline__ double log1p_neg_fast(double x);
+
+template <class LM>
 __device__ __forceinline__ void store_lm(const HopParams& p, void* dst, std::uint64_t i, double wp) {
-  const double x = log1p(-wp);
+  const double x = sizeof(LM) == 4 ? log1p_neg_fast(wp) : log1p(-wp);
   if constexpr (sizeof(LM) == 4) {
     // below FLT_MIN the float copy of log1p(-wp) ~ -wp loses relative accuracy:
     // flag it, and the host reruns the propagation with double storage
@@ -73,24 +78,48 @@ __device__ __forceinline__ void store_lm(const HopParams& p, void* dst, std::uin
   static_cast<LM*>(dst)[i] = (LM)x;
 }
 
+// Float-storage mode evaluates the epilogue's transcendentals in float
+// (relative error ~1e-7, inside the 1e-5 contract); tiny arguments take the
+// first-order form, which is exact to 1e-30 relative and keeps values far
+// below FLT_MIN. Double-storage mode (small graphs, the exact reference
+// checks) keeps the double functions.
+__device__ __forceinline__ double neg_expm1_fast(double s) {  // -expm1(s), s <= 0
+  if (s > -1e-30) return -s;
+  return -(double)expm1f((float)s);
+}
+__device__ __forceinline__ double log1p_neg_fast(double x) {  // log1p(-x), 0 <= x <= 1
+  if (x < 1e-30) return -x;
+  return (double)log1pf(-(float)x);
+}
+
+// TransitionModel::weight (vip.hpp:22-26) of sampler u for the next hop.
+__device__ __forceinline__ double next_weight(const HopParams& p, std::uint64_t u) {
+  const double d = (double)p.outdeg[u];
+  return d <= p.f_next ? 1.0 : p.f_next / d;
+}
+
 template <int C, class LM>
-__device__ __forceinline__ void epilogue(const HopParams& p, std::uint64_t u, int c, double s) {
-  const double cur = clamp_prob(-expm1(s));
+__device__ __forceinline__ void epilogue(const HopParams& p, std::uint64_t u, int c, double s, double w) {
+  constexpr bool kFast = sizeof(LM) == 4;
+  const double cur = clamp_prob(kFast ? neg_expm1_fast(s) : -expm1(s));
   if (p.write_hop) p.hop_out[c * p.hop_col_stride + (std::uint64_t)(p.h - 1) * p.n + u] = cur;
   double* acc = p.total + (std::uint64_t)c * p.n + u;
-  const double term = log1p(-cur);
+  const double term = kFast ? log1p_neg_fast(cur) : log1p(-cur);
   const double a = p.h == 1 ? term : (*acc + term);
   if (p.h == p.L) {
-    *acc = clamp_prob(-expm1(a));
+    *acc = clamp_prob(kFast ? neg_expm1_fast(a) : -expm1(a));
   } else {
     *acc = a;
-    // hoist for hop h+1: TransitionModel::weight (vip.hpp:22-26) of sampler u
-    const double d = (double)p.outdeg[u];
-    const double w = d <= p.f_next ? 1.0 : p.f_next / d;
     const double wp = cur == 0.0 ? 0.0 : w * cur;  // vip.cpp:58-60
     store_lm<LM>(p, p.lm_next, u * C + c, wp);
   }
 }
+
+// Accumulator of a pull: float when the lm terms are stored in float. The
+// sums are tree-shaped (4-term batches, per-lane batches, log2 lane
+// reduction), so the float error stays ~(log2(deg) + batches) x 6e-8 relative.
+template <class LM>
+using AccT = std::conditional_t<sizeof(LM) == 4, float, double>;
 
 template <int C>
 __device__ __forceinline__ void load_lm_f(const void* __restrict__ lmv, std::uint32_t v, float* out) {
@@ -153,7 +182,7 @@ __device__ __forceinline__ void load_lm(const void* __restrict__ lmv, std::uint3
 // flight).
 template <int C, int G, class LM>
 __device__ __forceinline__ void lane_sum(const HopParams& p, std::uint64_t a, std::uint64_t b, int lane,
-                                         double* s) {
+                                         AccT<LM>* s) {
   // batches of 4 predicated index loads, then 4 independent lm gathers: every
   // batch costs two memory round trips, whatever the row's length
   for (std::uint64_t i = a + lane; i < b; i += 4 * G) {
@@ -174,7 +203,7 @@ __device__ __forceinline__ void lane_sum(const HopParams& p, std::uint64_t a, st
         }
       }
 #pragma unroll
-      for (int c = 0; c < C; ++c) s[c] += (double)((x[0][c] + x[1][c]) + (x[2][c] + x[3][c]));
+      for (int c = 0; c < C; ++c) s[c] += (x[0][c] + x[1][c]) + (x[2][c] + x[3][c]);
     } else {
       double x[4][C];
 #pragma unroll
@@ -221,18 +250,19 @@ __global__ void __launch_bounds__(256) k_pull_group(HopParams p, const std::uint
       na = p.off[un];
       nb = p.off[un + 1];
     }
-    double s[C];
+    AccT<LM> s[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) s[c] = 0.0;
+    for (int c = 0; c < C; ++c) s[c] = 0;
     if (r < nrows) lane_sum<C, G, LM>(p, ra, rb, lane, s);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1)
 #pragma unroll
       for (int c = 0; c < C; ++c) s[c] += __shfl_xor_sync(0xffffffffu, s[c], o, G);
     if (r < nrows) {
+      const double w = p.h < p.L ? next_weight(p, u) : 1.0;
 #pragma unroll
       for (int c = 0; c < C; ++c)
-        if (c % G == lane) epilogue<C, LM>(p, u, c, s[c]);
+        if (c % G == lane) epilogue<C, LM>(p, u, c, s[c], w);
     }
     u = un;
     ra = na;
@@ -240,8 +270,8 @@ __global__ void __launch_bounds__(256) k_pull_group(HopParams p, const std::uint
   }
 }
 
-template <int C>
-__device__ __forceinline__ void block_reduce(double* s, double (*sh)[C]) {
+template <int C, class T>
+__device__ __forceinline__ void block_reduce(T* s, T (*sh)[C]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
@@ -254,7 +284,7 @@ __device__ __forceinline__ void block_reduce(double* s, double (*sh)[C]) {
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      double t = 0.0;
+      T t = 0;
       for (int k = 0; k < kCtaThreads / 32; ++k) t += sh[k][c];
       s[c] = t;
     }
@@ -266,17 +296,19 @@ __device__ __forceinline__ void block_reduce(double* s, double (*sh)[C]) {
 template <int C, class LM>
 __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(HopParams p, const std::uint32_t* __restrict__ rows,
                                                           std::uint64_t nrows) {
-  __shared__ double sh[kCtaThreads / 32][C];
+  __shared__ AccT<LM> sh[kCtaThreads / 32][C];
   for (std::uint64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const std::uint32_t u = rows[r];
-    double s[C];
+    AccT<LM> s[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) s[c] = 0.0;
+    for (int c = 0; c < C; ++c) s[c] = 0;
     lane_sum<C, kCtaThreads, LM>(p, p.off[u], p.off[u + 1], threadIdx.x, s);
-    block_reduce<C>(s, sh);
-    if (threadIdx.x == 0)
+    block_reduce<C, AccT<LM>>(s, sh);
+    if (threadIdx.x == 0) {
+      const double w = p.h < p.L ? next_weight(p, u) : 1.0;
 #pragma unroll
-      for (int c = 0; c < C; ++c) epilogue<C, LM>(p, u, c, s[c]);
+      for (int c = 0; c < C; ++c) epilogue<C, LM>(p, u, c, s[c], w);
+    }
   }
 }
 
@@ -286,16 +318,16 @@ template <int C, class LM>
 __global__ void __launch_bounds__(kCtaThreads) k_pull_chunk(HopParams p, const std::uint64_t* __restrict__ lo,
                                                             const std::uint64_t* __restrict__ hi,
                                                             std::uint64_t nchunks, double* __restrict__ partial) {
-  __shared__ double sh[kCtaThreads / 32][C];
+  __shared__ AccT<LM> sh[kCtaThreads / 32][C];
   for (std::uint64_t j = blockIdx.x; j < nchunks; j += gridDim.x) {
-    double s[C];
+    AccT<LM> s[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) s[c] = 0.0;
+    for (int c = 0; c < C; ++c) s[c] = 0;
     lane_sum<C, kCtaThreads, LM>(p, lo[j], hi[j], threadIdx.x, s);
-    block_reduce<C>(s, sh);
+    block_reduce<C, AccT<LM>>(s, sh);
     if (threadIdx.x == 0)
 #pragma unroll
-      for (int c = 0; c < C; ++c) partial[j * C + c] = s[c];
+      for (int c = 0; c < C; ++c) partial[j * C + c] = (double)s[c];
   }
 }
 
@@ -308,7 +340,7 @@ __global__ void k_split_finish(HopParams p, const std::uint32_t* __restrict__ ro
   for (int c = 0; c < C; ++c) {
     double s = 0.0;
     for (std::uint64_t j = first_chunk[r]; j < first_chunk[r + 1]; ++j) s += partial[j * C + c];
-    epilogue<C, LM>(p, rows[r], c, s);
+    epilogue<C, LM>(p, rows[r], c, s, p.h < p.L ? next_weight(p, rows[r]) : 1.0);
   }
 }
 
