@@ -135,19 +135,10 @@ def make_data(cfg, threads):
 
 
 def schedule(vk, cfg, roles, labels, parts, count):
-    """(epoch, partition, batch_index, seeds) in round-robin over `parts`,
-    epochs advancing as partitions run out (commsim.cpp:45-52 order per cell)."""
-    out, e = [], 0
-    b = cfg["b"]
-    while len(out) < count:
-        per = {k: vk.epoch_permutation(roles, labels, k, b, e, SAMPLE_SEED) for k in parts}
-        nb = {k: (len(per[k]) + b - 1) // b for k in parts}
-        for i in range(max(nb.values())):
-            for k in parts:
-                if i < nb[k]:
-                    out.append((e, k, i, per[k][i * b:(i + 1) * b]))
-        e += 1
-    return out[:count]
+    """(epoch, partition, batch_index, seeds), round-robin over `parts`."""
+    from paper_2305_03152_b200.dist import minibatch_schedule
+    return minibatch_schedule(lambda k, e: vk.epoch_permutation(roles, labels, k, cfg["b"], e, SAMPLE_SEED),
+                              parts, cfg["b"], count)
 
 
 # ------------------------------------------------------------------ b200 arm
@@ -199,18 +190,12 @@ def run_b200(args, cfg):
     plan = vk.build_cache(orders, cfg["alpha"], n)
     oon, ranges = vk.build_reorder(labels, K, totals, device=dev)
     plane = vk.FeaturePlane(n, K, cfg["dim"], labels, oon, ranges, dtype=cfg["dtype"], device=dev)
-    mine = [k for k in range(K) if k % world == rank]
+    from paper_2305_03152_b200.dist import exchange_plane_handles, max_over_ranks, owned_partitions
+    mine = owned_partitions(K, world, rank)
     for k in mine:
         plane.load_partition(k, plan.cached[k], feature_seed=FEATURE_SEED)
     if world > 1:
-        handles = {k: plane.export(k) for k in mine}
-        gathered = [None] * world
-        dist.all_gather_object(gathered, handles)
-        for r, hs in enumerate(gathered):
-            if r != rank:
-                for k, (h, rows) in hs.items():
-                    plane.attach(k, h, rows)
-        dist.barrier()
+        exchange_plane_handles(plane, mine)
 
     # ---- minibatch schedule + device-resident seeds
     W, S = args.warmup, args.steps
@@ -286,10 +271,7 @@ def run_b200(args, cfg):
     if world > 1:
         dist.barrier()
     e2e_ms = region(W + S, W + 2 * S, host=True, pinned=pinned)
-    tl = torch.tensor([ms, e2e_ms], dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(tl, op=dist.ReduceOp.MAX)
-    ms, e2e_ms = float(tl[0]), float(tl[1])
+    ms, e2e_ms = max_over_ranks([ms, e2e_ms])
 
     # ---- roofline of the dominant kernel (gather) and of the sampler, from the timed waves
     tally = hist_tally.cpu().numpy()
