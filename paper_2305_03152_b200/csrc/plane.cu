@@ -671,7 +671,8 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     gp.nmb = nmb;
     static const std::uint32_t tile_words = [] {
       const char* e = std::getenv("VK_GATHER_TILE_WORDS");
-      return e ? (std::uint32_t)std::atoi(e) : kGatherTileWords;
+      const std::uint32_t v = e ? (std::uint32_t)std::atoi(e) : kGatherTileWords;
+      return std::max<std::uint32_t>(64, (v + 63) / 64 * 64);  // rank words exist at multiples of 64
     }();
     gp.tile_words = tile_words;
     gp.tiles = (std::uint32_t)((gp.W + tile_words - 1) / tile_words);

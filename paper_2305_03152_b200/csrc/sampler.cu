@@ -193,6 +193,7 @@ struct SampleParams {
 // One thread per frontier vertex; FY state in shared memory (f <= 32) or in
 // local memory (MAXF > 0, large fanouts).
 constexpr int kSampleThreads = 128;
+constexpr std::uint64_t kRankStride = 64;  // rank words always written at multiples of this
 constexpr std::uint32_t kSampleTileWords = 64;  // 4096 source vertices per (tile, minibatch) CTA
 
 // Shared-memory sampler (every fanout <= 32). Per thread, in slot-major
@@ -410,7 +411,11 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
 #pragma unroll
   for (int k = 0; k < WPT; ++k) {
     const std::uint64_t w = w0 + k;
-    if (w < p.W)
+    // rank words are only ever read for set bits (relabel / relabel maps) and
+    // at tile starts (multiples of kRankStride words, the vertex-tile
+    // schedules): zero words elsewhere are skipped, which keeps sparse
+    // frontiers on huge graphs from paying 16 B per empty word
+    if (w < p.W && (wd[k] || (w % kRankStride) == 0))
       p.rank[mb * p.W + w] = make_uint4((unsigned)wd[k], (unsigned)(wd[k] >> 32), gbase + lpos, 0u);
     unsigned long long x = wd[k];
     while (x) {
@@ -534,7 +539,8 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
       // ~512 sources per (tile, minibatch) CTA at full frontier capacity,
       // at least kSampleTileWords words (4096 vertices) per tile
       const std::uint64_t want_tiles = std::max<std::uint64_t>(1, p.capFprev / 512);
-      const std::uint64_t tw = std::max<std::uint64_t>(kSampleTileWords, (s.W + want_tiles - 1) / want_tiles);
+      std::uint64_t tw = std::max<std::uint64_t>(kSampleTileWords, (s.W + want_tiles - 1) / want_tiles);
+      tw = (tw + kRankStride - 1) / kRankStride * kRankStride;  // tile starts carry rank words
       p.tile_words = (std::uint32_t)tw;
       const std::uint64_t tiles = (s.W + tw - 1) / tw;
       k_sample_smem<<<(unsigned)(tiles * nmb), kSampleThreads, smem, st>>>(p);
