@@ -57,6 +57,10 @@ CONFIGS = {
 # BASELINE.json configs[3]/[4]: ogbn-papers100M-shaped (111M nodes, 1.6B
 # edges = 3.3B CSR slots, 8 partitions). configs[4] is the VIP-analysis-only
 # sweep (2/3/4 hops, fanouts 5..25): `--config c5`.
+CONFIGS["c4"] = dict(workload="C4 ogbn-papers100M-shaped 111M nodes / 3.3B CSR slots, 128-d fp16, "
+                              "8 partitions, fanout (15,10,5), batch 1024, VIP cache 32% (sweep 0-32%)",
+                     n=111_059_956, d=15, K=8, p_in=0.8, train=0.011, dim=128, dtype=1, alpha=0.32,
+                     fanouts=(15, 10, 5), b=1024, alpha_sweep=(0.0, 0.04, 0.08, 0.16, 0.32))
 CONFIGS["c5"] = dict(workload="C5 VIP analysis on ogbn-papers100M-shaped 111M nodes / 3.3B CSR slots, "
                               "8 partitions, fanout sweep", n=111_059_956, d=15, K=8, p_in=0.8, train=0.011,
                      b=1024, fanouts=(15, 10, 5),
@@ -324,6 +328,32 @@ def run_b200(args, cfg):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if cfg.get("alpha_sweep"):
+        # miss rows of the same timed minibatches under each cache size
+        # (classification depends only on the plan; sampling is plan-free)
+        sweep = []
+        for a in cfg["alpha_sweep"]:
+            plan_a = vk.build_cache(orders, a, n)
+            plane_a = vk.FeaturePlane(n, K, cfg["dim"], labels, oon, ranges, dtype=cfg["dtype"], device=dev)
+            for k in range(K):
+                plane_a.load_partition(k, plan_a.cached[k], feature_seed=FEATURE_SEED)
+            tot = np.zeros(4, np.int64)
+            with torch.cuda.stream(stream):
+                for i in range(W, W + min(S, 4)):
+                    sp = samplers[0]
+                    wv = waves[i]
+                    sp.run(wave_offsets[i], [(e, k, bi) for (e, k, bi, _) in wv], stream=sh,
+                           seeds_device_ptr=seeds_d.data_ptr())
+                    plane_a.gather(sp, outs[0].data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh)
+                    torch.cuda.synchronize(dev)
+                    tot += hist_tally[i, :len(wv)].sum(0).cpu().numpy()
+            sweep.append({"alpha": a, "cache_rows_per_partition": len(plan_a.cached[0]),
+                          "local": int(tot[0]), "cache_hits": int(tot[1]), "miss_rows": int(tot[2])})
+            plane_a.close()
+        base = max(sweep[0]["miss_rows"], 1)
+        for r in sweep:
+            r["miss_reduction_vs_no_cache"] = 1.0 - r["miss_rows"] / base
+        result["alpha_sweep"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(cfg, off, tgt, labels, roles, plan, waves[W:W + S])
     if rank == 0:
@@ -502,13 +532,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--alpha-sweep", action="store_true", help="also tally misses for cache sizes 0-32%%")
     ap.add_argument("--wave", type=int, default=32, help="minibatches per step per GPU")
     ap.add_argument("--pipes", type=int, default=1, help="overlapped sampler+gather pipelines (streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.alpha_sweep and "alpha_sweep" not in cfg:
+        cfg["alpha_sweep"] = (0.0, 0.04, 0.08, 0.16, 0.32)
     if args.config == "c5" and args.impl != "reference":
         run_vip_sweep(args, cfg)
         return
