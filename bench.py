@@ -328,6 +328,11 @@ def run_b200(args, cfg):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if world > 1:
+        # the miss exchange of the last timed wave: distinct rows pulled over NVLink
+        pulled = plane.pulled_rows()
+        result["nvlink"] = {"rows_pulled_last_wave": pulled, "bytes_pulled_last_wave": pulled * rb,
+                            "rows_requested_last_wave": int(tally[W + 2 * S - 1, :len(waves[W + 2 * S - 1]), 3].sum())}
     if cfg.get("alpha_sweep"):
         # miss rows of the same timed minibatches under each cache size
         # (classification depends only on the plan; sampling is plan-free)

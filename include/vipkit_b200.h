@@ -242,10 +242,17 @@ VK_API int vk_plane_attach(vk_plane p, uint32_t k, const void* handle64, uint64_
  * out + i*out_stride_rows*row_bytes), from the local rows, the cache rows or
  * (miss) the owner partition's rows -- local HBM or a peer over NVLink.
  * counts_dev (device u64, nmb x 4, zeroed by the call): local, cache, miss,
- * miss rows served from another GPU. Asynchronous on `stream`. */
+ * miss rows served from another GPU. With attached peer partitions the wave's
+ * remote misses are first deduplicated (union over all minibatches of the
+ * wave) and each distinct row is pulled once over NVLink into local staging
+ * (the miss exchange); the rows are then copied from there. Asynchronous on
+ * `stream`. */
 VK_API int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_rows,
                            uint64_t* counts_dev, vk_stream_t stream);
 VK_API int vk_plane_row_bytes(vk_plane p, uint64_t* row_bytes);
+/* Distinct remote rows the last multi-GPU gather pulled over NVLink (the
+ * wave's deduplicated miss exchange); synchronises the device. */
+VK_API int vk_plane_pulled_rows(vk_plane p, uint64_t* rows);
 
 /* ------------------------------------------------------- synthetic data
  * Community-structured power-law generator for the BASELINE configs (builder

@@ -57,6 +57,11 @@ struct vk_plane_s {
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // remote-row gathers run here concurrently
   cudaEvent_t fork = nullptr, join = nullptr;
+  // per-wave deduplicated pull of remote rows (multi-GPU): union bitmap of
+  // the wave's remote misses, its rank prefix, the distinct list, and the
+  // local staging copy of those rows
+  vk::DevBuf ubits, uprefix, ulist, staging, scan_tmp;
+  std::size_t scan_bytes = 0;
 };
 
 namespace vk {
@@ -177,6 +182,10 @@ struct GatherParams {
   const uint4* all_rank;             // [nmb][W] {bits, rank prefix} of all_vertices
   std::uint64_t W;
   std::uint32_t nmb, tiles, tile_words;
+  // deduplicated remote rows: staged[rank of v in the wave's remote set]
+  const unsigned long long* ubits;
+  const std::uint32_t* uprefix;
+  const char* staging;
 };
 
 // Streaming 16/4/2-byte copies: the feature table is read through L1
@@ -208,6 +217,87 @@ __device__ __forceinline__ void st_stream(T* p, const T& v) {
 // owner partition's row, local HBM or a peer GPU over NVLink), then the warp
 // copies the group as one flat, fully coalesced range of 32*V vectors with
 // kUnroll independent loads in flight per lane.
+// Multi-GPU miss exchange, step 1: the union of the wave's remote misses
+// (rows whose owner partition lives on another GPU and that are neither
+// local nor cached for the minibatch's partition) as a bitmap over vertices.
+__global__ void __launch_bounds__(256) k_remote_mark(GatherParams p, unsigned long long* __restrict__ ubits) {
+  const std::uint32_t mb = blockIdx.y;
+  const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
+  const std::uint32_t cnt = p.all_count[mb];
+  const std::uint32_t* all = p.all + mb * p.all_stride;
+  const std::uint32_t* slot = p.slot[k];
+  for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < cnt; r += gridDim.x * blockDim.x) {
+    const std::uint32_t v = __ldg(all + r);
+    if (__ldg(slot + v) == VK_MISS && p.peer_mask[__ldg(p.part_of + v)])
+      atomicOr(ubits + (v >> 6), 1ull << (v & 63));
+  }
+}
+
+__global__ void k_word_popc(const unsigned long long* __restrict__ bits, std::uint64_t W,
+                            std::uint32_t* __restrict__ out) {
+  for (std::uint64_t w = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; w < W;
+       w += (std::uint64_t)gridDim.x * blockDim.x)
+    out[w] = (std::uint32_t)__popcll(bits[w]);
+}
+
+__global__ void k_emit_list(const unsigned long long* __restrict__ bits, const std::uint32_t* __restrict__ prefix,
+                            std::uint64_t W, std::uint32_t* __restrict__ list) {
+  for (std::uint64_t w = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; w < W;
+       w += (std::uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long x = bits[w];
+    std::uint32_t pos = prefix[w];
+    while (x) {
+      const int b = __ffsll(x) - 1;
+      x &= x - 1;
+      list[pos++] = (std::uint32_t)(w * 64 + b);
+    }
+  }
+}
+
+// Step 2: one NVLink read per distinct remote row into the staging buffer
+// (warp per 32 rows, 128-bit copies); the gather then serves every
+// minibatch's remote misses from local HBM.
+template <class T, int kUnroll>
+__global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::uint32_t* __restrict__ list,
+                                                     const std::uint32_t* __restrict__ count_ptr, T* __restrict__ staging) {
+  __shared__ const T* s_src[8][32];
+  const std::uint32_t cnt = *count_ptr;
+  const std::uint32_t V = p.V;
+  const std::uint32_t magic = p.magic32;
+  const std::uint64_t rowv = p.row_bytes / sizeof(T);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const std::uint32_t gw = blockIdx.x * (blockDim.x >> 5) + w, nw = gridDim.x * (blockDim.x >> 5);
+  for (std::uint32_t r0 = gw * 32; r0 < cnt; r0 += nw * 32) {
+    const std::uint32_t r = r0 + lane;
+    const T* src = nullptr;
+    if (r < cnt) {
+      const std::uint32_t v = __ldg(list + r);
+      src = reinterpret_cast<const T*>(p.base[__ldg(p.part_of + v)]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
+    }
+    s_src[w][lane] = src;
+    __syncwarp();
+    const std::uint32_t total = min(32u, cnt - r0) * V;
+    T* dst = staging + (std::uint64_t)r0 * V;
+    for (std::uint32_t e0 = lane; e0 < total; e0 += 32 * kUnroll) {
+      T val[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const std::uint32_t e = e0 + 32 * u;
+        if (e < total) {
+          const std::uint32_t row = V == 1 ? e : __umulhi(e, magic);
+          val[u] = s_src[w][row][e - row * V];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const std::uint32_t e = e0 + 32 * u;
+        if (e < total) dst[e] = val[u];
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // MODE 0: every row (no peer partitions). MODE 1: rows served from this GPU
 // (local rows, cache rows, misses owned by a co-resident partition). MODE 2:
 // rows owned by a partition on another GPU, read over NVLink. With peers the
@@ -254,7 +344,18 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
       } else {
         const std::uint32_t o = __ldg(p.part_of + v);
         const bool remote = p.peer_mask[o] != 0;
-        if ((MODE == 0) || (MODE == 1 && !remote) || (MODE == 2 && remote)) {
+        if (MODE == 3) {
+          if (remote) {  // pulled once per wave into the local staging buffer
+            const std::uint32_t wq = v >> 6;
+            const std::uint32_t idx = __ldg(p.uprefix + wq) +
+                                      (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (v & 63)) - 1ull));
+            src = reinterpret_cast<const T*>(p.staging) + (std::uint64_t)idx * rowv;
+          } else {
+            src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
+          }
+          ++c_miss;
+          c_peer += remote;
+        } else if ((MODE == 0) || (MODE == 1 && !remote) || (MODE == 2 && remote)) {
           src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
           ++c_miss;
           c_peer += remote;
@@ -262,7 +363,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
       }
     }
     std::uint32_t rows;
-    if (MODE == 0) {
+    if (MODE == 0 || MODE == 3) {
       s_src[w][lane] = src;
       s_row[w][lane] = lane;
       rows = min(32u, hi - r0);
@@ -616,6 +717,19 @@ int vk_plane_attach(vk_plane p, uint32_t k, const void* handle64, uint64_t rows)
   });
 }
 
+int vk_plane_pulled_rows(vk_plane p, uint64_t* rows) {
+  return guard([&] {
+    if (!p || !rows) raise(VK_ERR_PARAMETER, "null argument");
+    *rows = 0;
+    if (!p->uprefix.p) return;
+    DeviceGuard dg(p->device);
+    std::uint32_t c = 0;
+    VK_CUDA(cudaDeviceSynchronize());
+    VK_CUDA(cudaMemcpy(&c, p->uprefix.as<std::uint32_t>() + (p->n + 63) / 64, 4, cudaMemcpyDeviceToHost));
+    *rows = c;
+  });
+}
+
 int vk_plane_row_bytes(vk_plane p, uint64_t* row_bytes) {
   return guard([&] {
     if (!p || !row_bytes) raise(VK_ERR_PARAMETER, "null argument");
@@ -683,27 +797,81 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       const char* e = std::getenv("VK_GATHER_SPLIT");
       return e && std::atoi(e) != 0;
     }();
-    bool peers = false;
-    for (const auto& q : p->parts) peers |= q.attached;
-    peers = peers && split;
+    bool any_peer = false;
+    for (const auto& q : p->parts) any_peer |= q.attached;
+    const bool peers = any_peer && split;
+    const bool staged = any_peer && !split;
+    if (staged) {
+      // miss exchange: union of the wave's remote misses -> distinct list ->
+      // one NVLink pull per distinct row into local staging -> the gather
+      // reads staged rows from HBM
+      const std::uint64_t W = gp.W, n = p->n;
+      auto ensure = [](DevBuf& b, std::size_t bytes) {
+        if (b.bytes < bytes) b.alloc(bytes);
+      };
+      ensure(p->ubits, W * 8);
+      ensure(p->uprefix, (W + 1) * 4);
+      ensure(p->ulist, n * 4);
+      ensure(p->staging, n * p->row_bytes);
+      if (!p->scan_bytes) {
+        VK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, p->scan_bytes, p->uprefix.as<std::uint32_t>(),
+                                              p->uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), st));
+        p->scan_tmp.alloc(std::max<std::size_t>(p->scan_bytes, 1));
+      }
+      VK_CUDA(cudaMemsetAsync(p->ubits.p, 0, W * 8, st));
+      VK_CUDA(cudaMemsetAsync(p->uprefix.as<std::uint32_t>() + W, 0, 4, st));
+      const unsigned gx = (unsigned)std::max<std::uint64_t>(
+          1, std::min<std::uint64_t>(ceil_div(gp.all_stride, 256), (std::uint64_t)sm_count(p->device) * 8 / nmb + 1));
+      k_remote_mark<<<dim3(gx, nmb), 256, 0, st>>>(gp, p->ubits.as<unsigned long long>());
+      k_word_popc<<<grid_for(W, p->device), 256, 0, st>>>(p->ubits.as<unsigned long long>(), W,
+                                                          p->uprefix.as<std::uint32_t>());
+      std::size_t tb = p->scan_bytes;
+      VK_CUDA(cub::DeviceScan::ExclusiveSum(p->scan_tmp.p, tb, p->uprefix.as<std::uint32_t>(),
+                                            p->uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), st));
+      k_emit_list<<<grid_for(W, p->device), 256, 0, st>>>(p->ubits.as<unsigned long long>(),
+                                                          p->uprefix.as<std::uint32_t>(), W,
+                                                          p->ulist.as<std::uint32_t>());
+      const unsigned pg = (unsigned)sm_count(p->device) * 8;
+      if (v16)
+        k_remote_pull<uint4, 8><<<pg, 256, 0, st>>>(gp, p->ulist.as<std::uint32_t>(),
+                                                     p->uprefix.as<std::uint32_t>() + W, p->staging.as<uint4>());
+      else if (v4)
+        k_remote_pull<std::uint32_t, 8><<<pg, 256, 0, st>>>(gp, p->ulist.as<std::uint32_t>(),
+                                                             p->uprefix.as<std::uint32_t>() + W,
+                                                             p->staging.as<std::uint32_t>());
+      else
+        k_remote_pull<std::uint16_t, 8><<<pg, 256, 0, st>>>(gp, p->ulist.as<std::uint32_t>(),
+                                                             p->uprefix.as<std::uint32_t>() + W,
+                                                             p->staging.as<std::uint16_t>());
+      count_launch(6);
+      VK_LAUNCH_CHECK();
+      gp.ubits = p->ubits.as<unsigned long long>();
+      gp.uprefix = p->uprefix.as<std::uint32_t>();
+      gp.staging = p->staging.as<char>();
+    }
     auto launch = [&](int mode, cudaStream_t where) {
       if (v16) {
-        if (mode == 0) k_gather<uint4, 8, 4, 0><<<grid, 256, 0, where>>>(gp);
+        if (mode == 3) k_gather<uint4, 8, 4, 3><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 0) k_gather<uint4, 8, 4, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<uint4, 8, 4, 1><<<grid, 256, 0, where>>>(gp);
         else k_gather<uint4, 16, 2, 2, false><<<grid, 256, 0, where>>>(gp);  // peer rows: plain LDG
       } else if (v4) {
-        if (mode == 0) k_gather<std::uint32_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
+        if (mode == 3) k_gather<std::uint32_t, 8, 1, 3><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 0) k_gather<std::uint32_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<std::uint32_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
         else k_gather<std::uint32_t, 8, 1, 2><<<grid, 256, 0, where>>>(gp);
       } else {
-        if (mode == 0) k_gather<std::uint16_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
+        if (mode == 3) k_gather<std::uint16_t, 8, 1, 3><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 0) k_gather<std::uint16_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<std::uint16_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
         else k_gather<std::uint16_t, 8, 1, 2><<<grid, 256, 0, where>>>(gp);
       }
       count_launch();
       VK_LAUNCH_CHECK();
     };
-    if (!peers) {
+    if (staged) {
+      launch(3, st);
+    } else if (!peers) {
       launch(0, st);
     } else {
       // fork: remote (NVLink) rows on the plane's auxiliary stream, local rows on st

@@ -129,6 +129,7 @@ def lib():
     L.vk_plane_attach.argtypes = [c_vp, c_u32, c_vp, c_u64]
     L.vk_plane_gather.argtypes = [c_vp, c_vp, c_vp, c_u64, c_vp, c_vp]
     L.vk_plane_row_bytes.argtypes = [c_vp, C.POINTER(c_u64)]
+    L.vk_plane_pulled_rows.argtypes = [c_vp, C.POINTER(c_u64)]
     L.vk_synth_community_powerlaw.argtypes = [c_u64, c_u64, c_u32, c_double, c_u64, C.c_uint,
                                               C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), u32p]
     L.vk_debug_stream_draws.argtypes = [c_int, c_u64, c_u64, c_u64, u64p]
@@ -567,6 +568,12 @@ class FeaturePlane:
     def gather(self, sampler: Sampler, out_ptr, out_stride_rows, counts_ptr, stream=0):
         check(lib().vk_plane_gather(self._h, sampler.handle, out_ptr, out_stride_rows, counts_ptr,
                                     stream or None))
+
+    def pulled_rows(self) -> int:
+        """Distinct remote rows pulled over NVLink by the last gather."""
+        r = c_u64()
+        check(lib().vk_plane_pulled_rows(self._h, C.byref(r)))
+        return r.value
 
     def close(self):
         if self._h:
