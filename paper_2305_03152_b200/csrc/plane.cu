@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -60,8 +61,14 @@ struct vk_plane_s {
   // per-wave deduplicated pull of remote rows (multi-GPU): union bitmap of
   // the wave's remote misses, its rank prefix, the distinct list, and the
   // local staging copy of those rows
-  vk::DevBuf ubits, uprefix, ulist, staging, scan_tmp;
-  std::size_t scan_bytes = 0;
+  struct StageSet {
+    vk::DevBuf ubits, uprefix, ulist, staging, scan_tmp;
+    std::size_t scan_bytes = 0;
+  };
+  // one set per sampler, so overlapped waves (one sampler per pipeline
+  // stream) never share staging
+  std::map<const void*, StageSet> stage_sets;
+  const StageSet* last_set = nullptr;
 };
 
 namespace vk {
@@ -721,11 +728,11 @@ int vk_plane_pulled_rows(vk_plane p, uint64_t* rows) {
   return guard([&] {
     if (!p || !rows) raise(VK_ERR_PARAMETER, "null argument");
     *rows = 0;
-    if (!p->uprefix.p) return;
+    if (!p->last_set) return;
     DeviceGuard dg(p->device);
     std::uint32_t c = 0;
     VK_CUDA(cudaDeviceSynchronize());
-    VK_CUDA(cudaMemcpy(&c, p->uprefix.as<std::uint32_t>() + (p->n + 63) / 64, 4, cudaMemcpyDeviceToHost));
+    VK_CUDA(cudaMemcpy(&c, p->last_set->uprefix.as<std::uint32_t>() + (p->n + 63) / 64, 4, cudaMemcpyDeviceToHost));
     *rows = c;
   });
 }
@@ -809,45 +816,47 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       auto ensure = [](DevBuf& b, std::size_t bytes) {
         if (b.bytes < bytes) b.alloc(bytes);
       };
-      ensure(p->ubits, W * 8);
-      ensure(p->uprefix, (W + 1) * 4);
-      ensure(p->ulist, n * 4);
-      ensure(p->staging, n * p->row_bytes);
-      if (!p->scan_bytes) {
-        VK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, p->scan_bytes, p->uprefix.as<std::uint32_t>(),
-                                              p->uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), st));
-        p->scan_tmp.alloc(std::max<std::size_t>(p->scan_bytes, 1));
+      auto& ss = p->stage_sets[static_cast<const void*>(s)];
+      p->last_set = &ss;
+      ensure(ss.ubits, W * 8);
+      ensure(ss.uprefix, (W + 1) * 4);
+      ensure(ss.ulist, n * 4);
+      ensure(ss.staging, n * p->row_bytes);
+      if (!ss.scan_bytes) {
+        VK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, ss.scan_bytes, ss.uprefix.as<std::uint32_t>(),
+                                              ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), st));
+        ss.scan_tmp.alloc(std::max<std::size_t>(ss.scan_bytes, 1));
       }
-      VK_CUDA(cudaMemsetAsync(p->ubits.p, 0, W * 8, st));
-      VK_CUDA(cudaMemsetAsync(p->uprefix.as<std::uint32_t>() + W, 0, 4, st));
+      VK_CUDA(cudaMemsetAsync(ss.ubits.p, 0, W * 8, st));
+      VK_CUDA(cudaMemsetAsync(ss.uprefix.as<std::uint32_t>() + W, 0, 4, st));
       const unsigned gx = (unsigned)std::max<std::uint64_t>(
           1, std::min<std::uint64_t>(ceil_div(gp.all_stride, 256), (std::uint64_t)sm_count(p->device) * 8 / nmb + 1));
-      k_remote_mark<<<dim3(gx, nmb), 256, 0, st>>>(gp, p->ubits.as<unsigned long long>());
-      k_word_popc<<<grid_for(W, p->device), 256, 0, st>>>(p->ubits.as<unsigned long long>(), W,
-                                                          p->uprefix.as<std::uint32_t>());
-      std::size_t tb = p->scan_bytes;
-      VK_CUDA(cub::DeviceScan::ExclusiveSum(p->scan_tmp.p, tb, p->uprefix.as<std::uint32_t>(),
-                                            p->uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), st));
-      k_emit_list<<<grid_for(W, p->device), 256, 0, st>>>(p->ubits.as<unsigned long long>(),
-                                                          p->uprefix.as<std::uint32_t>(), W,
-                                                          p->ulist.as<std::uint32_t>());
+      k_remote_mark<<<dim3(gx, nmb), 256, 0, st>>>(gp, ss.ubits.as<unsigned long long>());
+      k_word_popc<<<grid_for(W, p->device), 256, 0, st>>>(ss.ubits.as<unsigned long long>(), W,
+                                                          ss.uprefix.as<std::uint32_t>());
+      std::size_t tb = ss.scan_bytes;
+      VK_CUDA(cub::DeviceScan::ExclusiveSum(ss.scan_tmp.p, tb, ss.uprefix.as<std::uint32_t>(),
+                                            ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), st));
+      k_emit_list<<<grid_for(W, p->device), 256, 0, st>>>(ss.ubits.as<unsigned long long>(),
+                                                          ss.uprefix.as<std::uint32_t>(), W,
+                                                          ss.ulist.as<std::uint32_t>());
       const unsigned pg = (unsigned)sm_count(p->device) * 8;
       if (v16)
-        k_remote_pull<uint4, 8><<<pg, 256, 0, st>>>(gp, p->ulist.as<std::uint32_t>(),
-                                                     p->uprefix.as<std::uint32_t>() + W, p->staging.as<uint4>());
+        k_remote_pull<uint4, 8><<<pg, 256, 0, st>>>(gp, ss.ulist.as<std::uint32_t>(),
+                                                     ss.uprefix.as<std::uint32_t>() + W, ss.staging.as<uint4>());
       else if (v4)
-        k_remote_pull<std::uint32_t, 8><<<pg, 256, 0, st>>>(gp, p->ulist.as<std::uint32_t>(),
-                                                             p->uprefix.as<std::uint32_t>() + W,
-                                                             p->staging.as<std::uint32_t>());
+        k_remote_pull<std::uint32_t, 8><<<pg, 256, 0, st>>>(gp, ss.ulist.as<std::uint32_t>(),
+                                                             ss.uprefix.as<std::uint32_t>() + W,
+                                                             ss.staging.as<std::uint32_t>());
       else
-        k_remote_pull<std::uint16_t, 8><<<pg, 256, 0, st>>>(gp, p->ulist.as<std::uint32_t>(),
-                                                             p->uprefix.as<std::uint32_t>() + W,
-                                                             p->staging.as<std::uint16_t>());
+        k_remote_pull<std::uint16_t, 8><<<pg, 256, 0, st>>>(gp, ss.ulist.as<std::uint32_t>(),
+                                                             ss.uprefix.as<std::uint32_t>() + W,
+                                                             ss.staging.as<std::uint16_t>());
       count_launch(6);
       VK_LAUNCH_CHECK();
-      gp.ubits = p->ubits.as<unsigned long long>();
-      gp.uprefix = p->uprefix.as<std::uint32_t>();
-      gp.staging = p->staging.as<char>();
+      gp.ubits = ss.ubits.as<unsigned long long>();
+      gp.uprefix = ss.uprefix.as<std::uint32_t>();
+      gp.staging = ss.staging.as<char>();
     }
     auto launch = [&](int mode, cudaStream_t where) {
       if (v16) {
