@@ -504,7 +504,8 @@ def run_reference(args, cfg):
         orders.append(R.rank_by_scores(labels, K, k, tot)[0])
     _, bits = R.build_cache(orders, cfg["alpha"], n)
     # per-step minibatch count bounded so the whole run stays within minutes
-    per_step = max(1, min(M, int(os.environ.get("VIPKIT_REF_MB_PER_STEP", "4"))))
+    # one minibatch per host thread per step (expand is pure; sampling.cpp:82)
+    per_step = max(1, min(M, int(os.environ.get("VIPKIT_REF_MB_PER_STEP", str(threads)))))
     sched = schedule(vk, cfg, roles, labels, list(range(K)), (W + S) * per_step)
     t_all = 0.0
     for i in range(W + S):
