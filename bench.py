@@ -297,6 +297,14 @@ def run_b200(args, cfg):
         s_bytes += int(sum(16 * fc[h - 1].sum() + 8 * ec[h].sum() for h in range(1, L + 1))
                        + 8 * (fc[1:].sum() + ac.sum()))
     hbm, peak_kind = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(args.config)
+        if t and t.get("minibatches_per_launch") == M:
+            traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+    except Exception:  # noqa: BLE001
+        pass
     g_ach = g_bytes / S / (statistics.mean(gather_ms) / 1e3) / 1e9
     s_ach = s_bytes / S / (statistics.mean(sample_ms) / 1e3) / 1e9
     total_mb = sum(len(waves[i]) for i in range(W, W + S)) * world
@@ -316,7 +324,9 @@ def run_b200(args, cfg):
         "e2e": {"value": e2e_val, "unit": "minibatches/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": M * 4 * 8},
         "roofline": {"bound": "hbm", "kernel": "k_gather (classify+gather)", "achieved": g_ach,
-                     "peak": hbm, "unit": "GB/s", "frac": g_ach / hbm, "traffic": None,
+                     "peak": hbm, "unit": "GB/s", "frac": g_ach / hbm, "traffic": traffic,
+                     "traffic_note": "ncu dram read+write per launch (profiles/traffic.json); below the algorithmic "
+                                     "bytes because rows shared by minibatches of a wave are L2 hits",
                      "peak_kind": peak_kind, "bytes_per_launch": g_bytes / S,
                      "ms_per_launch": statistics.mean(gather_ms)},
         "sampler": {"ms_per_wave": statistics.mean(sample_ms), "achieved_gbs": s_ach,
