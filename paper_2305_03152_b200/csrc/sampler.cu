@@ -383,11 +383,21 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     }
     vc += __popcll(wd[k]);
     if (HAS_NEXT) {
+      // next-hop row lengths min(f, deg): degree loads issued 8 at a time
       unsigned long long x = wd[k];
       while (x) {
-        const int b = __ffsll(x) - 1;
-        x &= x - 1;
-        dc += min(p.f_next, __ldg(p.outdeg + (std::uint32_t)((w0 + k) * 64 + b)));
+        std::uint32_t d[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          d[q] = 0;
+          if (x) {
+            const int b = __ffsll(x) - 1;
+            x &= x - 1;
+            d[q] = __ldg(p.outdeg + (std::uint32_t)((w0 + k) * 64 + b));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dc += min(p.f_next, d[q]);
       }
     }
   }
@@ -419,22 +429,39 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
       p.rank[mb * p.W + w] = make_uint4((unsigned)wd[k], (unsigned)(wd[k] >> 32), gbase + lpos, 0u);
     unsigned long long x = wd[k];
     while (x) {
-      const int b = __ffsll(x) - 1;
-      x &= x - 1;
-      const std::uint32_t v = (std::uint32_t)(w * 64 + b);
-      std::uint32_t d = 0;
-      if (HAS_NEXT) {
-        d = dpos;
-        dpos += min(p.f_next, __ldg(p.outdeg + v));
+      // up to 8 set bits per round; their degree loads are independent
+      std::uint32_t vv[8], dd[8];
+      int nq = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        dd[q] = 0;
+        if (x) {
+          const int b = __ffsll(x) - 1;
+          x &= x - 1;
+          vv[q] = (std::uint32_t)(w * 64 + b);
+          if (HAS_NEXT) dd[q] = __ldg(p.outdeg + vv[q]);
+          nq = q + 1;
+        }
       }
-      if (staged) {
-        s_ids[lpos] = v;
-        if (HAS_NEXT) s_ip[lpos] = d;
-      } else {
-        list[gbase + lpos] = v;
-        if (HAS_NEXT) ipn[gbase + lpos] = d;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < nq) {
+          const std::uint32_t v = vv[q];
+          std::uint32_t d = 0;
+          if (HAS_NEXT) {
+            d = dpos;
+            dpos += min(p.f_next, dd[q]);
+          }
+          if (staged) {
+            s_ids[lpos] = v;
+            if (HAS_NEXT) s_ip[lpos] = d;
+          } else {
+            list[gbase + lpos] = v;
+            if (HAS_NEXT) ipn[gbase + lpos] = d;
+          }
+          ++lpos;
+        }
       }
-      ++lpos;
     }
   }
   if (staged) {
