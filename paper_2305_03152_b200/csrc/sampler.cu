@@ -196,6 +196,66 @@ constexpr int kSampleThreads = 128;
 constexpr std::uint64_t kRankStride = 64;  // rank words always written at multiples of this
 constexpr std::uint32_t kSampleTileWords = 64;  // 4096 source vertices per (tile, minibatch) CTA
 
+// Register-resident sparse Fisher-Yates for fanouts <= FMAX (compile time):
+// the f draws are made first (they depend only on the counter stream), the
+// neighbour values at the drawn positions are loaded with independent loads,
+// then the swaps are replayed on register arrays -- data-dependent indices
+// become unrolled compare/selects instead of dependent shared-memory round
+// trips. Same draw sequence as sampling.cpp:87-91.
+template <int FMAX>
+__device__ __forceinline__ void fy_registers(const std::uint32_t* __restrict__ nbrs, std::uint32_t deg,
+                                             std::uint32_t f, Stream& s, std::uint32_t* out,
+                                             unsigned long long* __restrict__ hb) {
+  std::uint32_t jj[FMAX], lo[FMAX], pv[FMAX], hp[FMAX], hv[FMAX];
+#pragma unroll
+  for (int i = 0; i < FMAX; ++i) jj[i] = (std::uint32_t)i < f ? i + (std::uint32_t)s.next_below((std::uint64_t)(deg - i)) : 0u;
+#pragma unroll
+  for (int i = 0; i < FMAX; ++i) {
+    lo[i] = (std::uint32_t)i < f ? __ldg(nbrs + i) : 0u;
+    pv[i] = ((std::uint32_t)i < f && jj[i] >= f) ? __ldg(nbrs + jj[i]) : 0u;
+    hp[i] = 0xffffffffu;
+    hv[i] = 0u;
+  }
+  std::uint32_t nh = 0;
+#pragma unroll
+  for (int i = 0; i < FMAX; ++i) {
+    if ((std::uint32_t)i < f) {
+      const std::uint32_t ji = jj[i];
+      const std::uint32_t vi = lo[i];
+      std::uint32_t vj = 0;
+      if (ji < f) {
+#pragma unroll
+        for (int q = i; q < FMAX; ++q)
+          if ((std::uint32_t)q == ji) {
+            vj = lo[q];
+            lo[q] = vi;
+          }
+      } else {
+        bool found = false;
+#pragma unroll
+        for (int c = 0; c < FMAX; ++c)
+          if (hp[c] == ji) {
+            vj = hv[c];
+            hv[c] = vi;
+            found = true;
+          }
+        if (!found) {
+          vj = pv[i];  // untouched position: the original CSR value
+#pragma unroll
+          for (int c = 0; c < FMAX; ++c)
+            if ((std::uint32_t)c == nh) {
+              hp[c] = ji;
+              hv[c] = vi;
+            }
+          ++nh;
+        }
+      }
+      out[i] = vj;
+      atomicOr(hb + (vj >> 6), 1ull << (vj & 63));
+    }
+  }
+}
+
 // Shared-memory sampler (every fanout <= 32). Per thread, in slot-major
 // shared arrays (thread t's slot i at i*kSampleThreads + t, conflict free):
 //   lo[f] values at positions [0, f), hp/hv[f] the displaced-position map,
@@ -206,17 +266,20 @@ constexpr std::uint32_t kSampleTileWords = 64;  // 4096 source vertices per (til
 // Fisher-Yates swaps are then replayed in order on shared memory. Outputs of a
 // warp's 32 consecutive sources are contiguous in the MFG edge array, so they
 // are staged per warp and written back with coalesced stores.
+template <int FMAX>
 __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) {
   extern __shared__ std::uint32_t sm_fy[];
   constexpr unsigned S = kSampleThreads;
   const unsigned f = p.f;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // shared FY slots only for the FMAX == 0 (fanout 17..32) variant
+  constexpr unsigned kSlots = FMAX == 0 ? 5 : 0;
   std::uint32_t* lo = sm_fy + threadIdx.x;
   std::uint32_t* hp = lo + f * S;
   std::uint32_t* hv = hp + f * S;
   std::uint32_t* jj = hv + f * S;
   std::uint32_t* pv = jj + f * S;
-  std::uint32_t* stage = sm_fy + 5 * f * S + warp * 32 * f;
+  std::uint32_t* stage = sm_fy + kSlots * f * S + warp * 32 * f;
   std::uint32_t mb, hi, jstart, jstride;
   if (p.rank_prev) {
     mb = blockIdx.x % p.nmb;
@@ -260,6 +323,9 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
               atomicOr(hb + (t[u] >> 6), 1ull << (t[u] & 63));
             }
         }
+      } else if constexpr (FMAX > 0) {
+        Stream s(key_step(prefix, v));
+        fy_registers<FMAX>(nbrs, deg, f, s, out, hb);
       } else {
         Stream s(key_step(prefix, v));
         for (std::uint32_t i = 0; i < f; ++i) jj[i * S] = i + (std::uint32_t)s.next_below((std::uint64_t)(deg - i));
@@ -558,8 +624,17 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
   p.W = s.W;
   if constexpr (MAXF == 0) {
     // 5 FY slots per thread + a 32*f staging row per warp
-    const std::size_t smem = (std::size_t)(5 * kSampleThreads + kSampleThreads) * p.f * 4;
+    const int fmax = p.f <= 8 ? 8 : (p.f <= 16 ? 16 : 0);
+    const std::size_t smem = (std::size_t)((fmax ? 0 : 5) * kSampleThreads + kSampleThreads) * p.f * 4;
     p.nmb = nmb;
+    auto go = [&](dim3 grid) {
+      if (fmax == 8)
+        k_sample_smem<8><<<grid, kSampleThreads, smem, st>>>(p);
+      else if (fmax == 16)
+        k_sample_smem<16><<<grid, kSampleThreads, smem, st>>>(p);
+      else
+        k_sample_smem<0><<<grid, kSampleThreads, smem, st>>>(p);
+    };
     p.tile_words = kSampleTileWords;
     if (h >= 2) {
       p.rank_prev = s.hopprefix.as<uint4>();
@@ -570,11 +645,11 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
       tw = (tw + kRankStride - 1) / kRankStride * kRankStride;  // tile starts carry rank words
       p.tile_words = (std::uint32_t)tw;
       const std::uint64_t tiles = (s.W + tw - 1) / tw;
-      k_sample_smem<<<(unsigned)(tiles * nmb), kSampleThreads, smem, st>>>(p);
+      go(dim3((unsigned)(tiles * nmb)));
     } else {
       p.rank_prev = nullptr;
       const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, kSampleThreads), 8192);
-      k_sample_smem<<<dim3(gx, nmb), kSampleThreads, smem, st>>>(p);
+      go(dim3(gx, nmb));
     }
   } else {
     const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(p.capFprev, 256), 4096);
@@ -681,7 +756,7 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       s->counts.alloc(s->counts_words() * 4);
       s->desc.alloc(M * sizeof(WaveDesc));
       s->seed_stage.alloc(M * cfg->batch_size * 4);
-      VK_CUDA(cudaFuncSetAttribute(k_sample_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      VK_CUDA(cudaFuncSetAttribute(k_sample_smem<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    6 * 32 * kSampleThreads * 4));
       for (int k = 0; k < 2; ++k) {
         s->desc_host[k].ensure(M * sizeof(WaveDesc));
