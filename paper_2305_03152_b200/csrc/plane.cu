@@ -314,13 +314,18 @@ template <class T, int kUnroll, int kMinBlocks, int MODE, bool STREAM_LD = true>
 __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   __shared__ const T* s_src[8][32];
   __shared__ std::uint32_t s_row[8][32];
+  __shared__ unsigned sh[4][8];
+  // units are (vertex tile, minibatch) pairs, minibatch fastest; a capped
+  // grid (VK_GATHER_CTAS_PER_SM) walks them persistently so the gather can
+  // leave SM room for a concurrent sampler
+  for (std::uint32_t unit = blockIdx.x; unit < p.tiles * p.nmb; unit += gridDim.x) {
   // Vertex-tile-major schedule, minibatch fastest: the CTAs resident at any
   // moment serve the same vertex range for every minibatch of the wave, so a
   // feature row needed by several minibatches is read from HBM once and hit
   // in L2 by the others (all_vertices is sorted: a vertex range is a
   // contiguous run of output rows).
-  const std::uint32_t mb = blockIdx.x % p.nmb;
-  const std::uint32_t tile = blockIdx.x / p.nmb;
+  const std::uint32_t mb = unit % p.nmb;
+  const std::uint32_t tile = unit / p.nmb;
   const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
   const std::uint32_t cnt = p.all_count[mb];
   const uint4* rk = p.all_rank + mb * p.W;
@@ -412,7 +417,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
     __syncwarp();
   }
   // block-reduce the class counts, one atomic per class per CTA
-  __shared__ unsigned sh[4][8];
   unsigned vals[4] = {c_local, c_cache, c_miss, c_peer};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -424,6 +428,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
     unsigned long long t = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[threadIdx.x][w];
     if (t) atomicAdd(p.counts + mb * 4 + threadIdx.x, t);
+  }
+  __syncthreads();
   }
 }
 
@@ -797,7 +803,10 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     }();
     gp.tile_words = tile_words;
     gp.tiles = (std::uint32_t)((gp.W + tile_words - 1) / tile_words);
-    dim3 grid((unsigned)((std::uint64_t)gp.tiles * nmb));
+    const char* cap_env = std::getenv("VK_GATHER_CTAS_PER_SM");
+    const std::uint64_t units = (std::uint64_t)gp.tiles * nmb;
+    const std::uint64_t cap = cap_env ? (std::uint64_t)std::atoi(cap_env) * sm_count(p->device) : units;
+    dim3 grid((unsigned)std::max<std::uint64_t>(1, std::min(units, cap)));
     // split local / remote rows into concurrent kernels (VK_GATHER_SPLIT=1);
     // default: one kernel, each warp mixes HBM and NVLink rows
     static const bool split = [] {
