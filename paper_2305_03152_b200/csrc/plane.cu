@@ -801,11 +801,17 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       const std::uint32_t v = e ? (std::uint32_t)std::atoi(e) : kGatherTileWords;
       return std::max<std::uint32_t>(64, (v + 63) / 64 * 64);  // rank words exist at multiples of 64
     }();
-    gp.tile_words = tile_words;
-    gp.tiles = (std::uint32_t)((gp.W + tile_words - 1) / tile_words);
+    // ~1024 output rows per (tile, minibatch) unit: sparse neighbourhoods
+    // (papers-scale graphs) take proportionally wider vertex tiles
+    const double density = std::max(1e-9, (double)gp.all_stride / (double)p->n);
+    const std::uint64_t want_words = (std::uint64_t)(1024.0 / (64.0 * density));
+    std::uint64_t tw = std::max<std::uint64_t>(tile_words, (want_words + 63) / 64 * 64);
+    gp.tile_words = (std::uint32_t)tw;
+    gp.tiles = (std::uint32_t)((gp.W + tw - 1) / tw);
     const char* cap_env = std::getenv("VK_GATHER_CTAS_PER_SM");
     const std::uint64_t units = (std::uint64_t)gp.tiles * nmb;
-    const std::uint64_t cap = cap_env ? (std::uint64_t)std::atoi(cap_env) * sm_count(p->device) : units;
+    const int cap_per_sm = cap_env ? std::atoi(cap_env) : 0;
+    const std::uint64_t cap = cap_per_sm > 0 ? (std::uint64_t)cap_per_sm * sm_count(p->device) : units;
     dim3 grid((unsigned)std::max<std::uint64_t>(1, std::min(units, cap)));
     // split local / remote rows into concurrent kernels (VK_GATHER_SPLIT=1);
     // default: one kernel, each warp mixes HBM and NVLink rows
