@@ -20,6 +20,7 @@
 // Then all_vertices = compaction of the all bitmap (sampling.cpp:121-126) and
 // the relabel map F_h -> index in all_vertices.
 #include <algorithm>
+#include <type_traits>
 #include <cstring>
 #include <vector>
 
@@ -677,19 +678,32 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   p.ticket = s.tickets.as<unsigned>() + slot;
   p.W = s.W;
   p.nmb = nmb;
-  // sparse frontiers (every hop but the last) take 4 words per thread: fewer,
-  // fatter tiles; the dense last hop and all_vertices keep 1 word per thread so
-  // a tile's ids fit the shared staging buffer.
-  constexpr int kSparseWPT = 4;
-  const int wpt = has_next ? kSparseWPT : 1;
+  // Words per thread from the frontier's expected density (its capacity / n):
+  // the widest tile whose expected ids still fit the shared staging buffer.
+  // Sparse frontiers (early hops, papers-scale graphs) get few, fat tiles
+  // instead of ~W/256 tiny CTAs; the dense C3 last hop keeps 1 word/thread.
+  const double density = (double)p.cap_list / (double)std::max<std::uint64_t>(1, s.n);
+  int wpt = 1;
+  while (wpt < 32 && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage) wpt *= 2;
   p.tiles = (s.W + (std::uint64_t)kCompactThreads * wpt - 1) / ((std::uint64_t)kCompactThreads * wpt);
   const unsigned grid = (unsigned)(nmb * p.tiles);
+  auto go = [&](auto has_next_c, auto or_all_c) {
+    constexpr bool HN = decltype(has_next_c)::value, OA = decltype(or_all_c)::value;
+    switch (wpt) {
+      case 32: k_compact<HN, OA, 32><<<grid, kCompactThreads, 0, st>>>(p); break;
+      case 16: k_compact<HN, OA, 16><<<grid, kCompactThreads, 0, st>>>(p); break;
+      case 8: k_compact<HN, OA, 8><<<grid, kCompactThreads, 0, st>>>(p); break;
+      case 4: k_compact<HN, OA, 4><<<grid, kCompactThreads, 0, st>>>(p); break;
+      case 2: k_compact<HN, OA, 2><<<grid, kCompactThreads, 0, st>>>(p); break;
+      default: k_compact<HN, OA, 1><<<grid, kCompactThreads, 0, st>>>(p); break;
+    }
+  };
   if (has_next)
-    k_compact<true, true, kSparseWPT><<<grid, kCompactThreads, 0, st>>>(p);
+    go(std::true_type{}, std::true_type{});
   else if (hop)
-    k_compact<false, true, 1><<<grid, kCompactThreads, 0, st>>>(p);
+    go(std::false_type{}, std::true_type{});
   else
-    k_compact<false, false, 1><<<grid, kCompactThreads, 0, st>>>(p);
+    go(std::false_type{}, std::false_type{});
 }
 
 }  // namespace
