@@ -413,7 +413,7 @@ struct CompactParams {
   unsigned long long* status;      // [M][tiles]
   unsigned* ticket;
   std::uint64_t W, tiles;
-  std::uint32_t nmb;
+  std::uint32_t nmb, wpt;
 };
 
 constexpr int kStage = 5120;  // ids staged in shared memory per tile (else direct writes)
@@ -422,9 +422,35 @@ constexpr int kStage = 5120;  // ids staged in shared memory per tile (else dire
 // Tile ids are emitted into shared memory at their scanned positions and
 // copied out with coalesced stores (direct scattered stores only for the rare
 // tile denser than kStage).
-template <bool HAS_NEXT, bool OR_ALL, int WPT>
+// Degrees min(f, deg(v)) of the set bits of one word, loads 8 in flight.
+__device__ __forceinline__ unsigned long long capped_degree_sum(unsigned long long x, std::uint64_t w,
+                                                                const std::uint32_t* __restrict__ outdeg,
+                                                                std::uint32_t f) {
+  unsigned long long dc = 0;
+  while (x) {
+    std::uint32_t d[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      d[q] = 0;
+      if (x) {
+        const int b = __ffsll(x) - 1;
+        x &= x - 1;
+        d[q] = __ldg(outdeg + (std::uint32_t)(w * 64 + b));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dc += min(f, d[q]);
+  }
+  return dc;
+}
+
+// One CTA per tile of kCompactThreads * p.wpt words; each thread owns p.wpt
+// consecutive words (runtime: wide tiles for sparse frontiers, 1 word for the
+// dense ones; loops stay rolled so the kernel fits the instruction cache).
+// Pass 1 counts (ids and next-hop row lengths), the block scan + look-back
+// place the tile, pass 2 re-reads the words (L1/L2) and emits.
+template <bool HAS_NEXT, bool OR_ALL>
 __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
-  constexpr std::uint64_t TW = (std::uint64_t)kCompactThreads * WPT;  // words per tile
   __shared__ unsigned s_ticket;
   __shared__ unsigned long long s_sm[kCompactThreads / 32];
   __shared__ unsigned long long s_excl;
@@ -436,37 +462,16 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const std::uint32_t mb = ticket / (unsigned)p.tiles;
   const std::uint32_t tile = ticket % (unsigned)p.tiles;
   if (mb >= p.nmb) return;
+  const std::uint32_t wpt = p.wpt;
   unsigned long long* bits = p.bits + mb * p.W;
-  const std::uint64_t w0 = (std::uint64_t)tile * TW + (std::uint64_t)threadIdx.x * WPT;
-  unsigned long long wd[WPT];
-#pragma unroll
-  for (int k = 0; k < WPT; ++k) wd[k] = w0 + k < p.W ? bits[w0 + k] : 0ull;
+  const std::uint64_t w0 = ((std::uint64_t)tile * kCompactThreads + threadIdx.x) * wpt;
+  const std::uint64_t w_end = min(w0 + wpt, p.W);
   unsigned long long vc = 0, dc = 0;
-#pragma unroll
-  for (int k = 0; k < WPT; ++k) {
-    if (wd[k]) {
-      bits[w0 + k] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
-      if (OR_ALL) p.allbits[mb * p.W + w0 + k] |= wd[k];
-    }
-    vc += __popcll(wd[k]);
-    if (HAS_NEXT) {
-      // next-hop row lengths min(f, deg): degree loads issued 8 at a time
-      unsigned long long x = wd[k];
-      while (x) {
-        std::uint32_t d[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          d[q] = 0;
-          if (x) {
-            const int b = __ffsll(x) - 1;
-            x &= x - 1;
-            d[q] = __ldg(p.outdeg + (std::uint32_t)((w0 + k) * 64 + b));
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) dc += min(p.f_next, d[q]);
-      }
-    }
+#pragma unroll 1
+  for (std::uint64_t w = w0; w < w_end; ++w) {
+    const unsigned long long wd = bits[w];
+    vc += __popcll(wd);
+    if (HAS_NEXT && wd) dc += capped_degree_sum(wd, w, p.outdeg, p.f_next);
   }
   const unsigned long long mine = pack_vd(vc, dc);
   unsigned long long total;
@@ -485,16 +490,19 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   std::uint32_t* list = p.list + mb * p.cap_list;
   std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
   const bool staged = tcount <= (std::uint32_t)kStage;
-#pragma unroll
-  for (int k = 0; k < WPT; ++k) {
-    const std::uint64_t w = w0 + k;
+#pragma unroll 1
+  for (std::uint64_t w = w0; w < w_end; ++w) {
+    const unsigned long long wd = bits[w];
     // rank words are only ever read for set bits (relabel / relabel maps) and
     // at tile starts (multiples of kRankStride words, the vertex-tile
     // schedules): zero words elsewhere are skipped, which keeps sparse
     // frontiers on huge graphs from paying 16 B per empty word
-    if (w < p.W && (wd[k] || (w % kRankStride) == 0))
-      p.rank[mb * p.W + w] = make_uint4((unsigned)wd[k], (unsigned)(wd[k] >> 32), gbase + lpos, 0u);
-    unsigned long long x = wd[k];
+    if (wd || (w % kRankStride) == 0)
+      p.rank[mb * p.W + w] = make_uint4((unsigned)wd, (unsigned)(wd >> 32), gbase + lpos, 0u);
+    if (!wd) continue;
+    bits[w] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
+    if (OR_ALL) p.allbits[mb * p.W + w] |= wd;
+    unsigned long long x = wd;
     while (x) {
       // up to 8 set bits per round; their degree loads are independent
       std::uint32_t vv[8], dd[8];
@@ -684,26 +692,16 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   // instead of ~W/256 tiny CTAs; the dense C3 last hop keeps 1 word/thread.
   const double density = (double)p.cap_list / (double)std::max<std::uint64_t>(1, s.n);
   int wpt = 1;
-  while (wpt < 32 && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage) wpt *= 2;
+  while (wpt < 64 && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage) wpt *= 2;
   p.tiles = (s.W + (std::uint64_t)kCompactThreads * wpt - 1) / ((std::uint64_t)kCompactThreads * wpt);
   const unsigned grid = (unsigned)(nmb * p.tiles);
-  auto go = [&](auto has_next_c, auto or_all_c) {
-    constexpr bool HN = decltype(has_next_c)::value, OA = decltype(or_all_c)::value;
-    switch (wpt) {
-      case 32: k_compact<HN, OA, 32><<<grid, kCompactThreads, 0, st>>>(p); break;
-      case 16: k_compact<HN, OA, 16><<<grid, kCompactThreads, 0, st>>>(p); break;
-      case 8: k_compact<HN, OA, 8><<<grid, kCompactThreads, 0, st>>>(p); break;
-      case 4: k_compact<HN, OA, 4><<<grid, kCompactThreads, 0, st>>>(p); break;
-      case 2: k_compact<HN, OA, 2><<<grid, kCompactThreads, 0, st>>>(p); break;
-      default: k_compact<HN, OA, 1><<<grid, kCompactThreads, 0, st>>>(p); break;
-    }
-  };
+  p.wpt = (std::uint32_t)wpt;
   if (has_next)
-    go(std::true_type{}, std::true_type{});
+    k_compact<true, true><<<grid, kCompactThreads, 0, st>>>(p);
   else if (hop)
-    go(std::false_type{}, std::true_type{});
+    k_compact<false, true><<<grid, kCompactThreads, 0, st>>>(p);
   else
-    go(std::false_type{}, std::false_type{});
+    k_compact<false, false><<<grid, kCompactThreads, 0, st>>>(p);
 }
 
 }  // namespace
