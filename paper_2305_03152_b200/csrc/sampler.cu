@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const std::uint64_t w0 = ((std::uint64_t)tile * kCompactThreads + threadIdx.x) * wpt;
   const std::uint64_t w_end = min(w0 + wpt, p.W);
   unsigned long long vc = 0, dc = 0;
-#pragma unroll 1
+#pragma unroll 4
   for (std::uint64_t w = w0; w < w_end; ++w) {
     const unsigned long long wd = bits[w];
     vc += __popcll(wd);
@@ -692,7 +692,13 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   // instead of ~W/256 tiny CTAs; the dense C3 last hop keeps 1 word/thread.
   const double density = (double)p.cap_list / (double)std::max<std::uint64_t>(1, s.n);
   int wpt = 1;
-  while (wpt < 64 && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage) wpt *= 2;
+  // ... but never fewer than ~8 CTAs per SM in total
+  const std::uint64_t min_ctas = (std::uint64_t)sm_count(s.g->device) * 8;
+  auto ctas = [&](int w) { return (std::uint64_t)nmb * ((s.W + (std::uint64_t)kCompactThreads * w - 1) /
+                                                         ((std::uint64_t)kCompactThreads * w)); };
+  while (wpt < 64 && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage &&
+         ctas(wpt * 2) >= min_ctas)
+    wpt *= 2;
   p.tiles = (s.W + (std::uint64_t)kCompactThreads * wpt - 1) / ((std::uint64_t)kCompactThreads * wpt);
   const unsigned grid = (unsigned)(nmb * p.tiles);
   p.wpt = (std::uint32_t)wpt;
