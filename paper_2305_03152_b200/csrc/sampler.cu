@@ -464,12 +464,29 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   if (mb >= p.nmb) return;
   const std::uint32_t wpt = p.wpt;
   unsigned long long* bits = p.bits + mb * p.W;
-  const std::uint64_t w0 = ((std::uint64_t)tile * kCompactThreads + threadIdx.x) * wpt;
+  const std::uint64_t tbase = (std::uint64_t)tile * kCompactThreads * wpt;
+  const std::uint64_t w0 = tbase + (std::uint64_t)threadIdx.x * wpt;
   const std::uint64_t w_end = min(w0 + wpt, p.W);
+  // wide tiles: the tile's words are staged through shared memory with
+  // coalesced loads (thread-contiguous chunks would make every load
+  // instruction touch 32 lines); the row pitch wpt+1 avoids bank conflicts
+  extern __shared__ unsigned long long s_words[];
+  const bool smem_words = wpt > 1;
+  if (smem_words) {
+    const std::uint64_t tend = min(tbase + (std::uint64_t)kCompactThreads * wpt, p.W);
+    for (std::uint64_t i = tbase + threadIdx.x; i < tend; i += kCompactThreads) {
+      const std::uint64_t o = i - tbase;
+      s_words[(o / wpt) * (wpt + 1) + o % wpt] = bits[i];
+    }
+    __syncthreads();
+  }
+  auto word_at = [&](std::uint64_t w) -> unsigned long long {
+    return smem_words ? s_words[threadIdx.x * (wpt + 1) + (w - w0)] : bits[w];
+  };
   unsigned long long vc = 0, dc = 0;
 #pragma unroll 4
   for (std::uint64_t w = w0; w < w_end; ++w) {
-    const unsigned long long wd = bits[w];
+    const unsigned long long wd = word_at(w);
     vc += __popcll(wd);
     if (HAS_NEXT && wd) dc += capped_degree_sum(wd, w, p.outdeg, p.f_next);
   }
@@ -492,7 +509,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const bool staged = tcount <= (std::uint32_t)kStage;
 #pragma unroll 1
   for (std::uint64_t w = w0; w < w_end; ++w) {
-    const unsigned long long wd = bits[w];
+    const unsigned long long wd = word_at(w);
     // rank words are only ever read for set bits (relabel / relabel maps) and
     // at tile starts (multiples of kRankStride words, the vertex-tile
     // schedules): zero words elsewhere are skipped, which keeps sparse
@@ -696,18 +713,19 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   const std::uint64_t min_ctas = (std::uint64_t)sm_count(s.g->device) * 8;
   auto ctas = [&](int w) { return (std::uint64_t)nmb * ((s.W + (std::uint64_t)kCompactThreads * w - 1) /
                                                          ((std::uint64_t)kCompactThreads * w)); };
-  while (wpt < 64 && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage &&
+  while (wpt < 16 && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage &&
          ctas(wpt * 2) >= min_ctas)
     wpt *= 2;
   p.tiles = (s.W + (std::uint64_t)kCompactThreads * wpt - 1) / ((std::uint64_t)kCompactThreads * wpt);
   const unsigned grid = (unsigned)(nmb * p.tiles);
   p.wpt = (std::uint32_t)wpt;
+  const std::size_t smem = wpt > 1 ? (std::size_t)kCompactThreads * (wpt + 1) * 8 : 0;
   if (has_next)
-    k_compact<true, true><<<grid, kCompactThreads, 0, st>>>(p);
+    k_compact<true, true><<<grid, kCompactThreads, smem, st>>>(p);
   else if (hop)
-    k_compact<false, true><<<grid, kCompactThreads, 0, st>>>(p);
+    k_compact<false, true><<<grid, kCompactThreads, smem, st>>>(p);
   else
-    k_compact<false, false><<<grid, kCompactThreads, 0, st>>>(p);
+    k_compact<false, false><<<grid, kCompactThreads, smem, st>>>(p);
 }
 
 }  // namespace
@@ -774,6 +792,12 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       s->counts.alloc(s->counts_words() * 4);
       s->desc.alloc(M * sizeof(WaveDesc));
       s->seed_stage.alloc(M * cfg->batch_size * 4);
+      VK_CUDA(cudaFuncSetAttribute(k_compact<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kCompactThreads * 17 * 8));
+      VK_CUDA(cudaFuncSetAttribute(k_compact<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kCompactThreads * 17 * 8));
+      VK_CUDA(cudaFuncSetAttribute(k_compact<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kCompactThreads * 17 * 8));
       VK_CUDA(cudaFuncSetAttribute(k_sample_smem<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    6 * 32 * kSampleThreads * 4));
       for (int k = 0; k < 2; ++k) {
