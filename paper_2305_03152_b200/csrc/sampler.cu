@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   // coalesced loads (thread-contiguous chunks would make every load
   // instruction touch 32 lines); the row pitch wpt+1 avoids bank conflicts
   extern __shared__ unsigned long long s_words[];
-  const bool smem_words = wpt > 1;
+  const bool smem_words = wpt >= 8;
   if (smem_words) {
     const std::uint64_t tend = min(tbase + (std::uint64_t)kCompactThreads * wpt, p.W);
     for (std::uint64_t i = tbase + threadIdx.x; i < tend; i += kCompactThreads) {
@@ -719,7 +719,7 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   p.tiles = (s.W + (std::uint64_t)kCompactThreads * wpt - 1) / ((std::uint64_t)kCompactThreads * wpt);
   const unsigned grid = (unsigned)(nmb * p.tiles);
   p.wpt = (std::uint32_t)wpt;
-  const std::size_t smem = wpt > 1 ? (std::size_t)kCompactThreads * (wpt + 1) * 8 : 0;
+  const std::size_t smem = wpt >= 8 ? (std::size_t)kCompactThreads * (wpt + 1) * 8 : 0;
   if (has_next)
     k_compact<true, true><<<grid, kCompactThreads, smem, st>>>(p);
   else if (hop)
