@@ -444,6 +444,134 @@ __device__ __forceinline__ unsigned long long capped_degree_sum(unsigned long lo
   return dc;
 }
 
+// Narrow tiles (<= 4 words/thread): words held in registers, fully unrolled.
+template <bool HAS_NEXT, bool OR_ALL, int WPT>
+__global__ void __launch_bounds__(kCompactThreads) k_compact_reg(CompactParams p) {
+  constexpr std::uint64_t TW = (std::uint64_t)kCompactThreads * WPT;  // words per tile
+  __shared__ unsigned s_ticket;
+  __shared__ unsigned long long s_sm[kCompactThreads / 32];
+  __shared__ unsigned long long s_excl;
+  __shared__ std::uint32_t s_ids[kStage];
+  __shared__ std::uint32_t s_ip[HAS_NEXT ? kStage : 1];
+  if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1u);
+  __syncthreads();
+  const unsigned ticket = s_ticket;
+  const std::uint32_t mb = ticket / (unsigned)p.tiles;
+  const std::uint32_t tile = ticket % (unsigned)p.tiles;
+  if (mb >= p.nmb) return;
+  unsigned long long* bits = p.bits + mb * p.W;
+  const std::uint64_t w0 = (std::uint64_t)tile * TW + (std::uint64_t)threadIdx.x * WPT;
+  unsigned long long wd[WPT];
+#pragma unroll
+  for (int k = 0; k < WPT; ++k) wd[k] = w0 + k < p.W ? bits[w0 + k] : 0ull;
+  unsigned long long vc = 0, dc = 0;
+#pragma unroll
+  for (int k = 0; k < WPT; ++k) {
+    if (wd[k]) {
+      bits[w0 + k] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
+      if (OR_ALL) p.allbits[mb * p.W + w0 + k] |= wd[k];
+    }
+    vc += __popcll(wd[k]);
+    if (HAS_NEXT) {
+      // next-hop row lengths min(f, deg): degree loads issued 8 at a time
+      unsigned long long x = wd[k];
+      while (x) {
+        std::uint32_t d[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          d[q] = 0;
+          if (x) {
+            const int b = __ffsll(x) - 1;
+            x &= x - 1;
+            d[q] = __ldg(p.outdeg + (std::uint32_t)((w0 + k) * 64 + b));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dc += min(p.f_next, d[q]);
+      }
+    }
+  }
+  const unsigned long long mine = pack_vd(vc, dc);
+  unsigned long long total;
+  const unsigned long long inc = block_inclusive_scan<kCompactThreads>(mine, s_sm, &total);
+  if (threadIdx.x < 32) {
+    const unsigned long long ex = lookback_warp(p.status + mb * p.tiles, tile, total);
+    if (threadIdx.x == 0) s_excl = ex;
+  }
+  __syncthreads();
+  const unsigned long long base = s_excl;
+  const unsigned long long lex = inc - mine;  // tile-local exclusive prefix
+  std::uint32_t lpos = (std::uint32_t)unpack_v(lex);
+  std::uint32_t dpos = (std::uint32_t)(unpack_d(base) + unpack_d(lex));
+  const std::uint32_t gbase = (std::uint32_t)unpack_v(base);
+  const std::uint32_t tcount = (std::uint32_t)unpack_v(total);
+  std::uint32_t* list = p.list + mb * p.cap_list;
+  std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
+  const bool staged = tcount <= (std::uint32_t)kStage;
+#pragma unroll
+  for (int k = 0; k < WPT; ++k) {
+    const std::uint64_t w = w0 + k;
+    // rank words are only ever read for set bits (relabel / relabel maps) and
+    // at tile starts (multiples of kRankStride words, the vertex-tile
+    // schedules): zero words elsewhere are skipped, which keeps sparse
+    // frontiers on huge graphs from paying 16 B per empty word
+    if (w < p.W && (wd[k] || (w % kRankStride) == 0))
+      p.rank[mb * p.W + w] = make_uint4((unsigned)wd[k], (unsigned)(wd[k] >> 32), gbase + lpos, 0u);
+    unsigned long long x = wd[k];
+    while (x) {
+      // up to 8 set bits per round; their degree loads are independent
+      std::uint32_t vv[8], dd[8];
+      int nq = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        dd[q] = 0;
+        if (x) {
+          const int b = __ffsll(x) - 1;
+          x &= x - 1;
+          vv[q] = (std::uint32_t)(w * 64 + b);
+          if (HAS_NEXT) dd[q] = __ldg(p.outdeg + vv[q]);
+          nq = q + 1;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < nq) {
+          const std::uint32_t v = vv[q];
+          std::uint32_t d = 0;
+          if (HAS_NEXT) {
+            d = dpos;
+            dpos += min(p.f_next, dd[q]);
+          }
+          if (staged) {
+            s_ids[lpos] = v;
+            if (HAS_NEXT) s_ip[lpos] = d;
+          } else {
+            list[gbase + lpos] = v;
+            if (HAS_NEXT) ipn[gbase + lpos] = d;
+          }
+          ++lpos;
+        }
+      }
+    }
+  }
+  if (staged) {
+    __syncthreads();
+    for (std::uint32_t i = threadIdx.x; i < tcount; i += kCompactThreads) {
+      list[gbase + i] = s_ids[i];
+      if (HAS_NEXT) ipn[gbase + i] = s_ip[i];
+    }
+  }
+  if (tile == p.tiles - 1 && threadIdx.x == kCompactThreads - 1) {
+    const unsigned long long all = base + total;
+    const std::uint32_t tv = (std::uint32_t)unpack_v(all), td = (std::uint32_t)unpack_d(all);
+    p.count[mb] = tv;
+    if (HAS_NEXT) {
+      ipn[tv] = td;
+      p.ecount_next[mb] = td;
+    }
+  }
+}
+
 // One CTA per tile of kCompactThreads * p.wpt words; each thread owns p.wpt
 // consecutive words (runtime: wide tiles for sparse frontiers, 1 word for the
 // dense ones; loops stay rolled so the kernel fits the instruction cache).
@@ -720,12 +848,29 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   const unsigned grid = (unsigned)(nmb * p.tiles);
   p.wpt = (std::uint32_t)wpt;
   const std::size_t smem = wpt >= 8 ? (std::size_t)kCompactThreads * (wpt + 1) * 8 : 0;
-  if (has_next)
+  auto narrow = [&](auto hn, auto oa) {
+    constexpr bool HN = decltype(hn)::value, OA = decltype(oa)::value;
+    if (wpt == 4)
+      k_compact_reg<HN, OA, 4><<<grid, kCompactThreads, 0, st>>>(p);
+    else if (wpt == 2)
+      k_compact_reg<HN, OA, 2><<<grid, kCompactThreads, 0, st>>>(p);
+    else
+      k_compact_reg<HN, OA, 1><<<grid, kCompactThreads, 0, st>>>(p);
+  };
+  if (wpt <= 4) {
+    if (has_next)
+      narrow(std::true_type{}, std::true_type{});
+    else if (hop)
+      narrow(std::false_type{}, std::true_type{});
+    else
+      narrow(std::false_type{}, std::false_type{});
+  } else if (has_next) {
     k_compact<true, true><<<grid, kCompactThreads, smem, st>>>(p);
-  else if (hop)
+  } else if (hop) {
     k_compact<false, true><<<grid, kCompactThreads, smem, st>>>(p);
-  else
+  } else {
     k_compact<false, false><<<grid, kCompactThreads, smem, st>>>(p);
+  }
 }
 
 }  // namespace
