@@ -349,14 +349,23 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
       const std::uint32_t v = __ldg(all + r);
       const std::uint32_t s = __ldg(slot + v);
       if (s != VK_MISS) {
-        if (MODE != 2) {
+        if (MODE != 2 && MODE != 4) {
           src = store + (std::uint64_t)s * rowv;
           (s < nl ? c_local : c_cache)++;
         }
       } else {
         const std::uint32_t o = __ldg(p.part_of + v);
         const bool remote = p.peer_mask[o] != 0;
-        if (MODE == 3) {
+        if (MODE == 4) {  // staged remote rows only (the local ones ran concurrently with the pull)
+          if (remote) {
+            const std::uint32_t wq = v >> 6;
+            const std::uint32_t idx = __ldg(p.uprefix + wq) +
+                                      (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (v & 63)) - 1ull));
+            src = reinterpret_cast<const T*>(p.staging) + (std::uint64_t)idx * rowv;
+            ++c_miss;
+            ++c_peer;
+          }
+        } else if (MODE == 3) {
           if (remote) {  // pulled once per wave into the local staging buffer
             const std::uint32_t wq = v >> 6;
             const std::uint32_t idx = __ldg(p.uprefix + wq) +
@@ -823,6 +832,18 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     for (const auto& q : p->parts) any_peer |= q.attached;
     const bool peers = any_peer && split;
     const bool staged = any_peer && !split;
+    // overlap the miss exchange (aux stream) with the gather of the rows this
+    // GPU serves itself (VK_GATHER_OVERLAP=0 serialises them)
+    static const bool overlap = [] {
+      const char* e = std::getenv("VK_GATHER_OVERLAP");
+      return !e || std::atoi(e) != 0;
+    }();
+    cudaStream_t xs = st;  // exchange stream
+    if (staged && overlap) {
+      VK_CUDA(cudaEventRecord(p->fork, st));
+      VK_CUDA(cudaStreamWaitEvent(p->aux, p->fork, 0));
+      xs = p->aux;
+    }
     if (staged) {
       // miss exchange: union of the wave's remote misses -> distinct list ->
       // one NVLink pull per distinct row into local staging -> the gather
@@ -839,32 +860,34 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       ensure(ss.staging, n * p->row_bytes);
       if (!ss.scan_bytes) {
         VK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, ss.scan_bytes, ss.uprefix.as<std::uint32_t>(),
-                                              ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), st));
+                                              ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), xs));
         ss.scan_tmp.alloc(std::max<std::size_t>(ss.scan_bytes, 1));
       }
-      VK_CUDA(cudaMemsetAsync(ss.ubits.p, 0, W * 8, st));
-      VK_CUDA(cudaMemsetAsync(ss.uprefix.as<std::uint32_t>() + W, 0, 4, st));
+      VK_CUDA(cudaMemsetAsync(ss.ubits.p, 0, W * 8, xs));
+      VK_CUDA(cudaMemsetAsync(ss.uprefix.as<std::uint32_t>() + W, 0, 4, xs));
       const unsigned gx = (unsigned)std::max<std::uint64_t>(
           1, std::min<std::uint64_t>(ceil_div(gp.all_stride, 256), (std::uint64_t)sm_count(p->device) * 8 / nmb + 1));
-      k_remote_mark<<<dim3(gx, nmb), 256, 0, st>>>(gp, ss.ubits.as<unsigned long long>());
-      k_word_popc<<<grid_for(W, p->device), 256, 0, st>>>(ss.ubits.as<unsigned long long>(), W,
+      k_remote_mark<<<dim3(gx, nmb), 256, 0, xs>>>(gp, ss.ubits.as<unsigned long long>());
+      k_word_popc<<<grid_for(W, p->device), 256, 0, xs>>>(ss.ubits.as<unsigned long long>(), W,
                                                           ss.uprefix.as<std::uint32_t>());
       std::size_t tb = ss.scan_bytes;
       VK_CUDA(cub::DeviceScan::ExclusiveSum(ss.scan_tmp.p, tb, ss.uprefix.as<std::uint32_t>(),
-                                            ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), st));
-      k_emit_list<<<grid_for(W, p->device), 256, 0, st>>>(ss.ubits.as<unsigned long long>(),
+                                            ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), xs));
+      k_emit_list<<<grid_for(W, p->device), 256, 0, xs>>>(ss.ubits.as<unsigned long long>(),
                                                           ss.uprefix.as<std::uint32_t>(), W,
                                                           ss.ulist.as<std::uint32_t>());
-      const unsigned pg = (unsigned)sm_count(p->device) * 8;
+      // NVLink-bound: a few CTAs per SM keep enough bytes in flight and leave
+      // room for the concurrent local gather
+      const unsigned pg = (unsigned)sm_count(p->device) * (overlap ? 2 : 8);
       if (v16)
-        k_remote_pull<uint4, 8><<<pg, 256, 0, st>>>(gp, ss.ulist.as<std::uint32_t>(),
+        k_remote_pull<uint4, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
                                                      ss.uprefix.as<std::uint32_t>() + W, ss.staging.as<uint4>());
       else if (v4)
-        k_remote_pull<std::uint32_t, 8><<<pg, 256, 0, st>>>(gp, ss.ulist.as<std::uint32_t>(),
+        k_remote_pull<std::uint32_t, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
                                                              ss.uprefix.as<std::uint32_t>() + W,
                                                              ss.staging.as<std::uint32_t>());
       else
-        k_remote_pull<std::uint16_t, 8><<<pg, 256, 0, st>>>(gp, ss.ulist.as<std::uint32_t>(),
+        k_remote_pull<std::uint16_t, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
                                                              ss.uprefix.as<std::uint32_t>() + W,
                                                              ss.staging.as<std::uint16_t>());
       count_launch(6);
@@ -875,17 +898,20 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     }
     auto launch = [&](int mode, cudaStream_t where) {
       if (v16) {
-        if (mode == 3) k_gather<uint4, 8, 4, 3><<<grid, 256, 0, where>>>(gp);
+        if (mode == 4) k_gather<uint4, 8, 4, 4><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 3) k_gather<uint4, 8, 4, 3><<<grid, 256, 0, where>>>(gp);
         else if (mode == 0) k_gather<uint4, 8, 4, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<uint4, 8, 4, 1><<<grid, 256, 0, where>>>(gp);
         else k_gather<uint4, 16, 2, 2, false><<<grid, 256, 0, where>>>(gp);  // peer rows: plain LDG
       } else if (v4) {
-        if (mode == 3) k_gather<std::uint32_t, 8, 1, 3><<<grid, 256, 0, where>>>(gp);
+        if (mode == 4) k_gather<std::uint32_t, 8, 1, 4><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 3) k_gather<std::uint32_t, 8, 1, 3><<<grid, 256, 0, where>>>(gp);
         else if (mode == 0) k_gather<std::uint32_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<std::uint32_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
         else k_gather<std::uint32_t, 8, 1, 2><<<grid, 256, 0, where>>>(gp);
       } else {
-        if (mode == 3) k_gather<std::uint16_t, 8, 1, 3><<<grid, 256, 0, where>>>(gp);
+        if (mode == 4) k_gather<std::uint16_t, 8, 1, 4><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 3) k_gather<std::uint16_t, 8, 1, 3><<<grid, 256, 0, where>>>(gp);
         else if (mode == 0) k_gather<std::uint16_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<std::uint16_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
         else k_gather<std::uint16_t, 8, 1, 2><<<grid, 256, 0, where>>>(gp);
@@ -893,7 +919,12 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       count_launch();
       VK_LAUNCH_CHECK();
     };
-    if (staged) {
+    if (staged && overlap) {
+      launch(1, st);  // local + cache + co-resident rows while the pull runs
+      VK_CUDA(cudaEventRecord(p->join, p->aux));
+      VK_CUDA(cudaStreamWaitEvent(st, p->join, 0));
+      launch(4, st);  // remote rows from staging
+    } else if (staged) {
       launch(3, st);
     } else if (!peers) {
       launch(0, st);
