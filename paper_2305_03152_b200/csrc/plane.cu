@@ -832,11 +832,14 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     for (const auto& q : p->parts) any_peer |= q.attached;
     const bool peers = any_peer && split;
     const bool staged = any_peer && !split;
-    // overlap the miss exchange (aux stream) with the gather of the rows this
-    // GPU serves itself (VK_GATHER_OVERLAP=0 serialises them)
+    // VK_GATHER_OVERLAP=1 runs the miss exchange on the aux stream alongside
+    // a gather of the locally served rows, then gathers the staged remote rows.
+    // Measured slower on 2 B200s (14.4K vs 17.7K mb/s on C3: the split costs a
+    // second compaction of the vertex list and the two passes contend for HBM),
+    // so the serial exchange -> single gather is the default.
     static const bool overlap = [] {
       const char* e = std::getenv("VK_GATHER_OVERLAP");
-      return !e || std::atoi(e) != 0;
+      return e && std::atoi(e) != 0;
     }();
     cudaStream_t xs = st;  // exchange stream
     if (staged && overlap) {
@@ -878,7 +881,11 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
                                                           ss.ulist.as<std::uint32_t>());
       // NVLink-bound: a few CTAs per SM keep enough bytes in flight and leave
       // room for the concurrent local gather
-      const unsigned pg = (unsigned)sm_count(p->device) * (overlap ? 2 : 8);
+      static const unsigned pull_per_sm = [] {
+        const char* e = std::getenv("VK_PULL_CTAS_PER_SM");
+        return e && std::atoi(e) > 0 ? (unsigned)std::atoi(e) : 0u;
+      }();
+      const unsigned pg = (unsigned)sm_count(p->device) * (pull_per_sm ? pull_per_sm : (overlap ? 2 : 8));
       if (v16)
         k_remote_pull<uint4, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
                                                      ss.uprefix.as<std::uint32_t>() + W, ss.staging.as<uint4>());
