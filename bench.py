@@ -52,7 +52,7 @@ CONFIGS = {
     "c3": dict(workload="C3 ogbn-products-shaped 2.45M nodes / 122M CSR slots, 100-d fp32, "
                         "8 partitions, fanout (15,10,5), batch 1024, VIP cache 20%",
                n=2_449_029, d=25, K=8, p_in=0.8, train=0.08, dim=100, dtype=0, alpha=0.20,
-               fanouts=(15, 10, 5), b=1024),
+               fanouts=(15, 10, 5), b=1024, wave=128),
 }
 # BASELINE.json configs[3]/[4]: ogbn-papers100M-shaped (111M nodes, 1.6B
 # edges = 3.3B CSR slots, 8 partitions). configs[4] is the VIP-analysis-only
@@ -290,12 +290,19 @@ def run_b200(args, cfg):
         misses += int(tally[i, :nmb, 2].sum())
         cache_hits += int(tally[i, :nmb, 1].sum())
         peer += int(tally[i, :nmb, 3].sum())
-        g_bytes += int(allc.sum()) * (2 * rb + 8)
         fc = cnts[i, :(L + 1) * M].reshape(L + 1, M)[:, :nmb].astype(np.int64)
         ec = cnts[i, (L + 1) * M:2 * (L + 1) * M].reshape(L + 1, M)[:, :nmb].astype(np.int64)
         ac = cnts[i, 2 * (L + 1) * M:2 * (L + 1) * M + M][:nmb].astype(np.int64)
         s_bytes += int(sum(16 * fc[h - 1].sum() + 8 * ec[h].sum() for h in range(1, L + 1))
                        + 8 * (fc[1:].sum() + ac.sum()))
+    # compulsory gather bytes: every output row written once, its 4-byte id
+    # read once, and each DISTINCT source row of the wave read once (rows
+    # shared by minibatches of a wave are L2 hits, not HBM reads). The
+    # distinct count comes from the last wave still held by its sampler.
+    last = W + 2 * S - 1
+    distinct = distinct_rows(samplers[last % P], len(waves[last]), dev)
+    rows_last = int(tally[last, :len(waves[last]), :3].sum())
+    g_bytes = int(rows / S * (rb + 4) + distinct * rb) * S
     hbm, peak_kind = peaks()
     traffic = None
     try:
@@ -325,8 +332,9 @@ def run_b200(args, cfg):
                 "d2h_bytes_per_step": M * 4 * 8},
         "roofline": {"bound": "hbm", "kernel": "k_gather (classify+gather)", "achieved": g_ach,
                      "peak": hbm, "unit": "GB/s", "frac": g_ach / hbm, "traffic": traffic,
-                     "traffic_note": "ncu dram read+write per launch (profiles/traffic.json); below the algorithmic "
-                                     "bytes because rows shared by minibatches of a wave are L2 hits",
+                     "traffic_note": "ncu dram read+write per launch (profiles/traffic.json)",
+                     "algorithmic_bytes": "rows x (row_bytes + 4 B id) + distinct rows of the wave x row_bytes "
+                                          f"(distinct {distinct} of {rows_last} rows in the last wave)",
                      "peak_kind": peak_kind, "bytes_per_launch": g_bytes / S,
                      "ms_per_launch": statistics.mean(gather_ms)},
         "sampler": {"ms_per_wave": statistics.mean(sample_ms), "achieved_gbs": s_ach,
@@ -488,6 +496,25 @@ def cpu_baseline(cfg, off, tgt, labels, roles, plan, waves, budget_s=12.0):
                       f"threads; {done} minibatches single-threaded; gather excluded (not in reference)"}
 
 
+class _DevArray:
+    """Minimal __cuda_array_interface__ view of a device pointer (for torch)."""
+
+    def __init__(self, ptr, count, typestr="<u4"):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3}
+
+
+def distinct_rows(sampler, nmb, dev):
+    """Number of distinct vertices across the all_vertices lists of the
+    sampler's current wave (torch.unique on the device, outside timed regions)."""
+    import torch
+    v = sampler.view()
+    cnt = torch.as_tensor(_DevArray(v.all_count, nmb), device=f"cuda:{dev}").to(torch.int64).cpu().tolist()
+    allv = torch.as_tensor(_DevArray(v.all, nmb * v.all_stride), device=f"cuda:{dev}").view(torch.int32)
+    parts = [allv[i * v.all_stride:i * v.all_stride + c] for i, c in enumerate(cnt)]
+    return int(torch.unique(torch.cat(parts)).numel())
+
+
 def run_reference(args, cfg):
     """--impl reference: the unmodified reference CPU path on the same config."""
     rank = int(os.environ.get("RANK", "0"))
@@ -549,13 +576,16 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--alpha-sweep", action="store_true", help="also tally misses for cache sizes 0-32%%")
-    ap.add_argument("--wave", type=int, default=32, help="minibatches per step per GPU")
+    ap.add_argument("--wave", type=int, default=None,
+                    help="minibatches per step per GPU (default: the config's, 128 for c3, else 32)")
     ap.add_argument("--pipes", type=int, default=1, help="overlapped sampler+gather pipelines (streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = dict(CONFIGS[args.config])
+    if args.wave is None:
+        args.wave = cfg.get("wave", 32)
     if args.alpha_sweep and "alpha_sweep" not in cfg:
         cfg["alpha_sweep"] = (0.0, 0.04, 0.08, 0.16, 0.32)
     if args.config == "c5" and args.impl != "reference":

@@ -43,6 +43,8 @@ struct vk_plane_s {
   int dtype = VK_F32;
   std::uint64_t row_bytes = 0;
   vk::DevBuf part_of, owner_row;  // u32 [n] each
+  vk::DevBuf new_id;              // u32 [n]: reorder position (global row order)
+  vk::DevBuf d_rstart;            // u32 [K+1]: partition range starts in row order
   std::vector<std::uint64_t> rstart, rend;
   std::vector<std::uint32_t> old_of_new;  // host copy (local row order)
   struct Part {
@@ -178,6 +180,9 @@ struct GatherParams {
   const std::uint32_t* nlocal;       // [K]
   const std::uint32_t* part_of;
   const std::uint32_t* owner_row;
+  const std::uint32_t* new_id;       // [n] rstart[part_of[v]] + owner_row[v]
+  const std::uint32_t* rstart;       // [K+1]
+  std::uint32_t K;
   const unsigned char* peer_mask;    // [K] 1 if the partition's rows live on another GPU
   char* out;
   std::uint64_t out_stride_bytes;
@@ -189,11 +194,31 @@ struct GatherParams {
   const uint4* all_rank;             // [nmb][W] {bits, rank prefix} of all_vertices
   std::uint64_t W;
   std::uint32_t nmb, tiles, tile_words;
-  // deduplicated remote rows: staged[rank of v in the wave's remote set]
+  // deduplicated remote rows: staged[rank of new_id[v] in the wave's remote
+  // set] -- ranked in global row order so the pull streams each owner's
+  // store in ascending address order
   const unsigned long long* ubits;
   const std::uint32_t* uprefix;
   const char* staging;
 };
+
+// Owner partition of global row g: the last k with rstart[k] <= g (K+1
+// range starts, staged in shared memory when K <= kSmemParts).
+constexpr std::uint32_t kSmemParts = 256;
+__device__ __forceinline__ std::uint32_t owner_of(const std::uint32_t* rs, std::uint32_t K, std::uint32_t g) {
+  std::uint32_t lo = 0, hi = K;
+  while (hi - lo > 1) {
+    const std::uint32_t mid = (lo + hi) >> 1;
+    if (rs[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ const std::uint32_t* stage_rstart(const GatherParams& p, std::uint32_t* sm) {
+  if (p.K + 1 > kSmemParts) return p.rstart;
+  for (std::uint32_t i = threadIdx.x; i <= p.K; i += blockDim.x) sm[i] = p.rstart[i];
+  __syncthreads();
+  return sm;
+}
 
 // Streaming 16/4/2-byte copies: the feature table is read through L1
 // (no_allocate) and the gathered rows are written evict-first so neither
@@ -228,6 +253,8 @@ __device__ __forceinline__ void st_stream(T* p, const T& v) {
 // (rows whose owner partition lives on another GPU and that are neither
 // local nor cached for the minibatch's partition) as a bitmap over vertices.
 __global__ void __launch_bounds__(256) k_remote_mark(GatherParams p, unsigned long long* __restrict__ ubits) {
+  __shared__ std::uint32_t s_rs[kSmemParts];
+  const std::uint32_t* rs = stage_rstart(p, s_rs);
   const std::uint32_t mb = blockIdx.y;
   const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
   const std::uint32_t cnt = p.all_count[mb];
@@ -235,8 +262,10 @@ __global__ void __launch_bounds__(256) k_remote_mark(GatherParams p, unsigned lo
   const std::uint32_t* slot = p.slot[k];
   for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < cnt; r += gridDim.x * blockDim.x) {
     const std::uint32_t v = __ldg(all + r);
-    if (__ldg(slot + v) == VK_MISS && p.peer_mask[__ldg(p.part_of + v)])
-      atomicOr(ubits + (v >> 6), 1ull << (v & 63));
+    if (__ldg(slot + v) == VK_MISS) {
+      const std::uint32_t g = __ldg(p.new_id + v);
+      if (p.peer_mask[owner_of(rs, p.K, g)]) atomicOr(ubits + (g >> 6), 1ull << (g & 63));
+    }
   }
 }
 
@@ -268,6 +297,8 @@ template <class T, int kUnroll>
 __global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::uint32_t* __restrict__ list,
                                                      const std::uint32_t* __restrict__ count_ptr, T* __restrict__ staging) {
   __shared__ const T* s_src[8][32];
+  __shared__ std::uint32_t s_rs[kSmemParts];
+  const std::uint32_t* rs = stage_rstart(p, s_rs);
   const std::uint32_t cnt = *count_ptr;
   const std::uint32_t V = p.V;
   const std::uint32_t magic = p.magic32;
@@ -278,8 +309,9 @@ __global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::
     const std::uint32_t r = r0 + lane;
     const T* src = nullptr;
     if (r < cnt) {
-      const std::uint32_t v = __ldg(list + r);
-      src = reinterpret_cast<const T*>(p.base[__ldg(p.part_of + v)]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
+      const std::uint32_t g = __ldg(list + r);  // global row order
+      const std::uint32_t o = owner_of(rs, p.K, g);
+      src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)(g - rs[o]) * rowv;
     }
     s_src[w][lane] = src;
     __syncwarp();
@@ -315,6 +347,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   __shared__ const T* s_src[8][32];
   __shared__ std::uint32_t s_row[8][32];
   __shared__ unsigned sh[4][8];
+  __shared__ std::uint32_t s_rs[kSmemParts];
+  const std::uint32_t* rs = stage_rstart(p, s_rs);
   // units are (vertex tile, minibatch) pairs, minibatch fastest; a capped
   // grid (VK_GATHER_CTAS_PER_SM) walks them persistently so the gather can
   // leave SM room for a concurrent sampler
@@ -354,30 +388,26 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
           (s < nl ? c_local : c_cache)++;
         }
       } else {
-        const std::uint32_t o = __ldg(p.part_of + v);
+        // miss: the owner's row in global row order (reorder position)
+        const std::uint32_t g = __ldg(p.new_id + v);
+        const std::uint32_t o = owner_of(rs, p.K, g);
         const bool remote = p.peer_mask[o] != 0;
-        if (MODE == 4) {  // staged remote rows only (the local ones ran concurrently with the pull)
-          if (remote) {
-            const std::uint32_t wq = v >> 6;
-            const std::uint32_t idx = __ldg(p.uprefix + wq) +
-                                      (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (v & 63)) - 1ull));
-            src = reinterpret_cast<const T*>(p.staging) + (std::uint64_t)idx * rowv;
-            ++c_miss;
-            ++c_peer;
-          }
-        } else if (MODE == 3) {
+        const T* owner_src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)(g - rs[o]) * rowv;
+        if (MODE == 3 || MODE == 4) {
           if (remote) {  // pulled once per wave into the local staging buffer
-            const std::uint32_t wq = v >> 6;
+            const std::uint32_t wq = g >> 6;
             const std::uint32_t idx = __ldg(p.uprefix + wq) +
-                                      (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (v & 63)) - 1ull));
+                                      (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (g & 63)) - 1ull));
             src = reinterpret_cast<const T*>(p.staging) + (std::uint64_t)idx * rowv;
-          } else {
-            src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
+          } else if (MODE == 3) {
+            src = owner_src;
           }
-          ++c_miss;
-          c_peer += remote;
+          if (MODE == 3 || remote) {
+            ++c_miss;
+            c_peer += remote;
+          }
         } else if ((MODE == 0) || (MODE == 1 && !remote) || (MODE == 2 && remote)) {
-          src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)__ldg(p.owner_row + v) * rowv;
+          src = owner_src;
           ++c_miss;
           c_peer += remote;
         }
@@ -578,8 +608,16 @@ int vk_plane_create(int device, uint64_t n, uint32_t K, uint32_t dim, int dtype,
       VK_CUDA(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
       p->part_of.alloc(n * 4);
       p->owner_row.alloc(n * 4);
+      p->new_id.alloc(n * 4);
+      p->d_rstart.alloc((K + 1) * 4);
+      std::vector<std::uint32_t> nid(n), rst(K + 1);
+      for (std::uint32_t k = 0; k < K; ++k) rst[k] = (std::uint32_t)rs[k];
+      rst[K] = (std::uint32_t)n;
+      for (std::uint64_t i = 0; i < n; ++i) nid[old_of_new[i]] = (std::uint32_t)i;
       VK_CUDA(cudaMemcpyAsync(p->part_of.p, part_of, n * 4, cudaMemcpyHostToDevice, p->stream));
       VK_CUDA(cudaMemcpyAsync(p->owner_row.p, owner.data(), n * 4, cudaMemcpyHostToDevice, p->stream));
+      VK_CUDA(cudaMemcpyAsync(p->new_id.p, nid.data(), n * 4, cudaMemcpyHostToDevice, p->stream));
+      VK_CUDA(cudaMemcpyAsync(p->d_rstart.p, rst.data(), (K + 1) * 4, cudaMemcpyHostToDevice, p->stream));
       p->d_base.alloc(K * sizeof(void*));
       p->d_slot.alloc(K * sizeof(void*));
       p->d_nlocal.alloc(K * 4 + K);  // u32 nlocal[K] then u8 peer_mask[K]
@@ -793,6 +831,9 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     gp.peer_mask = p->d_nlocal.as<unsigned char>() + 4 * p->K;
     gp.part_of = p->part_of.as<std::uint32_t>();
     gp.owner_row = p->owner_row.as<std::uint32_t>();
+    gp.new_id = p->new_id.as<std::uint32_t>();
+    gp.rstart = p->d_rstart.as<std::uint32_t>();
+    gp.K = p->K;
     gp.out = static_cast<char*>(out_dev);
     gp.out_stride_bytes = out_stride_rows * p->row_bytes;
     gp.row_bytes = p->row_bytes;
@@ -847,6 +888,29 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       VK_CUDA(cudaStreamWaitEvent(p->aux, p->fork, 0));
       xs = p->aux;
     }
+    // VK_GATHER_TIMING=1: per-phase event timing (synchronises each call;
+    // diagnostics only), summed and printed to stderr at exit
+    static const bool timing = [] {
+      const char* e = std::getenv("VK_GATHER_TIMING");
+      return e && std::atoi(e) != 0;
+    }();
+    static double t_acc[4] = {0, 0, 0, 0};  // mark, scan+emit, pull, gather
+    static long t_calls = 0;
+    cudaEvent_t tev[5];
+    if (timing) {
+      static bool reg = false;
+      if (!reg) {
+        reg = true;
+        std::atexit([] {
+          if (t_calls)
+            std::fprintf(stderr,
+                         "[vk gather timing] calls %ld  mark %.3f  scan+emit %.3f  pull %.3f  gather %.3f ms/call\n",
+                         t_calls, t_acc[0] / t_calls, t_acc[1] / t_calls, t_acc[2] / t_calls, t_acc[3] / t_calls);
+        });
+      }
+      for (auto& e : tev) VK_CUDA(cudaEventCreate(&e));
+      VK_CUDA(cudaEventRecord(tev[0], xs));
+    }
     if (staged) {
       // miss exchange: union of the wave's remote misses -> distinct list ->
       // one NVLink pull per distinct row into local staging -> the gather
@@ -871,6 +935,7 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       const unsigned gx = (unsigned)std::max<std::uint64_t>(
           1, std::min<std::uint64_t>(ceil_div(gp.all_stride, 256), (std::uint64_t)sm_count(p->device) * 8 / nmb + 1));
       k_remote_mark<<<dim3(gx, nmb), 256, 0, xs>>>(gp, ss.ubits.as<unsigned long long>());
+      if (timing) VK_CUDA(cudaEventRecord(tev[1], xs));
       k_word_popc<<<grid_for(W, p->device), 256, 0, xs>>>(ss.ubits.as<unsigned long long>(), W,
                                                           ss.uprefix.as<std::uint32_t>());
       std::size_t tb = ss.scan_bytes;
@@ -879,6 +944,7 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       k_emit_list<<<grid_for(W, p->device), 256, 0, xs>>>(ss.ubits.as<unsigned long long>(),
                                                           ss.uprefix.as<std::uint32_t>(), W,
                                                           ss.ulist.as<std::uint32_t>());
+      if (timing) VK_CUDA(cudaEventRecord(tev[2], xs));
       // NVLink-bound: a few CTAs per SM keep enough bytes in flight and leave
       // room for the concurrent local gather
       static const unsigned pull_per_sm = [] {
@@ -926,6 +992,13 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       count_launch();
       VK_LAUNCH_CHECK();
     };
+    if (timing) {
+      if (!staged) {
+        VK_CUDA(cudaEventRecord(tev[1], xs));
+        VK_CUDA(cudaEventRecord(tev[2], xs));
+      }
+      VK_CUDA(cudaEventRecord(tev[3], xs));
+    }
     if (staged && overlap) {
       launch(1, st);  // local + cache + co-resident rows while the pull runs
       VK_CUDA(cudaEventRecord(p->join, p->aux));
@@ -943,6 +1016,17 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       launch(1, st);
       VK_CUDA(cudaEventRecord(p->join, p->aux));
       VK_CUDA(cudaStreamWaitEvent(st, p->join, 0));
+    }
+    if (timing) {
+      VK_CUDA(cudaEventRecord(tev[4], st));
+      VK_CUDA(cudaEventSynchronize(tev[4]));
+      for (int i = 0; i < 4; ++i) {
+        float ms = 0;
+        VK_CUDA(cudaEventElapsedTime(&ms, tev[i], tev[i + 1]));
+        t_acc[i] += ms;
+      }
+      ++t_calls;
+      for (auto& e : tev) VK_CUDA(cudaEventDestroy(e));
     }
   });
 }
