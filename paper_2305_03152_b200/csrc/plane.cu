@@ -32,6 +32,7 @@ void sampler_internal(vk_sampler_s* s, const std::uint32_t** all, std::uint64_t*
                       vk_graph_s** g, cudaStream_t* last_stream);
 std::uint64_t sampler_desc_stride();
 void sampler_all_rank(vk_sampler_s* s, const uint4** rank, std::uint64_t* W);
+bool sampler_all_rank_dense(vk_sampler_s* s);
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out);
 cudaEvent_t sampler_done_event(vk_sampler_s* s);
 }  // namespace vk
@@ -54,9 +55,11 @@ struct vk_plane_s {
     std::uint64_t n_local = 0, n_cache = 0;
     std::vector<std::uint64_t> cache_bits;  // CachePlan::member_bits[k]
     void* peer = nullptr;                   // IPC-mapped local rows of a remote partition
+    vk::DevBuf rmask;  // [W] bit v: v is neither local nor cached here and its owner is on a peer GPU
   };
   std::vector<Part> parts;
   vk::DevBuf d_base, d_slot, d_nlocal;  // K-entry tables for the gather kernel
+  vk::DevBuf d_rmask;                   // [K] Part::rmask pointers (resident partitions)
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // remote-row gathers run here concurrently
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -65,6 +68,7 @@ struct vk_plane_s {
   // local staging copy of those rows
   struct StageSet {
     vk::DevBuf ubits, uprefix, ulist, staging, scan_tmp;
+    vk::DevBuf vbits;  // vertex-space union (word mark); cleared as consumed
     std::size_t scan_bytes = 0;
   };
   // one set per sampler, so overlapped waves (one sampler per pipeline
@@ -184,6 +188,7 @@ struct GatherParams {
   const std::uint32_t* rstart;       // [K+1]
   std::uint32_t K;
   const unsigned char* peer_mask;    // [K] 1 if the partition's rows live on another GPU
+  const unsigned long long* const* rmask;  // [K] remote-miss masks (resident partitions)
   char* out;
   std::uint64_t out_stride_bytes;
   std::uint64_t row_bytes;
@@ -266,6 +271,60 @@ __global__ void __launch_bounds__(256) k_remote_mark(GatherParams p, unsigned lo
       const std::uint32_t g = __ldg(p.new_id + v);
       if (p.peer_mask[owner_of(rs, p.K, g)]) atomicOr(ubits + (g >> 6), 1ull << (g & 63));
     }
+  }
+}
+
+// Step 1 from the sampler's bitmaps (dense all-level rank words), in two
+// passes: (a) per (vertex word, chunk of kMarkChunk minibatches) OR the
+// all-vertex bits masked by each minibatch partition's remote-miss mask into
+// a vertex-space union; (b) per union word, set each vertex's bit in global
+// row order and clear the word for the next wave. Reads M*W*16 B of rank
+// words instead of every row's id, slot and new_id.
+constexpr std::uint32_t kMarkChunk = 8;
+__global__ void __launch_bounds__(256) k_remote_union(GatherParams p, unsigned long long* __restrict__ vbits) {
+  const std::uint64_t w = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (w >= p.W) return;
+  const std::uint32_t mb0 = blockIdx.y * kMarkChunk;
+  unsigned long long u = 0;
+#pragma unroll
+  for (std::uint32_t i = 0; i < kMarkChunk; ++i) {
+    const std::uint32_t mb = mb0 + i;
+    if (mb < p.nmb) {
+      const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
+      const uint4 r = __ldg(p.all_rank + mb * p.W + w);
+      u |= (((unsigned long long)r.y << 32) | r.x) & __ldg(p.rmask[k] + w);
+    }
+  }
+  if (u) atomicOr(vbits + w, u);
+}
+__global__ void __launch_bounds__(256) k_remote_to_rows(const GatherParams p, unsigned long long* __restrict__ vbits,
+                                                        unsigned long long* __restrict__ ubits) {
+  for (std::uint64_t w = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; w < p.W;
+       w += (std::uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long u = vbits[w];
+    if (!u) continue;
+    vbits[w] = 0ull;
+    while (u) {
+      const int b = __ffsll(u) - 1;
+      u &= u - 1;
+      const std::uint32_t g = __ldg(p.new_id + (w * 64 + b));
+      atomicOr(ubits + (g >> 6), 1ull << (g & 63));
+    }
+  }
+}
+
+__global__ void k_remote_miss_mask(const std::uint32_t* __restrict__ slot, const std::uint32_t* __restrict__ part_of,
+                                   const unsigned char* __restrict__ peer_mask, std::uint64_t n,
+                                   unsigned long long* __restrict__ out) {
+  const std::uint64_t W = (n + 63) / 64;
+  for (std::uint64_t w = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; w < W;
+       w += (std::uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long m = 0;
+    for (int b = 0; b < 64; ++b) {
+      const std::uint64_t v = w * 64 + b;
+      if (v < n && slot[v] == VK_MISS && peer_mask[part_of[v]]) m |= 1ull << b;
+    }
+    out[w] = m;
   }
 }
 
@@ -669,6 +728,20 @@ void publish_tables(vk_plane_s& p) {
   VK_CUDA(cudaMemcpyAsync(p.d_base.p, base.data(), p.K * sizeof(void*), cudaMemcpyHostToDevice, p.stream));
   VK_CUDA(cudaMemcpyAsync(p.d_slot.p, slot.data(), p.K * sizeof(void*), cudaMemcpyHostToDevice, p.stream));
   VK_CUDA(cudaMemcpyAsync(p.d_nlocal.p, nl.data(), nl.size(), cudaMemcpyHostToDevice, p.stream));
+  std::vector<const void*> rm(p.K, nullptr);
+  const std::uint64_t W = (p.n + 63) / 64;
+  for (std::uint32_t k = 0; k < p.K; ++k) {
+    auto& q = p.parts[k];
+    if (!q.resident) continue;
+    if (!q.rmask.p) q.rmask.alloc(W * 8);
+    k_remote_miss_mask<<<grid_for(W, p.device), 256, 0, p.stream>>>(
+        q.slot.as<std::uint32_t>(), p.part_of.as<std::uint32_t>(), p.d_nlocal.as<unsigned char>() + 4 * p.K, p.n,
+        q.rmask.as<unsigned long long>());
+    VK_LAUNCH_CHECK();
+    rm[k] = q.rmask.p;
+  }
+  if (!p.d_rmask.p) p.d_rmask.alloc(p.K * sizeof(void*));
+  VK_CUDA(cudaMemcpyAsync(p.d_rmask.p, rm.data(), p.K * sizeof(void*), cudaMemcpyHostToDevice, p.stream));
   VK_CUDA(cudaStreamSynchronize(p.stream));
 }
 
@@ -845,6 +918,7 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     if (gp.V >= (1u << 15)) raise(VK_ERR_UNSUPPORTED, "feature rows above 512 KiB are not supported");
     gp.magic32 = gp.V == 1 ? 0u : (std::uint32_t)((0xffffffffull / gp.V) + 1);  // ceil(2^32 / V)
     sampler_all_rank(s, &gp.all_rank, &gp.W);
+    gp.rmask = p->d_rmask.as<const unsigned long long* const>();
     gp.nmb = nmb;
     static const std::uint32_t tile_words = [] {
       const char* e = std::getenv("VK_GATHER_TILE_WORDS");
@@ -934,7 +1008,22 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       VK_CUDA(cudaMemsetAsync(ss.uprefix.as<std::uint32_t>() + W, 0, 4, xs));
       const unsigned gx = (unsigned)std::max<std::uint64_t>(
           1, std::min<std::uint64_t>(ceil_div(gp.all_stride, 256), (std::uint64_t)sm_count(p->device) * 8 / nmb + 1));
-      k_remote_mark<<<dim3(gx, nmb), 256, 0, xs>>>(gp, ss.ubits.as<unsigned long long>());
+      static const bool word_mark = [] {
+        const char* e = std::getenv("VK_MARK_WORDS");
+        return !e || std::atoi(e) != 0;
+      }();
+      if (word_mark && sampler_all_rank_dense(s)) {
+        if (!ss.vbits.p) {
+          ss.vbits.alloc(W * 8);
+          VK_CUDA(cudaMemsetAsync(ss.vbits.p, 0, W * 8, xs));
+        }
+        k_remote_union<<<dim3((unsigned)ceil_div(W, 256), (unsigned)ceil_div(nmb, kMarkChunk)), 256, 0, xs>>>(
+            gp, ss.vbits.as<unsigned long long>());
+        k_remote_to_rows<<<grid_for(W, p->device), 256, 0, xs>>>(gp, ss.vbits.as<unsigned long long>(),
+                                                                ss.ubits.as<unsigned long long>());
+        count_launch();  // the second mark pass
+      } else
+        k_remote_mark<<<dim3(gx, nmb), 256, 0, xs>>>(gp, ss.ubits.as<unsigned long long>());
       if (timing) VK_CUDA(cudaEventRecord(tev[1], xs));
       k_word_popc<<<grid_for(W, p->device), 256, 0, xs>>>(ss.ubits.as<unsigned long long>(), W,
                                                           ss.uprefix.as<std::uint32_t>());
@@ -963,7 +1052,7 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
         k_remote_pull<std::uint16_t, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
                                                              ss.uprefix.as<std::uint32_t>() + W,
                                                              ss.staging.as<std::uint16_t>());
-      count_launch(6);
+      count_launch(6);  // mark, popc, scan (2 cub kernels), emit, pull
       VK_LAUNCH_CHECK();
       gp.ubits = ss.ubits.as<unsigned long long>();
       gp.uprefix = ss.uprefix.as<std::uint32_t>();

@@ -54,6 +54,10 @@ struct vk_sampler_s {
   std::uint64_t capF[VK_MAX_HOPS + 1]{};  // [0] = batch size
   std::uint64_t capS[VK_MAX_HOPS + 1]{};  // [h] edges of hop h
   std::uint64_t capS_max = 0, capAll = 0;
+  // all-level rank words written for every word (not only nonzero ones) when
+  // that costs no more than the id list itself (16 W <= 4 capAll): the plane
+  // then derives the wave's remote-miss set from the bitmaps word by word
+  bool dense_all_rank = false;
   vk::DevBuf F[VK_MAX_HOPS + 1], allidx[VK_MAX_HOPS + 1], indptr[VK_MAX_HOPS + 1], dst[VK_MAX_HOPS + 1];
   vk::DevBuf counts;  // u32: fcount[(L+1)*M] | ecount[(L+1)*M] | allcount[M] | err[1]
   vk::DevBuf edges_tmp, all, hopbits, allbits, hopprefix, allprefix, status, tickets, desc, seed_stage;
@@ -414,6 +418,7 @@ struct CompactParams {
   unsigned* ticket;
   std::uint64_t W, tiles;
   std::uint32_t nmb, wpt;
+  std::uint32_t dense_rank;        // write every rank word (see vk_sampler_s::dense_all_rank)
 };
 
 constexpr int kStage = 5120;  // ids staged in shared memory per tile (else direct writes)
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_reg(CompactParams p
     // at tile starts (multiples of kRankStride words, the vertex-tile
     // schedules): zero words elsewhere are skipped, which keeps sparse
     // frontiers on huge graphs from paying 16 B per empty word
-    if (w < p.W && (wd[k] || (w % kRankStride) == 0))
+    if (w < p.W && (wd[k] || p.dense_rank || (w % kRankStride) == 0))
       p.rank[mb * p.W + w] = make_uint4((unsigned)wd[k], (unsigned)(wd[k] >> 32), gbase + lpos, 0u);
     unsigned long long x = wd[k];
     while (x) {
@@ -642,7 +647,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     // at tile starts (multiples of kRankStride words, the vertex-tile
     // schedules): zero words elsewhere are skipped, which keeps sparse
     // frontiers on huge graphs from paying 16 B per empty word
-    if (wd || (w % kRankStride) == 0)
+    if (wd || p.dense_rank || (w % kRankStride) == 0)
       p.rank[mb * p.W + w] = make_uint4((unsigned)wd, (unsigned)(wd >> 32), gbase + lpos, 0u);
     if (!wd) continue;
     bits[w] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
@@ -831,6 +836,7 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   p.ticket = s.tickets.as<unsigned>() + slot;
   p.W = s.W;
   p.nmb = nmb;
+  p.dense_rank = (!hop && s.dense_all_rank) ? 1u : 0u;
   // Words per thread from the frontier's expected density (its capacity / n):
   // the widest tile whose expected ids still fit the shared staging buffer.
   // Sparse frontiers (early hops, papers-scale graphs) get few, fat tiles
@@ -911,6 +917,7 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
         all += s->capF[h];
       }
       s->capAll = std::min<std::uint64_t>(s->n, all);
+      s->dense_all_rank = 4 * s->W <= s->capAll;
       for (std::uint32_t h = 1; h <= L; ++h)
         if (s->capS[h] >= (1ull << 31))
           raise(VK_ERR_UNSUPPORTED, "per-minibatch edge capacity exceeds 2^31; lower batch size or fanouts");
@@ -1235,6 +1242,7 @@ void sampler_all_rank(vk_sampler_s* s, const uint4** rank, std::uint64_t* W) {
   *rank = s->allprefix.as<uint4>();
   *W = s->W;
 }
+bool sampler_all_rank_dense(vk_sampler_s* s) { return s->dense_all_rank; }
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out) { out = s->last_parts; }
 cudaEvent_t sampler_done_event(vk_sampler_s* s) { return s->done; }
 std::uint64_t sampler_capacity_all(vk_sampler_s* s) { return s->capAll; }
