@@ -237,8 +237,9 @@ __device__ __forceinline__ void fy_registers(const std::uint32_t* __restrict__ n
           }
       } else {
         bool found = false;
+        // at most i displaced positions exist before step i
 #pragma unroll
-        for (int c = 0; c < FMAX; ++c)
+        for (int c = 0; c < i; ++c)
           if (hp[c] == ji) {
             vj = hv[c];
             hv[c] = vi;
@@ -247,7 +248,7 @@ __device__ __forceinline__ void fy_registers(const std::uint32_t* __restrict__ n
         if (!found) {
           vj = pv[i];  // untouched position: the original CSR value
 #pragma unroll
-          for (int c = 0; c < FMAX; ++c)
+          for (int c = 0; c <= i; ++c)
             if ((std::uint32_t)c == nh) {
               hp[c] = ji;
               hv[c] = vi;
@@ -271,11 +272,13 @@ __device__ __forceinline__ void fy_registers(const std::uint32_t* __restrict__ n
 // Fisher-Yates swaps are then replayed in order on shared memory. Outputs of a
 // warp's 32 consecutive sources are contiguous in the MFG edge array, so they
 // are staged per warp and written back with coalesced stores.
-template <int FMAX>
+// EXACT: the fanout equals FMAX at compile time (the common 5/10/15), so the
+// register Fisher-Yates unrolls to exactly f slots with no predication.
+template <int FMAX, bool EXACT = false>
 __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) {
   extern __shared__ std::uint32_t sm_fy[];
   constexpr unsigned S = kSampleThreads;
-  const unsigned f = p.f;
+  const unsigned f = EXACT ? (unsigned)FMAX : p.f;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // shared FY slots only for the FMAX == 0 (fanout 17..32) variant
   constexpr unsigned kSlots = FMAX == 0 ? 5 : 0;
@@ -787,7 +790,13 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
     const std::size_t smem = (std::size_t)((fmax ? 0 : 5) * kSampleThreads + kSampleThreads) * p.f * 4;
     p.nmb = nmb;
     auto go = [&](dim3 grid) {
-      if (fmax == 8)
+      if (p.f == 5)
+        k_sample_smem<5, true><<<grid, kSampleThreads, smem, st>>>(p);
+      else if (p.f == 10)
+        k_sample_smem<10, true><<<grid, kSampleThreads, smem, st>>>(p);
+      else if (p.f == 15)
+        k_sample_smem<15, true><<<grid, kSampleThreads, smem, st>>>(p);
+      else if (fmax == 8)
         k_sample_smem<8><<<grid, kSampleThreads, smem, st>>>(p);
       else if (fmax == 16)
         k_sample_smem<16><<<grid, kSampleThreads, smem, st>>>(p);

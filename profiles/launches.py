@@ -28,7 +28,9 @@ def main():
     waves = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     ids = sorted(per)
     starts = [i for i in ids if short(names[i]) == 'k_prepare']
-    sel = [i for i in ids if i >= starts[-waves]]
+    # the wave's own kernels only: torch kernels the bench runs after the timed
+    # regions (distinct-row count, tallies) are not part of a wave
+    sel = [i for i in ids if i >= starts[-waves] and not re.search(r'at_cuda_detail|at::', names[i])]
     agg = collections.OrderedDict()
     for i in sel:
         k = short(names[i])
