@@ -60,9 +60,13 @@ struct Stream {
         return 0;
       }
       const double inv = __drcp_rn((double)bound);
-      const std::uint64_t limit = ~0ull - mod_u64(~0ull, bound, inv);
       std::uint64_t x = next_u64();
-      while (x >= limit) x = next_u64();
+      // limit = ~0 - (~0 % bound) > ~0 - bound, so any x <= ~0 - bound is
+      // accepted without computing the limit (all but ~bound/2^64 draws)
+      if (x > ~0ull - bound) {
+        const std::uint64_t limit = ~0ull - mod_u64(~0ull, bound, inv);
+        while (x >= limit) x = next_u64();
+      }
       return mod_u64(x, bound, inv);
     }
 #endif
