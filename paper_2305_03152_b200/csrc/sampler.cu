@@ -502,72 +502,99 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_reg(CompactParams p
   const unsigned long long mine = pack_vd(vc, dc);
   unsigned long long total;
   const unsigned long long inc = block_inclusive_scan<kCompactThreads>(mine, s_sm, &total);
-  if (threadIdx.x < 32) {
-    const unsigned long long ex = lookback_warp(p.status + mb * p.tiles, tile, total);
-    if (threadIdx.x == 0) s_excl = ex;
-  }
-  __syncthreads();
-  const unsigned long long base = s_excl;
   const unsigned long long lex = inc - mine;  // tile-local exclusive prefix
-  std::uint32_t lpos = (std::uint32_t)unpack_v(lex);
-  std::uint32_t dpos = (std::uint32_t)(unpack_d(base) + unpack_d(lex));
-  const std::uint32_t gbase = (std::uint32_t)unpack_v(base);
   const std::uint32_t tcount = (std::uint32_t)unpack_v(total);
   std::uint32_t* list = p.list + mb * p.cap_list;
   std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
+  unsigned long long* status = p.status + mb * p.tiles;
   const bool staged = tcount <= (std::uint32_t)kStage;
+  // Emit this thread's ids (and next-hop row starts) at positions lpos,
+  // dpos; to shared memory at tile-local positions when staged, else
+  // directly to the global list.
+  auto emit = [&](std::uint32_t lpos, std::uint32_t dpos, std::uint32_t gbase, bool to_smem) {
 #pragma unroll
-  for (int k = 0; k < WPT; ++k) {
-    const std::uint64_t w = w0 + k;
-    // rank words are only ever read for set bits (relabel / relabel maps) and
-    // at tile starts (multiples of kRankStride words, the vertex-tile
-    // schedules): zero words elsewhere are skipped, which keeps sparse
-    // frontiers on huge graphs from paying 16 B per empty word
-    if (w < p.W && (wd[k] || p.dense_rank || (w % kRankStride) == 0))
-      p.rank[mb * p.W + w] = make_uint4((unsigned)wd[k], (unsigned)(wd[k] >> 32), gbase + lpos, 0u);
-    unsigned long long x = wd[k];
-    while (x) {
-      // up to 8 set bits per round; their degree loads are independent
-      std::uint32_t vv[8], dd[8];
-      int nq = 0;
+    for (int k = 0; k < WPT; ++k) {
+      const std::uint64_t w = w0 + k;
+      unsigned long long x = wd[k];
+      while (x) {
+        // up to 8 set bits per round; their degree loads are independent
+        std::uint32_t vv[8], dd[8];
+        int nq = 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        dd[q] = 0;
-        if (x) {
-          const int b = __ffsll(x) - 1;
-          x &= x - 1;
-          vv[q] = (std::uint32_t)(w * 64 + b);
-          if (HAS_NEXT) dd[q] = __ldg(p.outdeg + vv[q]);
-          nq = q + 1;
+        for (int q = 0; q < 8; ++q) {
+          dd[q] = 0;
+          if (x) {
+            const int b = __ffsll(x) - 1;
+            x &= x - 1;
+            vv[q] = (std::uint32_t)(w * 64 + b);
+            if (HAS_NEXT) dd[q] = __ldg(p.outdeg + vv[q]);
+            nq = q + 1;
+          }
         }
-      }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (q < nq) {
-          const std::uint32_t v = vv[q];
-          std::uint32_t d = 0;
-          if (HAS_NEXT) {
-            d = dpos;
-            dpos += min(p.f_next, dd[q]);
+        for (int q = 0; q < 8; ++q) {
+          if (q < nq) {
+            const std::uint32_t v = vv[q];
+            std::uint32_t d = 0;
+            if (HAS_NEXT) {
+              d = dpos;
+              dpos += min(p.f_next, dd[q]);
+            }
+            if (to_smem) {
+              s_ids[lpos] = v;
+              if (HAS_NEXT) s_ip[lpos] = d;
+            } else {
+              list[gbase + lpos] = v;
+              if (HAS_NEXT) ipn[gbase + lpos] = d;
+            }
+            ++lpos;
           }
-          if (staged) {
-            s_ids[lpos] = v;
-            if (HAS_NEXT) s_ip[lpos] = d;
-          } else {
-            list[gbase + lpos] = v;
-            if (HAS_NEXT) ipn[gbase + lpos] = d;
-          }
-          ++lpos;
         }
       }
     }
-  }
+  };
+  // rank words are only ever read for set bits (relabel / relabel maps) and
+  // at tile starts (multiples of kRankStride words, the vertex-tile
+  // schedules): zero words elsewhere are skipped (unless dense_rank), which
+  // keeps sparse frontiers on huge graphs from paying 16 B per empty word
+  auto write_rank = [&](std::uint32_t first) {
+#pragma unroll
+    for (int k = 0; k < WPT; ++k) {
+      const std::uint64_t w = w0 + k;
+      if (w < p.W && (wd[k] || p.dense_rank || (w % kRankStride) == 0))
+        p.rank[mb * p.W + w] = make_uint4((unsigned)wd[k], (unsigned)(wd[k] >> 32), first, 0u);
+      first += (std::uint32_t)__popcll(wd[k]);
+    }
+  };
+  unsigned long long base;
   if (staged) {
+    // ids go to shared memory at tile-local positions first; warp 0 resolves
+    // the look-back afterwards, so its latency overlaps the emission (the
+    // aggregate is published up front for the successors)
+    if (threadIdx.x == 0) publish_aggregate(status, tile, total);
+    emit((std::uint32_t)unpack_v(lex), (std::uint32_t)unpack_d(lex), 0u, true);
+    if (threadIdx.x < 32) {
+      const unsigned long long ex = lookback_resolve(status, tile, total);
+      if (threadIdx.x == 0) s_excl = ex;
+    }
     __syncthreads();
+    base = s_excl;
+    const std::uint32_t gbase = (std::uint32_t)unpack_v(base), dbase = (std::uint32_t)unpack_d(base);
+    write_rank(gbase + (std::uint32_t)unpack_v(lex));
     for (std::uint32_t i = threadIdx.x; i < tcount; i += kCompactThreads) {
       list[gbase + i] = s_ids[i];
-      if (HAS_NEXT) ipn[gbase + i] = s_ip[i];
+      if (HAS_NEXT) ipn[gbase + i] = dbase + s_ip[i];
     }
+  } else {
+    if (threadIdx.x < 32) {
+      const unsigned long long ex = lookback_warp(status, tile, total);
+      if (threadIdx.x == 0) s_excl = ex;
+    }
+    __syncthreads();
+    base = s_excl;
+    const std::uint32_t gbase = (std::uint32_t)unpack_v(base);
+    write_rank(gbase + (std::uint32_t)unpack_v(lex));
+    emit((std::uint32_t)unpack_v(lex), (std::uint32_t)(unpack_d(base) + unpack_d(lex)), gbase, false);
   }
   if (tile == p.tiles - 1 && threadIdx.x == kCompactThreads - 1) {
     const unsigned long long all = base + total;

@@ -57,19 +57,22 @@ __device__ __forceinline__ unsigned long long peek(const unsigned long long* st)
   return v;
 }
 
-// Warp 0 only (all 32 lanes): publish this tile's aggregate, then look back
-// over a window of 32 predecessors at a time: the nearest inclusive prefix in
-// the window ends the walk, the aggregates after it are summed; lanes whose
+// Publish this tile's aggregate (tile 0: its inclusive prefix) so that
+// successors can look past it; one thread.
+__device__ __forceinline__ void publish_aggregate(unsigned long long* status, unsigned tile,
+                                                  unsigned long long aggregate) {
+  publish(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | aggregate);
+}
+
+// Warp 0 only (all 32 lanes), after publish_aggregate: look back over a
+// window of 32 predecessors at a time: the nearest inclusive prefix in the
+// window ends the walk, the aggregates after it are summed; lanes whose
 // predecessor has not published yet make the warp re-poll. Publishes the
 // inclusive prefix and returns the exclusive prefix (packed v|d) to all lanes.
-__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* status, unsigned tile,
-                                                            unsigned long long aggregate) {
+__device__ __forceinline__ unsigned long long lookback_resolve(unsigned long long* status, unsigned tile,
+                                                               unsigned long long aggregate) {
   const unsigned lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) publish(status, kFlagInc | aggregate);
-    return 0ull;
-  }
-  if (lane == 0) publish(status + tile, kFlagAgg | aggregate);
+  if (tile == 0) return 0ull;
   unsigned long long ex = 0;
   int top = (int)tile - 1;  // highest predecessor not yet accounted for
   while (true) {
@@ -100,6 +103,13 @@ __device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* 
   }
   if (lane == 0) publish(status + tile, kFlagInc | (ex + aggregate));
   return ex;
+}
+
+// Warp 0 only: publish the aggregate, then resolve the look-back.
+__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* status, unsigned tile,
+                                                            unsigned long long aggregate) {
+  if ((threadIdx.x & 31) == 0) publish_aggregate(status, tile, aggregate);
+  return lookback_resolve(status, tile, aggregate);
 }
 
 }  // namespace vk
