@@ -656,33 +656,14 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const unsigned long long mine = pack_vd(vc, dc);
   unsigned long long total;
   const unsigned long long inc = block_inclusive_scan<kCompactThreads>(mine, s_sm, &total);
-  if (threadIdx.x < 32) {
-    const unsigned long long ex = lookback_warp(p.status + mb * p.tiles, tile, total);
-    if (threadIdx.x == 0) s_excl = ex;
-  }
-  __syncthreads();
-  const unsigned long long base = s_excl;
   const unsigned long long lex = inc - mine;  // tile-local exclusive prefix
-  std::uint32_t lpos = (std::uint32_t)unpack_v(lex);
-  std::uint32_t dpos = (std::uint32_t)(unpack_d(base) + unpack_d(lex));
-  const std::uint32_t gbase = (std::uint32_t)unpack_v(base);
   const std::uint32_t tcount = (std::uint32_t)unpack_v(total);
   std::uint32_t* list = p.list + mb * p.cap_list;
   std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
+  unsigned long long* status = p.status + mb * p.tiles;
   const bool staged = tcount <= (std::uint32_t)kStage;
-#pragma unroll 1
-  for (std::uint64_t w = w0; w < w_end; ++w) {
-    const unsigned long long wd = word_at(w);
-    // rank words are only ever read for set bits (relabel / relabel maps) and
-    // at tile starts (multiples of kRankStride words, the vertex-tile
-    // schedules): zero words elsewhere are skipped, which keeps sparse
-    // frontiers on huge graphs from paying 16 B per empty word
-    if (wd || p.dense_rank || (w % kRankStride) == 0)
-      p.rank[mb * p.W + w] = make_uint4((unsigned)wd, (unsigned)(wd >> 32), gbase + lpos, 0u);
-    if (!wd) continue;
-    bits[w] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
-    if (OR_ALL) p.allbits[mb * p.W + w] |= wd;
-    unsigned long long x = wd;
+  auto emit_word = [&](std::uint64_t w, unsigned long long x, std::uint32_t& lpos, std::uint32_t& dpos,
+                       std::uint32_t gbase, bool to_smem) {
     while (x) {
       // up to 8 set bits per round; their degree loads are independent
       std::uint32_t vv[8], dd[8];
@@ -707,7 +688,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
             d = dpos;
             dpos += min(p.f_next, dd[q]);
           }
-          if (staged) {
+          if (to_smem) {
             s_ids[lpos] = v;
             if (HAS_NEXT) s_ip[lpos] = d;
           } else {
@@ -718,12 +699,64 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
         }
       }
     }
-  }
+  };
+  // rank words are only ever read for set bits (relabel / relabel maps) and
+  // at tile starts (multiples of kRankStride words, the vertex-tile
+  // schedules): zero words elsewhere are skipped (unless dense_rank), which
+  // keeps sparse frontiers on huge graphs from paying 16 B per empty word.
+  // Consumed words are cleared (the rank array keeps the bits).
+  auto finish_word = [&](std::uint64_t w, unsigned long long wd, std::uint32_t first) {
+    if (wd || p.dense_rank || (w % kRankStride) == 0)
+      p.rank[mb * p.W + w] = make_uint4((unsigned)wd, (unsigned)(wd >> 32), first, 0u);
+    if (wd) {
+      bits[w] = 0ull;
+      if (OR_ALL) p.allbits[mb * p.W + w] |= wd;
+    }
+  };
+  unsigned long long base;
   if (staged) {
+    // ids to shared memory at tile-local positions first, then warp 0
+    // resolves the look-back (its latency overlaps the emission)
+    if (threadIdx.x == 0) publish_aggregate(status, tile, total);
+    std::uint32_t lpos = (std::uint32_t)unpack_v(lex), dpos = (std::uint32_t)unpack_d(lex);
+#pragma unroll 1
+    for (std::uint64_t w = w0; w < w_end; ++w) {
+      const unsigned long long wd = word_at(w);
+      if (wd) emit_word(w, wd, lpos, dpos, 0u, true);
+    }
+    if (threadIdx.x < 32) {
+      const unsigned long long ex = lookback_resolve(status, tile, total);
+      if (threadIdx.x == 0) s_excl = ex;
+    }
     __syncthreads();
+    base = s_excl;
+    const std::uint32_t gbase = (std::uint32_t)unpack_v(base), dbase = (std::uint32_t)unpack_d(base);
+    std::uint32_t first = gbase + (std::uint32_t)unpack_v(lex);
+#pragma unroll 1
+    for (std::uint64_t w = w0; w < w_end; ++w) {
+      const unsigned long long wd = word_at(w);
+      finish_word(w, wd, first);
+      first += (std::uint32_t)__popcll(wd);
+    }
     for (std::uint32_t i = threadIdx.x; i < tcount; i += kCompactThreads) {
       list[gbase + i] = s_ids[i];
-      if (HAS_NEXT) ipn[gbase + i] = s_ip[i];
+      if (HAS_NEXT) ipn[gbase + i] = dbase + s_ip[i];
+    }
+  } else {
+    if (threadIdx.x < 32) {
+      const unsigned long long ex = lookback_warp(status, tile, total);
+      if (threadIdx.x == 0) s_excl = ex;
+    }
+    __syncthreads();
+    base = s_excl;
+    const std::uint32_t gbase = (std::uint32_t)unpack_v(base);
+    std::uint32_t lpos = (std::uint32_t)unpack_v(lex);
+    std::uint32_t dpos = (std::uint32_t)(unpack_d(base) + unpack_d(lex));
+#pragma unroll 1
+    for (std::uint64_t w = w0; w < w_end; ++w) {
+      const unsigned long long wd = word_at(w);
+      finish_word(w, wd, gbase + lpos);
+      if (wd) emit_word(w, wd, lpos, dpos, gbase, false);
     }
   }
   if (tile == p.tiles - 1 && threadIdx.x == kCompactThreads - 1) {
