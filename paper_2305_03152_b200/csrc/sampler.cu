@@ -607,11 +607,11 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_reg(CompactParams p
   }
 }
 
-// One CTA per tile of kCompactThreads * p.wpt words; each thread owns p.wpt
-// consecutive words (runtime: wide tiles for sparse frontiers, 1 word for the
-// dense ones; loops stay rolled so the kernel fits the instruction cache).
-// Pass 1 counts (ids and next-hop row lengths), the block scan + look-back
-// place the tile, pass 2 re-reads the words (L1/L2) and emits.
+// Wide tiles (8 or 16 words per thread; sparse frontiers, papers-scale
+// graphs): the tile's words are staged through shared memory with coalesced
+// loads, each thread notes which of its words are nonzero, and every later
+// pass visits only those (plus the rank-stride word), so an empty word costs
+// one shared load and a compare.
 template <bool HAS_NEXT, bool OR_ALL>
 __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   __shared__ unsigned s_ticket;
@@ -625,33 +625,40 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   const std::uint32_t mb = ticket / (unsigned)p.tiles;
   const std::uint32_t tile = ticket % (unsigned)p.tiles;
   if (mb >= p.nmb) return;
-  const std::uint32_t wpt = p.wpt;
+  const unsigned wpt = p.wpt;  // power of two, 8..32
   unsigned long long* bits = p.bits + mb * p.W;
   const std::uint64_t tbase = (std::uint64_t)tile * kCompactThreads * wpt;
   const std::uint64_t w0 = tbase + (std::uint64_t)threadIdx.x * wpt;
-  const std::uint64_t w_end = min(w0 + wpt, p.W);
-  // wide tiles: the tile's words are staged through shared memory with
-  // coalesced loads (thread-contiguous chunks would make every load
-  // instruction touch 32 lines); the row pitch wpt+1 avoids bank conflicts
+  const unsigned nw = w0 < p.W ? (unsigned)min((std::uint64_t)wpt, p.W - w0) : 0u;
+  // row pitch wpt+1 avoids bank conflicts; 32-bit shifts, no division
   extern __shared__ unsigned long long s_words[];
-  const bool smem_words = wpt >= 8;
-  if (smem_words) {
-    const std::uint64_t tend = min(tbase + (std::uint64_t)kCompactThreads * wpt, p.W);
-    for (std::uint64_t i = tbase + threadIdx.x; i < tend; i += kCompactThreads) {
-      const std::uint64_t o = i - tbase;
-      s_words[(o / wpt) * (wpt + 1) + o % wpt] = bits[i];
-    }
+  {
+    const unsigned n_t = (unsigned)(min(tbase + (std::uint64_t)kCompactThreads * wpt, p.W) - tbase);
+    const unsigned lw = (unsigned)(__ffs((int)wpt) - 1);
+    const unsigned long long* tb = bits + tbase;
+    for (unsigned o = threadIdx.x; o < n_t; o += kCompactThreads)
+      s_words[(o >> lw) * (wpt + 1) + (o & (wpt - 1))] = tb[o];
     __syncthreads();
   }
-  auto word_at = [&](std::uint64_t w) -> unsigned long long {
-    return smem_words ? s_words[threadIdx.x * (wpt + 1) + (w - w0)] : bits[w];
-  };
+  const unsigned long long* my = s_words + threadIdx.x * (wpt + 1);
+  unsigned nz = 0;
   unsigned long long vc = 0, dc = 0;
-#pragma unroll 4
-  for (std::uint64_t w = w0; w < w_end; ++w) {
-    const unsigned long long wd = word_at(w);
-    vc += __popcll(wd);
-    if (HAS_NEXT && wd) dc += capped_degree_sum(wd, w, p.outdeg, p.f_next);
+  for (unsigned j = 0; j < nw; ++j) {
+    const unsigned long long wd = my[j];
+    if (wd) {
+      nz |= 1u << j;
+      vc += __popcll(wd);
+      if (HAS_NEXT) dc += capped_degree_sum(wd, w0 + j, p.outdeg, p.f_next);
+    }
+  }
+  // words that get a rank entry: nonzero ones, the kRankStride multiple (tile
+  // starts of the vertex-tile schedules), or all of them (dense_rank)
+  unsigned rmask = nz;
+  if (p.dense_rank) {
+    rmask = nw >= 32 ? ~0u : ((1u << nw) - 1u);
+  } else {
+    const unsigned jr = (unsigned)((kRankStride - (w0 % kRankStride)) % kRankStride);
+    if (jr < nw) rmask |= 1u << jr;
   }
   const unsigned long long mine = pack_vd(vc, dc);
   unsigned long long total;
@@ -700,17 +707,19 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
       }
     }
   };
-  // rank words are only ever read for set bits (relabel / relabel maps) and
-  // at tile starts (multiples of kRankStride words, the vertex-tile
-  // schedules): zero words elsewhere are skipped (unless dense_rank), which
-  // keeps sparse frontiers on huge graphs from paying 16 B per empty word.
-  // Consumed words are cleared (the rank array keeps the bits).
-  auto finish_word = [&](std::uint64_t w, unsigned long long wd, std::uint32_t first) {
-    if (wd || p.dense_rank || (w % kRankStride) == 0)
+  // rank entries (the rank array keeps the bits) and clearing of consumed
+  // words, in word order so `first` advances by each word's count
+  auto finish = [&](std::uint32_t first) {
+    for (unsigned m = rmask; m; m &= m - 1) {
+      const unsigned j = (unsigned)(__ffs((int)m) - 1);
+      const std::uint64_t w = w0 + j;
+      const unsigned long long wd = my[j];
       p.rank[mb * p.W + w] = make_uint4((unsigned)wd, (unsigned)(wd >> 32), first, 0u);
-    if (wd) {
-      bits[w] = 0ull;
-      if (OR_ALL) p.allbits[mb * p.W + w] |= wd;
+      if (wd) {
+        bits[w] = 0ull;
+        if (OR_ALL) p.allbits[mb * p.W + w] |= wd;
+        first += (std::uint32_t)__popcll(wd);
+      }
     }
   };
   unsigned long long base;
@@ -719,10 +728,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     // resolves the look-back (its latency overlaps the emission)
     if (threadIdx.x == 0) publish_aggregate(status, tile, total);
     std::uint32_t lpos = (std::uint32_t)unpack_v(lex), dpos = (std::uint32_t)unpack_d(lex);
-#pragma unroll 1
-    for (std::uint64_t w = w0; w < w_end; ++w) {
-      const unsigned long long wd = word_at(w);
-      if (wd) emit_word(w, wd, lpos, dpos, 0u, true);
+    for (unsigned m = nz; m; m &= m - 1) {
+      const unsigned j = (unsigned)(__ffs((int)m) - 1);
+      emit_word(w0 + j, my[j], lpos, dpos, 0u, true);
     }
     if (threadIdx.x < 32) {
       const unsigned long long ex = lookback_resolve(status, tile, total);
@@ -731,13 +739,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     __syncthreads();
     base = s_excl;
     const std::uint32_t gbase = (std::uint32_t)unpack_v(base), dbase = (std::uint32_t)unpack_d(base);
-    std::uint32_t first = gbase + (std::uint32_t)unpack_v(lex);
-#pragma unroll 1
-    for (std::uint64_t w = w0; w < w_end; ++w) {
-      const unsigned long long wd = word_at(w);
-      finish_word(w, wd, first);
-      first += (std::uint32_t)__popcll(wd);
-    }
+    finish(gbase + (std::uint32_t)unpack_v(lex));
     for (std::uint32_t i = threadIdx.x; i < tcount; i += kCompactThreads) {
       list[gbase + i] = s_ids[i];
       if (HAS_NEXT) ipn[gbase + i] = dbase + s_ip[i];
@@ -750,13 +752,12 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     __syncthreads();
     base = s_excl;
     const std::uint32_t gbase = (std::uint32_t)unpack_v(base);
+    finish(gbase + (std::uint32_t)unpack_v(lex));
     std::uint32_t lpos = (std::uint32_t)unpack_v(lex);
     std::uint32_t dpos = (std::uint32_t)(unpack_d(base) + unpack_d(lex));
-#pragma unroll 1
-    for (std::uint64_t w = w0; w < w_end; ++w) {
-      const unsigned long long wd = word_at(w);
-      finish_word(w, wd, gbase + lpos);
-      if (wd) emit_word(w, wd, lpos, dpos, gbase, false);
+    for (unsigned m = nz; m; m &= m - 1) {
+      const unsigned j = (unsigned)(__ffs((int)m) - 1);
+      emit_word(w0 + j, my[j], lpos, dpos, gbase, false);
     }
   }
   if (tile == p.tiles - 1 && threadIdx.x == kCompactThreads - 1) {
@@ -916,7 +917,12 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   const std::uint64_t min_ctas = (std::uint64_t)sm_count(s.g->device) * 8;
   auto ctas = [&](int w) { return (std::uint64_t)nmb * ((s.W + (std::uint64_t)kCompactThreads * w - 1) /
                                                          ((std::uint64_t)kCompactThreads * w)); };
-  while (wpt < 16 && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage &&
+  static const int max_wpt = [] {
+    const char* e = std::getenv("VK_COMPACT_MAX_WPT");
+    const int v = e ? std::atoi(e) : 16;
+    return v >= 32 ? 32 : 16;
+  }();
+  while (wpt < max_wpt && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage &&
          ctas(wpt * 2) >= min_ctas)
     wpt *= 2;
   p.tiles = (s.W + (std::uint64_t)kCompactThreads * wpt - 1) / ((std::uint64_t)kCompactThreads * wpt);
@@ -932,6 +938,12 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
     else
       k_compact_reg<HN, OA, 1><<<grid, kCompactThreads, 0, st>>>(p);
   };
+  if (wpt >= 32) {  // 32 words/thread stage 67 KB
+    const int mx = (int)smem;
+    VK_CUDA(cudaFuncSetAttribute(k_compact<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    VK_CUDA(cudaFuncSetAttribute(k_compact<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    VK_CUDA(cudaFuncSetAttribute(k_compact<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  }
   if (wpt <= 4) {
     if (has_next)
       narrow(std::true_type{}, std::true_type{});
