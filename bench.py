@@ -43,11 +43,11 @@ CONFIGS = {
     # BASELINE.json configs[0]: synthetic power-law 100K / 2M edges, 64-d fp32, 1 partition
     "c1": dict(workload="C1 synthetic power-law 100K nodes / 2M edges, 64-d fp32, 1 partition",
                n=100_000, d=10, K=1, p_in=1.0, train=0.10, dim=64, dtype=0, alpha=0.0,
-               fanouts=(15, 10, 5), b=1024),
+               fanouts=(15, 10, 5), b=1024, wave=128),
     # configs[1]: ogbn-arxiv-shaped, 169K nodes, ~1.2M edges (x2 slots), 128-d, 2 partitions, cache 10%
     "c2": dict(workload="C2 ogbn-arxiv-shaped 169K nodes, 128-d fp32, 2 partitions, VIP cache 10%",
                n=169_343, d=7, K=2, p_in=0.8, train=0.537, dim=128, dtype=0, alpha=0.10,
-               fanouts=(15, 10, 5), b=1024),
+               fanouts=(15, 10, 5), b=1024, wave=128),
     # configs[2]: ogbn-products-shaped, 2.45M nodes, 62M edges (x2 slots), 100-d, 8 partitions, cache 20%
     "c3": dict(workload="C3 ogbn-products-shaped 2.45M nodes / 122M CSR slots, 100-d fp32, "
                         "8 partitions, fanout (15,10,5), batch 1024, VIP cache 20%",
@@ -577,7 +577,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--alpha-sweep", action="store_true", help="also tally misses for cache sizes 0-32%%")
     ap.add_argument("--wave", type=int, default=None,
-                    help="minibatches per step per GPU (default: the config's, 128 for c3, else 32)")
+                    help="minibatches per step per GPU (default: the config's; 128 for c1-c3, 32 for c4)")
     ap.add_argument("--pipes", type=int, default=1, help="overlapped sampler+gather pipelines (streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
