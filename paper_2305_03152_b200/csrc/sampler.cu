@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_reg(CompactParams p
   for (int k = 0; k < WPT; ++k) {
     if (wd[k]) {
       bits[w0 + k] = 0ull;  // the rank array keeps the bits; the bitmap is clean for reuse
-      if (OR_ALL) p.allbits[mb * p.W + w0 + k] |= wd[k];
+      if (OR_ALL) atomicOr(p.allbits + mb * p.W + w0 + k, wd[k]);  // RED: no load latency
     }
     vc += __popcll(wd[k]);
     if (HAS_NEXT) {
@@ -636,8 +636,22 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     const unsigned n_t = (unsigned)(min(tbase + (std::uint64_t)kCompactThreads * wpt, p.W) - tbase);
     const unsigned lw = (unsigned)(__ffs((int)wpt) - 1);
     const unsigned long long* tb = bits + tbase;
-    for (unsigned o = threadIdx.x; o < n_t; o += kCompactThreads)
-      s_words[(o >> lw) * (wpt + 1) + (o & (wpt - 1))] = tb[o];
+    // wpt (8..32) coalesced rounds, 8 loads in flight per thread before the
+    // shared stores (a dependent load->store loop would pay one DRAM latency
+    // per round)
+    for (unsigned i0 = 0; i0 < wpt; i0 += 8) {
+      unsigned long long r[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const unsigned o = (i0 + q) * kCompactThreads + threadIdx.x;
+        r[q] = o < n_t ? tb[o] : 0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const unsigned o = (i0 + q) * kCompactThreads + threadIdx.x;
+        if (o < n_t) s_words[(o >> lw) * (wpt + 1) + (o & (wpt - 1))] = r[q];
+      }
+    }
     __syncthreads();
   }
   const unsigned long long* my = s_words + threadIdx.x * (wpt + 1);
@@ -648,7 +662,40 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     if (wd) {
       nz |= 1u << j;
       vc += __popcll(wd);
-      if (HAS_NEXT) dc += capped_degree_sum(wd, w0 + j, p.outdeg, p.f_next);
+    }
+  }
+  // Cursor over this thread's set bits in vertex order, across its nonzero
+  // words: sparse tiles have ~1 bit per word, so gathering 8 bits per round
+  // across words keeps 8 degree loads in flight instead of one per word.
+  auto next8 = [&](unsigned& m, unsigned long long& x, unsigned& j, std::uint32_t* vv) -> int {
+    int nq = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      while (!x && m) {
+        j = (unsigned)(__ffs((int)m) - 1);
+        m &= m - 1;
+        x = my[j];
+      }
+      if (x) {
+        const int b = __ffsll(x) - 1;
+        x &= x - 1;
+        vv[q] = (std::uint32_t)((w0 + j) * 64 + b);
+        nq = q + 1;
+      }
+    }
+    return nq;
+  };
+  if (HAS_NEXT) {
+    unsigned m = nz, j = 0;
+    unsigned long long x = 0;
+    while (true) {
+      std::uint32_t vv[8], d[8];
+      const int nq = next8(m, x, j, vv);
+      if (!nq) break;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d[q] = q < nq ? __ldg(p.outdeg + vv[q]) : 0u;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dc += min(p.f_next, d[q]);
     }
   }
   // words that get a rank entry: nonzero ones, the kRankStride multiple (tile
@@ -669,37 +716,30 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
   unsigned long long* status = p.status + mb * p.tiles;
   const bool staged = tcount <= (std::uint32_t)kStage;
-  auto emit_word = [&](std::uint64_t w, unsigned long long x, std::uint32_t& lpos, std::uint32_t& dpos,
-                       std::uint32_t gbase, bool to_smem) {
-    while (x) {
-      // up to 8 set bits per round; their degree loads are independent
+  // Emit this thread's ids (and next-hop row starts) at positions lpos,
+  // dpos: to shared memory at tile-local positions, or to the global list.
+  auto emit_all = [&](std::uint32_t lpos, std::uint32_t dpos, std::uint32_t gbase, bool to_smem) {
+    unsigned m = nz, j = 0;
+    unsigned long long x = 0;
+    while (true) {
       std::uint32_t vv[8], dd[8];
-      int nq = 0;
+      const int nq = next8(m, x, j, vv);
+      if (!nq) break;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        dd[q] = 0;
-        if (x) {
-          const int b = __ffsll(x) - 1;
-          x &= x - 1;
-          vv[q] = (std::uint32_t)(w * 64 + b);
-          if (HAS_NEXT) dd[q] = __ldg(p.outdeg + vv[q]);
-          nq = q + 1;
-        }
-      }
+      for (int q = 0; q < 8; ++q) dd[q] = (HAS_NEXT && q < nq) ? __ldg(p.outdeg + vv[q]) : 0u;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         if (q < nq) {
-          const std::uint32_t v = vv[q];
           std::uint32_t d = 0;
           if (HAS_NEXT) {
             d = dpos;
             dpos += min(p.f_next, dd[q]);
           }
           if (to_smem) {
-            s_ids[lpos] = v;
+            s_ids[lpos] = vv[q];
             if (HAS_NEXT) s_ip[lpos] = d;
           } else {
-            list[gbase + lpos] = v;
+            list[gbase + lpos] = vv[q];
             if (HAS_NEXT) ipn[gbase + lpos] = d;
           }
           ++lpos;
@@ -707,8 +747,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
       }
     }
   };
-  // rank entries (the rank array keeps the bits) and clearing of consumed
-  // words, in word order so `first` advances by each word's count
+  // Tiles with many nonzero words (>= 1 id per 4 words) clear the whole tile
+  // with coalesced stores instead of one partial-sector store per word.
+  const bool clear_tile = (std::uint64_t)tcount * 4 >= (std::uint64_t)kCompactThreads * wpt;
   auto finish = [&](std::uint32_t first) {
     for (unsigned m = rmask; m; m &= m - 1) {
       const unsigned j = (unsigned)(__ffs((int)m) - 1);
@@ -716,10 +757,15 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
       const unsigned long long wd = my[j];
       p.rank[mb * p.W + w] = make_uint4((unsigned)wd, (unsigned)(wd >> 32), first, 0u);
       if (wd) {
-        bits[w] = 0ull;
-        if (OR_ALL) p.allbits[mb * p.W + w] |= wd;
+        if (!clear_tile) bits[w] = 0ull;
+        if (OR_ALL) atomicOr(p.allbits + mb * p.W + w, wd);  // RED: no load latency
         first += (std::uint32_t)__popcll(wd);
       }
+    }
+    if (clear_tile) {
+      const unsigned n_t = (unsigned)(min(tbase + (std::uint64_t)kCompactThreads * wpt, p.W) - tbase);
+      unsigned long long* tb = bits + tbase;
+      for (unsigned o = threadIdx.x; o < n_t; o += kCompactThreads) tb[o] = 0ull;
     }
   };
   unsigned long long base;
@@ -727,11 +773,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     // ids to shared memory at tile-local positions first, then warp 0
     // resolves the look-back (its latency overlaps the emission)
     if (threadIdx.x == 0) publish_aggregate(status, tile, total);
-    std::uint32_t lpos = (std::uint32_t)unpack_v(lex), dpos = (std::uint32_t)unpack_d(lex);
-    for (unsigned m = nz; m; m &= m - 1) {
-      const unsigned j = (unsigned)(__ffs((int)m) - 1);
-      emit_word(w0 + j, my[j], lpos, dpos, 0u, true);
-    }
+    emit_all((std::uint32_t)unpack_v(lex), (std::uint32_t)unpack_d(lex), 0u, true);
     if (threadIdx.x < 32) {
       const unsigned long long ex = lookback_resolve(status, tile, total);
       if (threadIdx.x == 0) s_excl = ex;
@@ -753,12 +795,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     base = s_excl;
     const std::uint32_t gbase = (std::uint32_t)unpack_v(base);
     finish(gbase + (std::uint32_t)unpack_v(lex));
-    std::uint32_t lpos = (std::uint32_t)unpack_v(lex);
-    std::uint32_t dpos = (std::uint32_t)(unpack_d(base) + unpack_d(lex));
-    for (unsigned m = nz; m; m &= m - 1) {
-      const unsigned j = (unsigned)(__ffs((int)m) - 1);
-      emit_word(w0 + j, my[j], lpos, dpos, gbase, false);
-    }
+    emit_all((std::uint32_t)unpack_v(lex), (std::uint32_t)(unpack_d(base) + unpack_d(lex)), gbase, false);
   }
   if (tile == p.tiles - 1 && threadIdx.x == kCompactThreads - 1) {
     const unsigned long long all = base + total;
