@@ -254,6 +254,25 @@ VK_API int vk_plane_row_bytes(vk_plane p, uint64_t* row_bytes);
  * wave's deduplicated miss exchange); synchronises the device. */
 VK_API int vk_plane_pulled_rows(vk_plane p, uint64_t* rows);
 
+/* ------------------------------------------------ communication tallies
+ * vipkit::simulate (commsim.hpp:56-59, commsim.cpp:77-127) and the alpha
+ * axis of sweep (commsim.cpp:140-259): expands every minibatch
+ * of every partition for `epochs` epochs in for_each_expansion order
+ * (commsim.cpp:45-52) with the device sampler (waves of `wave` minibatches,
+ * 0 = 128) and classifies each distinct neighbourhood vertex of a minibatch
+ * of partition k as local / cache hit / remote miss (commsim.cpp:61-73).
+ * Cache plans: partition k's cached ids are cached_ids[cached_offsets[k] ..
+ * cached_offsets[k+1]) in ranking order; plan a caches the first
+ * takes[a*K + k] of them (build_cache's ranking prefixes), takes == NULL
+ * means one plan caching every listed id. cells[num_plans][epochs][K][3] =
+ * {local_hits, cache_hits, remote_misses} (CommReport::Cell). Errors as the
+ * reference: VK_ERR_SAMPLING for a partition without train vertices,
+ * VK_ERR_PARAMETER for batch_size 0. */
+VK_API int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K,
+                       const uint32_t* fanouts, uint32_t num_hops, uint64_t batch_size, uint64_t epochs,
+                       uint64_t global_seed, const uint32_t* cached_ids, const uint64_t* cached_offsets,
+                       const uint64_t* takes, uint32_t num_plans, uint32_t wave, uint64_t* cells);
+
 /* ------------------------------------------------------- synthetic data
  * Community-structured power-law generator for the BASELINE configs (builder
  * addition: the reference PA generator is sequential and

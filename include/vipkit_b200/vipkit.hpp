@@ -17,6 +17,7 @@
 // does not have.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <initializer_list>
 #include <memory>
@@ -432,6 +433,118 @@ inline CachePlan build_cache(const std::vector<Ranking>& rankings, double alpha,
     for (vertex_t v : plan.cached[k]) plan.member_bits[k][v >> 6] |= 1ull << (v & 63);
   }
   return plan;
+}
+
+// ---- commsim.hpp:14-59 -----------------------------------------
+/// Per-(epoch, partition) tallies of distinct neighbourhood vertices.
+struct CommReport {
+  std::string policy;
+  double alpha = 0.0;
+  std::string fanout_label;
+  std::uint64_t epochs = 0;
+  std::uint32_t partitions = 0;
+  struct Cell {
+    std::uint64_t local_hits = 0;
+    std::uint64_t cache_hits = 0;
+    std::uint64_t remote_misses = 0;
+  };
+  std::vector<Cell> cells;  // epoch-major: cells[e * partitions + k]
+  Cell& at(std::uint64_t e, std::uint32_t k) { return cells[e * partitions + k]; }
+  const Cell& at(std::uint64_t e, std::uint32_t k) const { return cells[e * partitions + k]; }
+  std::uint64_t total_misses() const {
+    std::uint64_t t = 0;
+    for (const auto& c : cells) t += c.remote_misses;
+    return t;
+  }
+  std::uint64_t total_cache_hits() const {
+    std::uint64_t t = 0;
+    for (const auto& c : cells) t += c.cache_hits;
+    return t;
+  }
+  std::uint64_t total_local_hits() const {
+    std::uint64_t t = 0;
+    for (const auto& c : cells) t += c.local_hits;
+    return t;
+  }
+  double avg_epoch_misses() const {
+    return epochs ? static_cast<double>(total_misses()) / static_cast<double>(epochs) : 0.0;
+  }
+};
+
+namespace detail {
+inline std::vector<CommReport> simulate_plans(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
+                                              const FanoutSpec& fanouts, std::uint64_t b, std::uint64_t E,
+                                              const SeedSpec& seeds, const std::vector<vertex_t>& ids,
+                                              const std::vector<std::uint64_t>& offsets,
+                                              const std::vector<std::uint64_t>* takes,
+                                              const std::vector<double>& alphas) {
+  fanouts.validate();
+  const std::uint32_t A = static_cast<std::uint32_t>(alphas.size());
+  std::vector<std::uint64_t> cells(static_cast<std::size_t>(A) * E * part.K * 3);
+  check(vk_simulate(g.handle(), roles.role.data(), part.part_of.data(), part.K, fanouts.fanouts.data(),
+                    static_cast<std::uint32_t>(fanouts.hops()), b, E, seeds.global_seed,
+                    ids.empty() ? nullptr : ids.data(), offsets.data(), takes ? takes->data() : nullptr, A, 0,
+                    cells.data()));
+  std::vector<CommReport> out(A);
+  for (std::uint32_t a = 0; a < A; ++a) {
+    CommReport& r = out[a];
+    r.alpha = alphas[a];
+    r.fanout_label = fanouts.label();
+    r.epochs = E;
+    r.partitions = part.K;
+    r.cells.resize(E * part.K);
+    for (std::size_t c = 0; c < r.cells.size(); ++c) {
+      const std::uint64_t* x = cells.data() + (static_cast<std::size_t>(a) * E * part.K + c) * 3;
+      r.cells[c] = {x[0], x[1], x[2]};
+    }
+  }
+  return out;
+}
+}  // namespace detail
+
+/// simulate (commsim.hpp:56-59) on the device: every minibatch of every
+/// partition for E epochs, classified against the plan.
+inline CommReport simulate(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
+                           const FanoutSpec& fanouts, std::uint64_t b, std::uint64_t E, const SeedSpec& seeds,
+                           const CachePlan& plan) {
+  if (plan.K != part.K) throw config_error("cache plan partition count differs from partition map");
+  std::vector<vertex_t> ids;
+  std::vector<std::uint64_t> offs{0};
+  for (const auto& c : plan.cached) {
+    ids.insert(ids.end(), c.begin(), c.end());
+    offs.push_back(ids.size());
+  }
+  return detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, nullptr, {plan.alpha})[0];
+}
+
+/// The alpha axis of sweep (commsim.cpp:140-259) for one ranking policy:
+/// build_cache(rankings, alpha) for every alpha, all scored from one
+/// expansion pass (the plans are nested ranking prefixes).
+inline std::vector<CommReport> simulate_alphas(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
+                                               const FanoutSpec& fanouts, std::uint64_t b, std::uint64_t E,
+                                               const SeedSpec& seeds, const std::vector<Ranking>& rankings,
+                                               const std::vector<double>& alphas) {
+  if (rankings.size() != part.K) throw config_error("need one ranking per partition");
+  if (alphas.empty() || alphas.size() > 32) throw parameter_error("between 1 and 32 alphas per pass");
+  std::vector<vertex_t> ids;
+  std::vector<std::uint64_t> offs{0}, takes;
+  std::uint64_t cap_max = 0;
+  for (double a : alphas) {
+    std::uint64_t cap = 0;
+    detail::check(vk_cache_capacity(a, part.part_of.size(), part.K, &cap));
+    cap_max = std::max(cap_max, cap);
+  }
+  for (const auto& r : rankings) {
+    const auto take = std::min<std::uint64_t>(cap_max, r.order.size());
+    ids.insert(ids.end(), r.order.begin(), r.order.begin() + take);
+    offs.push_back(ids.size());
+  }
+  for (double a : alphas) {
+    std::uint64_t cap = 0;
+    detail::check(vk_cache_capacity(a, part.part_of.size(), part.K, &cap));
+    for (const auto& r : rankings) takes.push_back(std::min<std::uint64_t>(cap, r.order.size()));
+  }
+  return detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, &takes, alphas);
 }
 
 // ---- reorder.hpp:15-26 --------------------------------------------------------

@@ -39,6 +39,18 @@ int sm_count(int device) {
   return cache[device];
 }
 
+// The epoch shuffle of epoch_minibatches (sampling.cpp:54-63): stream
+// (0xB1, epoch, k) folded from the global seed, Fisher-Yates from the back.
+void epoch_shuffle(std::uint32_t* perm, std::uint64_t T, std::uint32_t k, std::uint64_t epoch,
+                   std::uint64_t global_seed) {
+  std::uint64_t h = global_seed;
+  h = key_step(h, tag::minibatch_perm);
+  h = key_step(h, epoch);
+  h = key_step(h, k);
+  Stream rng(h);
+  for (std::uint64_t i = T; i > 1; --i) std::swap(perm[i - 1], perm[rng.next_below(i)]);
+}
+
 }  // namespace vk
 
 using namespace vk;
@@ -129,12 +141,7 @@ int vk_epoch_minibatches(uint64_t n, const uint8_t* roles, const uint32_t* part_
     if (seed_keys)
       std::stable_sort(out_perm, out_perm + T,
                        [&](std::uint32_t a, std::uint32_t c) { return seed_keys[a] < seed_keys[c]; });
-    std::uint64_t h = global_seed;
-    h = key_step(h, tag::minibatch_perm);
-    h = key_step(h, epoch);
-    h = key_step(h, k);
-    Stream rng(h);
-    for (std::uint64_t i = T; i > 1; --i) std::swap(out_perm[i - 1], out_perm[rng.next_below(i)]);
+    vk::epoch_shuffle(out_perm, T, k, epoch, global_seed);
     *out_count = T;
   });
 }

@@ -9,6 +9,9 @@
 namespace vk {
 extern std::atomic<std::uint64_t> g_launches;
 inline void count_launch(std::uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+// epoch_minibatches' shuffle of partition k's train members (capi.cu)
+void epoch_shuffle(std::uint32_t* perm, std::uint64_t T, std::uint32_t k, std::uint64_t epoch,
+                   std::uint64_t global_seed);
 }  // namespace vk
 
 // Device-resident graph (replaces vipkit::Graph, graph.hpp:20-46). Offsets

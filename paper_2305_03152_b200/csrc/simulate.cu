@@ -1,0 +1,265 @@
+// simulate (commsim.cpp:77-127) and the alpha axis of sweep
+// (commsim.cpp:140-259) on the device -- SURVEY §8f row F1.
+//
+// The reference expands every minibatch of every partition for E epochs
+// (for_each_expansion, commsim.cpp:38-52: epoch-major, then partition, then
+// batch index) and classifies each distinct neighbourhood vertex of the
+// minibatch of partition k as local (part_of[v] == k), cache hit
+// (CachePlan::is_cached(k, v)) or remote miss (classify, commsim.cpp:61-73),
+// summing per (epoch, partition) cell. Expansion depends only on the seeds, so
+// here the minibatches stream through the batched device sampler in waves and
+// one classification pass scores them against several cache plans at once:
+// plan a caches the first takes[a][k] ids of partition k's cached list (the
+// ranking prefixes build_cache produces, policies.cpp:149-163), so a vertex
+// at list position p is a hit for every plan with takes > p.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+#include "rng.cuh"
+
+struct vk_sampler_s;
+namespace vk {
+void sampler_internal(vk_sampler_s* s, const std::uint32_t** all, std::uint64_t* all_stride,
+                      const std::uint32_t** all_count, std::uint32_t* nmb, const std::uint32_t** partitions,
+                      vk_graph_s** g, cudaStream_t* last_stream);
+}  // namespace vk
+
+namespace vk {
+namespace {
+
+constexpr std::uint32_t kMaxPlans = 32;
+
+unsigned fill_grid(std::uint64_t work, int device) {
+  const std::uint64_t g = (work + 255) / 256;
+  const std::uint64_t cap = (std::uint64_t)sm_count(device) * 16;
+  return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+__global__ void k_fill_positions(const std::uint32_t* __restrict__ ids, std::uint64_t count,
+                                 std::uint32_t* __restrict__ pos) {
+  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (std::uint64_t)gridDim.x * blockDim.x)
+    pos[ids[i]] = (std::uint32_t)i;
+}
+
+// One (chunk, minibatch) CTA: per vertex of all_vertices, local / per-plan
+// hit counts, reduced in shared memory and added to the minibatch's cell.
+__global__ void __launch_bounds__(256) k_classify_plans(const std::uint32_t* __restrict__ all, std::uint64_t stride,
+                                                        const std::uint32_t* __restrict__ count,
+                                                        const std::uint32_t* __restrict__ cell_of,
+                                                        const std::uint32_t* __restrict__ part_of,
+                                                        const std::uint32_t* __restrict__ pos, std::uint64_t n,
+                                                        const std::uint64_t* __restrict__ takes, std::uint32_t K,
+                                                        std::uint32_t A, std::uint64_t cells_per_plan,
+                                                        unsigned long long* __restrict__ cells) {
+  __shared__ unsigned long long s_cnt[2 + kMaxPlans];
+  const std::uint32_t mb = blockIdx.y;
+  const std::uint32_t cell = cell_of[mb];
+  const std::uint32_t k = cell % K;
+  for (std::uint32_t i = threadIdx.x; i < 2 + A; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  std::uint64_t tk[kMaxPlans];
+#pragma unroll
+  for (std::uint32_t a = 0; a < kMaxPlans; ++a) tk[a] = a < A ? takes[a * K + k] : 0;
+  unsigned long long local = 0, remote = 0;
+  unsigned hits[kMaxPlans];
+#pragma unroll
+  for (std::uint32_t a = 0; a < kMaxPlans; ++a) hits[a] = 0;
+  const std::uint32_t c = count[mb];
+  const std::uint32_t* av = all + mb * stride;
+  const std::uint32_t* pk = pos + (std::uint64_t)k * n;
+  for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < c; r += gridDim.x * blockDim.x) {
+    const std::uint32_t v = __ldg(av + r);
+    if (__ldg(part_of + v) == k) {
+      ++local;
+    } else {
+      ++remote;
+      const std::uint32_t p = __ldg(pk + v);
+#pragma unroll
+      for (std::uint32_t a = 0; a < kMaxPlans; ++a) hits[a] += (a < A && p < tk[a]) ? 1u : 0u;
+    }
+  }
+  // warp reduction, then one shared atomic per warp and counter
+  auto wsum = [](unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+  };
+  local = wsum(local);
+  remote = wsum(remote);
+  const bool lead = (threadIdx.x & 31) == 0;
+  if (lead) {
+    atomicAdd(&s_cnt[0], local);
+    atomicAdd(&s_cnt[1], remote);
+  }
+#pragma unroll
+  for (std::uint32_t a = 0; a < kMaxPlans; ++a) {
+    if (a < A) {
+      const unsigned long long h = wsum(hits[a]);
+      if (lead) atomicAdd(&s_cnt[2 + a], h);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < A) {
+    const std::uint32_t a = threadIdx.x;
+    unsigned long long* cl = cells + a * cells_per_plan + (std::uint64_t)cell * 3;
+    const unsigned long long h = s_cnt[2 + a];
+    if (s_cnt[0]) atomicAdd(cl + 0, s_cnt[0]);
+    if (h) atomicAdd(cl + 1, h);
+    if (s_cnt[1] - h) atomicAdd(cl + 2, s_cnt[1] - h);
+  }
+}
+
+}  // namespace
+}  // namespace vk
+
+using namespace vk;
+
+extern "C" {
+
+int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, const uint32_t* fanouts,
+                uint32_t num_hops, uint64_t batch_size, uint64_t epochs, uint64_t global_seed,
+                const uint32_t* cached_ids, const uint64_t* cached_offsets, const uint64_t* takes,
+                uint32_t num_plans, uint32_t wave, uint64_t* cells) {
+  vk_sampler sampler = nullptr;
+  const int rc = guard([&] {
+    if (!g || !roles || !part_of || !fanouts || !cached_offsets || !cells) raise(VK_ERR_PARAMETER, "null argument");
+    if (K == 0) raise(VK_ERR_PARAMETER, "need at least one partition");
+    if (batch_size == 0) raise(VK_ERR_PARAMETER, "batch size must be >= 1");  // sampling.cpp:50-53
+    const std::uint32_t A = takes ? num_plans : 1u;
+    if (A == 0 || A > kMaxPlans) raise(VK_ERR_PARAMETER, "between 1 and 32 cache plans per call");
+    const std::uint64_t n = g->n;
+    for (std::uint64_t v = 0; v < n; ++v)
+      if (part_of[v] >= K) raise(VK_ERR_FORMAT, "partition label out of range");
+    if (cached_offsets[0] != 0) raise(VK_ERR_SHAPE, "cached_offsets must start at 0");
+    for (std::uint32_t k = 0; k < K; ++k)
+      if (cached_offsets[k + 1] < cached_offsets[k]) raise(VK_ERR_SHAPE, "cached_offsets must be non-decreasing");
+    const std::uint64_t ncached = cached_offsets[K];
+    if (ncached && !cached_ids) raise(VK_ERR_PARAMETER, "null cached_ids");
+    for (std::uint64_t i = 0; i < ncached; ++i)
+      if (cached_ids[i] >= n) raise(VK_ERR_RANGE, "cached vertex id out of range");
+    std::vector<std::uint64_t> tk(A * K);
+    for (std::uint32_t a = 0; a < A; ++a)
+      for (std::uint32_t k = 0; k < K; ++k) {
+        const std::uint64_t len = cached_offsets[k + 1] - cached_offsets[k];
+        tk[a * K + k] = takes ? takes[a * K + k] : len;
+        if (tk[a * K + k] > len) raise(VK_ERR_SHAPE, "plan takes more ids than the cached list holds");
+      }
+    const std::uint32_t M = wave ? wave : 128u;
+    vk_sampler_config cfg{};
+    if (num_hops == 0 || num_hops > VK_MAX_HOPS) raise(VK_ERR_PARAMETER, "1..VK_MAX_HOPS hops");
+    cfg.num_hops = num_hops;
+    for (std::uint32_t h = 0; h < num_hops; ++h) cfg.fanouts[h] = fanouts[h];
+    cfg.batch_size = batch_size;
+    cfg.max_minibatches = M;
+    cfg.global_seed = global_seed;
+    if (int e = vk_sampler_create(g, &cfg, &sampler)) raise(e, vk_last_error());
+
+    DeviceGuard dg(g->device);
+    const std::uint64_t ncell = epochs * K;
+    DevBuf d_part, d_pos, d_takes, d_cells, d_cell_of, d_ids;
+    d_part.alloc(n * 4);
+    VK_CUDA(cudaMemcpy(d_part.p, part_of, n * 4, cudaMemcpyHostToDevice));
+    d_pos.alloc((std::uint64_t)K * n * 4);
+    VK_CUDA(cudaMemset(d_pos.p, 0xff, d_pos.bytes));
+    if (ncached) {
+      d_ids.alloc(ncached * 4);
+      VK_CUDA(cudaMemcpy(d_ids.p, cached_ids, ncached * 4, cudaMemcpyHostToDevice));
+      for (std::uint32_t k = 0; k < K; ++k) {
+        const std::uint64_t c = cached_offsets[k + 1] - cached_offsets[k];
+        if (c)
+          k_fill_positions<<<fill_grid(c, g->device), 256>>>(d_ids.as<std::uint32_t>() + cached_offsets[k], c,
+                                                           d_pos.as<std::uint32_t>() + (std::uint64_t)k * n);
+      }
+      VK_LAUNCH_CHECK();
+    }
+    d_takes.alloc(A * K * 8);
+    VK_CUDA(cudaMemcpy(d_takes.p, tk.data(), A * K * 8, cudaMemcpyHostToDevice));
+    d_cells.alloc(std::max<std::uint64_t>(1, A * ncell * 3 * 8));
+    VK_CUDA(cudaMemset(d_cells.p, 0, d_cells.bytes));
+    d_cell_of.alloc(2 * M * 4);  // double-buffered: the host fills wave i+1 while wave i runs
+    VK_CUDA(cudaDeviceSynchronize());
+
+    // host queue of the wave being assembled
+    std::vector<std::uint32_t> perm(n), seeds;
+    std::vector<std::uint64_t> offs{0};
+    std::vector<vk_batch_ref> refs;
+    std::vector<std::uint32_t> cell_of;
+    PinnedBuf cell_host;
+    cell_host.ensure(2 * M * 4);
+    cudaEvent_t copied[2] = {nullptr, nullptr};
+    struct EvGuard {
+      cudaEvent_t* e;
+      ~EvGuard() {
+        for (int i = 0; i < 2; ++i)
+          if (e[i]) cudaEventDestroy(e[i]);
+      }
+    } evg{copied};
+    for (auto& ev : copied) VK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    int parity = 0;
+    auto flush = [&] {
+      if (refs.empty()) return;
+      const std::uint32_t nmb = (std::uint32_t)refs.size();
+      if (int e = vk_sampler_run(sampler, nmb, refs.data(), seeds.data(), offs.data(), 0, nullptr))
+        raise(e, vk_last_error());
+      const std::uint32_t *all, *count, *parts;
+      std::uint64_t stride;
+      std::uint32_t got;
+      vk_graph_s* gg;
+      cudaStream_t st;
+      sampler_internal(sampler, &all, &stride, &count, &got, &parts, &gg, &st);
+      std::uint32_t* ch = cell_host.as<std::uint32_t>() + parity * M;
+      std::uint32_t* cd = d_cell_of.as<std::uint32_t>() + parity * M;
+      VK_CUDA(cudaEventSynchronize(copied[parity]));  // wave i-2's classify has consumed this buffer
+      std::memcpy(ch, cell_of.data(), nmb * 4);
+      VK_CUDA(cudaMemcpyAsync(cd, ch, nmb * 4, cudaMemcpyHostToDevice, st));
+      const unsigned gx = (unsigned)std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(stride, 256 * 8), 64));
+      k_classify_plans<<<dim3(gx, nmb), 256, 0, st>>>(all, stride, count, cd, d_part.as<std::uint32_t>(),
+                                                      d_pos.as<std::uint32_t>(), n, d_takes.as<std::uint64_t>(), K,
+                                                      A, ncell * 3, d_cells.as<unsigned long long>());
+      count_launch();
+      VK_LAUNCH_CHECK();
+      VK_CUDA(cudaEventRecord(copied[parity], st));
+      parity ^= 1;
+      seeds.clear();
+      offs.assign(1, 0);
+      refs.clear();
+      cell_of.clear();
+    };
+    // train members of every partition in ascending id order (train_members,
+    // graph.cpp:106-111), gathered in one pass instead of one per (e, k)
+    std::vector<std::vector<std::uint32_t>> members(K);
+    for (std::uint64_t v = 0; v < n; ++v)
+      if (roles[v] == 0) members[part_of[v]].push_back((std::uint32_t)v);
+    for (std::uint32_t k = 0; k < K; ++k)
+      if (members[k].empty())  // sampling.cpp:50-53
+        raise(VK_ERR_SAMPLING, "partition " + std::to_string(k) + " has no train vertices");
+    // for_each_expansion order (commsim.cpp:45-52)
+    for (std::uint64_t e = 0; e < epochs; ++e)
+      for (std::uint32_t k = 0; k < K; ++k) {
+        const std::uint64_t T = members[k].size();
+        std::copy(members[k].begin(), members[k].end(), perm.begin());
+        epoch_shuffle(perm.data(), T, k, e, global_seed);
+        for (std::uint64_t i = 0, bi = 0; i < T; i += batch_size, ++bi) {
+          const std::uint64_t c = std::min<std::uint64_t>(batch_size, T - i);
+          seeds.insert(seeds.end(), perm.begin() + i, perm.begin() + i + c);
+          offs.push_back(seeds.size());
+          refs.push_back(vk_batch_ref{e, bi, k, 0});
+          cell_of.push_back((std::uint32_t)(e * K + k));
+          if (refs.size() == M) flush();
+        }
+      }
+    flush();
+    std::vector<unsigned long long> host(A * ncell * 3);
+    VK_CUDA(cudaDeviceSynchronize());  // the classify kernels ran on the sampler's (non-blocking) stream
+    if (!host.empty()) VK_CUDA(cudaMemcpy(host.data(), d_cells.p, host.size() * 8, cudaMemcpyDeviceToHost));
+    for (std::size_t i = 0; i < host.size(); ++i) cells[i] = host[i];
+  });
+  if (sampler) vk_sampler_destroy(sampler);
+  return rc;
+}
+
+}  // extern "C"

@@ -130,6 +130,8 @@ def lib():
     L.vk_plane_gather.argtypes = [c_vp, c_vp, c_vp, c_u64, c_vp, c_vp]
     L.vk_plane_row_bytes.argtypes = [c_vp, C.POINTER(c_u64)]
     L.vk_plane_pulled_rows.argtypes = [c_vp, C.POINTER(c_u64)]
+    L.vk_simulate.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, c_vp, u64p, c_vp,
+                              c_u32, c_u32, u64p]
     L.vk_synth_community_powerlaw.argtypes = [c_u64, c_u64, c_u32, c_double, c_u64, C.c_uint,
                                               C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), u32p]
     L.vk_debug_stream_draws.argtypes = [c_int, c_u64, c_u64, c_u64, u64p]
@@ -511,6 +513,32 @@ def build_cache(rankings: Sequence, alpha: float, n: int) -> CachePlan:
         np.bitwise_or.at(bits[k], (c64 >> np.uint64(6)).astype(np.int64),
                          np.left_shift(np.uint64(1), c64 & np.uint64(63)))
     return CachePlan(K, alpha, cached, bits)
+
+
+def simulate(g: Graph, roles, part_of, K, fanouts, b, epochs, seed, cached, takes=None, wave=0):
+    """vipkit::simulate (commsim.hpp:56-59) on the device -> cells[E, K, 3]
+    = (local_hits, cache_hits, remote_misses) per (epoch, partition).
+
+    `cached` is each partition's cached id list (CachePlan::cached). With
+    `takes` (shape [A, K]) it is read as ranking prefixes and A nested plans
+    are scored from one expansion pass -> cells[A, E, K, 3] (the alpha axis
+    of sweep, commsim.cpp:140-259)."""
+    part_of = _a32(part_of)
+    fan = _a32(fanouts)
+    offs = np.zeros(K + 1, np.uint64)
+    offs[1:] = np.cumsum([len(c) for c in cached])
+    ids = _a32(np.concatenate([np.asarray(c, np.uint32) for c in cached]) if K else [])
+    A = 1
+    tk = None
+    if takes is not None:
+        tk = np.ascontiguousarray(np.asarray(takes, np.uint64).reshape(-1, K))
+        A = tk.shape[0]
+    cells = np.zeros(A * epochs * K * 3, np.uint64)
+    check(lib().vk_simulate(g.handle, np.ascontiguousarray(roles, np.uint8), part_of, K, fan, len(fan), b,
+                            epochs, seed, ids.ctypes.data if ids.size else None, offs,
+                            tk.ctypes.data if tk is not None else None, A, wave, cells))
+    cells = cells.reshape(A, epochs, K, 3)
+    return cells if takes is not None else cells[0]
 
 
 def build_reorder(part_of, K, scores, device=0):

@@ -219,6 +219,77 @@ static void test_vcsr_roundtrip() {  // graph.cpp:553-598 file format
   CHECK_THROWS_AS(load_binary_csr("/tmp/vipkit_b200_bad.vcsr"), format_error);
 }
 
+// test_commsim.cpp:32-105 on a seeded random graph (the reference's PA
+// generator is not part of the mirror): zero/full cache, conservation per
+// cell, nested-alpha monotonicity, and simulate_alphas == per-plan simulate.
+static void test_commsim() {
+  const std::size_t n = 600;
+  std::vector<std::pair<vertex_t, vertex_t>> e;
+  std::uint64_t x = 12345;
+  for (std::size_t i = 0; i < 4 * n; ++i) {
+    x = x * 6364136223846793005ull + 1442695040888963407ull;
+    e.emplace_back(static_cast<vertex_t>((x >> 33) % n), static_cast<vertex_t>((x >> 13) % n));
+  }
+  const Graph g = from_edges(n, e, true);
+  VertexRoles roles;
+  roles.role.assign(n, 1);
+  for (std::size_t v = 0; v < n; v += 3) roles.role[v] = 0;
+  std::vector<std::uint32_t> labels(n);
+  for (std::size_t v = 0; v < n; ++v) labels[v] = static_cast<std::uint32_t>(v % 4);
+  const auto part = PartitionMap::from_labels(labels, 4);
+  const FanoutSpec fan{{4, 3}};
+  const SeedSpec seeds{77};
+  const CommReport r0 = simulate(g, roles, part, fan, 16, 3, seeds, CachePlan::empty(4, n));
+  CHECK(r0.total_cache_hits() == 0);
+  CHECK(r0.total_misses() > 0);
+  std::vector<Ranking> rk;
+  std::vector<double> sc(n);
+  for (std::size_t v = 0; v < n; ++v) sc[v] = static_cast<double>((v * 7919) % 101);
+  for (std::uint32_t k = 0; k < 4; ++k) rk.push_back(rank_by_scores(part, k, sc));
+  const CommReport rf = simulate(g, roles, part, fan, 16, 3, seeds, build_cache(rk, 3.0, n));
+  CHECK(rf.total_misses() == 0);
+  CHECK(rf.total_local_hits() == r0.total_local_hits());
+  CHECK(rf.total_cache_hits() == r0.total_misses());
+  // conservation: every cell partitions the expanded neighbourhoods
+  const CommReport r = simulate(g, roles, part, fan, 16, 3, seeds, build_cache(rk, 0.1, n));
+  for (std::uint64_t ep = 0; ep < 3; ++ep)
+    for (std::uint32_t k = 0; k < 4; ++k) {
+      const auto batches = epoch_minibatches(roles, part, k, 16, ep, seeds);
+      std::uint64_t total = 0;
+      for (std::size_t i = 0; i < batches.size(); ++i)
+        total += expand(g, batches[i], fan, seeds, BatchRef{ep, k, i}).all_vertices.size();
+      const auto& c = r.at(ep, k);
+      CHECK(c.local_hits + c.cache_hits + c.remote_misses == total);
+    }
+  const std::vector<double> alphas{0.0, 0.05, 0.1, 0.2, 0.5, 1.0};
+  const auto sweep = simulate_alphas(g, roles, part, fan, 16, 3, seeds, rk, alphas);
+  std::uint64_t prev = ~0ull;
+  for (std::size_t i = 0; i < alphas.size(); ++i) {
+    const CommReport one = simulate(g, roles, part, fan, 16, 3, seeds, build_cache(rk, alphas[i], n));
+    for (std::size_t c = 0; c < one.cells.size(); ++c) {
+      CHECK(one.cells[c].local_hits == sweep[i].cells[c].local_hits);
+      CHECK(one.cells[c].cache_hits == sweep[i].cells[c].cache_hits);
+      CHECK(one.cells[c].remote_misses == sweep[i].cells[c].remote_misses);
+    }
+    CHECK(sweep[i].total_misses() <= prev);
+    prev = sweep[i].total_misses();
+  }
+  CHECK_THROWS_AS(simulate(g, roles, part, fan, 16, 1, seeds, CachePlan::empty(2, n)), config_error);
+}
+
+// test_commsim.cpp:50-72: partitions {0,1} | {2,3} of a 4-path, all train,
+// b = 1, fanout (1): exactly 1 expected miss per epoch (variance 1/2).
+static void test_commsim_four_path_law() {
+  const Graph g = path(4);
+  VertexRoles roles;
+  roles.role.assign(4, 0);
+  const auto part = PartitionMap::from_labels({0, 0, 1, 1}, 2);
+  const std::uint64_t E = 10000;
+  const CommReport r = simulate(g, roles, part, FanoutSpec{{1}}, 1, E, SeedSpec{123}, CachePlan::empty(2, 4));
+  const double mean = static_cast<double>(r.total_misses()) / static_cast<double>(E);
+  CHECK(std::fabs(mean - 1.0) < 3 * std::sqrt(0.5 / static_cast<double>(E)));
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"initial probabilities", test_initial_probabilities},
@@ -229,6 +300,8 @@ int main() {
       {"expansion invariants + MFG", test_expansion_invariants},
       {"ranking ties, capacity, full cache", test_ranking_and_cache},
       {"VCSR load round trip", test_vcsr_roundtrip},
+      {"simulate: zero/full cache, conservation, alpha sweep", test_commsim},
+      {"simulate: 4-path exact expectation", test_commsim_four_path_law},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

@@ -1,0 +1,70 @@
+"""GPU: vipkit::simulate / the alpha axis of sweep through
+vk_simulate vs the reference's own tallies: the golden CommReport cells of the
+reference's SmallSetup (written by the real reference, oracle/make_golden.py)
+and, at C2 size, the live compiled reference (oracle/_ref). Exact counts."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_small_setup_cells_vs_golden(vk, port, golden):
+    pol = golden("policy.npz")
+    csr = port.generate("pa", 400, 4, 15)
+    roles = port.make_roles(400, 0.25, 0, 0, 6)
+    np.testing.assert_array_equal(roles, pol["roles"])
+    labels = pol["labels"]
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    orders = [pol[f"order_{k}"] for k in range(4)]
+    alphas = (0.0, 0.1, 0.15, 3.0)
+    plans = [vk.build_cache(orders, a, 400) for a in alphas]
+    for a, plan in zip(alphas, plans):
+        np.testing.assert_array_equal(plan.member_bits, pol["bits_" + str(a).replace(".", "p")])
+    # one plan at a time (CachePlan semantics) ...
+    for a, plan in zip(alphas, plans):
+        cells = vk.simulate(g, roles, labels, 4, [4, 3], 16, 3, 77, plan.cached)
+        np.testing.assert_array_equal(cells, pol["cells_" + str(a).replace(".", "p")])
+    # ... and all four from one expansion pass (nested ranking prefixes)
+    takes = [[len(p.cached[k]) for k in range(4)] for p in plans]
+    multi = vk.simulate(g, roles, labels, 4, [4, 3], 16, 3, 77, plans[-1].cached, takes=takes, wave=5)
+    for i, a in enumerate(alphas):
+        np.testing.assert_array_equal(multi[i], pol["cells_" + str(a).replace(".", "p")])
+
+
+def test_c2_alpha_sweep_vs_reference(vk, port, ref):
+    """C2-shaped (169,343 vertices, PA d=7, 2 partitions): one epoch, VIP
+    rankings, alpha in {0, 0.1, 0.2} against the reference's simulate."""
+    n, K, b, fan, seed = 169_343, 2, 1024, [15, 10, 5], 42
+    csr = port.generate("pa", n, 7, 7)
+    roles = port.make_roles(n, 0.537, 0, 0, 3)
+    labels = ((np.arange(n, dtype=np.uint64) * 2654435761) % K).astype(np.uint32)
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    p0 = np.stack([vk.initial_probs(roles, labels, k, b) for k in range(K)])
+    totals = np.stack([s.total for s in vk.propagate(g, fan, p0, with_hops=False)])
+    orders = [vk.rank_by_scores(labels, k, totals[k])[0] for k in range(K)]
+    alphas = (0.0, 0.1, 0.2)
+    plans = [vk.build_cache(orders, a, n) for a in alphas]
+    takes = [[len(p.cached[k]) for k in range(K)] for p in plans]
+    got = vk.simulate(g, roles, labels, K, fan, b, 1, seed, plans[-1].cached, takes=takes)
+    for i, plan in enumerate(plans):
+        exp = ref.simulate(csr, roles, labels, K, fan, b, 1, seed, plan.cached)
+        np.testing.assert_array_equal(got[i], exp)
+    misses = [int(got[i][..., 2].sum()) for i in range(len(alphas))]
+    assert misses[0] > misses[1] > misses[2]  # the VIP cache cuts remote misses
+
+
+def test_simulate_errors(vk, port):
+    csr = port.generate("pa", 300, 3, 1)
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    roles = port.make_roles(300, 0.3, 0, 0, 2)
+    labels = np.zeros(300, np.uint32)
+    labels[:5] = 1
+    roles_no_train_in_1 = roles.copy()
+    roles_no_train_in_1[:5] = 1
+    empty = [np.zeros(0, np.uint32)] * 2
+    with pytest.raises(vk.SamplingError):
+        vk.simulate(g, roles_no_train_in_1, labels, 2, [3], 8, 1, 1, empty)
+    with pytest.raises(vk.ParameterError):
+        vk.simulate(g, roles, labels, 2, [3], 0, 1, 1, empty)
+    with pytest.raises(vk.FormatError):
+        vk.simulate(g, roles, labels, 1, [3], 8, 1, 1, empty[:1])
