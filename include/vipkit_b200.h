@@ -272,6 +272,14 @@ VK_API int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of
                        const uint32_t* fanouts, uint32_t num_hops, uint64_t batch_size, uint64_t epochs,
                        uint64_t global_seed, const uint32_t* cached_ids, const uint64_t* cached_offsets,
                        const uint64_t* takes, uint32_t num_plans, uint32_t wave, uint64_t* cells);
+/* vipkit::empirical_vip (vip.hpp:52-55, vip.cpp:85-105), the "sim." policy's
+ * estimate: S epochs of partition k's minibatches under
+ * SeedSpec::derived(0xC1) through the device sampler; freq[v] = (number of
+ * minibatches whose all_vertices contain v) / (number of minibatches).
+ * Bit-identical to the reference. VK_ERR_PARAMETER for S = 0. */
+VK_API int vk_empirical_vip(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, uint32_t k,
+                            uint64_t batch_size, const uint32_t* fanouts, uint32_t num_hops, uint64_t epochs,
+                            uint64_t global_seed, double* freq);
 
 /* ------------------------------------------------------- synthetic data
  * Community-structured power-law generator for the BASELINE configs (builder

@@ -435,6 +435,19 @@ inline CachePlan build_cache(const std::vector<Ranking>& rankings, double alpha,
   return plan;
 }
 
+/// empirical_vip (vip.hpp:52-55): the simulated inclusion frequency of every
+/// vertex over S epochs of partition k's minibatches (device sampler).
+inline std::vector<double> empirical_vip(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
+                                         std::uint32_t k, std::uint64_t b, const FanoutSpec& fanouts,
+                                         std::uint64_t S, const SeedSpec& seeds) {
+  fanouts.validate();
+  std::vector<double> freq(g.num_vertices());
+  detail::check(vk_empirical_vip(g.handle(), roles.role.data(), part.part_of.data(), part.K, k, b,
+                                 fanouts.fanouts.data(), static_cast<std::uint32_t>(fanouts.hops()), S,
+                                 seeds.global_seed, freq.data()));
+  return freq;
+}
+
 // ---- commsim.hpp:14-59 -----------------------------------------
 /// Per-(epoch, partition) tallies of distinct neighbourhood vertices.
 struct CommReport {

@@ -113,6 +113,93 @@ __global__ void __launch_bounds__(256) k_classify_plans(const std::uint32_t* __r
   }
 }
 
+// empirical_vip's histogram: one count per distinct neighbourhood vertex of
+// every minibatch of the wave.
+__global__ void __launch_bounds__(256) k_histogram(const std::uint32_t* __restrict__ all, std::uint64_t stride,
+                                                   const std::uint32_t* __restrict__ count,
+                                                   unsigned* __restrict__ hits) {
+  const std::uint32_t mb = blockIdx.y;
+  const std::uint32_t c = count[mb];
+  const std::uint32_t* av = all + mb * stride;
+  for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < c; r += gridDim.x * blockDim.x)
+    atomicAdd(hits + __ldg(av + r), 1u);
+}
+
+// for_each_expansion (commsim.cpp:38-52) over the device sampler: the
+// minibatches of epochs x `parts` in the reference's order (epoch-major, then
+// partition, then batch index) go through the sampler in waves of M; after
+// each wave on_wave(all, stride, count, nmb, cells_of_wave, stream) launches
+// the consumer on the sampler's stream. cells_of_wave[i] = e * K + k of
+// minibatch i (host array, valid during the call). Returns the minibatch count.
+template <class OnWave>
+std::uint64_t stream_expansions(vk_graph g, const std::uint8_t* roles, const std::uint32_t* part_of,
+                                std::uint32_t K, const std::vector<std::uint32_t>& parts,
+                                const std::uint32_t* fanouts, std::uint32_t num_hops, std::uint64_t batch_size,
+                                std::uint64_t epochs, std::uint64_t seed, std::uint32_t M, OnWave&& on_wave) {
+  if (num_hops == 0 || num_hops > VK_MAX_HOPS) raise(VK_ERR_PARAMETER, "1..VK_MAX_HOPS hops");
+  vk_sampler_config cfg{};
+  cfg.num_hops = num_hops;
+  for (std::uint32_t h = 0; h < num_hops; ++h) cfg.fanouts[h] = fanouts[h];
+  cfg.batch_size = batch_size;
+  cfg.max_minibatches = M;
+  cfg.global_seed = seed;
+  vk_sampler sampler = nullptr;
+  if (int e = vk_sampler_create(g, &cfg, &sampler)) raise(e, vk_last_error());
+  struct SamplerGuard {
+    vk_sampler s;
+    ~SamplerGuard() { vk_sampler_destroy(s); }
+  } sg{sampler};
+  const std::uint64_t n = g->n;
+  // train members of the partitions in ascending id order (train_members,
+  // graph.cpp:106-111), gathered in one pass instead of one per (e, k)
+  std::vector<int> want(K, 0);
+  for (std::uint32_t k : parts) want[k] = 1;
+  std::vector<std::vector<std::uint32_t>> members(K);
+  for (std::uint64_t v = 0; v < n; ++v)
+    if (roles[v] == 0 && want[part_of[v]]) members[part_of[v]].push_back((std::uint32_t)v);
+  std::vector<std::uint32_t> perm, seeds, cell_of;
+  std::vector<std::uint64_t> offs{0};
+  std::vector<vk_batch_ref> refs;
+  std::uint64_t total = 0;
+  auto flush = [&] {
+    if (refs.empty()) return;
+    const std::uint32_t nmb = (std::uint32_t)refs.size();
+    if (int e = vk_sampler_run(sampler, nmb, refs.data(), seeds.data(), offs.data(), 0, nullptr))
+      raise(e, vk_last_error());
+    const std::uint32_t *all, *count, *pt;
+    std::uint64_t stride;
+    std::uint32_t got;
+    vk_graph_s* gg;
+    cudaStream_t st;
+    sampler_internal(sampler, &all, &stride, &count, &got, &pt, &gg, &st);
+    on_wave(all, stride, count, nmb, cell_of.data(), st);
+    total += nmb;
+    seeds.clear();
+    offs.assign(1, 0);
+    refs.clear();
+    cell_of.clear();
+  };
+  for (std::uint64_t e = 0; e < epochs; ++e)
+    for (std::uint32_t k : parts) {
+      if (members[k].empty())  // sampling.cpp:50-53
+        raise(VK_ERR_SAMPLING, "partition " + std::to_string(k) + " has no train vertices");
+      const std::uint64_t T = members[k].size();
+      perm.assign(members[k].begin(), members[k].end());
+      epoch_shuffle(perm.data(), T, k, e, seed);  // epoch_minibatches (sampling.cpp:45-70)
+      for (std::uint64_t i = 0, bi = 0; i < T; i += batch_size, ++bi) {
+        const std::uint64_t c = std::min<std::uint64_t>(batch_size, T - i);
+        seeds.insert(seeds.end(), perm.begin() + i, perm.begin() + i + c);
+        offs.push_back(seeds.size());
+        refs.push_back(vk_batch_ref{e, bi, k, 0});
+        cell_of.push_back((std::uint32_t)(e * K + k));
+        if (refs.size() == M) flush();
+      }
+    }
+  flush();
+  VK_CUDA(cudaDeviceSynchronize());  // consumers ran on the sampler's (non-blocking) stream
+  return total;
+}
+
 }  // namespace
 }  // namespace vk
 
@@ -124,8 +211,7 @@ int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint3
                 uint32_t num_hops, uint64_t batch_size, uint64_t epochs, uint64_t global_seed,
                 const uint32_t* cached_ids, const uint64_t* cached_offsets, const uint64_t* takes,
                 uint32_t num_plans, uint32_t wave, uint64_t* cells) {
-  vk_sampler sampler = nullptr;
-  const int rc = guard([&] {
+  return guard([&] {
     if (!g || !roles || !part_of || !fanouts || !cached_offsets || !cells) raise(VK_ERR_PARAMETER, "null argument");
     if (K == 0) raise(VK_ERR_PARAMETER, "need at least one partition");
     if (batch_size == 0) raise(VK_ERR_PARAMETER, "batch size must be >= 1");  // sampling.cpp:50-53
@@ -149,15 +235,6 @@ int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint3
         if (tk[a * K + k] > len) raise(VK_ERR_SHAPE, "plan takes more ids than the cached list holds");
       }
     const std::uint32_t M = wave ? wave : 128u;
-    vk_sampler_config cfg{};
-    if (num_hops == 0 || num_hops > VK_MAX_HOPS) raise(VK_ERR_PARAMETER, "1..VK_MAX_HOPS hops");
-    cfg.num_hops = num_hops;
-    for (std::uint32_t h = 0; h < num_hops; ++h) cfg.fanouts[h] = fanouts[h];
-    cfg.batch_size = batch_size;
-    cfg.max_minibatches = M;
-    cfg.global_seed = global_seed;
-    if (int e = vk_sampler_create(g, &cfg, &sampler)) raise(e, vk_last_error());
-
     DeviceGuard dg(g->device);
     const std::uint64_t ncell = epochs * K;
     DevBuf d_part, d_pos, d_takes, d_cells, d_cell_of, d_ids;
@@ -182,12 +259,6 @@ int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint3
     VK_CUDA(cudaMemset(d_cells.p, 0, d_cells.bytes));
     d_cell_of.alloc(2 * M * 4);  // double-buffered: the host fills wave i+1 while wave i runs
     VK_CUDA(cudaDeviceSynchronize());
-
-    // host queue of the wave being assembled
-    std::vector<std::uint32_t> perm(n), seeds;
-    std::vector<std::uint64_t> offs{0};
-    std::vector<vk_batch_ref> refs;
-    std::vector<std::uint32_t> cell_of;
     PinnedBuf cell_host;
     cell_host.ensure(2 * M * 4);
     cudaEvent_t copied[2] = {nullptr, nullptr};
@@ -200,66 +271,67 @@ int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint3
     } evg{copied};
     for (auto& ev : copied) VK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     int parity = 0;
-    auto flush = [&] {
-      if (refs.empty()) return;
-      const std::uint32_t nmb = (std::uint32_t)refs.size();
-      if (int e = vk_sampler_run(sampler, nmb, refs.data(), seeds.data(), offs.data(), 0, nullptr))
-        raise(e, vk_last_error());
-      const std::uint32_t *all, *count, *parts;
-      std::uint64_t stride;
-      std::uint32_t got;
-      vk_graph_s* gg;
-      cudaStream_t st;
-      sampler_internal(sampler, &all, &stride, &count, &got, &parts, &gg, &st);
-      std::uint32_t* ch = cell_host.as<std::uint32_t>() + parity * M;
-      std::uint32_t* cd = d_cell_of.as<std::uint32_t>() + parity * M;
-      VK_CUDA(cudaEventSynchronize(copied[parity]));  // wave i-2's classify has consumed this buffer
-      std::memcpy(ch, cell_of.data(), nmb * 4);
-      VK_CUDA(cudaMemcpyAsync(cd, ch, nmb * 4, cudaMemcpyHostToDevice, st));
-      const unsigned gx = (unsigned)std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(stride, 256 * 8), 64));
-      k_classify_plans<<<dim3(gx, nmb), 256, 0, st>>>(all, stride, count, cd, d_part.as<std::uint32_t>(),
-                                                      d_pos.as<std::uint32_t>(), n, d_takes.as<std::uint64_t>(), K,
-                                                      A, ncell * 3, d_cells.as<unsigned long long>());
-      count_launch();
-      VK_LAUNCH_CHECK();
-      VK_CUDA(cudaEventRecord(copied[parity], st));
-      parity ^= 1;
-      seeds.clear();
-      offs.assign(1, 0);
-      refs.clear();
-      cell_of.clear();
-    };
-    // train members of every partition in ascending id order (train_members,
-    // graph.cpp:106-111), gathered in one pass instead of one per (e, k)
-    std::vector<std::vector<std::uint32_t>> members(K);
-    for (std::uint64_t v = 0; v < n; ++v)
-      if (roles[v] == 0) members[part_of[v]].push_back((std::uint32_t)v);
-    for (std::uint32_t k = 0; k < K; ++k)
-      if (members[k].empty())  // sampling.cpp:50-53
-        raise(VK_ERR_SAMPLING, "partition " + std::to_string(k) + " has no train vertices");
-    // for_each_expansion order (commsim.cpp:45-52)
-    for (std::uint64_t e = 0; e < epochs; ++e)
-      for (std::uint32_t k = 0; k < K; ++k) {
-        const std::uint64_t T = members[k].size();
-        std::copy(members[k].begin(), members[k].end(), perm.begin());
-        epoch_shuffle(perm.data(), T, k, e, global_seed);
-        for (std::uint64_t i = 0, bi = 0; i < T; i += batch_size, ++bi) {
-          const std::uint64_t c = std::min<std::uint64_t>(batch_size, T - i);
-          seeds.insert(seeds.end(), perm.begin() + i, perm.begin() + i + c);
-          offs.push_back(seeds.size());
-          refs.push_back(vk_batch_ref{e, bi, k, 0});
-          cell_of.push_back((std::uint32_t)(e * K + k));
-          if (refs.size() == M) flush();
-        }
-      }
-    flush();
+    std::vector<std::uint32_t> parts(K);
+    for (std::uint32_t k = 0; k < K; ++k) parts[k] = k;
+    stream_expansions(g, roles, part_of, K, parts, fanouts, num_hops, batch_size, epochs, global_seed, M,
+                      [&](const std::uint32_t* all, std::uint64_t stride, const std::uint32_t* count,
+                          std::uint32_t nmb, const std::uint32_t* cell_of, cudaStream_t st) {
+                        std::uint32_t* ch = cell_host.as<std::uint32_t>() + parity * M;
+                        std::uint32_t* cd = d_cell_of.as<std::uint32_t>() + parity * M;
+                        VK_CUDA(cudaEventSynchronize(copied[parity]));  // wave i-2 consumed this buffer
+                        std::memcpy(ch, cell_of, nmb * 4);
+                        VK_CUDA(cudaMemcpyAsync(cd, ch, nmb * 4, cudaMemcpyHostToDevice, st));
+                        const unsigned gx = (unsigned)std::max<std::uint64_t>(
+                            1, std::min<std::uint64_t>(ceil_div(stride, 256 * 8), 64));
+                        k_classify_plans<<<dim3(gx, nmb), 256, 0, st>>>(
+                            all, stride, count, cd, d_part.as<std::uint32_t>(), d_pos.as<std::uint32_t>(), n,
+                            d_takes.as<std::uint64_t>(), K, A, ncell * 3, d_cells.as<unsigned long long>());
+                        count_launch();
+                        VK_LAUNCH_CHECK();
+                        VK_CUDA(cudaEventRecord(copied[parity], st));
+                        parity ^= 1;
+                      });
     std::vector<unsigned long long> host(A * ncell * 3);
-    VK_CUDA(cudaDeviceSynchronize());  // the classify kernels ran on the sampler's (non-blocking) stream
     if (!host.empty()) VK_CUDA(cudaMemcpy(host.data(), d_cells.p, host.size() * 8, cudaMemcpyDeviceToHost));
     for (std::size_t i = 0; i < host.size(); ++i) cells[i] = host[i];
   });
-  if (sampler) vk_sampler_destroy(sampler);
-  return rc;
+}
+
+// empirical_vip (vip.cpp:85-105): for S epochs, every minibatch of
+// partition k under the derived seed (0xC1, rng.hpp:54), a histogram of
+// all_vertices; freq[v] = hits[v] / batches.
+int vk_empirical_vip(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, uint32_t k,
+                     uint64_t batch_size, const uint32_t* fanouts, uint32_t num_hops, uint64_t epochs,
+                     uint64_t global_seed, double* freq) {
+  return guard([&] {
+    if (!g || !roles || !part_of || !fanouts || !freq) raise(VK_ERR_PARAMETER, "null argument");
+    if (epochs < 1) raise(VK_ERR_PARAMETER, "epoch count must be >= 1");  // vip.cpp:89
+    if (batch_size == 0) raise(VK_ERR_PARAMETER, "batch size must be >= 1");
+    if (K == 0 || k >= K) raise(VK_ERR_PARAMETER, "partition index out of range");
+    const std::uint64_t n = g->n;
+    for (std::uint64_t v = 0; v < n; ++v)
+      if (part_of[v] >= K) raise(VK_ERR_FORMAT, "partition label out of range");
+    for (std::uint32_t h = 0; h < num_hops; ++h)
+      if (fanouts[h] < 1) raise(VK_ERR_PARAMETER, "each fanout must be >= 1");
+    DeviceGuard dg(g->device);
+    const std::uint64_t seed = mix64(global_seed ^ mix64(tag::empirical_vip));  // SeedSpec::derived
+    DevBuf hits;
+    hits.alloc(std::max<std::uint64_t>(1, n * 4));
+    VK_CUDA(cudaMemset(hits.p, 0, hits.bytes));
+    VK_CUDA(cudaDeviceSynchronize());
+    const std::uint64_t batches = stream_expansions(
+        g, roles, part_of, K, {k}, fanouts, num_hops, batch_size, epochs, seed, 128u,
+        [&](const std::uint32_t* all, std::uint64_t stride, const std::uint32_t* count, std::uint32_t nmb,
+            const std::uint32_t*, cudaStream_t st) {
+          const unsigned gx = (unsigned)std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(stride, 256 * 8), 64));
+          k_histogram<<<dim3(gx, nmb), 256, 0, st>>>(all, stride, count, hits.as<unsigned>());
+          count_launch();
+          VK_LAUNCH_CHECK();
+        });
+    std::vector<unsigned> h(n);
+    if (n) VK_CUDA(cudaMemcpy(h.data(), hits.p, n * 4, cudaMemcpyDeviceToHost));
+    for (std::uint64_t v = 0; v < n; ++v) freq[v] = static_cast<double>(h[v]) / static_cast<double>(batches);
+  });
 }
 
 }  // extern "C"

@@ -290,6 +290,36 @@ static void test_commsim_four_path_law() {
   CHECK(std::fabs(mean - 1.0) < 3 * std::sqrt(0.5 / static_cast<double>(E)));
 }
 
+// test_vip.cpp:147-182: saturating fanouts reach exactly the 2-hop ball; the
+// 3-path law (freq[2] = 1/2 within 3 sigma); determinism; additivity in S.
+static void test_empirical_vip() {
+  {
+    const Graph g = from_edges(7, {{0, 1}, {1, 2}, {2, 3}, {5, 6}}, true);
+    VertexRoles roles;
+    roles.role.assign(7, 1);
+    roles.role[0] = 0;
+    const auto part = single_partition(7);
+    const auto freq = empirical_vip(g, roles, part, 0, 1, FanoutSpec{{100, 100}}, 3, SeedSpec{5});
+    CHECK(freq[0] == 1.0 && freq[1] == 1.0 && freq[2] == 1.0);
+    CHECK(freq[3] == 0.0 && freq[5] == 0.0);
+  }
+  const Graph g = path(3);
+  VertexRoles roles;
+  roles.role.assign(3, 1);
+  roles.role[0] = 0;
+  const auto part = single_partition(3);
+  const FanoutSpec f{{1, 1}};
+  const std::uint64_t S = 20000;
+  const auto freq = empirical_vip(g, roles, part, 0, 1, f, S, SeedSpec{31});
+  CHECK(freq[0] == 1.0 && freq[1] == 1.0);
+  CHECK(std::fabs(freq[2] - 0.5) < 3 * std::sqrt(0.25 / static_cast<double>(S)));
+  CHECK(empirical_vip(g, roles, part, 0, 1, f, S, SeedSpec{31}) == freq);
+  const auto freq2 = empirical_vip(g, roles, part, 0, 1, f, 2 * S, SeedSpec{31});
+  const double c1 = freq[2] * static_cast<double>(S), c2 = freq2[2] * static_cast<double>(2 * S);
+  CHECK(c2 >= c1 - 1e-6 && c2 - c1 <= static_cast<double>(S) + 1e-6);
+  CHECK_THROWS_AS(empirical_vip(g, roles, part, 0, 1, f, 0, SeedSpec{31}), parameter_error);
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"initial probabilities", test_initial_probabilities},
@@ -302,6 +332,7 @@ int main() {
       {"VCSR load round trip", test_vcsr_roundtrip},
       {"simulate: zero/full cache, conservation, alpha sweep", test_commsim},
       {"simulate: 4-path exact expectation", test_commsim_four_path_law},
+      {"empirical VIP: saturating ball, 3-path law, determinism", test_empirical_vip},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

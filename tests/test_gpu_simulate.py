@@ -68,3 +68,17 @@ def test_simulate_errors(vk, port):
         vk.simulate(g, roles, labels, 2, [3], 0, 1, 1, empty)
     with pytest.raises(vk.FormatError):
         vk.simulate(g, roles, labels, 1, [3], 8, 1, 1, empty[:1])
+
+
+@pytest.mark.parametrize("K,k,b,fan,S", [(1, 0, 64, [10, 5], 3), (4, 2, 32, [15, 10, 5], 2)])
+def test_empirical_vip_vs_reference(vk, port, ref, K, k, b, fan, S):
+    """vipkit::empirical_vip (vip.cpp:85-105): frequencies bit-identical to
+    the live reference (same derived streams, same double division)."""
+    csr = port.generate("pa", 20000, 6, 13)
+    roles = port.make_roles(csr.n, 0.1, 0, 0, 4)
+    labels = (np.arange(csr.n) % K).astype(np.uint32)
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    got = vk.empirical_vip(g, roles, labels, K, k, b, fan, S, 42)
+    exp = ref.empirical_vip(csr, roles, labels, K, k, b, fan, S, 42)
+    np.testing.assert_array_equal(got, exp)
+    assert got.max() == 1.0 and 0.0 < got.mean() < 1.0
