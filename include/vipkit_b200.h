@@ -96,6 +96,13 @@ VK_API int vk_graph_load_vcsr(int device, const char* path, uint32_t flags, vk_g
 VK_API int vk_graph_destroy(vk_graph g);
 VK_API int vk_graph_info(vk_graph g, uint64_t* n, uint64_t* m, int* symmetric, int* device);
 VK_API int vk_graph_copy_forward(vk_graph g, uint64_t* fwd_offsets, uint32_t* fwd_targets);
+/* vipkit::apply_reorder's graph part (reorder.hpp:34-35, reorder.cpp:36-70):
+ * a new device graph whose vertex u is old vertex old_of_new[u] (n entries,
+ * host), every neighbour list relabelled through the inverse map and sorted
+ * ascending, reverse CSR rebuilt. Roles and labels permute on the host
+ * (role'[u] = role[old_of_new[u]]). VK_ERR_SHAPE if the map is not a
+ * permutation. */
+VK_API int vk_graph_apply_reorder(vk_graph g, const uint32_t* old_of_new, vk_graph* out);
 VK_API int vk_graph_copy_reverse(vk_graph g, uint64_t* rev_offsets, uint32_t* rev_targets);
 
 /* ------------------------------------------------------------------- VIP
@@ -143,6 +150,15 @@ typedef struct vk_sampler_config {
 
 VK_API int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out);
 VK_API int vk_sampler_destroy(vk_sampler s);
+/* seed_keys replay (sampling.hpp:43-64, `seed_keys` of expand /
+ * sample_neighbors): vertex v's stream is keyed by seed_keys[v] instead of v
+ * and a partial Fisher-Yates draws from v's neighbours ordered by their keys
+ * (sampling.cpp:83-85, 108-112), so expansions of a relabelled graph replay
+ * the original graph's (with seed_keys = old_of_new). seed_keys: n entries,
+ * distinct within every neighbour list (a relabelling); NULL turns replay off.
+ * Batches given to vk_sampler_run are taken as is (order them with
+ * vk_epoch_minibatches' seed_keys). */
+VK_API int vk_sampler_set_seed_keys(vk_sampler s, const uint32_t* seed_keys);
 /* vipkit::expand (sampling.hpp:62-64, sampling.cpp:94-128) for a wave of
  * `nmb` minibatches: per hop h, every vertex of F_{h-1} draws with stream
  * (0xB2, epoch, partition, batch_index, h, v) -> bit-identical frontiers
@@ -264,13 +280,16 @@ VK_API int vk_plane_pulled_rows(vk_plane p, uint64_t* rows);
  * Cache plans: partition k's cached ids are cached_ids[cached_offsets[k] ..
  * cached_offsets[k+1]) in ranking order; plan a caches the first
  * takes[a*K + k] of them (build_cache's ranking prefixes), takes == NULL
- * means one plan caching every listed id. cells[num_plans][epochs][K][3] =
+ * means one plan caching every listed id. seed_keys (n entries or NULL) is
+ * SimulateOptions::seed_keys: replay streams keyed by e.g. original ids
+ * (vk_sampler_set_seed_keys). cells[num_plans][epochs][K][3] =
  * {local_hits, cache_hits, remote_misses} (CommReport::Cell). Errors as the
  * reference: VK_ERR_SAMPLING for a partition without train vertices,
  * VK_ERR_PARAMETER for batch_size 0. */
 VK_API int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K,
                        const uint32_t* fanouts, uint32_t num_hops, uint64_t batch_size, uint64_t epochs,
-                       uint64_t global_seed, const uint32_t* cached_ids, const uint64_t* cached_offsets,
+                       uint64_t global_seed, const uint32_t* seed_keys, const uint32_t* cached_ids,
+                       const uint64_t* cached_offsets,
                        const uint64_t* takes, uint32_t num_plans, uint32_t wave, uint64_t* cells);
 /* vipkit::empirical_vip (vip.hpp:52-55, vip.cpp:85-105), the "sim." policy's
  * estimate: S epochs of partition k's minibatches under

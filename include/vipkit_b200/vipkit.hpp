@@ -304,6 +304,10 @@ class Sampler {
     return nb;
   }
   vk_sampler handle() const { return s_.get(); }
+  /// seed_keys replay for the following runs (nullptr: off).
+  void set_seed_keys(const std::vector<vertex_t>* seed_keys) {
+    detail::check(vk_sampler_set_seed_keys(s_.get(), seed_keys ? seed_keys->data() : nullptr));
+  }
 
  private:
   std::shared_ptr<vk_sampler_s> s_;
@@ -314,9 +318,10 @@ class Sampler {
 inline ExpandedNeighborhood expand(const Graph& g, std::span<const vertex_t> batch, const FanoutSpec& fanouts,
                                    const SeedSpec& seeds, const BatchRef& ref,
                                    const std::vector<vertex_t>* seed_keys = nullptr) {
-  if (seed_keys) throw device_error("seed_keys replay is not supported on the device path");
   if (batch.empty()) throw sampling_error("cannot expand an empty batch");  // sampling.cpp:97
+  if (seed_keys && seed_keys->size() != g.num_vertices()) throw shape_error("seed_keys length does not match vertex count");
   Sampler s(g, fanouts, batch.size(), 1, seeds);
+  if (seed_keys) s.set_seed_keys(seed_keys);
   s.run({batch}, {ref});
   return s.result(0);
 }
@@ -490,13 +495,14 @@ inline std::vector<CommReport> simulate_plans(const Graph& g, const VertexRoles&
                                               const SeedSpec& seeds, const std::vector<vertex_t>& ids,
                                               const std::vector<std::uint64_t>& offsets,
                                               const std::vector<std::uint64_t>* takes,
-                                              const std::vector<double>& alphas) {
+                                              const std::vector<double>& alphas,
+                                              const std::vector<vertex_t>* seed_keys) {
   fanouts.validate();
   const std::uint32_t A = static_cast<std::uint32_t>(alphas.size());
   std::vector<std::uint64_t> cells(static_cast<std::size_t>(A) * E * part.K * 3);
   check(vk_simulate(g.handle(), roles.role.data(), part.part_of.data(), part.K, fanouts.fanouts.data(),
                     static_cast<std::uint32_t>(fanouts.hops()), b, E, seeds.global_seed,
-                    ids.empty() ? nullptr : ids.data(), offsets.data(), takes ? takes->data() : nullptr, A, 0,
+                    seed_keys ? seed_keys->data() : nullptr, ids.empty() ? nullptr : ids.data(), offsets.data(), takes ? takes->data() : nullptr, A, 0,
                     cells.data()));
   std::vector<CommReport> out(A);
   for (std::uint32_t a = 0; a < A; ++a) {
@@ -519,7 +525,7 @@ inline std::vector<CommReport> simulate_plans(const Graph& g, const VertexRoles&
 /// partition for E epochs, classified against the plan.
 inline CommReport simulate(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
                            const FanoutSpec& fanouts, std::uint64_t b, std::uint64_t E, const SeedSpec& seeds,
-                           const CachePlan& plan) {
+                           const CachePlan& plan, const std::vector<vertex_t>* seed_keys = nullptr) {
   if (plan.K != part.K) throw config_error("cache plan partition count differs from partition map");
   std::vector<vertex_t> ids;
   std::vector<std::uint64_t> offs{0};
@@ -527,7 +533,8 @@ inline CommReport simulate(const Graph& g, const VertexRoles& roles, const Parti
     ids.insert(ids.end(), c.begin(), c.end());
     offs.push_back(ids.size());
   }
-  return detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, nullptr, {plan.alpha})[0];
+  return detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, nullptr, {plan.alpha},
+                                seed_keys)[0];
 }
 
 /// The alpha axis of sweep (commsim.cpp:140-259) for one ranking policy:
@@ -557,7 +564,7 @@ inline std::vector<CommReport> simulate_alphas(const Graph& g, const VertexRoles
     detail::check(vk_cache_capacity(a, part.part_of.size(), part.K, &cap));
     for (const auto& r : rankings) takes.push_back(std::min<std::uint64_t>(cap, r.order.size()));
   }
-  return detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, &takes, alphas);
+  return detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, &takes, alphas, nullptr);
 }
 
 // ---- reorder.hpp:15-26 --------------------------------------------------------
@@ -586,6 +593,43 @@ inline ReorderMap build_reorder(const PartitionMap& part, const std::vector<std:
   for (std::size_t i = 0; i < n; ++i) m.new_of_old[m.old_of_new[i]] = static_cast<vertex_t>(i);
   for (std::uint32_t k = 0; k < part.K; ++k) m.ranges.emplace_back(ranges[2 * k], ranges[2 * k + 1]);
   return m;
+}
+
+struct ReorderedDataset {
+  Graph graph;
+  VertexRoles roles;
+  PartitionMap part;
+};
+
+/// apply_reorder (reorder.hpp:34-35): the relabelled graph is built on the
+/// device (vk_graph_apply_reorder); roles and labels permute on the host.
+inline ReorderedDataset apply_reorder(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
+                                      const ReorderMap& map) {
+  const std::size_t n = g.num_vertices();
+  if (map.size() != n) throw shape_error("reorder map size does not match vertex count");  // reorder.cpp:39
+  vk_graph h = nullptr;
+  detail::check(vk_graph_apply_reorder(g.handle(), map.old_of_new.data(), &h));
+  ReorderedDataset out;
+  Graph& ng = out.graph;
+  ng.device = g.device;
+  std::uint64_t nn = 0, m = 0;
+  int sym = 0, dev = 0;
+  detail::check(vk_graph_info(h, &nn, &m, &sym, &dev));
+  ng.fwd_offsets.resize(n + 1);
+  ng.fwd_targets.resize(m);
+  ng.rev_offsets.resize(n + 1);
+  ng.rev_targets.resize(m);
+  detail::check(vk_graph_copy_forward(h, ng.fwd_offsets.data(), ng.fwd_targets.data()));
+  detail::check(vk_graph_copy_reverse(h, ng.rev_offsets.data(), ng.rev_targets.data()));
+  ng.adopt(h);
+  out.roles.role.resize(n);
+  std::vector<std::uint32_t> labels(n);
+  for (std::size_t u = 0; u < n; ++u) {
+    out.roles.role[u] = roles.role[map.old_of_new[u]];
+    labels[u] = part.part_of[map.old_of_new[u]];
+  }
+  out.part = PartitionMap::from_labels(std::move(labels), part.K);
+  return out;
 }
 
 // ---- feature gather (new: the reference never materialises features) -------

@@ -335,7 +335,7 @@ class Ref:
         L.ref_partition_graph.argtypes = [c_vp, u8p, c_u64, c_u32, c_int, c_u64, u32p]
         L.ref_epoch_minibatches.argtypes = [u8p, c_u64, u32p, c_u32, c_u32, c_u64, c_u64, c_u64,
                                             c_vp, u32p, C.POINTER(c_u64)]
-        L.ref_expand.argtypes = [c_vp, u32p, c_u64, u32p, c_u32, c_u64, c_u64, c_u32, c_u64, c_int]
+        L.ref_expand.argtypes = [c_vp, u32p, c_u64, u32p, c_u32, c_u64, c_u64, c_u32, c_u64, c_int, c_vp]
         for fn in ("ref_exp_frontier_size", "ref_exp_edges_size"):
             getattr(L, fn).restype = c_u64
             getattr(L, fn).argtypes = [c_vp, c_u32]
@@ -360,8 +360,10 @@ class Ref:
                                          C.POINTER(c_u64)]
         L.ref_build_cache.argtypes = [u32p, u64p, c_u32, c_double, c_u64, u64p, u64p]
         L.ref_simulate.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, u32p,
-                                   u64p, u64p]
+                                   u64p, u64p, c_vp]
         L.ref_build_reorder.argtypes = [u32p, c_u64, c_u32, f64p, u32p, u64p]
+        L.ref_apply_reorder.restype = c_vp
+        L.ref_apply_reorder.argtypes = [c_vp, u8p, u32p, c_u32, u32p, u8p, u32p]
         self._handles = {}
 
     def _check(self, rc):
@@ -466,11 +468,12 @@ class Ref:
         return [perm[i:i + b] for i in range(0, len(perm), b)]
 
     def expand(self, g: CSR, batch, fanouts, seed, epoch=0, part=0, batch_index=0,
-               with_mfg=True) -> Expansion:
+               with_mfg=True, seed_keys=None) -> Expansion:
         b = _a32(batch)
         f = _a32(fanouts)
+        sk = None if seed_keys is None else _a32(seed_keys)
         p = self._ptr(self.lib.ref_expand(self._graph(g), b, len(b), f, len(f), seed, epoch, part,
-                                          batch_index, int(with_mfg)))
+                                          batch_index, int(with_mfg), None if sk is None else sk.ctypes.data))
         L = self.lib
         out = Expansion(batch=b.copy())
         for h in range(len(f)):
@@ -548,14 +551,15 @@ class Ref:
         cached = [np.asarray(orders[k][:int(take[k])], np.uint32) for k in range(K)]
         return cached, bits.reshape(max(K, 1), W)[:K]
 
-    def simulate(self, g: CSR, roles, labels, K, fanouts, b, E, seed, cached):
+    def simulate(self, g: CSR, roles, labels, K, fanouts, b, E, seed, cached, seed_keys=None):
         offs = np.zeros(K + 1, np.uint64)
         offs[1:] = np.cumsum([len(c) for c in cached])
         cat = _a32(np.concatenate([np.asarray(c, np.uint32) for c in cached]) if K else [])
         cells = np.zeros(E * K * 3, np.uint64)
         f = _a32(fanouts)
         self._check(self.lib.ref_simulate(self._graph(g), np.ascontiguousarray(roles, np.uint8),
-                                          _a32(labels), K, f, len(f), b, E, seed, cat, offs, cells))
+                                          _a32(labels), K, f, len(f), b, E, seed, cat, offs, cells,
+                                          None if seed_keys is None else _a32(seed_keys).ctypes.data))
         return cells.reshape(E, K, 3)
 
     def build_reorder(self, labels, K, scores):
@@ -566,6 +570,19 @@ class Ref:
         ranges = np.zeros(2 * K, np.uint64)
         self._check(self.lib.ref_build_reorder(labels, n, K, s, oon, ranges))
         return oon, ranges.reshape(K, 2)
+
+    def apply_reorder(self, g: CSR, roles, labels, K, old_of_new):
+        """apply_reorder (reorder.cpp:36-70) -> (CSR incl. reverse, roles, labels)."""
+        n = g.n
+        r_out = np.zeros(n, np.uint8)
+        l_out = np.zeros(n, np.uint32)
+        p = self._ptr(self.lib.ref_apply_reorder(self._graph(g), np.ascontiguousarray(roles, np.uint8),
+                                                 _a32(labels), K, _a32(old_of_new), r_out, l_out))
+        try:
+            out = self._copy_graph(p)
+        finally:
+            self.lib.ref_graph_free(p)
+        return out, r_out, l_out
 
 
 def port() -> Port:

@@ -216,15 +216,18 @@ int ref_epoch_minibatches(const std::uint8_t* roles, std::uint64_t n, const std:
 
 void* ref_expand(void* gp, const std::uint32_t* batch, std::uint64_t nb, const std::uint32_t* fan,
                  std::uint32_t L, std::uint64_t seed, std::uint64_t epoch, std::uint32_t part,
-                 std::uint64_t batch_index, int with_mfg) {
+                 std::uint64_t batch_index, int with_mfg, const std::uint32_t* seed_keys) {
   Expansion* out = nullptr;
   const int rc = guard([&] {
     const Graph& g = *static_cast<Graph*>(gp);
     const FanoutSpec fanouts = make_fanouts(fan, L);
     const SeedSpec seeds{seed};
     const BatchRef ref{epoch, part, batch_index};
+    std::vector<vertex_t> keys;
+    if (seed_keys) keys.assign(seed_keys, seed_keys + g.num_vertices());
+    const std::vector<vertex_t>* sk = seed_keys ? &keys : nullptr;
     auto* x = new Expansion();
-    x->nb = expand(g, std::span<const vertex_t>(batch, nb), fanouts, seeds, ref);  // sampling.cpp:94
+    x->nb = expand(g, std::span<const vertex_t>(batch, nb), fanouts, seeds, ref, sk);  // sampling.cpp:94
     if (with_mfg) {
       // MFG: the per-source draw sequence of expand's hop loop
       // (sampling.cpp:106-114), replayed with the reference's own stream
@@ -235,8 +238,9 @@ void* ref_expand(void* gp, const std::uint32_t* batch, std::uint64_t nb, const s
         std::vector<vertex_t> ed;
         for (vertex_t v : *cur) {
           RngStream s = seeds.stream({stream_tag::neighbor_sample, ref.epoch, ref.partition,
-                                      ref.batch_index, static_cast<std::uint64_t>(h), v});
-          sample_neighbors(g, v, fanouts.fanouts[h - 1], s, ed);
+                                      ref.batch_index, static_cast<std::uint64_t>(h),
+                                      sk ? static_cast<std::uint64_t>((*sk)[v]) : v});
+          sample_neighbors(g, v, fanouts.fanouts[h - 1], s, ed, sk);
           ip.push_back(ed.size());
         }
         x->indptr.push_back(std::move(ip));
@@ -394,7 +398,7 @@ int ref_build_cache(const std::uint32_t* orders, const std::uint64_t* order_offs
 int ref_simulate(void* gp, const std::uint8_t* roles, const std::uint32_t* labels, std::uint32_t K,
                  const std::uint32_t* fan, std::uint32_t L, std::uint64_t b, std::uint64_t E,
                  std::uint64_t seed, const std::uint32_t* cached, const std::uint64_t* cached_off,
-                 std::uint64_t* cells_out) {
+                 std::uint64_t* cells_out, const std::uint32_t* seed_keys) {
   return guard([&] {
     const Graph& g = *static_cast<Graph*>(gp);
     const std::uint64_t n = g.num_vertices();
@@ -404,8 +408,14 @@ int ref_simulate(void* gp, const std::uint8_t* roles, const std::uint32_t* label
         plan.cached[k].push_back(cached[i]);
         plan.member_bits[k][cached[i] >> 6] |= 1ull << (cached[i] & 63);
       }
+    std::vector<vertex_t> keys;
+    SimulateOptions opts;
+    if (seed_keys) {
+      keys.assign(seed_keys, seed_keys + n);
+      opts.seed_keys = &keys;  // commsim.hpp:44
+    }
     const CommReport r = simulate(g, make_roles_view(roles, n), make_part(labels, n, K),
-                                  make_fanouts(fan, L), b, E, SeedSpec{seed}, plan);
+                                  make_fanouts(fan, L), b, E, SeedSpec{seed}, plan, opts);
     for (std::uint64_t e = 0; e < E; ++e)
       for (std::uint32_t k = 0; k < K; ++k) {
         const auto& c = r.at(e, k);
@@ -430,6 +440,26 @@ int ref_build_reorder(const std::uint32_t* labels, std::uint64_t n, std::uint32_
       ranges[2 * k + 1] = map.ranges[k].second;
     }
   });
+}
+
+// apply_reorder (reorder.cpp:36-70): the relabelled graph (a new handle),
+// roles and labels. The map's ranges are not consulted by apply_reorder.
+void* ref_apply_reorder(void* gp, const std::uint8_t* roles, const std::uint32_t* labels, std::uint32_t K,
+                        const std::uint32_t* old_of_new, std::uint8_t* roles_out, std::uint32_t* labels_out) {
+  Graph* out = nullptr;
+  const int rc = guard([&] {
+    const Graph& g = *static_cast<Graph*>(gp);
+    const std::size_t n = g.num_vertices();
+    ReorderMap map;
+    map.old_of_new.assign(old_of_new, old_of_new + n);
+    map.new_of_old.resize(n);
+    for (std::size_t i = 0; i < n; ++i) map.new_of_old[map.old_of_new[i]] = static_cast<vertex_t>(i);
+    ReorderedDataset d = apply_reorder(g, make_roles_view(roles, n), make_part(labels, n, K), map);
+    std::memcpy(roles_out, d.roles.role.data(), n);
+    std::memcpy(labels_out, d.part.part_of.data(), n * 4);
+    out = new Graph(std::move(d.graph));
+  });
+  return rc == 0 ? out : nullptr;
 }
 
 // ---- rng ----

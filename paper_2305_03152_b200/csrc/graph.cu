@@ -70,6 +70,47 @@ __global__ void k_split_keys(const std::uint64_t* __restrict__ keys, std::uint64
   }
 }
 
+// apply_reorder (reorder.cpp:36-70): new row u is old row old_of_new[u] with
+// every target mapped through new_of_old, emitted as sortable (u, t') keys.
+__global__ void k_invert_perm(const std::uint32_t* __restrict__ old_of_new, std::uint64_t n,
+                              std::uint32_t* __restrict__ new_of_old, unsigned* __restrict__ bad) {
+  for (std::uint64_t u = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; u < n;
+       u += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint32_t o = old_of_new[u];
+    if (o >= n) {
+      atomicOr(bad, 1u);
+    } else if (atomicExch(new_of_old + o, (std::uint32_t)u) != 0xffffffffu) {
+      atomicOr(bad, 2u);  // two new ids for one old vertex
+    }
+  }
+}
+__global__ void k_new_degrees(const std::uint32_t* __restrict__ old_of_new, const std::uint32_t* __restrict__ deg,
+                              std::uint64_t n, std::uint64_t* __restrict__ new_off) {
+  for (std::uint64_t u = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; u < n;
+       u += (std::uint64_t)gridDim.x * blockDim.x)
+    new_off[u + 1] = deg[old_of_new[u]];
+}
+// warp per new row (power-law rows: lanes stride the row)
+__global__ void k_relabel_rows(const std::uint64_t* __restrict__ off, const std::uint32_t* __restrict__ tgt,
+                               const std::uint32_t* __restrict__ old_of_new,
+                               const std::uint32_t* __restrict__ new_of_old, const std::uint64_t* __restrict__ new_off,
+                               std::uint64_t n, std::uint64_t* __restrict__ keys) {
+  const unsigned lane = threadIdx.x & 31;
+  const std::uint64_t w0 = (blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const std::uint64_t nw = ((std::uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (std::uint64_t u = w0; u < n; u += nw) {
+    const std::uint32_t o = old_of_new[u];
+    const std::uint64_t b = off[o], e = off[o + 1], d = new_off[u];
+    for (std::uint64_t i = b + lane; i < e; i += 32)
+      keys[d + (i - b)] = (u << 32) | new_of_old[__ldg(tgt + i)];
+  }
+}
+__global__ void k_low_words(const std::uint64_t* __restrict__ keys, std::uint64_t m, std::uint32_t* __restrict__ out) {
+  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (std::uint64_t)gridDim.x * blockDim.x)
+    out[i] = (std::uint32_t)keys[i];
+}
+
 __global__ void k_compare(const std::uint64_t* __restrict__ a, const std::uint64_t* __restrict__ b,
                           std::uint64_t n64, const std::uint32_t* __restrict__ c,
                           const std::uint32_t* __restrict__ d, std::uint64_t n32, unsigned* __restrict__ diff) {
@@ -268,6 +309,79 @@ int vk_graph_create(int device, uint64_t n, uint64_t m, const uint64_t* fwd_offs
       throw;
     }
     *out = g;
+  });
+}
+
+int vk_graph_apply_reorder(vk_graph src, const uint32_t* old_of_new, vk_graph* out) {
+  return guard([&] {
+    if (!src || !old_of_new || !out) raise(VK_ERR_PARAMETER, "null argument");
+    vk_graph_s& g = *src;
+    DeviceGuard dg(g.device);
+    const std::uint64_t n = g.n, m = g.m;
+    vk_graph_s* ng = new_graph(g.device, n, m);
+    try {
+      cudaStream_t st = ng->stream;
+      VK_CUDA(cudaStreamSynchronize(g.stream));
+      DevBuf oon(n * 4), noo(n * 4), bad(4);
+      VK_CUDA(cudaMemcpyAsync(oon.p, old_of_new, n * 4, cudaMemcpyHostToDevice, st));
+      VK_CUDA(cudaMemsetAsync(noo.p, 0xff, n * 4, st));
+      VK_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+      k_invert_perm<<<grid_for(n, g.device), 256, 0, st>>>(oon.as<std::uint32_t>(), n, noo.as<std::uint32_t>(),
+                                                          bad.as<unsigned>());
+      count_launch();
+      VK_LAUNCH_CHECK();
+      unsigned hb = 0;
+      VK_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, st));
+      VK_CUDA(cudaStreamSynchronize(st));
+      if (hb) raise(VK_ERR_SHAPE, "reorder map is not a permutation of the vertex ids");  // reorder.cpp:39
+      // offsets: new row u has old row old_of_new[u]'s degree
+      ng->fwd_off.alloc((n + 1) * 8);
+      ng->fwd_tgt.alloc(m ? m * 4 : 4);
+      std::uint64_t* no = ng->fwd_off.as<std::uint64_t>();
+      VK_CUDA(cudaMemsetAsync(no, 0, 8, st));
+      k_new_degrees<<<grid_for(n, g.device), 256, 0, st>>>(oon.as<std::uint32_t>(), g.out_deg.as<std::uint32_t>(),
+                                                          n, no);
+      count_launch();
+      std::size_t tmp = 0;
+      VK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, no, no, (std::int64_t)(n + 1), st));
+      {
+        DevBuf t(tmp);
+        VK_CUDA(cub::DeviceScan::InclusiveSum(t.p, tmp, no, no, (std::int64_t)(n + 1), st));
+        count_launch();
+        VK_CUDA(cudaStreamSynchronize(st));
+      }
+      if (m) {
+        // relabelled rows as (u, t') keys; one radix sort orders every row
+        // (std::sort per row, reorder.cpp:50) since rows are already grouped
+        DevBuf keys(m * 8), keys2(m * 8);
+        k_relabel_rows<<<grid_for(n * 32, g.device), 256, 0, st>>>(g.d_off(), g.d_tgt(), oon.as<std::uint32_t>(),
+                                                                   noo.as<std::uint32_t>(), no, n,
+                                                                   keys.as<std::uint64_t>());
+        count_launch();
+        VK_LAUNCH_CHECK();
+        int end_bit = 32;
+        while ((1ull << (end_bit - 32)) < n && end_bit < 64) ++end_bit;
+        std::size_t t2 = 0;
+        VK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t2, keys.as<std::uint64_t>(), keys2.as<std::uint64_t>(),
+                                               (std::int64_t)m, 0, end_bit, st));
+        DevBuf tb(t2);
+        VK_CUDA(cub::DeviceRadixSort::SortKeys(tb.p, t2, keys.as<std::uint64_t>(), keys2.as<std::uint64_t>(),
+                                               (std::int64_t)m, 0, end_bit, st));
+        count_launch(4);
+        k_low_words<<<grid_for(m, g.device), 256, 0, st>>>(keys2.as<std::uint64_t>(), m,
+                                                           ng->fwd_tgt.as<std::uint32_t>());
+        count_launch();
+        VK_LAUNCH_CHECK();
+        VK_CUDA(cudaStreamSynchronize(st));
+      }
+      // a relabelling of a symmetric graph is symmetric (rev aliases fwd);
+      // otherwise the reverse CSR is rebuilt on the device
+      finish_graph(*ng, nullptr, nullptr, g.symmetric ? VK_GRAPH_UNDIRECTED : 0u);
+    } catch (...) {
+      vk_graph_destroy(ng);
+      throw;
+    }
+    *out = ng;
   });
 }
 

@@ -19,6 +19,8 @@
 //              word + popc).
 // Then all_vertices = compaction of the all bitmap (sampling.cpp:121-126) and
 // the relabel map F_h -> index in all_vertices.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <type_traits>
 #include <cstring>
@@ -70,6 +72,11 @@ struct vk_sampler_s {
   cudaEvent_t done = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t last_stream = nullptr;
+  // seed_keys replay (sampling.hpp:46-56): per-vertex stream keys and a copy
+  // of the CSR with every row ordered by key (sample_neighbors' sorted
+  // scratch, sampling.cpp:83-85)
+  vk::DevBuf keys, tgt_keyed;
+  bool keyed = false;
 
   std::uint32_t* fcount(std::uint32_t h) const { return counts.as<std::uint32_t>() + (std::uint64_t)h * M; }
   std::uint32_t* ecount(std::uint32_t h) const {
@@ -193,7 +200,19 @@ struct SampleParams {
   // vertex range L2-resident for every minibatch that samples from them.
   const uint4* rank_prev;
   std::uint32_t nmb, tile_words;
+  // seed_keys replay (null: keys are the vertex ids, rows in CSR order)
+  const std::uint32_t* keys;
+  const std::uint32_t* tgt_keyed;
 };
+
+// The stream key of v and the row the partial Fisher-Yates draws from
+// (sampling.cpp:108-112 and 83-85; CSR order when not replaying keys).
+__device__ __forceinline__ std::uint64_t vertex_key(const SampleParams& p, std::uint32_t v) {
+  return p.keys ? (std::uint64_t)__ldg(p.keys + v) : (std::uint64_t)v;
+}
+__device__ __forceinline__ const std::uint32_t* draw_row(const SampleParams& p, std::uint32_t v) {
+  return (p.keys ? p.tgt_keyed : p.tgt) + p.off[v];
+}
 
 // One thread per frontier vertex; FY state in shared memory (f <= 32) or in
 // local memory (MAXF > 0, large fanouts).
@@ -317,7 +336,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
     if (j < cnt) {
       const std::uint32_t v = fp[j];
       const std::uint32_t deg = p.outdeg[v];
-      const std::uint32_t* nbrs = p.tgt + p.off[v];
+      const std::uint32_t* nbrs = p.tgt + p.off[v];  // CSR order (the deg <= f case)
       std::uint32_t* out = stage + (ip[j] - base);
       if (deg <= f) {  // sampling.cpp:76-78: all neighbours, CSR order
         for (std::uint32_t i0 = 0; i0 < deg; i0 += 4) {
@@ -332,10 +351,11 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
             }
         }
       } else if constexpr (FMAX > 0) {
-        Stream s(key_step(prefix, v));
-        fy_registers<FMAX>(nbrs, deg, f, s, out, hb);
+        Stream s(key_step(prefix, vertex_key(p, v)));
+        fy_registers<FMAX>(draw_row(p, v), deg, f, s, out, hb);
       } else {
-        Stream s(key_step(prefix, v));
+        Stream s(key_step(prefix, vertex_key(p, v)));
+        nbrs = draw_row(p, v);
         for (std::uint32_t i = 0; i < f; ++i) jj[i * S] = i + (std::uint32_t)s.next_below((std::uint64_t)(deg - i));
         for (std::uint32_t i0 = 0; i0 < f; i0 += 4) {
           std::uint32_t a[4], b[4];
@@ -399,10 +419,27 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
   unsigned long long* hb = p.hopbits + mb * p.W;
   for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x) {
     const std::uint32_t v = fp[j];
-    Stream s(key_step(prefix, v));
+    Stream s(key_step(prefix, vertex_key(p, v)));
     std::uint32_t lo[MAXF], hp[MAXF], hv[MAXF];
-    sample_one(p.tgt + p.off[v], p.outdeg[v], p.f, s, ed + ip[j], hb, lo, hp, hv, 1);
+    const std::uint32_t deg = p.outdeg[v];
+    sample_one(deg <= p.f ? p.tgt + p.off[v] : draw_row(p, v), deg, p.f, s, ed + ip[j], hb, lo, hp, hv, 1);
   }
+}
+
+// seed_keys replay: (row, key of target) pairs, warp per row, so one radix
+// sort orders every row by key (sample_neighbors' scratch sort).
+__global__ void k_keyed_pairs(const std::uint64_t* __restrict__ off, const std::uint32_t* __restrict__ tgt,
+                              const std::uint32_t* __restrict__ keys, std::uint64_t n,
+                              std::uint64_t* __restrict__ kout, std::uint32_t* __restrict__ vout) {
+  const unsigned lane = threadIdx.x & 31;
+  const std::uint64_t w0 = (blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const std::uint64_t nw = ((std::uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (std::uint64_t u = w0; u < n; u += nw)
+    for (std::uint64_t i = off[u] + lane; i < off[u + 1]; i += 32) {
+      const std::uint32_t t = __ldg(tgt + i);
+      kout[i] = (u << 32) | __ldg(keys + t);
+      vout[i] = t;
+    }
 }
 
 struct CompactParams {
@@ -874,6 +911,8 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
   p.off = g.d_off();
   p.tgt = g.d_tgt();
   p.outdeg = g.out_deg.as<std::uint32_t>();
+  p.keys = s.keyed ? s.keys.as<std::uint32_t>() : nullptr;
+  p.tgt_keyed = s.keyed ? s.tgt_keyed.as<std::uint32_t>() : nullptr;
   p.Fprev = s.F[h - 1].as<std::uint32_t>();
   p.capFprev = s.capF[h - 1];
   p.fcount_prev = s.fcount(h - 1);
@@ -1086,6 +1125,47 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       throw;
     }
     *out = s;
+  });
+}
+
+int vk_sampler_set_seed_keys(vk_sampler s, const uint32_t* seed_keys) {
+  return guard([&] {
+    if (!s) raise(VK_ERR_PARAMETER, "null argument");
+    vk_graph_s& g = *s->g;
+    DeviceGuard dg(g.device);
+    if (s->last_stream) VK_CUDA(cudaStreamSynchronize(s->last_stream));
+    if (!seed_keys) {
+      s->keyed = false;
+      s->keys.release();
+      s->tgt_keyed.release();
+      return;
+    }
+    const std::uint64_t n = g.n, m = g.m;
+    cudaStream_t st = s->stream;
+    s->keys.alloc(n * 4);
+    VK_CUDA(cudaMemcpyAsync(s->keys.p, seed_keys, n * 4, cudaMemcpyHostToDevice, st));
+    s->tgt_keyed.alloc(m ? m * 4 : 4);
+    if (m) {
+      DevBuf k1(m * 8), k2(m * 8), v1(m * 4);
+      const unsigned grid = (unsigned)std::min<std::uint64_t>((n * 32 + 255) / 256, (std::uint64_t)sm_count(g.device) * 16);
+      k_keyed_pairs<<<std::max(1u, grid), 256, 0, st>>>(g.d_off(), g.d_tgt(), s->keys.as<std::uint32_t>(), n,
+                                                       k1.as<std::uint64_t>(), v1.as<std::uint32_t>());
+      count_launch();
+      VK_LAUNCH_CHECK();
+      int end_bit = 32;
+      while ((1ull << (end_bit - 32)) < n && end_bit < 64) ++end_bit;
+      std::size_t tmp = 0;
+      VK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k1.as<std::uint64_t>(), k2.as<std::uint64_t>(),
+                                              v1.as<std::uint32_t>(), s->tgt_keyed.as<std::uint32_t>(),
+                                              (std::int64_t)m, 0, end_bit, st));
+      DevBuf tb(tmp);
+      VK_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, tmp, k1.as<std::uint64_t>(), k2.as<std::uint64_t>(),
+                                              v1.as<std::uint32_t>(), s->tgt_keyed.as<std::uint32_t>(),
+                                              (std::int64_t)m, 0, end_bit, st));
+      count_launch(4);
+    }
+    VK_CUDA(cudaStreamSynchronize(st));
+    s->keyed = true;
   });
 }
 

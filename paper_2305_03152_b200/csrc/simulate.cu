@@ -135,7 +135,8 @@ template <class OnWave>
 std::uint64_t stream_expansions(vk_graph g, const std::uint8_t* roles, const std::uint32_t* part_of,
                                 std::uint32_t K, const std::vector<std::uint32_t>& parts,
                                 const std::uint32_t* fanouts, std::uint32_t num_hops, std::uint64_t batch_size,
-                                std::uint64_t epochs, std::uint64_t seed, std::uint32_t M, OnWave&& on_wave) {
+                                std::uint64_t epochs, std::uint64_t seed, const std::uint32_t* seed_keys,
+                                std::uint32_t M, OnWave&& on_wave) {
   if (num_hops == 0 || num_hops > VK_MAX_HOPS) raise(VK_ERR_PARAMETER, "1..VK_MAX_HOPS hops");
   vk_sampler_config cfg{};
   cfg.num_hops = num_hops;
@@ -149,6 +150,8 @@ std::uint64_t stream_expansions(vk_graph g, const std::uint8_t* roles, const std
     vk_sampler s;
     ~SamplerGuard() { vk_sampler_destroy(s); }
   } sg{sampler};
+  if (seed_keys)
+    if (int e = vk_sampler_set_seed_keys(sampler, seed_keys)) raise(e, vk_last_error());
   const std::uint64_t n = g->n;
   // train members of the partitions in ascending id order (train_members,
   // graph.cpp:106-111), gathered in one pass instead of one per (e, k)
@@ -157,6 +160,10 @@ std::uint64_t stream_expansions(vk_graph g, const std::uint8_t* roles, const std
   std::vector<std::vector<std::uint32_t>> members(K);
   for (std::uint64_t v = 0; v < n; ++v)
     if (roles[v] == 0 && want[part_of[v]]) members[part_of[v]].push_back((std::uint32_t)v);
+  if (seed_keys)  // canonical order follows the replay keys (sampling.cpp:54-58)
+    for (auto& mk : members)
+      std::stable_sort(mk.begin(), mk.end(),
+                       [&](std::uint32_t a, std::uint32_t c) { return seed_keys[a] < seed_keys[c]; });
   std::vector<std::uint32_t> perm, seeds, cell_of;
   std::vector<std::uint64_t> offs{0};
   std::vector<vk_batch_ref> refs;
@@ -209,7 +216,7 @@ extern "C" {
 
 int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, const uint32_t* fanouts,
                 uint32_t num_hops, uint64_t batch_size, uint64_t epochs, uint64_t global_seed,
-                const uint32_t* cached_ids, const uint64_t* cached_offsets, const uint64_t* takes,
+                const uint32_t* seed_keys, const uint32_t* cached_ids, const uint64_t* cached_offsets, const uint64_t* takes,
                 uint32_t num_plans, uint32_t wave, uint64_t* cells) {
   return guard([&] {
     if (!g || !roles || !part_of || !fanouts || !cached_offsets || !cells) raise(VK_ERR_PARAMETER, "null argument");
@@ -273,7 +280,7 @@ int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint3
     int parity = 0;
     std::vector<std::uint32_t> parts(K);
     for (std::uint32_t k = 0; k < K; ++k) parts[k] = k;
-    stream_expansions(g, roles, part_of, K, parts, fanouts, num_hops, batch_size, epochs, global_seed, M,
+    stream_expansions(g, roles, part_of, K, parts, fanouts, num_hops, batch_size, epochs, global_seed, seed_keys, M,
                       [&](const std::uint32_t* all, std::uint64_t stride, const std::uint32_t* count,
                           std::uint32_t nmb, const std::uint32_t* cell_of, cudaStream_t st) {
                         std::uint32_t* ch = cell_host.as<std::uint32_t>() + parity * M;
@@ -320,7 +327,7 @@ int vk_empirical_vip(vk_graph g, const uint8_t* roles, const uint32_t* part_of, 
     VK_CUDA(cudaMemset(hits.p, 0, hits.bytes));
     VK_CUDA(cudaDeviceSynchronize());
     const std::uint64_t batches = stream_expansions(
-        g, roles, part_of, K, {k}, fanouts, num_hops, batch_size, epochs, seed, 128u,
+        g, roles, part_of, K, {k}, fanouts, num_hops, batch_size, epochs, seed, nullptr, 128u,
         [&](const std::uint32_t* all, std::uint64_t stride, const std::uint32_t* count, std::uint32_t nmb,
             const std::uint32_t*, cudaStream_t st) {
           const unsigned gx = (unsigned)std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(stride, 256 * 8), 64));

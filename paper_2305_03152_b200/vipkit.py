@@ -103,6 +103,8 @@ def lib():
     L.vk_graph_destroy.argtypes = [c_vp]
     L.vk_graph_info.argtypes = [c_vp, C.POINTER(c_u64), C.POINTER(c_u64), C.POINTER(c_int), C.POINTER(c_int)]
     L.vk_graph_copy_reverse.argtypes = [c_vp, u64p, u32p]
+    L.vk_graph_copy_forward.argtypes = [c_vp, u64p, u32p]
+    L.vk_graph_apply_reorder.argtypes = [c_vp, u32p, C.POINTER(c_vp)]
     L.vk_initial_probs.argtypes = [c_u64, u8p, u32p, c_u32, c_u64, f64p]
     L.vk_vip_propagate.argtypes = [c_vp, u32p, c_u32, c_u32, f64p, c_vp, f64p]
     L.vk_vip_propagate_device.argtypes = [c_vp, u32p, c_u32, c_u32, c_vp, c_vp, c_vp, c_vp]
@@ -110,6 +112,7 @@ def lib():
                                        C.POINTER(c_u64)]
     L.vk_sampler_create.argtypes = [c_vp, C.POINTER(SamplerConfig), C.POINTER(c_vp)]
     L.vk_sampler_destroy.argtypes = [c_vp]
+    L.vk_sampler_set_seed_keys.argtypes = [c_vp, c_vp]
     L.vk_sampler_run.argtypes = [c_vp, c_u32, C.POINTER(BatchRef), c_vp, u64p, c_int, c_vp]
     L.vk_sampler_sizes.argtypes = [c_vp, c_vp, c_vp, c_vp]
     L.vk_sampler_copy_frontier.argtypes = [c_vp, c_u32, c_u32, u32p]
@@ -130,8 +133,8 @@ def lib():
     L.vk_plane_gather.argtypes = [c_vp, c_vp, c_vp, c_u64, c_vp, c_vp]
     L.vk_plane_row_bytes.argtypes = [c_vp, C.POINTER(c_u64)]
     L.vk_plane_pulled_rows.argtypes = [c_vp, C.POINTER(c_u64)]
-    L.vk_simulate.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, c_vp, u64p, c_vp,
-                              c_u32, c_u32, u64p]
+    L.vk_simulate.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, c_vp, c_vp, u64p,
+                              c_vp, c_u32, c_u32, u64p]
     L.vk_empirical_vip.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u64, u32p, c_u32, c_u64, c_u64, f64p]
     L.vk_synth_community_powerlaw.argtypes = [c_u64, c_u64, c_u32, c_double, c_u64, C.c_uint,
                                               C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), u32p]
@@ -207,6 +210,12 @@ class Graph:
         h = c_vp()
         check(lib().vk_graph_load_vcsr(device, os.fsencode(path), 0, C.byref(h)))
         return cls(h, device)
+
+    def forward(self):
+        off = np.zeros(self.n + 1, np.uint64)
+        tgt = np.zeros(self.m, np.uint32)
+        check(lib().vk_graph_copy_forward(self._h, off, tgt))
+        return off, tgt
 
     def reverse(self):
         roff = np.zeros(self.n + 1, np.uint64)
@@ -357,6 +366,22 @@ class Sampler:
         check(lib().vk_sampler_create(g.handle, C.byref(cfg), C.byref(h)))
         self._h = h
         self.nmb = 0
+        self._keys = None
+
+    def set_seed_keys(self, seed_keys):
+        """seed_keys replay (vk_sampler_set_seed_keys); None turns it off."""
+        if seed_keys is None:
+            if self._keys is not None:
+                check(lib().vk_sampler_set_seed_keys(self._h, None))
+                self._keys = None
+            return
+        sk = _a32(seed_keys)
+        if len(sk) != self.g.n:
+            raise ShapeError("seed_keys length does not match vertex count")
+        if self._keys is not None and np.array_equal(self._keys, sk):
+            return
+        check(lib().vk_sampler_set_seed_keys(self._h, sk.ctypes.data))
+        self._keys = sk.copy()
 
     @property
     def handle(self):
@@ -447,9 +472,10 @@ class Sampler:
             pass
 
 
-def expand(g: Graph, batch, fanouts, seeds, ref=(0, 0, 0)) -> ExpandedNeighborhood:
+def expand(g: Graph, batch, fanouts, seeds, ref=(0, 0, 0), seed_keys=None) -> ExpandedNeighborhood:
     """vipkit::expand (sampling.hpp:62-64) for one minibatch. `seeds` is the
-    SeedSpec global seed; `ref` = (epoch, partition, batch_index)."""
+    SeedSpec global seed; `ref` = (epoch, partition, batch_index);
+    `seed_keys` replays another labelling's streams (sampling.hpp:46-56)."""
     f = tuple(int(x) for x in _fan(fanouts))
     if len(f) == 0:
         raise ParameterError("fanout list must have at least one hop")
@@ -465,6 +491,7 @@ def expand(g: Graph, batch, fanouts, seeds, ref=(0, 0, 0)) -> ExpandedNeighborho
             s.close()
         s = Sampler(g, f, max(len(b), 1024), 1, seeds)
         g._samplers[key] = s
+    s.set_seed_keys(seed_keys)
     s.run([b], [ref])
     return s.result(0)
 
@@ -516,7 +543,8 @@ def build_cache(rankings: Sequence, alpha: float, n: int) -> CachePlan:
     return CachePlan(K, alpha, cached, bits)
 
 
-def simulate(g: Graph, roles, part_of, K, fanouts, b, epochs, seed, cached, takes=None, wave=0):
+def simulate(g: Graph, roles, part_of, K, fanouts, b, epochs, seed, cached, takes=None, wave=0,
+             seed_keys=None):
     """vipkit::simulate (commsim.hpp:56-59) on the device -> cells[E, K, 3]
     = (local_hits, cache_hits, remote_misses) per (epoch, partition).
 
@@ -535,8 +563,10 @@ def simulate(g: Graph, roles, part_of, K, fanouts, b, epochs, seed, cached, take
         tk = np.ascontiguousarray(np.asarray(takes, np.uint64).reshape(-1, K))
         A = tk.shape[0]
     cells = np.zeros(A * epochs * K * 3, np.uint64)
+    sk = None if seed_keys is None else _a32(seed_keys)
     check(lib().vk_simulate(g.handle, np.ascontiguousarray(roles, np.uint8), part_of, K, fan, len(fan), b,
-                            epochs, seed, ids.ctypes.data if ids.size else None, offs,
+                            epochs, seed, None if sk is None else sk.ctypes.data,
+                            ids.ctypes.data if ids.size else None, offs,
                             tk.ctypes.data if tk is not None else None, A, wave, cells))
     cells = cells.reshape(A, epochs, K, 3)
     return cells if takes is not None else cells[0]
@@ -550,6 +580,18 @@ def empirical_vip(g: Graph, roles, part_of, K, k, b, fanouts, S, seed):
     check(lib().vk_empirical_vip(g.handle, np.ascontiguousarray(roles, np.uint8), part_of, K, k, b, fan,
                                  len(fan), S, seed, out))
     return out
+
+
+def apply_reorder(g: Graph, roles, part_of, old_of_new):
+    """vipkit::apply_reorder (reorder.hpp:34-35) -> (Graph, roles, part_of):
+    the relabelled graph is built on the device; roles/labels permute."""
+    oon = _a32(old_of_new)
+    if len(oon) != g.n:
+        raise ShapeError("reorder map size does not match vertex count")  # reorder.cpp:39
+    h = c_vp()
+    check(lib().vk_graph_apply_reorder(g.handle, oon, C.byref(h)))
+    ng = Graph(h, g.device)
+    return ng, np.ascontiguousarray(roles, np.uint8)[oon], _a32(part_of)[oon]
 
 
 def build_reorder(part_of, K, scores, device=0):

@@ -320,6 +320,57 @@ static void test_empirical_vip() {
   CHECK_THROWS_AS(empirical_vip(g, roles, part, 0, 1, f, 0, SeedSpec{31}), parameter_error);
 }
 
+// test_reorder.cpp:113-179: apply_reorder preserves the graph up to
+// relabelling; with seed_keys replay the miss counts are invariant.
+static void test_reorder_and_replay() {
+  const std::size_t n = 400;
+  std::vector<std::pair<vertex_t, vertex_t>> e;
+  std::uint64_t x = 777;
+  for (std::size_t i = 0; i < 3 * n; ++i) {
+    x = x * 6364136223846793005ull + 1442695040888963407ull;
+    e.emplace_back(static_cast<vertex_t>((x >> 33) % n), static_cast<vertex_t>((x >> 13) % n));
+  }
+  const Graph g = from_edges(n, e, true);
+  VertexRoles roles;
+  roles.role.assign(n, 1);
+  for (std::size_t v = 0; v < n; v += 3) roles.role[v] = 0;
+  std::vector<std::uint32_t> labels(n);
+  for (std::size_t v = 0; v < n; ++v) labels[v] = static_cast<std::uint32_t>((v * 7) % 2);
+  const auto part = PartitionMap::from_labels(labels, 2);
+  const FanoutSpec fan{{3, 2}};
+  std::vector<std::vector<double>> scores;
+  for (std::uint32_t k = 0; k < 2; ++k)
+    scores.push_back(propagate(g, TransitionModel{TransitionModel::Kind::uniform_fanout, fan},
+                               initial_probs(roles, part, k, 8), k)
+                         .total);
+  const ReorderMap map = build_reorder(part, scores);
+  const ReorderedDataset out = apply_reorder(g, roles, part, map);
+  CHECK(out.graph.num_edges() == g.num_edges());
+  for (std::size_t v = 0; v < n; ++v) {
+    const vertex_t u = map.new_of_old[v];
+    CHECK(out.graph.out_degree(u) == g.out_degree(static_cast<vertex_t>(v)));
+    CHECK(out.roles.role[u] == roles.role[v]);
+    CHECK(out.part.part_of[u] == part.part_of[v]);
+    std::vector<vertex_t> a, b;
+    for (vertex_t t : g.out_neighbors(static_cast<vertex_t>(v))) a.push_back(map.new_of_old[t]);
+    for (vertex_t t : out.graph.out_neighbors(u)) b.push_back(t);
+    std::sort(a.begin(), a.end());
+    CHECK(a == b);
+  }
+  for (std::uint32_t k = 0; k < 2; ++k)
+    for (std::size_t i = 1; i < out.part.members[k].size(); ++i)
+      CHECK(out.part.members[k][i] == out.part.members[k][i - 1] + 1);
+  const SeedSpec seeds{2024};
+  const CommReport before = simulate(g, roles, part, fan, 8, 3, seeds, CachePlan::empty(2, n));
+  const CommReport after =
+      simulate(out.graph, out.roles, out.part, fan, 8, 3, seeds, CachePlan::empty(2, n), &map.old_of_new);
+  CHECK(before.cells.size() == after.cells.size());
+  for (std::size_t i = 0; i < before.cells.size(); ++i) {
+    CHECK(before.cells[i].local_hits == after.cells[i].local_hits);
+    CHECK(before.cells[i].remote_misses == after.cells[i].remote_misses);
+  }
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"initial probabilities", test_initial_probabilities},
@@ -333,6 +384,7 @@ int main() {
       {"simulate: zero/full cache, conservation, alpha sweep", test_commsim},
       {"simulate: 4-path exact expectation", test_commsim_four_path_law},
       {"empirical VIP: saturating ball, 3-path law, determinism", test_empirical_vip},
+      {"apply_reorder isomorphism + seed_keys replay invariance", test_reorder_and_replay},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

@@ -122,3 +122,67 @@ def test_cache_reduces_misses(vk, port):
         if prev is not None:
             assert miss <= prev
         prev = miss
+
+
+@pytest.mark.parametrize("graph,directed", [("pa5000", False), ("dtree13", True)])
+def test_apply_reorder_vs_reference(vk, ref, golden, graph, directed):
+    """apply_reorder (reorder.cpp:36-70) on the device: relabelled forward
+    and reverse CSR, roles and labels bit-exact vs the live reference."""
+    csr = csr_from(golden("graphs.npz"), graph)
+    n = csr.n
+    rng = np.random.default_rng(7)
+    K = 3
+    labels = rng.integers(0, K, n).astype(np.uint32)
+    roles = rng.integers(0, 3, n).astype(np.uint8)
+    scores = rng.random((K, n))
+    oon, _ = vk.build_reorder(labels, K, scores)
+    if directed:
+        g = vk.Graph.from_csr(csr.off, csr.tgt, validate=True)
+    else:
+        g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    ng, r2, l2 = vk.apply_reorder(g, roles, labels, oon)
+    exp, er, el = ref.apply_reorder(csr, roles, labels, K, oon)
+    off, tgt = ng.forward()
+    roff, rtgt = ng.reverse()
+    np.testing.assert_array_equal(off, exp.off)
+    np.testing.assert_array_equal(tgt, exp.tgt)
+    np.testing.assert_array_equal(roff, exp.rev_off)
+    np.testing.assert_array_equal(rtgt, exp.rev_tgt)
+    np.testing.assert_array_equal(r2, er)
+    np.testing.assert_array_equal(l2, el)
+    bad = oon.copy()
+    bad[0] = bad[1]
+    with pytest.raises(vk.ShapeError):
+        vk.apply_reorder(g, roles, labels, bad)
+    with pytest.raises(vk.ShapeError):
+        vk.apply_reorder(g, roles, labels, oon[:-1])
+
+
+def test_apply_reorder_c3_scale(vk, port):
+    """BASELINE C3 shape (2.45 M vertices, 122 M slots): the relabelled graph
+    is isomorphic (degree multiset, sorted rows, every edge maps back) and a
+    sampled minibatch of the relabelled graph expands bit-exact vs the oracle."""
+    from oracle.oracle import CSR
+    n = 2_449_029
+    off, tgt, labels = vk.synth_community_powerlaw(n, 25, 8, 0.8, 7, 0)
+    roles = vk.synth_roles(n, 0.08, 0, 0, 3)
+    g = vk.Graph.from_csr(off, tgt, undirected=True)
+    scores = np.random.default_rng(1).random((8, n))
+    oon, _ = vk.build_reorder(labels, 8, scores)
+    ng, r2, l2 = vk.apply_reorder(g, roles, labels, oon)
+    noff, ntgt = ng.forward()
+    assert ng.symmetric and ng.m == g.m
+    deg_old = np.diff(off.astype(np.int64))
+    np.testing.assert_array_equal(np.diff(noff.astype(np.int64)), deg_old[oon])
+    new_of_old = np.empty(n, np.uint32)
+    new_of_old[oon] = np.arange(n, dtype=np.uint32)
+    for u in np.random.default_rng(2).integers(0, n, 500):
+        row = ntgt[noff[u]:noff[u + 1]]
+        assert np.all(np.diff(row.astype(np.int64)) > 0)
+        o = oon[u]
+        np.testing.assert_array_equal(np.sort(new_of_old[tgt[off[o]:off[o + 1]]]), row)
+    perm = vk.epoch_permutation(r2, l2, 3, 1024, 0, 42)
+    s = vk.Sampler(ng, [15, 10, 5], 1024, 1, 42)
+    s.run([perm[:1024]], [(0, 3, 0)])
+    x = port.expand(CSR(n, noff, ntgt), perm[:1024], [15, 10, 5], 42, 0, 3, 0)
+    np.testing.assert_array_equal(s.result(0).all_vertices, x.all_vertices)

@@ -127,3 +127,39 @@ def test_device_rng_matches_reference_draws(vk, golden, port):
     for b in list(rng.integers(2, 1 << 32, 200)) + [(1 << 40) - 1, 3, 7, 1 << 31, (1 << 32) - 5]:
         key = int(rng.integers(0, 1 << 62))
         np.testing.assert_array_equal(vk.stream_draws(key, int(b), 300), port.stream_draws(key, int(b), 300))
+
+
+def test_seed_keys_replay_vs_reference(vk, ref, golden):
+    """seed_keys replay (sampling.hpp:46-64): on a relabelled graph with
+    seed_keys = old_of_new the device expansion is bit-exact with the
+    reference's keyed expand, and maps back onto the original graph's
+    expansion vertex for vertex."""
+    from oracle.oracle import CSR
+    csr = csr_from(golden("graphs.npz"), "pa5000")
+    n = csr.n
+    rng = np.random.default_rng(3)
+    K = 4
+    labels = rng.integers(0, K, n).astype(np.uint32)
+    roles = np.zeros(n, np.uint8)
+    oon, _ = vk.build_reorder(labels, K, rng.random((K, n)))
+    g = dev_graph(vk, csr)
+    ng, r2, l2 = vk.apply_reorder(g, roles, labels, oon)
+    noff, ntgt = ng.forward()
+    ncsr = CSR(n, noff, ntgt)
+    new_of_old = np.empty(n, np.uint32)
+    new_of_old[oon] = np.arange(n, dtype=np.uint32)
+    fan = [15, 10, 5]
+    for i in range(3):
+        batch_old = rng.choice(n, 64, replace=False).astype(np.uint32)
+        batch_new = new_of_old[batch_old]
+        got = vk.expand(ng, batch_new, fan, 42, (1, 2, i), seed_keys=oon)
+        exp = ref.expand(ncsr, batch_new, fan, 42, 1, 2, i, seed_keys=oon)
+        assert_same(got, 3, exp.frontier, exp.all_vertices, exp.indptr, exp.edges)
+        orig = vk.expand(g, batch_old, fan, 42, (1, 2, i))
+        np.testing.assert_array_equal(np.sort(oon[got.all_vertices]), orig.all_vertices)
+        for h in range(3):
+            np.testing.assert_array_equal(np.sort(oon[got.frontier[h]]), orig.frontier[h])
+    # replay off again: plain expansion of the relabelled graph
+    plain = vk.expand(ng, batch_new, fan, 42, (1, 2, 2))
+    x = ref.expand(ncsr, batch_new, fan, 42, 1, 2, 2)
+    assert_same(plain, 3, x.frontier, x.all_vertices, x.indptr, x.edges)

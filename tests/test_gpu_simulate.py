@@ -82,3 +82,27 @@ def test_empirical_vip_vs_reference(vk, port, ref, K, k, b, fan, S):
     exp = ref.empirical_vip(csr, roles, labels, K, k, b, fan, S, 42)
     np.testing.assert_array_equal(got, exp)
     assert got.max() == 1.0 and 0.0 < got.mean() < 1.0
+
+
+def test_simulate_with_seed_keys_is_reorder_invariant(vk, port, ref):
+    """test_reorder.cpp:154-179 + SimulateOptions::seed_keys: after
+    apply_reorder, simulate with seed_keys = old_of_new reproduces the
+    original graph's local/miss cells; bit-exact vs the keyed reference."""
+    from oracle.oracle import CSR
+    csr = port.generate("pa", 2500, 4, 51)
+    n, K = csr.n, 2
+    roles = port.make_roles(n, 0.3, 0, 0, 2)
+    labels = (np.arange(n) % K).astype(np.uint32)
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    p0 = np.stack([vk.initial_probs(roles, labels, k, 8) for k in range(K)])
+    totals = np.stack([s.total for s in vk.propagate(g, [3, 2], p0, with_hops=False)])
+    oon, _ = vk.build_reorder(labels, K, totals)
+    ng, r2, l2 = vk.apply_reorder(g, roles, labels, oon)
+    noff, ntgt = ng.forward()
+    empty = [np.zeros(0, np.uint32)] * K
+    before = vk.simulate(g, roles, labels, K, [3, 2], 8, 3, 2024, empty)
+    after = vk.simulate(ng, r2, l2, K, [3, 2], 8, 3, 2024, empty, seed_keys=oon)
+    np.testing.assert_array_equal(before[..., 0], after[..., 0])
+    np.testing.assert_array_equal(before[..., 2], after[..., 2])
+    exp = ref.simulate(CSR(n, noff, ntgt), r2, l2, K, [3, 2], 8, 3, 2024, empty, seed_keys=oon)
+    np.testing.assert_array_equal(after, exp)
