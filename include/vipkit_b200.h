@@ -219,6 +219,27 @@ VK_API int vk_debug_stream_draws(int device, uint64_t key, uint64_t bound, uint6
 VK_API int vk_rank_by_scores(int device, uint64_t n, const uint32_t* part_of, uint32_t k,
                              const double* scores, uint64_t n_scores, uint32_t* order_out,
                              double* score_out, uint64_t* count_out);
+/* Baseline rankings of the Fig. 3 sweep (policies.hpp:24-45, policies.cpp:
+ * 57-132), scores computed on the device, remotes ordered as order_remotes.
+ * Bit-identical to the reference (sequential in-neighbour sums in CSR order,
+ * round-to-nearest f64).
+ *  - rank_degree: remotes reachable within L forward hops of partition k's
+ *    train vertices first, by decreasing out-degree; unreachable score 0.
+ *  - rank_halo_1hop: remote out-neighbours of partition k (score 1);
+ *    *effective_alpha = |halo| * K / n (may be NULL).
+ *  - rank_wpr: weighted reverse PageRank, restart uniform over k's train
+ *    vertices, hop-1 weights of TransitionModel{hop1_fanout}, `iters` power
+ *    steps with `damping` (reference defaults 5, 0.85).
+ *  - rank_numpaths: walks of length <= L from k's train vertices (f64). */
+VK_API int vk_rank_degree(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, uint32_t k,
+                          uint32_t L, uint32_t* order_out, double* score_out, uint64_t* count_out);
+VK_API int vk_rank_halo_1hop(vk_graph g, const uint32_t* part_of, uint32_t K, uint32_t k, uint32_t* order_out,
+                             double* score_out, uint64_t* count_out, double* effective_alpha);
+VK_API int vk_rank_wpr(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, uint32_t k,
+                       uint32_t hop1_fanout, uint32_t iters, double damping, uint32_t* order_out,
+                       double* score_out, uint64_t* count_out);
+VK_API int vk_rank_numpaths(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, uint32_t k,
+                            uint32_t L, uint32_t* order_out, double* score_out, uint64_t* count_out);
 /* build_cache capacity (policies.cpp:155-156): floor(alpha*n/K + 1e-9). */
 VK_API int vk_cache_capacity(double alpha, uint64_t n, uint32_t K, uint64_t* capacity);
 /* vipkit::build_reorder (reorder.hpp:25-26, reorder.cpp:11-34) on the device:

@@ -409,6 +409,52 @@ inline Ranking rank_by_scores(const PartitionMap& part, std::uint32_t k, std::sp
   return r;
 }
 
+namespace detail {
+template <class F>
+Ranking device_ranking(const Graph& g, std::uint32_t k, F&& call) {
+  Ranking r;
+  r.partition = k;
+  r.order.resize(g.num_vertices());
+  r.score.resize(g.num_vertices());
+  std::uint64_t cnt = 0;
+  check(call(r.order.data(), r.score.data(), &cnt));
+  r.order.resize(cnt);
+  r.score.resize(cnt);
+  return r;
+}
+}  // namespace detail
+
+/// Baseline rankings of the Fig. 3 sweep (policies.hpp:24-45) on the device.
+inline Ranking rank_degree(const Graph& g, const VertexRoles& roles, const PartitionMap& part, std::uint32_t k,
+                           std::size_t L) {
+  return detail::device_ranking(g, k, [&](vertex_t* o, double* s, std::uint64_t* c) {
+    return vk_rank_degree(g.handle(), roles.role.data(), part.part_of.data(), part.K, k,
+                          static_cast<std::uint32_t>(L), o, s, c);
+  });
+}
+inline Ranking rank_halo_1hop(const Graph& g, const PartitionMap& part, std::uint32_t k) {
+  double ea = -1.0;
+  Ranking r = detail::device_ranking(g, k, [&](vertex_t* o, double* s, std::uint64_t* c) {
+    return vk_rank_halo_1hop(g.handle(), part.part_of.data(), part.K, k, o, s, c, &ea);
+  });
+  r.effective_alpha = ea;
+  return r;
+}
+inline Ranking rank_wpr(const Graph& g, const VertexRoles& roles, const PartitionMap& part, std::uint32_t k,
+                        const TransitionModel& tm, std::uint32_t iters = 5, double damping = 0.85) {
+  return detail::device_ranking(g, k, [&](vertex_t* o, double* s, std::uint64_t* c) {
+    return vk_rank_wpr(g.handle(), roles.role.data(), part.part_of.data(), part.K, k, tm.fanouts.fanouts.at(0),
+                       iters, damping, o, s, c);
+  });
+}
+inline Ranking rank_numpaths(const Graph& g, const VertexRoles& roles, const PartitionMap& part, std::uint32_t k,
+                             std::size_t L) {
+  return detail::device_ranking(g, k, [&](vertex_t* o, double* s, std::uint64_t* c) {
+    return vk_rank_numpaths(g.handle(), roles.role.data(), part.part_of.data(), part.K, k,
+                            static_cast<std::uint32_t>(L), o, s, c);
+  });
+}
+
 struct CachePlan {
   std::uint32_t K = 1;
   double alpha = 0.0;

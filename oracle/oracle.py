@@ -363,6 +363,8 @@ class Ref:
                                    u64p, u64p, c_vp]
         L.ref_build_reorder.argtypes = [u32p, c_u64, c_u32, f64p, u32p, u64p]
         L.ref_apply_reorder.restype = c_vp
+        L.ref_rank_policy.argtypes = [c_vp, c_int, u8p, u32p, c_u32, c_u32, c_u64, c_u32, c_u32, c_double,
+                                      u32p, f64p, C.POINTER(c_u64), C.POINTER(c_double)]
         L.ref_apply_reorder.argtypes = [c_vp, u8p, u32p, c_u32, u32p, u8p, u32p]
         self._handles = {}
 
@@ -570,6 +572,17 @@ class Ref:
         ranges = np.zeros(2 * K, np.uint64)
         self._check(self.lib.ref_build_reorder(labels, n, K, s, oon, ranges))
         return oon, ranges.reshape(K, 2)
+
+    def rank_policy(self, g: CSR, which, roles, labels, K, k, L=0, f1=1, iters=5, damping=0.85):
+        """rank_degree (0) / rank_halo_1hop (1) / rank_wpr (2) / rank_numpaths (3)
+        (policies.cpp:57-132) -> (order, score, effective_alpha)."""
+        order = np.zeros(g.n, np.uint32)
+        score = np.zeros(g.n, np.float64)
+        cnt, ea = c_u64(), c_double()
+        self._check(self.lib.ref_rank_policy(self._graph(g), which, np.ascontiguousarray(roles, np.uint8),
+                                             _a32(labels), K, k, L, f1, iters, damping, order, score,
+                                             C.byref(cnt), C.byref(ea)))
+        return order[:cnt.value], score[:cnt.value], ea.value
 
     def apply_reorder(self, g: CSR, roles, labels, K, old_of_new):
         """apply_reorder (reorder.cpp:36-70) -> (CSR incl. reverse, roles, labels)."""

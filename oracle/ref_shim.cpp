@@ -426,6 +426,30 @@ int ref_simulate(void* gp, const std::uint8_t* roles, const std::uint32_t* label
   });
 }
 
+// Baseline rankings (policies.cpp:57-132). which: 0 degree (L), 1 halo,
+// 2 wpr (TransitionModel{f1}, iters, damping), 3 numpaths (L).
+int ref_rank_policy(void* gp, int which, const std::uint8_t* roles, const std::uint32_t* labels, std::uint32_t K,
+                    std::uint32_t k, std::uint64_t L, std::uint32_t f1, std::uint32_t iters, double damping,
+                    std::uint32_t* order, double* score, std::uint64_t* count, double* eff_alpha) {
+  return guard([&] {
+    const Graph& g = *static_cast<Graph*>(gp);
+    const std::uint64_t n = g.num_vertices();
+    const PartitionMap part = make_part(labels, n, K);
+    const VertexRoles r = make_roles_view(roles, n);
+    Ranking rk;
+    if (which == 0) rk = rank_degree(g, r, part, k, L);
+    else if (which == 1) rk = rank_halo_1hop(g, part, k);
+    else if (which == 2)
+      rk = rank_wpr(g, r, part, k, TransitionModel{TransitionModel::Kind::uniform_fanout, FanoutSpec{{f1}}}, iters,
+                    damping);
+    else rk = rank_numpaths(g, r, part, k, L);
+    std::memcpy(order, rk.order.data(), rk.order.size() * 4);
+    std::memcpy(score, rk.score.data(), rk.score.size() * 8);
+    *count = rk.order.size();
+    *eff_alpha = rk.effective_alpha;
+  });
+}
+
 // ---- reorder ----
 int ref_build_reorder(const std::uint32_t* labels, std::uint64_t n, std::uint32_t K,
                       const double* scores /* K*n */, std::uint32_t* old_of_new,

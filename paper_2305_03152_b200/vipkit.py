@@ -123,6 +123,12 @@ def lib():
     L.vk_sampler_snapshot_counts.argtypes = [c_vp, c_vp, C.POINTER(c_u64), c_vp]
     L.vk_rank_by_scores.argtypes = [c_int, c_u64, u32p, c_u32, f64p, c_u64, u32p, f64p, C.POINTER(c_u64)]
     L.vk_cache_capacity.argtypes = [c_double, c_u64, c_u32, C.POINTER(c_u64)]
+    L.vk_rank_degree.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u32, u32p, f64p, C.POINTER(c_u64)]
+    L.vk_rank_halo_1hop.argtypes = [c_vp, u32p, c_u32, c_u32, u32p, f64p, C.POINTER(c_u64),
+                                    C.POINTER(c_double)]
+    L.vk_rank_wpr.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u32, c_u32, c_double, u32p, f64p,
+                              C.POINTER(c_u64)]
+    L.vk_rank_numpaths.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u32, u32p, f64p, C.POINTER(c_u64)]
     L.vk_build_reorder.argtypes = [c_int, c_u64, c_u32, u32p, f64p, u32p, u64p]
     L.vk_plane_create.argtypes = [c_int, c_u64, c_u32, c_u32, c_int, u32p, u32p, u64p, C.POINTER(c_vp)]
     L.vk_plane_destroy.argtypes = [c_vp]
@@ -507,6 +513,40 @@ def rank_by_scores(part_of, k, scores, device=0):
     cnt = c_u64()
     check(lib().vk_rank_by_scores(device, n, part_of, k, scores, len(scores), order, sc, C.byref(cnt)))
     return order[:cnt.value], sc[:cnt.value]
+
+
+def _ranked(fn, g, *args):
+    order = np.zeros(g.n, np.uint32)
+    sc = np.zeros(g.n, np.float64)
+    cnt = c_u64()
+    fn(*args, order, sc, C.byref(cnt))
+    return order[:cnt.value], sc[:cnt.value]
+
+
+def rank_degree(g: Graph, roles, part_of, K, k, L):
+    """vipkit::rank_degree (policies.hpp:28-29) -> (order, score)."""
+    return _ranked(lambda *a: check(lib().vk_rank_degree(g.handle, np.ascontiguousarray(roles, np.uint8),
+                                                         _a32(part_of), K, k, L, *a)), g)
+
+
+def rank_halo_1hop(g: Graph, part_of, K, k):
+    """vipkit::rank_halo_1hop (policies.hpp:32) -> (order, score, effective_alpha)."""
+    ea = c_double()
+    o, sc = _ranked(lambda *a: check(lib().vk_rank_halo_1hop(g.handle, _a32(part_of), K, k, *a, C.byref(ea))), g)
+    return o, sc, ea.value
+
+
+def rank_wpr(g: Graph, roles, part_of, K, k, hop1_fanout, iters=5, damping=0.85):
+    """vipkit::rank_wpr (policies.hpp:38-40), TransitionModel of fanout
+    hop1_fanout at hop 1 -> (order, score)."""
+    return _ranked(lambda *a: check(lib().vk_rank_wpr(g.handle, np.ascontiguousarray(roles, np.uint8),
+                                                      _a32(part_of), K, k, hop1_fanout, iters, damping, *a)), g)
+
+
+def rank_numpaths(g: Graph, roles, part_of, K, k, L):
+    """vipkit::rank_numpaths (policies.hpp:44-45) -> (order, score)."""
+    return _ranked(lambda *a: check(lib().vk_rank_numpaths(g.handle, np.ascontiguousarray(roles, np.uint8),
+                                                           _a32(part_of), K, k, L, *a)), g)
 
 
 def cache_capacity(alpha, n, K) -> int:

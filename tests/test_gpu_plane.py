@@ -186,3 +186,41 @@ def test_apply_reorder_c3_scale(vk, port):
     s.run([perm[:1024]], [(0, 3, 0)])
     x = port.expand(CSR(n, noff, ntgt), perm[:1024], [15, 10, 5], 42, 0, 3, 0)
     np.testing.assert_array_equal(s.result(0).all_vertices, x.all_vertices)
+
+
+@pytest.mark.parametrize("graph,directed", [("pa5000", False), ("dtree13", True)])
+def test_baseline_rankings_vs_reference(vk, ref, golden, graph, directed):
+    """Fig. 3 baseline rankings (policies.cpp:57-132) on the device: order,
+    scores (f64, incl. wPR's dangling mass on the directed tree) and the
+    halo's effective alpha bit-identical to the live reference."""
+    csr = csr_from(golden("graphs.npz"), graph)
+    n = csr.n
+    rng = np.random.default_rng(11)
+    K = 3
+    labels = (np.arange(n) % K).astype(np.uint32)
+    roles = np.where(rng.random(n) < 0.4, 0, 1).astype(np.uint8)
+    roles[:K] = 0  # every partition has train vertices
+    g = (vk.Graph.from_csr(csr.off, csr.tgt, validate=True) if directed
+         else vk.Graph.from_csr(csr.off, csr.tgt, undirected=True))
+    for k in range(K):
+        for L in (1, 2, 3):
+            o, s = vk.rank_degree(g, roles, labels, K, k, L)
+            eo, es, _ = ref.rank_policy(csr, 0, roles, labels, K, k, L=L)
+            np.testing.assert_array_equal(o, eo)
+            np.testing.assert_array_equal(s, es)
+            o, s = vk.rank_numpaths(g, roles, labels, K, k, L)
+            eo, es, _ = ref.rank_policy(csr, 3, roles, labels, K, k, L=L)
+            np.testing.assert_array_equal(o, eo)
+            np.testing.assert_array_equal(s, es)
+        o, s, ea = vk.rank_halo_1hop(g, labels, K, k)
+        eo, es, eea = ref.rank_policy(csr, 1, roles, labels, K, k)
+        np.testing.assert_array_equal(o, eo)
+        np.testing.assert_array_equal(s, es)
+        assert ea == eea
+        for f1, iters, d in ((2, 5, 0.85), (10, 3, 0.5)):
+            o, s = vk.rank_wpr(g, roles, labels, K, k, f1, iters, d)
+            eo, es, _ = ref.rank_policy(csr, 2, roles, labels, K, k, f1=f1, iters=iters, damping=d)
+            np.testing.assert_array_equal(o, eo)
+            np.testing.assert_array_equal(s, es)
+    with pytest.raises(vk.ParameterError):
+        vk.rank_wpr(g, roles, labels, K, 0, 2, 0)
