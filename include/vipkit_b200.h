@@ -312,6 +312,12 @@ VK_API int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of
                        uint64_t global_seed, const uint32_t* seed_keys, const uint32_t* cached_ids,
                        const uint64_t* cached_offsets,
                        const uint64_t* takes, uint32_t num_plans, uint32_t wave, uint64_t* cells);
+/* The "oracle" policy's retrospective access counts (sweep pass 1,
+ * commsim.cpp:155-166): counts[k*n + v] = minibatches of partition k over
+ * `epochs` epochs (for_each_expansion order) whose all_vertices contain v. */
+VK_API int vk_access_counts(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K,
+                            const uint32_t* fanouts, uint32_t num_hops, uint64_t batch_size, uint64_t epochs,
+                            uint64_t global_seed, double* counts);
 /* vipkit::empirical_vip (vip.hpp:52-55, vip.cpp:85-105), the "sim." policy's
  * estimate: S epochs of partition k's minibatches under
  * SeedSpec::derived(0xC1) through the device sampler; freq[v] = (number of

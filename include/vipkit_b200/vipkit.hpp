@@ -18,7 +18,9 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <limits>
 #include <initializer_list>
 #include <memory>
 #include <span>
@@ -533,6 +535,7 @@ struct CommReport {
   double avg_epoch_misses() const {
     return epochs ? static_cast<double>(total_misses()) / static_cast<double>(epochs) : 0.0;
   }
+  double improvement_vs_nocache = std::numeric_limits<double>::quiet_NaN();
 };
 
 namespace detail {
@@ -611,6 +614,113 @@ inline std::vector<CommReport> simulate_alphas(const Graph& g, const VertexRoles
     for (const auto& r : rankings) takes.push_back(std::min<std::uint64_t>(cap, r.order.size()));
   }
   return detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, &takes, alphas, nullptr);
+}
+
+// ---- sweep (commsim.hpp:62-100, commsim.cpp:140-259) --------------------------
+inline const std::vector<std::string> kAllPolicies = {"deg", "1hop", "wpr", "numpaths", "sim", "vip", "oracle"};
+
+struct SweepConfig {
+  std::vector<FanoutSpec> fanouts;
+  std::uint64_t batch_size = 0;
+  std::uint64_t epochs = 0;
+  std::vector<double> alphas;
+  std::vector<std::string> policies;
+  SeedSpec seeds;
+  std::uint64_t sim_epochs = 2;  // epochs behind the "sim" policy estimate
+};
+
+struct SweepResult {
+  std::vector<CommReport> reports;
+  struct Geomean {
+    std::string policy;
+    double alpha;
+    double geomean_improvement;
+  };
+  std::vector<Geomean> geomeans;
+};
+
+inline double geometric_mean(std::span<const double> xs) {  // commsim.cpp:129-138
+  if (xs.empty()) throw parameter_error("geometric mean of empty set");
+  double log_sum = 0.0;
+  for (double x : xs) {
+    if (std::isinf(x)) return x;
+    if (!(x > 0)) throw parameter_error("geometric mean needs positive values");
+    log_sum += std::log(x);
+  }
+  return std::exp(log_sum / static_cast<double>(xs.size()));
+}
+
+/// The policy x alpha x fanout grid on the device: every ranking, the
+/// oracle's access counts and each policy's alpha axis (vk_simulate) run on
+/// the GPU; expansions are identical across plans by construction.
+inline SweepResult sweep(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
+                         const SweepConfig& cfg) {
+  if (cfg.fanouts.empty() || cfg.alphas.empty() || cfg.policies.empty())
+    throw parameter_error("sweep needs non-empty fanout, alpha, and policy grids");
+  for (const auto& p : cfg.policies)
+    if (std::find(kAllPolicies.begin(), kAllPolicies.end(), p) == kAllPolicies.end())
+      throw parameter_error("unknown policy: " + p);
+  const std::size_t n = g.num_vertices();
+  SweepResult result;
+  std::vector<std::vector<std::vector<double>>> improvements(
+      cfg.policies.size(), std::vector<std::vector<double>>(cfg.alphas.size()));
+  for (const FanoutSpec& fanouts : cfg.fanouts) {
+    fanouts.validate();
+    const std::size_t L = fanouts.hops();
+    const TransitionModel tm{TransitionModel::Kind::uniform_fanout, fanouts};
+    std::vector<double> access;
+    if (std::find(cfg.policies.begin(), cfg.policies.end(), "oracle") != cfg.policies.end()) {
+      access.resize(part.K * n);
+      detail::check(vk_access_counts(g.handle(), roles.role.data(), part.part_of.data(), part.K,
+                                     fanouts.fanouts.data(), static_cast<std::uint32_t>(L), cfg.batch_size,
+                                     cfg.epochs, cfg.seeds.global_seed, access.data()));
+    }
+    std::vector<CommReport> reports;
+    for (const std::string& policy : cfg.policies) {
+      std::vector<Ranking> rk;
+      for (std::uint32_t k = 0; k < part.K; ++k) {
+        if (policy == "deg")
+          rk.push_back(rank_degree(g, roles, part, k, L));
+        else if (policy == "1hop")
+          rk.push_back(rank_halo_1hop(g, part, k));
+        else if (policy == "wpr")
+          rk.push_back(rank_wpr(g, roles, part, k, tm));
+        else if (policy == "numpaths")
+          rk.push_back(rank_numpaths(g, roles, part, k, L));
+        else if (policy == "sim")
+          rk.push_back(rank_by_scores(
+              part, k, empirical_vip(g, roles, part, k, cfg.batch_size, fanouts, cfg.sim_epochs, cfg.seeds),
+              g.device));
+        else if (policy == "vip")
+          rk.push_back(rank_by_scores(
+              part, k, propagate(g, tm, initial_probs(roles, part, k, cfg.batch_size), k).total, g.device));
+        else  // oracle
+          rk.push_back(rank_by_scores(part, k, std::span<const double>(access.data() + k * n, n), g.device));
+      }
+      auto r = simulate_alphas(g, roles, part, fanouts, cfg.batch_size, cfg.epochs, cfg.seeds, rk, cfg.alphas);
+      for (auto& x : r) x.policy = policy;
+      reports.insert(reports.end(), r.begin(), r.end());
+    }
+    // no-cache baseline: every cache hit of any report is a miss without it
+    const std::uint64_t base = reports[0].total_cache_hits() + reports[0].total_misses();
+    for (std::size_t p = 0; p < cfg.policies.size(); ++p)
+      for (std::size_t a = 0; a < cfg.alphas.size(); ++a) {
+        CommReport& r = reports[p * cfg.alphas.size() + a];
+        const auto misses = r.total_misses();
+        if (base == 0)
+          r.improvement_vs_nocache = 1.0;
+        else if (misses == 0)
+          r.improvement_vs_nocache = std::numeric_limits<double>::infinity();
+        else
+          r.improvement_vs_nocache = static_cast<double>(base) / static_cast<double>(misses);
+        improvements[p][a].push_back(r.improvement_vs_nocache);
+        result.reports.push_back(std::move(r));
+      }
+  }
+  for (std::size_t p = 0; p < cfg.policies.size(); ++p)
+    for (std::size_t a = 0; a < cfg.alphas.size(); ++a)
+      result.geomeans.push_back({cfg.policies[p], cfg.alphas[a], geometric_mean(improvements[p][a])});
+  return result;
 }
 
 // ---- reorder.hpp:15-26 --------------------------------------------------------

@@ -341,4 +341,47 @@ int vk_empirical_vip(vk_graph g, const uint8_t* roles, const uint32_t* part_of, 
   });
 }
 
+// The oracle policy's retrospective access counts (sweep pass 1,
+// commsim.cpp:155-166): counts[k*n + v] = number of minibatches of partition k
+// over the epochs whose all_vertices contain v.
+int vk_access_counts(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, const uint32_t* fanouts,
+                     uint32_t num_hops, uint64_t batch_size, uint64_t epochs, uint64_t global_seed,
+                     double* counts) {
+  return guard([&] {
+    if (!g || !roles || !part_of || !fanouts || !counts) raise(VK_ERR_PARAMETER, "null argument");
+    if (K == 0) raise(VK_ERR_PARAMETER, "need at least one partition");
+    if (batch_size == 0) raise(VK_ERR_PARAMETER, "batch size must be >= 1");
+    const std::uint64_t n = g->n;
+    for (std::uint64_t v = 0; v < n; ++v)
+      if (part_of[v] >= K) raise(VK_ERR_FORMAT, "partition label out of range");
+    DeviceGuard dg(g->device);
+    DevBuf hits(std::max<std::uint64_t>(1, (std::uint64_t)K * n * 4));
+    VK_CUDA(cudaMemset(hits.p, 0, hits.bytes));
+    VK_CUDA(cudaDeviceSynchronize());
+    std::vector<std::uint32_t> parts(K);
+    for (std::uint32_t k = 0; k < K; ++k) parts[k] = k;
+    stream_expansions(g, roles, part_of, K, parts, fanouts, num_hops, batch_size, epochs, global_seed, nullptr, 128u,
+                      [&](const std::uint32_t* all, std::uint64_t stride, const std::uint32_t* count,
+                          std::uint32_t nmb, const std::uint32_t* cell_of, cudaStream_t st) {
+                        // minibatches of one wave may belong to several partitions
+                        std::uint32_t i = 0;
+                        while (i < nmb) {
+                          const std::uint32_t k = cell_of[i] % K;
+                          std::uint32_t j = i;
+                          while (j < nmb && cell_of[j] % K == k) ++j;
+                          const unsigned gx = (unsigned)std::max<std::uint64_t>(
+                              1, std::min<std::uint64_t>(ceil_div(stride, 256 * 8), 64));
+                          k_histogram<<<dim3(gx, j - i), 256, 0, st>>>(all + i * stride, stride, count + i,
+                                                                      hits.as<unsigned>() + (std::uint64_t)k * n);
+                          count_launch();
+                          VK_LAUNCH_CHECK();
+                          i = j;
+                        }
+                      });
+    std::vector<unsigned> h((std::uint64_t)K * n);
+    if (!h.empty()) VK_CUDA(cudaMemcpy(h.data(), hits.p, h.size() * 4, cudaMemcpyDeviceToHost));
+    for (std::size_t i = 0; i < h.size(); ++i) counts[i] = (double)h[i];
+  });
+}
+
 }  // extern "C"

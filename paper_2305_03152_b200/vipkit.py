@@ -142,6 +142,7 @@ def lib():
     L.vk_simulate.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, c_vp, c_vp, u64p,
                               c_vp, c_u32, c_u32, u64p]
     L.vk_empirical_vip.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u64, u32p, c_u32, c_u64, c_u64, f64p]
+    L.vk_access_counts.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, f64p]
     L.vk_synth_community_powerlaw.argtypes = [c_u64, c_u64, c_u32, c_double, c_u64, C.c_uint,
                                               C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), u32p]
     L.vk_debug_stream_draws.argtypes = [c_int, c_u64, c_u64, c_u64, u64p]
@@ -610,6 +611,16 @@ def simulate(g: Graph, roles, part_of, K, fanouts, b, epochs, seed, cached, take
                             tk.ctypes.data if tk is not None else None, A, wave, cells))
     cells = cells.reshape(A, epochs, K, 3)
     return cells if takes is not None else cells[0]
+
+
+def access_counts(g: Graph, roles, part_of, K, fanouts, b, epochs, seed):
+    """The oracle policy's access counts (commsim.cpp:155-166) -> [K, n] f64."""
+    part_of = _a32(part_of)
+    fan = _a32(fanouts)
+    out = np.zeros(K * len(part_of), np.float64)
+    check(lib().vk_access_counts(g.handle, np.ascontiguousarray(roles, np.uint8), part_of, K, fan, len(fan), b,
+                                 epochs, seed, out))
+    return out.reshape(K, -1)
 
 
 def empirical_vip(g: Graph, roles, part_of, K, k, b, fanouts, S, seed):

@@ -371,6 +371,67 @@ static void test_reorder_and_replay() {
   }
 }
 
+// test_commsim.cpp:139-180: sweep grid determinism, oracle dominance,
+// alpha monotonicity, shared no-cache baseline; plus geometric_mean.
+static void test_sweep_grid() {
+  const std::size_t n = 500;
+  std::vector<std::pair<vertex_t, vertex_t>> e;
+  std::uint64_t x = 4242;
+  for (std::size_t i = 0; i < 4 * n; ++i) {
+    x = x * 6364136223846793005ull + 1442695040888963407ull;
+    const auto a = static_cast<vertex_t>((x >> 33) % n);
+    x = x * 6364136223846793005ull + 1442695040888963407ull;
+    // preferential-ish: half the targets among the first 50 vertices
+    const auto b = static_cast<vertex_t>(((x >> 40) & 1) ? (x >> 13) % 50 : (x >> 13) % n);
+    e.emplace_back(a, b);
+  }
+  const Graph g = from_edges(n, e, true);
+  VertexRoles roles;
+  roles.role.assign(n, 1);
+  for (std::size_t v = 0; v < n; v += 4) roles.role[v] = 0;
+  std::vector<std::uint32_t> labels(n);
+  for (std::size_t v = 0; v < n; ++v) labels[v] = static_cast<std::uint32_t>((v / 7) % 4);
+  const auto part = PartitionMap::from_labels(labels, 4);
+  SweepConfig cfg;
+  cfg.fanouts = {FanoutSpec{{4, 3}}, FanoutSpec{{2, 2}}};
+  cfg.batch_size = 16;
+  cfg.epochs = 4;
+  cfg.alphas = {0.0, 0.1, 0.3};
+  cfg.policies = kAllPolicies;
+  cfg.seeds = SeedSpec{77};
+  const SweepResult a = sweep(g, roles, part, cfg);
+  const SweepResult b = sweep(g, roles, part, cfg);
+  CHECK(a.reports.size() == b.reports.size());
+  CHECK(a.reports.size() == cfg.fanouts.size() * cfg.policies.size() * cfg.alphas.size());
+  for (std::size_t i = 0; i < a.reports.size() && i < b.reports.size(); ++i) {
+    CHECK(a.reports[i].total_misses() == b.reports[i].total_misses());
+    CHECK(a.reports[i].improvement_vs_nocache == b.reports[i].improvement_vs_nocache);
+  }
+  auto find = [&](const std::string& policy, double alpha, const std::string& fl) {
+    for (const CommReport& r : a.reports)
+      if (r.policy == policy && r.alpha == alpha && r.fanout_label == fl) return r;
+    CHECK(false && "report not found");
+    return CommReport{};
+  };
+  for (const std::string& fl : {std::string("4-3"), std::string("2-2")}) {
+    for (double alpha : cfg.alphas) {
+      const auto oracle = find("oracle", alpha, fl);
+      for (const std::string& p : cfg.policies) CHECK(oracle.total_misses() <= find(p, alpha, fl).total_misses());
+    }
+    for (const std::string& p : cfg.policies) {
+      CHECK(find(p, 0.0, fl).total_misses() == find("vip", 0.0, fl).total_misses());
+      CHECK(find(p, 0.0, fl).improvement_vs_nocache == 1.0);
+      CHECK(find(p, 0.3, fl).total_misses() <= find(p, 0.1, fl).total_misses());
+    }
+  }
+  CHECK(a.geomeans.size() == cfg.policies.size() * cfg.alphas.size());
+  const std::vector<double> xs{2.0, 8.0};
+  CHECK(APPROX(geometric_mean(xs), 4.0, 1e-12));
+  CHECK_THROWS_AS(geometric_mean(std::vector<double>{}), parameter_error);
+  cfg.policies = {"nope"};
+  CHECK_THROWS_AS(sweep(g, roles, part, cfg), parameter_error);
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"initial probabilities", test_initial_probabilities},
@@ -385,6 +446,7 @@ int main() {
       {"simulate: 4-path exact expectation", test_commsim_four_path_law},
       {"empirical VIP: saturating ball, 3-path law, determinism", test_empirical_vip},
       {"apply_reorder isomorphism + seed_keys replay invariance", test_reorder_and_replay},
+      {"sweep grid: determinism, oracle dominance, alpha monotonicity", test_sweep_grid},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

@@ -106,3 +106,21 @@ def test_simulate_with_seed_keys_is_reorder_invariant(vk, port, ref):
     np.testing.assert_array_equal(before[..., 2], after[..., 2])
     exp = ref.simulate(CSR(n, noff, ntgt), r2, l2, K, [3, 2], 8, 3, 2024, empty, seed_keys=oon)
     np.testing.assert_array_equal(after, exp)
+
+
+def test_access_counts_vs_reference_expansions(vk, port, ref, golden):
+    """The oracle policy's access counts (commsim.cpp:155-166) equal a
+    histogram of the reference's own expansions in for_each_expansion order."""
+    pol = golden("policy.npz")
+    csr = port.generate("pa", 400, 4, 15)
+    roles, labels = pol["roles"], pol["labels"]
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    got = vk.access_counts(g, roles, labels, 4, [4, 3], 16, 3, 77)
+    exp = np.zeros((4, 400))
+    for e in range(3):
+        for k in range(4):
+            perm = ref.epoch_permutation(roles, labels, k, 16, e, 77, K=4)
+            for i in range((len(perm) + 15) // 16):
+                x = ref.expand(csr, perm[i * 16:(i + 1) * 16], [4, 3], 77, e, k, i, with_mfg=False)
+                exp[k, x.all_vertices] += 1
+    np.testing.assert_array_equal(got, exp)
