@@ -205,6 +205,7 @@ struct GatherParams {
   const unsigned long long* ubits;
   const std::uint32_t* uprefix;
   const char* staging;
+  int st_variant;  // VK_GATHER_ST: 0 .cs (evict-first), 1 plain, 2 L1::no_allocate
   int ld_variant;  // VK_GATHER_LD: 0 nc/no_allocate, 1 +L2 evict_last policy, 2 +evict_normal, 3 coherent
 };
 
@@ -254,10 +255,18 @@ __device__ __forceinline__ T ld_stream(const T* p, int variant = 0) {
   }
 }
 template <class T>
-__device__ __forceinline__ void st_stream(T* p, const T& v) {
+__device__ __forceinline__ void st_stream(T* p, const T& v, int variant = 0) {
   if constexpr (sizeof(T) == 16) {
-    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
+    if (variant == 1)
+      asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
+    else if (variant == 2)
+      asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                   "r"(v.w)
+                   : "memory");
+    else
+      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
   } else {
     __stcs(p, v);
   }
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
         const std::uint32_t e = e0 + 32 * u;
         if (e < total) {
           const std::uint32_t row = V == 1 ? e : __umulhi(e, magic);
-          st_stream(dst + (std::uint64_t)s_row[w][row] * V + (e - row * V), val[u]);
+          st_stream(dst + (std::uint64_t)s_row[w][row] * V + (e - row * V), val[u], p.st_variant);
         }
       }
     }
@@ -941,6 +950,11 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       return e ? std::atoi(e) : 1;
     }();
     gp.ld_variant = ld_variant;
+    static const int st_variant = [] {
+      const char* e = std::getenv("VK_GATHER_ST");
+      return e ? std::atoi(e) : 0;
+    }();
+    gp.st_variant = st_variant;
     gp.nmb = nmb;
     static const std::uint32_t tile_words = [] {
       const char* e = std::getenv("VK_GATHER_TILE_WORDS");
