@@ -205,8 +205,11 @@ def run_b200(args, cfg):
     W, S = args.warmup, args.steps
     sched = schedule(vk, cfg, roles, labels, mine, (W + 2 * S) * M)
     waves = [sched[i * M:(i + 1) * M] for i in range(W + 2 * S)]
-    P = args.pipes
-    samplers = [vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED) for _ in range(P)]
+    # multi-GPU: two samplers alternate so wave i+1 samples while wave i's
+    # NVLink miss exchange runs (vk_plane_prefetch on the plane's aux stream)
+    prefetch = (world > 1) if args.prefetch == "auto" else args.prefetch == "1"
+    P = 1 if prefetch else args.pipes
+    samplers = [vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED) for _ in range(2 if prefetch else P)]
     view = samplers[0].view()
     cap_all = view.all_stride
     rb = plane.row_bytes
@@ -223,7 +226,8 @@ def run_b200(args, cfg):
     cw = samplers[0].count_words()
     hist_counts = torch.zeros((W + 2 * S, cw), dtype=torch.int32, device=f"cuda:{dev}")
     hist_tally = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64, device=f"cuda:{dev}")
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(W + 2 * S)]
+    # per wave: sampler start/end, gather start/end
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(W + 2 * S)]
 
     def wave(i, host=False, pinned=None):
         # wave i runs on pipe i % P: sampler and gather of consecutive waves
@@ -239,20 +243,53 @@ def run_b200(args, cfg):
         else:
             sp.run(wave_offsets[i], refs, stream=sh_p, seeds_device_ptr=seeds_d.data_ptr())
         evs[i][1].record(st)
-        plane.gather(sp, outs[p].data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh_p)
         evs[i][2].record(st)
+        plane.gather(sp, outs[p].data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh_p)
+        evs[i][3].record(st)
         sp.snapshot_counts(hist_counts[i].data_ptr(), stream=sh_p)
         if pinned is not None:
             with torch.cuda.stream(st):
                 pinned[i].copy_(hist_tally[i], non_blocking=True)
+
+    def sample(i, host):
+        sp = samplers[i % 2]
+        wv = waves[i]
+        refs = [(e, k, bi) for (e, k, bi, _) in wv]
+        evs[i][0].record(stream)
+        if host:
+            sp.run([w[3] for w in wv], refs, stream=sh)
+        else:
+            sp.run(wave_offsets[i], refs, stream=sh, seeds_device_ptr=seeds_d.data_ptr())
+        evs[i][1].record(stream)
+
+    def waves_prefetch(lo, hi, host, pinned):
+        # main: S(i+1) G(i) S(i+2) G(i+1) ...; aux: the NVLink exchange of
+        # wave i+1 (issued after S(i+1)) runs during the HBM-bound G(i)
+        sample(lo, host)
+        plane.prefetch(samplers[lo % 2])
+        for i in range(lo, hi):
+            sp = samplers[i % 2]
+            if i + 1 < hi:
+                sample(i + 1, host)
+                plane.prefetch(samplers[(i + 1) % 2])
+            evs[i][2].record(stream)
+            plane.gather(sp, outs[0].data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh)
+            evs[i][3].record(stream)
+            sp.snapshot_counts(hist_counts[i].data_ptr(), stream=sh)
+            if pinned is not None:
+                with torch.cuda.stream(stream):
+                    pinned[i].copy_(hist_tally[i], non_blocking=True)
 
     def region(lo, hi, host=False, pinned=None):
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for st in streams[1:]:
             st.wait_event(t0)
-        for i in range(lo, hi):
-            wave(i, host, pinned)
+        if prefetch:
+            waves_prefetch(lo, hi, host, pinned)
+        else:
+            for i in range(lo, hi):
+                wave(i, host, pinned)
         for st in streams[1:]:
             e = torch.cuda.Event()
             e.record(st)
@@ -280,7 +317,7 @@ def run_b200(args, cfg):
     # ---- roofline of the dominant kernel (gather) and of the sampler, from the timed waves
     tally = hist_tally.cpu().numpy()
     cnts = hist_counts.cpu().numpy().view(np.uint32)
-    gather_ms = [evs[i][1].elapsed_time(evs[i][2]) for i in range(W, W + S)]
+    gather_ms = [evs[i][2].elapsed_time(evs[i][3]) for i in range(W, W + S)]
     sample_ms = [evs[i][0].elapsed_time(evs[i][1]) for i in range(W, W + S)]
     g_bytes, s_bytes, rows, misses, peer, cache_hits = 0, 0, 0, 0, 0, 0
     for i in range(W, W + S):
@@ -300,7 +337,7 @@ def run_b200(args, cfg):
     # shared by minibatches of a wave are L2 hits, not HBM reads). The
     # distinct count comes from the last wave still held by its sampler.
     last = W + 2 * S - 1
-    distinct = distinct_rows(samplers[last % P], len(waves[last]), dev)
+    distinct = distinct_rows(samplers[last % len(samplers)], len(waves[last]), dev)
     rows_last = int(tally[last, :len(waves[last]), :3].sum())
     g_bytes = int(rows / S * (rb + 4) + distinct * rb) * S
     hbm, peak_kind = peaks()
@@ -324,6 +361,7 @@ def run_b200(args, cfg):
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 ids / fp32 rows / fp64 VIP",
         "data": "synthetic (community power-law graph, counter-hashed feature rows)",
         "config": {"workload": cfg["workload"], "n": n, "m_slots": m, "partitions": K, "pipes": P,
+                   "exchange_prefetch": bool(prefetch),
                    "fanouts": list(cfg["fanouts"]), "batch": cfg["b"], "minibatches_per_step_per_gpu": M,
                    "feature_dim": cfg["dim"], "row_bytes": rb, "alpha": cfg["alpha"],
                    "partitions_per_gpu": len(mine), "l2": "inputs larger than L2 (graph "
@@ -578,6 +616,8 @@ def main():
     ap.add_argument("--wave", type=int, default=None,
                     help="minibatches per step per GPU (default: the config's; 128 for c1-c3, 32 for c4)")
     ap.add_argument("--pipes", type=int, default=1, help="overlapped sampler+gather pipelines (streams)")
+    ap.add_argument("--prefetch", default="auto", choices=["auto", "0", "1"],
+                    help="overlap the multi-GPU miss exchange with the next wave's sampling (auto: on for N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

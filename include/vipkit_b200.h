@@ -287,6 +287,13 @@ VK_API int vk_plane_attach(vk_plane p, uint32_t k, const void* handle64, uint64_
 VK_API int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_rows,
                            uint64_t* counts_dev, vk_stream_t stream);
 VK_API int vk_plane_row_bytes(vk_plane p, uint64_t* row_bytes);
+/* Multi-GPU: issue the miss exchange (remote-miss union, NVLink pull into
+ * staging) of sampler s's last run now, on the plane's auxiliary stream
+ * (after the sampler's work), so it overlaps whatever the caller queues next
+ * (e.g. the next wave's vk_sampler_run on a second sampler); the following
+ * vk_plane_gather of that run waits for it instead of exchanging again.
+ * No-op without attached peer partitions. */
+VK_API int vk_plane_prefetch(vk_plane p, vk_sampler s);
 /* Distinct remote rows the last multi-GPU gather pulled over NVLink (the
  * wave's deduplicated miss exchange); synchronises the device. */
 VK_API int vk_plane_pulled_rows(vk_plane p, uint64_t* rows);

@@ -33,6 +33,7 @@ void sampler_internal(vk_sampler_s* s, const std::uint32_t** all, std::uint64_t*
 std::uint64_t sampler_desc_stride();
 void sampler_all_rank(vk_sampler_s* s, const uint4** rank, std::uint64_t* W);
 bool sampler_all_rank_dense(vk_sampler_s* s);
+std::uint64_t sampler_run_id(vk_sampler_s* s);
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out);
 cudaEvent_t sampler_done_event(vk_sampler_s* s);
 }  // namespace vk
@@ -70,6 +71,13 @@ struct vk_plane_s {
     vk::DevBuf ubits, uprefix, ulist, staging, scan_tmp;
     vk::DevBuf vbits;  // vertex-space union (word mark); cleared as consumed
     std::size_t scan_bytes = 0;
+    // vk_plane_prefetch: the exchange of sampler run `prefetched` was issued
+    // on the aux stream and completes at `ready`
+    std::uint64_t prefetched = ~0ull;
+    cudaEvent_t ready = nullptr;
+    ~StageSet() {
+      if (ready) cudaEventDestroy(ready);
+    }
   };
   // one set per sampler, so overlapped waves (one sampler per pipeline
   // stream) never share staging
@@ -685,7 +693,15 @@ int vk_plane_create(int device, uint64_t n, uint32_t K, uint32_t dim, int dtype,
       p->old_of_new.assign(old_of_new, old_of_new + n);
       p->parts.resize(K);
       VK_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-      VK_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+      {
+        // the aux stream (miss exchange) runs at the highest priority: its
+        // CTAs take SM slots as soon as the running gather's retire, so a
+        // prefetched exchange overlaps the HBM-bound gather instead of
+        // waiting for it to drain
+        int lo = 0, hi = 0;
+        VK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        VK_CUDA(cudaStreamCreateWithPriority(&p->aux, cudaStreamNonBlocking, hi));
+      }
       VK_CUDA(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
       VK_CUDA(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
       p->part_of.alloc(n * 4);
@@ -893,10 +909,18 @@ int vk_plane_row_bytes(vk_plane p, uint64_t* row_bytes) {
   });
 }
 
-int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_rows, uint64_t* counts_dev,
-                    vk_stream_t stream) {
-  return guard([&] {
-    if (!p || !s || !out_dev || !counts_dev) raise(VK_ERR_PARAMETER, "null argument");
+}  // extern "C"
+
+namespace {
+
+// The classify + gather of a sampler's last wave (prefetch_only = false), or
+// only its multi-GPU miss exchange, issued on the plane's aux stream so it
+// overlaps whatever the caller queues next (prefetch_only = true; a later
+// gather of the same run then waits for it instead of exchanging again).
+void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_rows, uint64_t* counts_dev,
+                 vk_stream_t stream, bool prefetch_only) {
+  {
+    if (!p || !s || (!prefetch_only && (!out_dev || !counts_dev))) raise(VK_ERR_PARAMETER, "null argument");
     GatherParams gp{};
     std::uint32_t nmb = 0;
     vk_graph_s* g = nullptr;
@@ -916,9 +940,10 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       if (!p->parts[k].resident && !p->parts[k].attached)
         raise(VK_ERR_CONFIG, "partition " + std::to_string(k) + " is neither resident nor attached");
     DeviceGuard dg(p->device);
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : (last ? last : p->stream);
+    cudaStream_t st = prefetch_only ? p->aux
+                                    : (stream ? static_cast<cudaStream_t>(stream) : (last ? last : p->stream));
     if (st != last) VK_CUDA(cudaStreamWaitEvent(st, sampler_done_event(s), 0));
-    VK_CUDA(cudaMemsetAsync(counts_dev, 0, (std::uint64_t)nmb * 4 * 8, st));
+    if (!prefetch_only) VK_CUDA(cudaMemsetAsync(counts_dev, 0, (std::uint64_t)nmb * 4 * 8, st));
     gp.desc = reinterpret_cast<const char*>(parts);
     gp.desc_stride = sampler_desc_stride();
     gp.base = reinterpret_cast<const char* const*>(p->d_base.p);
@@ -936,6 +961,9 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
     gp.counts = reinterpret_cast<unsigned long long*>(counts_dev);
     const bool v16 = (p->row_bytes % 16 == 0) && ((std::uintptr_t)out_dev % 16 == 0);
     const bool v4 = (p->row_bytes % 4 == 0) && ((std::uintptr_t)out_dev % 4 == 0);
+    // staged rows are plain rows of row_bytes in cudaMalloc'd memory: the
+    // pull's vector width depends on the row size only
+    const bool pv16 = p->row_bytes % 16 == 0, pv4 = p->row_bytes % 4 == 0;
     const std::uint64_t esz = v16 ? 16 : (v4 ? 4 : 2);
     gp.V = (std::uint32_t)(p->row_bytes / esz);
     if (gp.V >= (1u << 15)) raise(VK_ERR_UNSUPPORTED, "feature rows above 512 KiB are not supported");
@@ -1021,7 +1049,23 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       for (auto& e : tev) VK_CUDA(cudaEventCreate(&e));
       VK_CUDA(cudaEventRecord(tev[0], xs));
     }
-    if (staged) {
+    if (prefetch_only && !staged) return;  // nothing to exchange on one GPU
+    auto& ss = p->stage_sets[static_cast<const void*>(s)];
+    const std::uint64_t run = sampler_run_id(s);
+    const bool have_prefetch = staged && !prefetch_only && ss.prefetched == run;
+    if (have_prefetch) {
+      VK_CUDA(cudaStreamWaitEvent(st, ss.ready, 0));
+      ss.prefetched = ~0ull;
+      p->last_set = &ss;
+      gp.ubits = ss.ubits.as<unsigned long long>();
+      gp.uprefix = ss.uprefix.as<std::uint32_t>();
+      gp.staging = ss.staging.as<char>();
+    }
+    if (timing && have_prefetch) {
+      VK_CUDA(cudaEventRecord(tev[1], xs));
+      VK_CUDA(cudaEventRecord(tev[2], xs));
+    }
+    if (staged && !have_prefetch) {
       // miss exchange: union of the wave's remote misses -> distinct list ->
       // one NVLink pull per distinct row into local staging -> the gather
       // reads staged rows from HBM
@@ -1029,7 +1073,6 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       auto ensure = [](DevBuf& b, std::size_t bytes) {
         if (b.bytes < bytes) b.alloc(bytes);
       };
-      auto& ss = p->stage_sets[static_cast<const void*>(s)];
       p->last_set = &ss;
       ensure(ss.ubits, W * 8);
       ensure(ss.uprefix, (W + 1) * 4);
@@ -1076,11 +1119,13 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
         const char* e = std::getenv("VK_PULL_CTAS_PER_SM");
         return e && std::atoi(e) > 0 ? (unsigned)std::atoi(e) : 0u;
       }();
-      const unsigned pg = (unsigned)sm_count(p->device) * (pull_per_sm ? pull_per_sm : (overlap ? 2 : 8));
-      if (v16)
+      // prefetched exchanges share the SMs with a running gather: 2 CTAs/SM
+      const unsigned pg =
+          (unsigned)sm_count(p->device) * (pull_per_sm ? pull_per_sm : ((overlap || prefetch_only) ? 2 : 8));
+      if (pv16)
         k_remote_pull<uint4, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
                                                      ss.uprefix.as<std::uint32_t>() + W, ss.staging.as<uint4>());
-      else if (v4)
+      else if (pv4)
         k_remote_pull<std::uint32_t, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
                                                              ss.uprefix.as<std::uint32_t>() + W,
                                                              ss.staging.as<std::uint32_t>());
@@ -1093,6 +1138,15 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       gp.ubits = ss.ubits.as<unsigned long long>();
       gp.uprefix = ss.uprefix.as<std::uint32_t>();
       gp.staging = ss.staging.as<char>();
+      if (prefetch_only) {
+        if (!ss.ready) VK_CUDA(cudaEventCreateWithFlags(&ss.ready, cudaEventDisableTiming));
+        VK_CUDA(cudaEventRecord(ss.ready, xs));
+        ss.prefetched = run;
+        if (timing) {
+          for (auto& e : tev) VK_CUDA(cudaEventDestroy(e));
+        }
+        return;
+      }
     }
     auto launch = [&](int mode, cudaStream_t where) {
       if (v16) {
@@ -1153,7 +1207,20 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
       ++t_calls;
       for (auto& e : tev) VK_CUDA(cudaEventDestroy(e));
     }
-  });
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_rows, uint64_t* counts_dev,
+                    vk_stream_t stream) {
+  return guard([&] { gather_impl(p, s, out_dev, out_stride_rows, counts_dev, stream, false); });
+}
+
+int vk_plane_prefetch(vk_plane p, vk_sampler s) {
+  return guard([&] { gather_impl(p, s, nullptr, 0, nullptr, nullptr, true); });
 }
 
 }  // extern "C"

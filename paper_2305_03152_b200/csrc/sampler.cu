@@ -77,6 +77,7 @@ struct vk_sampler_s {
   // scratch, sampling.cpp:83-85)
   vk::DevBuf keys, tgt_keyed;
   bool keyed = false;
+  std::uint64_t runs = 0;  // completed vk_sampler_run calls (plane prefetch bookkeeping)
 
   std::uint32_t* fcount(std::uint32_t h) const { return counts.as<std::uint32_t>() + (std::uint64_t)h * M; }
   std::uint32_t* ecount(std::uint32_t h) const {
@@ -1276,6 +1277,7 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
     VK_LAUNCH_CHECK();
     VK_CUDA(cudaEventRecord(s->done, st));
     s->last_nmb = nmb;
+    ++s->runs;
     s->last_stream = st;
     s->last_parts.resize(nmb);
     for (std::uint32_t i = 0; i < nmb; ++i) s->last_parts[i] = refs[i].partition;
@@ -1441,6 +1443,7 @@ void sampler_all_rank(vk_sampler_s* s, const uint4** rank, std::uint64_t* W) {
   *W = s->W;
 }
 bool sampler_all_rank_dense(vk_sampler_s* s) { return s->dense_all_rank; }
+std::uint64_t sampler_run_id(vk_sampler_s* s) { return s->runs; }
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out) { out = s->last_parts; }
 cudaEvent_t sampler_done_event(vk_sampler_s* s) { return s->done; }
 std::uint64_t sampler_capacity_all(vk_sampler_s* s) { return s->capAll; }

@@ -139,6 +139,7 @@ def lib():
     L.vk_plane_gather.argtypes = [c_vp, c_vp, c_vp, c_u64, c_vp, c_vp]
     L.vk_plane_row_bytes.argtypes = [c_vp, C.POINTER(c_u64)]
     L.vk_plane_pulled_rows.argtypes = [c_vp, C.POINTER(c_u64)]
+    L.vk_plane_prefetch.argtypes = [c_vp, c_vp]
     L.vk_simulate.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, c_vp, c_vp, u64p,
                               c_vp, c_u32, c_u32, u64p]
     L.vk_empirical_vip.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u64, u32p, c_u32, c_u64, c_u64, f64p]
@@ -700,6 +701,11 @@ class FeaturePlane:
     def gather(self, sampler: Sampler, out_ptr, out_stride_rows, counts_ptr, stream=0):
         check(lib().vk_plane_gather(self._h, sampler.handle, out_ptr, out_stride_rows, counts_ptr,
                                     stream or None))
+
+    def prefetch(self, sampler: Sampler):
+        """Issue the multi-GPU miss exchange of the sampler's last run now
+        (vk_plane_prefetch); no-op on a single GPU."""
+        check(lib().vk_plane_prefetch(self._h, sampler.handle))
 
     def pulled_rows(self) -> int:
         """Distinct remote rows pulled over NVLink by the last gather."""

@@ -59,6 +59,29 @@ def main():
     out, cnt = C.c_void_p(), C.c_void_p()
     vk.check(vk.lib().vk_device_alloc(local, len(batches) * view.all_stride * plane.row_bytes, C.byref(out)))
     vk.check(vk.lib().vk_device_alloc(local, len(batches) * 32, C.byref(cnt)))
+    ok = check_wave(vk, P, csr, plane, plan, labels, batches, refs, s, out, cnt, dim, local, rank, world,
+                    prefetch=False)
+    # the same wave again, exchange prefetched on the aux stream, into fresh buffers
+    out2, cnt2 = C.c_void_p(), C.c_void_p()
+    vk.check(vk.lib().vk_device_alloc(local, len(batches) * view.all_stride * plane.row_bytes, C.byref(out2)))
+    vk.check(vk.lib().vk_device_alloc(local, len(batches) * 32, C.byref(cnt2)))
+    s.run(batches, refs)
+    ok &= check_wave(vk, P, csr, plane, plan, labels, batches, refs, s, out2, cnt2, dim, local, rank, world,
+                     prefetch=True)
+    for b_ in (out, cnt, out2, cnt2):
+        vk.lib().vk_device_free(b_)
+    flag = torch.tensor([1 if ok else 0])
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    dist.barrier()
+    print(f"rank {rank}: {'ok' if ok else 'FAIL'} ({len(refs)} minibatches x 2)", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if int(flag) == 1 else 1)
+
+
+def check_wave(vk, P, csr, plane, plan, labels, batches, refs, s, out, cnt, dim, local, rank, world, prefetch):
+    view = s.view()
+    if prefetch:
+        plane.prefetch(s)
     plane.gather(s, out.value, view.all_stride, cnt.value)
     counts = np.zeros(len(batches) * 4, np.uint64)
     vk.check(vk.lib().vk_memcpy(counts.ctypes.data, cnt, counts.nbytes, 2))
@@ -85,15 +108,8 @@ def main():
             print(f"rank {rank}: peer rows {counts[i][3]} vs {remote.sum()}", flush=True)
             ok = False
         peer_rows += int(counts[i][3])
-    vk.lib().vk_device_free(out)
-    vk.lib().vk_device_free(cnt)
-    flag = torch.tensor([1 if ok else 0])
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    dist.barrier()
-    print(f"rank {rank}: {'ok' if ok else 'FAIL'} ({len(refs)} minibatches, {peer_rows} rows over NVLink)",
-          flush=True)
-    dist.destroy_process_group()
-    sys.exit(0 if int(flag) == 1 else 1)
+    print(f"rank {rank}: prefetch={prefetch} {'ok' if ok else 'FAIL'} ({peer_rows} rows over NVLink)", flush=True)
+    return ok
 
 
 if __name__ == "__main__":
