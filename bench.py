@@ -208,8 +208,14 @@ def run_b200(args, cfg):
     # multi-GPU: two samplers alternate so wave i+1 samples while wave i's
     # NVLink miss exchange runs (vk_plane_prefetch on the plane's aux stream)
     prefetch = (world > 1) if args.prefetch == "auto" else args.prefetch == "1"
-    P = 1 if prefetch else args.pipes
-    samplers = [vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED) for _ in range(2 if prefetch else P)]
+    overlap = args.sched == "overlap"
+    P = 1 if (prefetch or overlap) else args.pipes
+    samplers = [vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED)
+                for _ in range(2 if (prefetch or overlap) else P)]
+    # overlap schedule: samplers on a high-priority stream, gathers on the
+    # main one, so wave i+1 samples (L2/latency bound) while wave i gathers
+    # (HBM bound); the sampler's CTAs take SM slots as gather CTAs retire
+    hi_stream = torch.cuda.Stream(device=dev, priority=-1) if overlap else None
     view = samplers[0].view()
     cap_all = view.all_stride
     rb = plane.row_bytes
@@ -280,12 +286,43 @@ def run_b200(args, cfg):
                 with torch.cuda.stream(stream):
                     pinned[i].copy_(hist_tally[i], non_blocking=True)
 
+    def waves_overlap(lo, hi, host, pinned):
+        hs = hi_stream.cuda_stream
+        for i in range(lo, hi):
+            sp = samplers[i % 2]
+            wv = waves[i]
+            refs = [(e, k, bi) for (e, k, bi, _) in wv]
+            if i - 2 >= lo:
+                hi_stream.wait_event(evs[i - 2][3])  # same sampler: its gather has read it
+            evs[i][0].record(hi_stream)
+            if host:
+                sp.run([w[3] for w in wv], refs, stream=hs)
+            else:
+                sp.run(wave_offsets[i], refs, stream=hs, seeds_device_ptr=seeds_d.data_ptr())
+            evs[i][1].record(hi_stream)
+            stream.wait_event(evs[i][1])
+            if prefetch:
+                plane.prefetch(sp)
+            evs[i][2].record(stream)
+            plane.gather(sp, outs[0].data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh)
+            evs[i][3].record(stream)
+            sp.snapshot_counts(hist_counts[i].data_ptr(), stream=sh)
+            if pinned is not None:
+                with torch.cuda.stream(stream):
+                    pinned[i].copy_(hist_tally[i], non_blocking=True)
+
     def region(lo, hi, host=False, pinned=None):
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for st in streams[1:]:
             st.wait_event(t0)
-        if prefetch:
+        if overlap:
+            hi_stream.wait_event(t0)
+            waves_overlap(lo, hi, host, pinned)
+            e_hi = torch.cuda.Event()
+            e_hi.record(hi_stream)
+            stream.wait_event(e_hi)
+        elif prefetch:
             waves_prefetch(lo, hi, host, pinned)
         else:
             for i in range(lo, hi):
@@ -349,6 +386,15 @@ def run_b200(args, cfg):
             traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
     except Exception:  # noqa: BLE001
         pass
+    sampler_bound = {"bound": "l2"}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            ts = json.load(f).get(args.config + "_sampler")
+        if ts and ts.get("minibatches_per_launch") == M:
+            sampler_bound.update({"ncu_kernel": ts["kernel"], "ncu_l2_throughput_pct": ts["lts_throughput_pct"],
+                                  "ncu_dram_throughput_pct": ts["dram_throughput_pct"], "note": ts["note"]})
+    except Exception:  # noqa: BLE001
+        pass
     g_ach = g_bytes / S / (statistics.mean(gather_ms) / 1e3) / 1e9
     s_ach = s_bytes / S / (statistics.mean(sample_ms) / 1e3) / 1e9
     total_mb = sum(len(waves[i]) for i in range(W, W + S)) * world
@@ -361,7 +407,7 @@ def run_b200(args, cfg):
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 ids / fp32 rows / fp64 VIP",
         "data": "synthetic (community power-law graph, counter-hashed feature rows)",
         "config": {"workload": cfg["workload"], "n": n, "m_slots": m, "partitions": K, "pipes": P,
-                   "exchange_prefetch": bool(prefetch),
+                   "exchange_prefetch": bool(prefetch), "schedule": args.sched,
                    "fanouts": list(cfg["fanouts"]), "batch": cfg["b"], "minibatches_per_step_per_gpu": M,
                    "feature_dim": cfg["dim"], "row_bytes": rb, "alpha": cfg["alpha"],
                    "partitions_per_gpu": len(mine), "l2": "inputs larger than L2 (graph "
@@ -376,7 +422,7 @@ def run_b200(args, cfg):
                      "peak_kind": peak_kind, "bytes_per_launch": g_bytes / S,
                      "ms_per_launch": statistics.mean(gather_ms)},
         "sampler": {"ms_per_wave": statistics.mean(sample_ms), "achieved_gbs": s_ach,
-                    "frac": s_ach / hbm, "bytes_per_wave": s_bytes / S},
+                    "frac": s_ach / hbm, "bytes_per_wave": s_bytes / S, **sampler_bound},
         "vip": {**vip, "unit": "edges/s", "frac": vip["achieved_gbs"] / hbm},
         "tallies": {"rows": rows, "miss_rows": misses, "miss_rows_no_cache": misses + cache_hits,
                     "miss_reduction_by_vip_cache": 1.0 - misses / max(misses + cache_hits, 1),
@@ -618,6 +664,8 @@ def main():
     ap.add_argument("--pipes", type=int, default=1, help="overlapped sampler+gather pipelines (streams)")
     ap.add_argument("--prefetch", default="auto", choices=["auto", "0", "1"],
                     help="overlap the multi-GPU miss exchange with the next wave's sampling (auto: on for N>1)")
+    ap.add_argument("--sched", default="serial", choices=["serial", "overlap"],
+                    help="overlap: sample wave i+1 on a high-priority stream while wave i gathers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
