@@ -65,6 +65,7 @@ CONFIGS["c5"] = dict(workload="C5 VIP analysis on ogbn-papers100M-shaped 111M no
                               "8 partitions, fanout sweep", n=111_059_956, d=15, K=8, p_in=0.8, train=0.011,
                      b=1024, fanouts=(15, 10, 5),
                      sweep=[(15, 10, 5), (5, 5), (25, 15), (20, 20, 20), (25, 25, 25, 25)])
+RANDOM_READ_GBS = 1400.0  # measured random-record HBM reads, profiles/r01_random_read_bw.txt
 PAPER_VIP_SECONDS = 11.8  # PAPER.md:1760-1763 (papers100M, fanouts 15,10,5, 8x A10G)
 GRAPH_SEED, ROLES_SEED, SAMPLE_SEED, FEATURE_SEED = 7, 3, 42, 1234
 
@@ -517,6 +518,19 @@ def run_vip_sweep(args, cfg):
                      "edge_hops_per_s": K * len(fan) * m / sec})
         log(f"[bench] VIP {fan}: {sec * 1e3:.1f} ms for {K} partitions")
     head = rows[0]
+    # roofline: the pull kernels gather one 32 B sector of hoisted log terms
+    # (float, up to 8 columns per pass) per in-edge per hop from a table far
+    # larger than L2 -> bound by random-record HBM reads, measured at
+    # ~1.4 TB/s on this part (profiles/r01_random_read_bw.txt)
+    passes = (len(mine) + 7) // 8
+    sector_bytes = 3 * m * 32 * passes
+    ach = sector_bytes / head["seconds_all_partitions"] / 1e9
+    formula = 3 * (12 * m + 40 * n) * len(mine)  # SURVEY §8d per hop per column (fp64 lm)
+    roof = {"bound": "hbm-random", "achieved": ach, "peak": RANDOM_READ_GBS, "unit": "GB/s",
+            "frac": ach / RANDOM_READ_GBS, "traffic": None,
+            "peak_kind": "measured random 32-128 B record reads (profiles/r01_random_read_bw.txt)",
+            "algorithmic": "3 hops x m in-edges x one 32 B sector per pass of <= 8 float columns",
+            "survey_formula_gbs": formula / head["seconds_all_partitions"] / 1e9}
     # the paper's 11.8 s produced every partition's VIP on 8 machines in parallel
     paper_rate = K * 3 * 3.2e9 / PAPER_VIP_SECONDS
     if rank == 0:
@@ -531,7 +545,7 @@ def run_vip_sweep(args, cfg):
             "dtype": "fp64 (hoisted log terms stored fp32, accumulation fp64)", "data": "synthetic",
             "config": {"workload": cfg["workload"], "n": n, "m_slots": m, "partitions": K,
                        "partitions_per_gpu": len(mine)},
-            "sweep": rows, "gpu_launches": None}), flush=True)
+            "roofline": roof, "sweep": rows, "gpu_launches": None}), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
