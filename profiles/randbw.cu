@@ -32,6 +32,10 @@ int main() {
   uint4* out; cudaMalloc(&out, 64);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const int per = 64; const int threads = 256; const int blocks = 148 * 64;
+  for (int gran : {128, 64, 32}) {
+  cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+  size_t got = 0; cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+  printf("L2 fetch granularity limit %d (reads back %zu)\n", gran, got);
   for (int rec : {32, 64, 128}) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
@@ -43,6 +47,7 @@ int main() {
       const double moved = (double)blocks * threads * per * rec;
       if (rep == 2) printf("record %3d B: %.1f GB/s useful (%.2f G records/s)\n", rec, moved / ms / 1e6, (double)blocks * threads * per / ms / 1e6);
     }
+  }
   }
   return 0;
 }
