@@ -211,8 +211,8 @@ struct SampleParams {
 __device__ __forceinline__ std::uint64_t vertex_key(const SampleParams& p, std::uint32_t v) {
   return p.keys ? (std::uint64_t)__ldg(p.keys + v) : (std::uint64_t)v;
 }
-__device__ __forceinline__ const std::uint32_t* draw_row(const SampleParams& p, std::uint32_t v) {
-  return (p.keys ? p.tgt_keyed : p.tgt) + p.off[v];
+__device__ __forceinline__ const std::uint32_t* draw_row(const SampleParams& p, std::uint32_t v, std::uint64_t o0) {
+  return (p.keys ? p.tgt_keyed : p.tgt) + o0;
 }
 
 // One thread per frontier vertex; FY state in shared memory (f <= 32) or in
@@ -336,8 +336,11 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
     const std::uint32_t base = ip[j0];
     if (j < cnt) {
       const std::uint32_t v = fp[j];
-      const std::uint32_t deg = p.outdeg[v];
-      const std::uint32_t* nbrs = p.tgt + p.off[v];  // CSR order (the deg <= f case)
+      // degree from the two offsets (same 128 B line but at line ends): one
+      // random DRAM burst per source instead of a second one into outdeg
+      const std::uint64_t o0 = __ldg(p.off + v), o1 = __ldg(p.off + v + 1);
+      const std::uint32_t deg = (std::uint32_t)(o1 - o0);
+      const std::uint32_t* nbrs = p.tgt + o0;  // CSR order (the deg <= f case)
       std::uint32_t* out = stage + (ip[j] - base);
       if (deg <= f) {  // sampling.cpp:76-78: all neighbours, CSR order
         for (std::uint32_t i0 = 0; i0 < deg; i0 += 4) {
@@ -353,10 +356,10 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
         }
       } else if constexpr (FMAX > 0) {
         Stream s(key_step(prefix, vertex_key(p, v)));
-        fy_registers<FMAX>(draw_row(p, v), deg, f, s, out, hb);
+        fy_registers<FMAX>(draw_row(p, v, o0), deg, f, s, out, hb);
       } else {
         Stream s(key_step(prefix, vertex_key(p, v)));
-        nbrs = draw_row(p, v);
+        nbrs = draw_row(p, v, o0);
         for (std::uint32_t i = 0; i < f; ++i) jj[i * S] = i + (std::uint32_t)s.next_below((std::uint64_t)(deg - i));
         for (std::uint32_t i0 = 0; i0 < f; i0 += 4) {
           std::uint32_t a[4], b[4];
@@ -422,8 +425,9 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
     const std::uint32_t v = fp[j];
     Stream s(key_step(prefix, vertex_key(p, v)));
     std::uint32_t lo[MAXF], hp[MAXF], hv[MAXF];
-    const std::uint32_t deg = p.outdeg[v];
-    sample_one(deg <= p.f ? p.tgt + p.off[v] : draw_row(p, v), deg, p.f, s, ed + ip[j], hb, lo, hp, hv, 1);
+    const std::uint64_t o0 = p.off[v];
+    const std::uint32_t deg = (std::uint32_t)(p.off[v + 1] - o0);
+    sample_one(deg <= p.f ? p.tgt + o0 : draw_row(p, v, o0), deg, p.f, s, ed + ip[j], hb, lo, hp, hv, 1);
   }
 }
 
