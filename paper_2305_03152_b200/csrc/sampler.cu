@@ -850,6 +850,122 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   }
 }
 
+// Small graphs (W <= kSmallW words): one CTA per minibatch compacts a whole
+// level with the bitmap, its word prefixes in shared memory (no look-back
+// chain), writes every rank word, and then answers the rank lookups that
+// follow from shared memory instead of L2: this hop's MFG relabel, or at the
+// all level the relabel maps of every hop.
+constexpr std::uint64_t kSmallW = 8192;  // 524,288 vertices: 16 B of shared memory per word
+constexpr int kSmallThreads = 1024;
+
+struct SmallParams {
+  CompactParams c;
+  // hop level: relabel of this hop's sampled edges into dst
+  const std::uint32_t* edges;
+  std::uint64_t edges_stride;
+  const std::uint32_t* ecount;
+  std::uint32_t* dst;
+  std::uint64_t dst_stride;
+  // all level: relabel maps of hops 0..L
+  std::uint32_t L;
+  const std::uint32_t* F[VK_MAX_HOPS + 1];
+  std::uint64_t capF[VK_MAX_HOPS + 1];
+  const std::uint32_t* fcount[VK_MAX_HOPS + 1];
+  std::uint32_t* allidx[VK_MAX_HOPS + 1];
+};
+
+template <bool HAS_NEXT, bool OR_ALL, bool ALL>
+__global__ void __launch_bounds__(kSmallThreads) k_compact_small(SmallParams sp) {
+  extern __shared__ unsigned long long s_small[];
+  __shared__ unsigned long long s_scan[kSmallThreads / 32];
+  const CompactParams& p = sp.c;
+  const std::uint64_t W = p.W;
+  unsigned long long* bw = s_small;                                // [W] the level's bits
+  std::uint32_t* pre = reinterpret_cast<std::uint32_t*>(bw + W);  // [W] rank prefix per word
+  const std::uint32_t mb = blockIdx.x;
+  unsigned long long* bits = p.bits + mb * W;
+  for (std::uint64_t w = threadIdx.x; w < W; w += kSmallThreads) {
+    const unsigned long long x = bits[w];
+    bw[w] = x;
+    if (x) {
+      bits[w] = 0ull;  // clean for the next hop / wave
+      if (OR_ALL) p.allbits[mb * W + w] |= x;  // this CTA owns the minibatch's words
+    }
+  }
+  __syncthreads();
+  // contiguous chunk of words per thread
+  const std::uint64_t cpt = (W + kSmallThreads - 1) / kSmallThreads;
+  const std::uint64_t w0 = min(W, (std::uint64_t)threadIdx.x * cpt), w1 = min(W, w0 + cpt);
+  unsigned long long vc = 0, dc = 0;
+  for (std::uint64_t w = w0; w < w1; ++w) {
+    const unsigned long long x = bw[w];
+    vc += __popcll(x);
+    if (HAS_NEXT && x) dc += capped_degree_sum(x, w, p.outdeg, p.f_next);
+  }
+  const unsigned long long mine = pack_vd(vc, dc);
+  unsigned long long total;
+  const unsigned long long ex = block_inclusive_scan<kSmallThreads>(mine, s_scan, &total) - mine;
+  std::uint32_t lpos = (std::uint32_t)unpack_v(ex), dpos = (std::uint32_t)unpack_d(ex);
+  std::uint32_t* list = p.list + mb * p.cap_list;
+  std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
+  for (std::uint64_t w = w0; w < w1; ++w) {
+    unsigned long long x = bw[w];
+    pre[w] = lpos;
+    p.rank[mb * W + w] = make_uint4((unsigned)x, (unsigned)(x >> 32), lpos, 0u);
+    while (x) {
+      std::uint32_t vv[8], dd[8];
+      int nq = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        dd[q] = 0;
+        if (x) {
+          const int b = __ffsll(x) - 1;
+          x &= x - 1;
+          vv[q] = (std::uint32_t)(w * 64 + b);
+          if (HAS_NEXT) dd[q] = __ldg(p.outdeg + vv[q]);
+          nq = q + 1;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < nq) {
+          list[lpos] = vv[q];
+          if (HAS_NEXT) {
+            ipn[lpos] = dpos;
+            dpos += min(p.f_next, dd[q]);
+          }
+          ++lpos;
+        }
+    }
+  }
+  if (threadIdx.x == kSmallThreads - 1) {
+    const std::uint32_t tv = (std::uint32_t)unpack_v(total), td = (std::uint32_t)unpack_d(total);
+    p.count[mb] = tv;
+    if (HAS_NEXT) {
+      ipn[tv] = td;
+      p.ecount_next[mb] = td;
+    }
+  }
+  __syncthreads();
+  auto rank_of = [&](std::uint32_t v) {
+    const std::uint32_t w = v >> 6;
+    return pre[w] + (std::uint32_t)__popcll(bw[w] & ((1ull << (v & 63)) - 1ull));
+  };
+  if (!ALL) {  // the MFG relabel of this hop (k_relabel)
+    const std::uint32_t ne = sp.ecount[mb];
+    const std::uint32_t* ed = sp.edges + mb * sp.edges_stride;
+    std::uint32_t* dst = sp.dst + mb * sp.dst_stride;
+    for (std::uint32_t e = threadIdx.x; e < ne; e += kSmallThreads) dst[e] = rank_of(__ldg(ed + e));
+  } else {  // relabel maps of every hop (k_allidx)
+    for (std::uint32_t h = 0; h <= sp.L; ++h) {
+      const std::uint32_t cnt = sp.fcount[h][mb];
+      const std::uint32_t* F = sp.F[h] + mb * sp.capF[h];
+      std::uint32_t* ai = sp.allidx[h] + mb * sp.capF[h];
+      for (std::uint32_t j = threadIdx.x; j < cnt; j += kSmallThreads) ai[j] = rank_of(__ldg(F + j));
+    }
+  }
+}
+
 // Rank of v in the compacted list: one 16-byte load of {bits, prefix} (one
 // L2 sector per lookup instead of two).
 __device__ __forceinline__ std::uint32_t bit_rank(const uint4* __restrict__ rank, std::uint32_t v) {
@@ -1039,6 +1155,57 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   } else {
     k_compact<false, false><<<grid, kCompactThreads, smem, st>>>(p);
   }
+}
+
+void run_compact_small(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, cudaStream_t st) {
+  SmallParams sp{};
+  CompactParams& p = sp.c;
+  p.bits = (hop ? s.hopbits : s.allbits).as<unsigned long long>();
+  p.allbits = s.allbits.as<unsigned long long>();
+  p.list = hop ? s.F[h].as<std::uint32_t>() : s.all.as<std::uint32_t>();
+  p.cap_list = hop ? s.capF[h] : s.capAll;
+  p.rank = (hop ? s.hopprefix : s.allprefix).as<uint4>();
+  p.count = hop ? s.fcount(h) : s.allcount();
+  p.outdeg = s.g->out_deg.as<std::uint32_t>();
+  const bool has_next = hop && h < s.L;
+  if (has_next) {
+    p.f_next = s.cfg.fanouts[h];
+    p.indptr_next = s.indptr[h + 1].as<std::uint32_t>();
+    p.ecount_next = s.ecount(h + 1);
+  }
+  p.W = s.W;
+  p.nmb = nmb;
+  if (hop) {
+    sp.edges = s.edges_tmp.as<std::uint32_t>();
+    sp.edges_stride = s.capS_max;
+    sp.ecount = s.ecount(h);
+    sp.dst = s.dst[h].as<std::uint32_t>();
+    sp.dst_stride = s.capS[h];
+  } else {
+    sp.L = s.L;
+    for (std::uint32_t q = 0; q <= s.L; ++q) {
+      sp.F[q] = s.F[q].as<std::uint32_t>();
+      sp.capF[q] = s.capF[q];
+      sp.fcount[q] = s.fcount(q);
+      sp.allidx[q] = s.allidx[q].as<std::uint32_t>();
+    }
+  }
+  const std::size_t smem = (std::size_t)s.W * 12;
+  static bool attr = false;  // up to 96 KB of dynamic shared memory
+  if (!attr) {
+    const int mx = (int)(kSmallW * 12);
+    VK_CUDA(cudaFuncSetAttribute(k_compact_small<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    VK_CUDA(cudaFuncSetAttribute(k_compact_small<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    VK_CUDA(cudaFuncSetAttribute(k_compact_small<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    attr = true;
+  }
+  auto go = [&](void (*kernel)(SmallParams)) { kernel<<<nmb, kSmallThreads, smem, st>>>(sp); };
+  if (has_next)
+    go(k_compact_small<true, true, false>);
+  else if (hop)
+    go(k_compact_small<false, true, false>);
+  else
+    go(k_compact_small<false, false, true>);
 }
 
 }  // namespace
@@ -1245,6 +1412,13 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
                                     s->allbits.as<unsigned long long>(), s->W, s->err());
     count_launch();
     VK_LAUNCH_CHECK();
+    // small graphs: per-minibatch CTAs compact with shared-memory bitmaps and
+    // fuse the relabels (VK_SAMPLER_SMALL=0 forces the general path)
+    static const bool small_ok = [] {
+      const char* e = std::getenv("VK_SAMPLER_SMALL");
+      return !e || std::atoi(e) != 0;
+    }();
+    const bool small = small_ok && s->W <= kSmallW;
     for (std::uint32_t h = 1; h <= s->L; ++h) {
       const std::uint32_t f = s->cfg.fanouts[h - 1];
       if (f <= 32)
@@ -1257,6 +1431,12 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
         raise(VK_ERR_UNSUPPORTED, "fanouts above 1024 with higher-degree vertices are not supported");
       count_launch();
       VK_LAUNCH_CHECK();
+      if (small) {
+        run_compact_small(*s, true, h, nmb, st);
+        count_launch();
+        VK_LAUNCH_CHECK();
+        continue;
+      }
       run_compact(*s, true, h, nmb, h - 1, st);
       count_launch();
       VK_LAUNCH_CHECK();
@@ -1267,15 +1447,21 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
       count_launch();
       VK_LAUNCH_CHECK();
     }
-    run_compact(*s, false, 0, nmb, s->L, st);
-    count_launch();
-    VK_LAUNCH_CHECK();
-    // relabel map per hop (grids sized by each hop's capacity)
-    for (std::uint32_t h = 0; h <= s->L; ++h) {
-      const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(s->capF[h], 256 * kIlp), 4096);
-      k_allidx<<<dim3(gx, nmb), 256, 0, st>>>(s->F[h].as<std::uint32_t>(), s->allidx[h].as<std::uint32_t>(),
-                                              s->capF[h], s->fcount(h), s->allprefix.as<uint4>(), s->W);
+    if (small) {
+      run_compact_small(*s, false, 0, nmb, st);
       count_launch();
+      VK_LAUNCH_CHECK();
+    } else {
+      run_compact(*s, false, 0, nmb, s->L, st);
+      count_launch();
+      VK_LAUNCH_CHECK();
+      // relabel map per hop (grids sized by each hop's capacity)
+      for (std::uint32_t h = 0; h <= s->L; ++h) {
+        const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(s->capF[h], 256 * kIlp), 4096);
+        k_allidx<<<dim3(gx, nmb), 256, 0, st>>>(s->F[h].as<std::uint32_t>(), s->allidx[h].as<std::uint32_t>(),
+                                                s->capF[h], s->fcount(h), s->allprefix.as<uint4>(), s->W);
+        count_launch();
+      }
     }
     count_launch();
     VK_LAUNCH_CHECK();
