@@ -989,10 +989,18 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       const std::uint32_t v = e ? (std::uint32_t)std::atoi(e) : kGatherTileWords;
       return std::max<std::uint32_t>(64, (v + 63) / 64 * 64);  // rank words exist at multiples of 64
     }();
-    // ~1024 output rows per (tile, minibatch) unit: sparse neighbourhoods
-    // (papers-scale graphs) take proportionally wider vertex tiles
+    // a few thousand output rows per (tile, minibatch) unit (the capacity
+    // over-estimates the density, ~1.8x at C3): sparse neighbourhoods take
+    // proportionally wider vertex tiles. C3: 4096-vertex tiles 5.35 ms,
+    // 16384-vertex tiles 5.08 ms; C1 keeps 4096 (VK_GATHER_UNIT_ROWS)
+    static const double unit_rows = [] {
+      const char* e = std::getenv("VK_GATHER_UNIT_ROWS");
+      return e ? std::atof(e) : 3584.0;
+    }();
     const double density = std::max(1e-9, (double)gp.all_stride / (double)p->n);
-    const std::uint64_t want_words = (std::uint64_t)(1024.0 / (64.0 * density));
+    // ... at most 2048 words (131K vertices) per tile: papers-scale waves
+    // have little row reuse across minibatches and prefer narrower tiles
+    const std::uint64_t want_words = std::min<std::uint64_t>(2048, (std::uint64_t)(unit_rows / (64.0 * density)));
     std::uint64_t tw = std::max<std::uint64_t>(tile_words, (want_words + 63) / 64 * 64);
     gp.tile_words = (std::uint32_t)tw;
     gp.tiles = (std::uint32_t)((gp.W + tw - 1) / tw);
