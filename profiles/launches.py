@@ -27,10 +27,19 @@ def main():
     per, names = load(sys.argv[1])
     waves = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     ids = sorted(per)
+    # wave starts (k_prepare) that are followed by a gather before the next
+    # wave: the bench's own waves, not the device simulate() of the alpha
+    # sweep the bench runs after its timed regions
     starts = [i for i in ids if short(names[i]) == 'k_prepare']
+    bounds = starts + [ids[-1] + 1]
+    starts = [a for a, b in zip(bounds, bounds[1:])
+              if any(re.match(r'k_gather(<|$)', short(names[j])) for j in ids if a <= j < b)]
+    lo = starts[-waves]
+    nxt = next((b for b in bounds if b > starts[-1]), ids[-1] + 1)
+    hi = max(j for j in ids if starts[-1] <= j < nxt and re.match(r'k_gather(<|$)', short(names[j]))) + 1
     # the wave's own kernels only: torch kernels the bench runs after the timed
     # regions (distinct-row count, tallies) are not part of a wave
-    sel = [i for i in ids if i >= starts[-waves] and not re.search(r'at_cuda_detail|at::', names[i])]
+    sel = [i for i in ids if lo <= i < hi and not re.search(r'at_cuda_detail|at::', names[i])]
     agg = collections.OrderedDict()
     for i in sel:
         k = short(names[i])
