@@ -1066,7 +1066,11 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
       p.rank_prev = s.hopprefix.as<uint4>();
       // ~512 sources per (tile, minibatch) CTA at full frontier capacity,
       // at least kSampleTileWords words (4096 vertices) per tile
-      const std::uint64_t want_tiles = std::max<std::uint64_t>(1, p.capFprev / 512);
+      static const std::uint64_t tile_sources = [] {
+        const char* e = std::getenv("VK_SAMPLE_TILE_SOURCES");
+        return (std::uint64_t)(e && std::atoi(e) > 0 ? std::atoi(e) : 512);
+      }();
+      const std::uint64_t want_tiles = std::max<std::uint64_t>(1, p.capFprev / tile_sources);
       std::uint64_t tw = std::max<std::uint64_t>(kSampleTileWords, (s.W + want_tiles - 1) / want_tiles);
       tw = (tw + kRankStride - 1) / kRankStride * kRankStride;  // tile starts carry rank words
       p.tile_words = (std::uint32_t)tw;
