@@ -60,7 +60,7 @@ CONFIGS = {
 CONFIGS["c4"] = dict(workload="C4 ogbn-papers100M-shaped 111M nodes / 3.3B CSR slots, 128-d fp16, "
                               "8 partitions, fanout (15,10,5), batch 1024, VIP cache 32% (sweep 0-32%)",
                      n=111_059_956, d=15, K=8, p_in=0.8, train=0.011, dim=128, dtype=1, alpha=0.32,
-                     fanouts=(15, 10, 5), b=1024, alpha_sweep=(0.0, 0.04, 0.08, 0.16, 0.32))
+                     fanouts=(15, 10, 5), b=1024, wave=64, alpha_sweep=(0.0, 0.04, 0.08, 0.16, 0.32))
 CONFIGS["c5"] = dict(workload="C5 VIP analysis on ogbn-papers100M-shaped 111M nodes / 3.3B CSR slots, "
                               "8 partitions, fanout sweep", n=111_059_956, d=15, K=8, p_in=0.8, train=0.011,
                      b=1024, fanouts=(15, 10, 5),
@@ -674,7 +674,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--alpha-sweep", action="store_true", help="also tally misses for cache sizes 0-32%%")
     ap.add_argument("--wave", type=int, default=None,
-                    help="minibatches per step per GPU (default: the config's; 128 for c1-c3, 32 for c4)")
+                    help="minibatches per step per GPU (default: the config's; 128 for c1-c3, 64 for c4)")
     ap.add_argument("--pipes", type=int, default=1, help="overlapped sampler+gather pipelines (streams)")
     ap.add_argument("--prefetch", default="auto", choices=["auto", "0", "1"],
                     help="overlap the multi-GPU miss exchange with the next wave's sampling (auto: on for N>1)")

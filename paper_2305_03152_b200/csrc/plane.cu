@@ -1156,10 +1156,19 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
         return;
       }
     }
+    // VK_GATHER_CFG: (unroll, min CTAs/SM) 0 (8,4) 1 (16,2) 2 (4,8) 3 (8,2);
+    // C3: 5.05 / 6.73 / 5.62 / 6.62 ms, so (8,4) is the default
+    static const int gcfg = [] {
+      const char* e = std::getenv("VK_GATHER_CFG");
+      return e ? std::atoi(e) : 0;
+    }();
     auto launch = [&](int mode, cudaStream_t where) {
       if (v16) {
         if (mode == 4) k_gather<uint4, 8, 4, 4><<<grid, 256, 0, where>>>(gp);
         else if (mode == 3) k_gather<uint4, 8, 4, 3><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 0 && gcfg == 1) k_gather<uint4, 16, 2, 0><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 0 && gcfg == 2) k_gather<uint4, 4, 8, 0><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 0 && gcfg == 3) k_gather<uint4, 8, 2, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 0) k_gather<uint4, 8, 4, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 1) k_gather<uint4, 8, 4, 1><<<grid, 256, 0, where>>>(gp);
         else k_gather<uint4, 16, 2, 2, false><<<grid, 256, 0, where>>>(gp);  // peer rows: plain LDG
