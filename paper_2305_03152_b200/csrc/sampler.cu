@@ -727,9 +727,15 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     }
     return nq;
   };
+  // the first 8 degrees stay in registers for the emission pass (sparse
+  // tiles: every degree; no second random DRAM burst per vertex)
+  std::uint32_t cd[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) cd[q] = 0u;
   if (HAS_NEXT) {
     unsigned m = nz, j = 0;
     unsigned long long x = 0;
+    bool first = true;
     while (true) {
       std::uint32_t vv[8], d[8];
       const int nq = next8(m, x, j, vv);
@@ -737,7 +743,11 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) d[q] = q < nq ? __ldg(p.outdeg + vv[q]) : 0u;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) dc += min(p.f_next, d[q]);
+      for (int q = 0; q < 8; ++q) {
+        if (first) cd[q] = d[q];
+        dc += min(p.f_next, d[q]);
+      }
+      first = false;
     }
   }
   // words that get a rank entry: nonzero ones, the kRankStride multiple (tile
@@ -763,12 +773,14 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
   auto emit_all = [&](std::uint32_t lpos, std::uint32_t dpos, std::uint32_t gbase, bool to_smem) {
     unsigned m = nz, j = 0;
     unsigned long long x = 0;
+    bool first = true;
     while (true) {
       std::uint32_t vv[8], dd[8];
       const int nq = next8(m, x, j, vv);
       if (!nq) break;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) dd[q] = (HAS_NEXT && q < nq) ? __ldg(p.outdeg + vv[q]) : 0u;
+      for (int q = 0; q < 8; ++q) dd[q] = (HAS_NEXT && q < nq) ? (first ? cd[q] : __ldg(p.outdeg + vv[q])) : 0u;
+      first = false;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         if (q < nq) {
