@@ -213,6 +213,7 @@ struct GatherParams {
   const unsigned long long* ubits;
   const std::uint32_t* uprefix;
   const char* staging;
+  int idx_hint;    // VK_GATHER_IDX_HINT (see ld_u32_hint)
   int st_variant;  // VK_GATHER_ST: 0 .cs (evict-first), 1 plain, 2 L1::no_allocate
   int ld_variant;  // VK_GATHER_LD: 0 nc/no_allocate, 1 +L2 evict_last policy, 2 +evict_normal, 3 coherent
 };
@@ -233,6 +234,21 @@ __device__ __forceinline__ const std::uint32_t* stage_rstart(const GatherParams&
   for (std::uint32_t i = threadIdx.x; i <= p.K; i += blockDim.x) sm[i] = p.rstart[i];
   __syncthreads();
   return sm;
+}
+
+// 4-byte index loads with an optional L2 policy (0 none, 1 evict_last,
+// 2 evict_first); VK_GATHER_IDX_HINT bit 0: the all-vertex list streamed
+// evict-first, bit 1: slot-map lookups kept evict-last.
+__device__ __forceinline__ std::uint32_t ld_u32_hint(const std::uint32_t* p, int hint) {
+  if (hint == 0) return __ldg(p);
+  std::uint64_t pol;
+  if (hint == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  std::uint32_t r;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
 }
 
 // Streaming 16/4/2-byte copies: the feature table is read through L1
@@ -470,8 +486,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
     const std::uint32_t r = r0 + lane;
     const T* src = nullptr;
     if (r < hi) {
-      const std::uint32_t v = __ldg(all + r);
-      const std::uint32_t s = __ldg(slot + v);
+      const std::uint32_t v = ld_u32_hint(all + r, p.idx_hint & 1 ? 2 : 0);     // streamed once
+      const std::uint32_t s = ld_u32_hint(slot + v, p.idx_hint & 2 ? 1 : 0);    // reused by every row
+
       if (s != VK_MISS) {
         if (MODE != 2 && MODE != 4) {
           src = store + (std::uint64_t)s * rowv;
@@ -983,6 +1000,11 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       return e ? std::atoi(e) : 0;
     }();
     gp.st_variant = st_variant;
+    static const int idx_hint = [] {
+      const char* e = std::getenv("VK_GATHER_IDX_HINT");
+      return e ? std::atoi(e) : 0;
+    }();
+    gp.idx_hint = idx_hint;
     gp.nmb = nmb;
     static const std::uint32_t tile_words = [] {
       const char* e = std::getenv("VK_GATHER_TILE_WORDS");
