@@ -579,6 +579,117 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   }
 }
 
+// Single-GPU gather on the Tensor Memory Accelerator's bulk-copy path
+// (VK_GATHER_TMA=1): per warp and group of 32 output rows, every lane issues
+// one cp.async.bulk of its source row (global -> the warp's shared buffer,
+// completion counted in bytes on an mbarrier), then one elected lane writes
+// the group's rows -- contiguous in the output -- with a single bulk store.
+// Rows must be 16 B multiples of at most 512 B.
+constexpr int kTmaWarps = 8;
+constexpr std::uint32_t kTmaMaxRow = 512;
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* ptr) {
+  return (std::uint32_t)__cvta_generic_to_shared(ptr);
+}
+
+__global__ void __launch_bounds__(kTmaWarps * 32, 1) k_gather_tma(GatherParams p) {
+  extern __shared__ __align__(128) unsigned char s_tma[];
+  __shared__ __align__(8) unsigned long long s_bar[kTmaWarps];
+  __shared__ unsigned sh[4][kTmaWarps];
+  __shared__ std::uint32_t s_rs[kSmemParts];
+  const std::uint32_t* rs = stage_rstart(p, s_rs);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const std::uint32_t rb = (std::uint32_t)p.row_bytes;
+  unsigned char* buf = s_tma + (std::size_t)w * 32 * rb;
+  const std::uint32_t bar = smem_u32(&s_bar[w]);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  std::uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  std::uint32_t phase = 0;
+  for (std::uint32_t unit = blockIdx.x; unit < p.tiles * p.nmb; unit += gridDim.x) {
+    const std::uint32_t mb = unit % p.nmb;
+    const std::uint32_t tile = unit / p.nmb;
+    const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
+    const std::uint32_t cnt = p.all_count[mb];
+    const uint4* rk = p.all_rank + mb * p.W;
+    const std::uint64_t w0 = (std::uint64_t)tile * p.tile_words, w1 = w0 + p.tile_words;
+    const std::uint32_t lo = w0 < p.W ? rk[w0].z : cnt;
+    const std::uint32_t hi = w1 < p.W ? rk[w1].z : cnt;
+    const std::uint32_t* all = p.all + mb * p.all_stride;
+    const std::uint32_t* slot = p.slot[k];
+    const std::uint32_t nl = p.nlocal[k];
+    const char* store = p.base[k];
+    char* out = p.out + mb * p.out_stride_bytes;
+    unsigned c_local = 0, c_cache = 0, c_miss = 0;
+    for (std::uint32_t r0 = lo + w * 32; r0 < hi; r0 += kTmaWarps * 32) {
+      const std::uint32_t r = r0 + lane;
+      const std::uint32_t rows = min(32u, hi - r0);
+      const char* src = nullptr;
+      if (r < hi) {
+        const std::uint32_t v = __ldg(all + r);
+        const std::uint32_t s = __ldg(slot + v);
+        if (s != VK_MISS) {
+          src = store + (std::uint64_t)s * rb;
+          (s < nl ? c_local : c_cache)++;
+        } else {
+          const std::uint32_t g = __ldg(p.new_id + v);
+          const std::uint32_t o = owner_of(rs, p.K, g);
+          src = p.base[o] + (std::uint64_t)(g - rs[o]) * rb;
+          ++c_miss;
+        }
+      }
+      if (lane == 0) {
+        // the previous group's bulk store has finished reading the buffer
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * rb)
+                     : "memory");
+      }
+      __syncwarp();
+      if (r < hi)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+            "%4;" ::"r"(smem_u32(buf + (std::size_t)lane * rb)),
+            "l"(src), "r"(rb), "r"(bar), "l"(pol)
+            : "memory");
+      // wait for this group's bytes
+      std::uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+      }
+      phase ^= 1u;
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + (std::uint64_t)r0 * rb),
+                     "r"(smem_u32(buf)), "r"(rows * rb)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      __syncwarp();
+    }
+    unsigned vals[3] = {c_local, c_cache, c_miss};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      unsigned x = __reduce_add_sync(0xffffffffu, vals[q]);
+      if (lane == 0) sh[q][w] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      unsigned long long t = 0;
+      for (int q = 0; q < kTmaWarps; ++q) t += sh[threadIdx.x][q];
+      if (t) atomicAdd(p.counts + mb * 4 + threadIdx.x, t);
+    }
+    __syncthreads();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 }  // namespace
 }  // namespace vk
 
@@ -1184,10 +1295,25 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       const char* e = std::getenv("VK_GATHER_CFG");
       return e ? std::atoi(e) : 0;
     }();
+    static const bool tma_env = [] {
+      const char* e = std::getenv("VK_GATHER_TMA");
+      return e && std::atoi(e) != 0;
+    }();
+    const bool use_tma = tma_env && v16 && p->row_bytes <= kTmaMaxRow;
     auto launch = [&](int mode, cudaStream_t where) {
       if (v16) {
         if (mode == 4) k_gather<uint4, 8, 4, 4><<<grid, 256, 0, where>>>(gp);
         else if (mode == 3) k_gather<uint4, 8, 4, 3><<<grid, 256, 0, where>>>(gp);
+        else if (mode == 0 && use_tma) {
+          static bool attr = false;
+          if (!attr) {
+            VK_CUDA(cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kTmaWarps * 32 * kTmaMaxRow)));
+            attr = true;
+          }
+          const unsigned tgrid = (unsigned)std::min<std::uint64_t>(units, (std::uint64_t)sm_count(p->device) * 2);
+          k_gather_tma<<<tgrid, kTmaWarps * 32, (std::size_t)kTmaWarps * 32 * p->row_bytes, where>>>(gp);
+        }
         else if (mode == 0 && gcfg == 1) k_gather<uint4, 16, 2, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 0 && gcfg == 2) k_gather<uint4, 4, 8, 0><<<grid, 256, 0, where>>>(gp);
         else if (mode == 0 && gcfg == 3) k_gather<uint4, 8, 2, 0><<<grid, 256, 0, where>>>(gp);
