@@ -163,3 +163,31 @@ def test_seed_keys_replay_vs_reference(vk, ref, golden):
     plain = vk.expand(ng, batch_new, fan, 42, (1, 2, 2))
     x = ref.expand(ncsr, batch_new, fan, 42, 1, 2, 2)
     assert_same(plain, 3, x.frontier, x.all_vertices, x.indptr, x.edges)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_random_configs_vs_oracle(vk, port, case):
+    """Seeded random sampler configurations around the code-path boundaries:
+    1-3 hops, fanouts 1..40 (register / shared / local Fisher-Yates), batch
+    sizes 1..300, waves of 1..9, graphs on both sides of the small-graph
+    (shared-memory compaction) limit of 524,288 vertices."""
+    rng = np.random.default_rng(1000 + case)
+    n = [3000, 40000, 524288, 524289, 200000, 7000, 524288, 600000,
+         1000, 65536, 65537, 300000, 524224, 12345, 100000, 2000000][case]
+    d = int(rng.integers(2, 8))
+    csr = port.generate("pa", n, d, int(rng.integers(0, 99)))
+    L = int(rng.integers(1, 4))
+    fan = [int(x) for x in rng.choice([1, 2, 3, 5, 8, 10, 15, 17, 25, 33, 40], L)]
+    b = int(rng.integers(1, 301))
+    nmb = int(rng.integers(1, 10))
+    seed = int(rng.integers(0, 1 << 31))
+    g = dev_graph(vk, csr)
+    batches = [np.unique(rng.integers(0, n, b)).astype(np.uint32) for _ in range(nmb)]
+    rng.shuffle(batches[0])  # batch order is expand's hop-1 visiting order
+    refs = [(int(rng.integers(0, 5)), int(rng.integers(0, 4)), i) for i in range(nmb)]
+    s = vk.Sampler(g, fan, b, nmb, seed)
+    s.run(batches, refs)
+    for i in range(nmb):
+        e, k, bi = refs[i]
+        x = port.expand(csr, batches[i], fan, seed, e, k, bi)
+        assert_same(s.result(i), L, x.frontier, x.all_vertices, x.indptr, x.edges)
