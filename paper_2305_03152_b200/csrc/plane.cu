@@ -12,8 +12,10 @@
 //  * vk_plane_gather     = classify (commsim.cpp:61-73) + row gather for a
 //    whole wave: 128-bit loads/stores, flattened over (row, 16-byte chunk) so
 //    every lane moves data and writes are fully coalesced; misses read the
-//    owner partition's rows from local HBM or, multi-GPU, a peer's HBM over
-//    NVLink (CUDA IPC mapping) inside the same kernel.
+//    owner partition's rows from local HBM or, multi-GPU, from a staging
+//    buffer filled by the wave's deduplicated miss exchange (remote-miss
+//    union -> one NVLink pull per distinct row from the owner's HBM through
+//    a CUDA IPC mapping), optionally issued early by vk_plane_prefetch.
 #include <cub/cub.cuh>
 
 #include <cmath>
