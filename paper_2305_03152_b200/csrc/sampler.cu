@@ -78,6 +78,14 @@ struct vk_sampler_s {
   vk::DevBuf keys, tgt_keyed;
   bool keyed = false;
   std::uint64_t runs = 0;  // completed vk_sampler_run calls (plane prefetch bookkeeping)
+  // the MFG relabel of hop h runs on `aux` while the main stream samples hop
+  // h+1 (or compacts the all level after the last hop); sampled edges are
+  // double-buffered by hop parity in edges_tmp
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  std::uint32_t* edges_buf(std::uint32_t h) const {
+    return edges_tmp.as<std::uint32_t>() + (std::uint64_t)(h & 1u) * M * capS_max;
+  }
 
   std::uint32_t* fcount(std::uint32_t h) const { return counts.as<std::uint32_t>() + (std::uint64_t)h * M; }
   std::uint32_t* ecount(std::uint32_t h) const {
@@ -1050,7 +1058,7 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
   p.capFprev = s.capF[h - 1];
   p.fcount_prev = s.fcount(h - 1);
   p.indptr = s.indptr[h].as<std::uint32_t>();
-  p.edges = s.edges_tmp.as<std::uint32_t>();
+  p.edges = s.edges_buf(h);
   p.capS = s.capS_max;
   p.hopbits = s.hopbits.as<unsigned long long>();
   p.W = s.W;
@@ -1192,7 +1200,7 @@ void run_compact_small(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t
   p.W = s.W;
   p.nmb = nmb;
   if (hop) {
-    sp.edges = s.edges_tmp.as<std::uint32_t>();
+    sp.edges = s.edges_buf(h);
     sp.edges_stride = s.capS_max;
     sp.ecount = s.ecount(h);
     sp.dst = s.dst[h].as<std::uint32_t>();
@@ -1278,7 +1286,7 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
           s->indptr[h].alloc(M * (s->capF[h - 1] + 1) * 4);
         }
       }
-      s->edges_tmp.alloc(M * s->capS_max * 4);
+      s->edges_tmp.alloc(2 * M * s->capS_max * 4);
       s->all.alloc(M * s->capAll * 4);
       s->hopbits.alloc(M * s->W * 8);
       s->allbits.alloc(M * s->W * 8);
@@ -1304,6 +1312,9 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       }
       VK_CUDA(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
       VK_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+      VK_CUDA(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking));
+      VK_CUDA(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
+      VK_CUDA(cudaEventCreateWithFlags(&s->join_ev, cudaEventDisableTiming));
       VK_CUDA(cudaMemsetAsync(s->hopbits.p, 0, s->hopbits.bytes, s->stream));
       VK_CUDA(cudaMemsetAsync(s->allbits.p, 0, s->allbits.bytes, s->stream));
       VK_CUDA(cudaMemsetAsync(s->counts.p, 0, s->counts.bytes, s->stream));
@@ -1362,7 +1373,11 @@ int vk_sampler_destroy(vk_sampler s) {
     if (!s) return;
     DeviceGuard dg(s->g->device);
     if (s->last_stream) cudaStreamSynchronize(s->last_stream);
+    if (s->aux) cudaStreamSynchronize(s->aux);
     if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->aux) cudaStreamDestroy(s->aux);
+    if (s->fork_ev) cudaEventDestroy(s->fork_ev);
+    if (s->join_ev) cudaEventDestroy(s->join_ev);
     for (int k = 0; k < 2; ++k)
       if (s->staged[k]) cudaEventDestroy(s->staged[k]);
     if (s->done) cudaEventDestroy(s->done);
@@ -1435,6 +1450,11 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
       return !e || std::atoi(e) != 0;
     }();
     const bool small = small_ok && s->W <= kSmallW;
+    static const bool relabel_overlap = [] {
+      const char* e = std::getenv("VK_RELABEL_OVERLAP");
+      return !e || std::atoi(e) != 0;
+    }();
+    bool relabel_pending = false;  // a relabel is running on aux (join before the next compaction)
     for (std::uint32_t h = 1; h <= s->L; ++h) {
       const std::uint32_t f = s->cfg.fanouts[h - 1];
       if (f <= 32)
@@ -1453,15 +1473,29 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
         VK_LAUNCH_CHECK();
         continue;
       }
+      if (relabel_pending) {  // hop h-1's relabel still reads hopprefix
+        VK_CUDA(cudaStreamWaitEvent(st, s->join_ev, 0));
+        relabel_pending = false;
+      }
       run_compact(*s, true, h, nmb, h - 1, st);
       count_launch();
       VK_LAUNCH_CHECK();
       const unsigned gx = (unsigned)std::min<std::uint64_t>(ceil_div(s->capS[h], 256 * kIlp), 4096);
-      k_relabel<<<dim3(gx, nmb), 256, 0, st>>>(s->edges_tmp.as<std::uint32_t>(), s->capS_max, s->ecount(h),
-                                               s->hopprefix.as<uint4>(), s->W, s->dst[h].as<std::uint32_t>(),
-                                               s->capS[h]);
+      cudaStream_t rs_ = st;
+      if (relabel_overlap) {
+        VK_CUDA(cudaEventRecord(s->fork_ev, st));
+        VK_CUDA(cudaStreamWaitEvent(s->aux, s->fork_ev, 0));
+        rs_ = s->aux;
+      }
+      k_relabel<<<dim3(gx, nmb), 256, 0, rs_>>>(s->edges_buf(h), s->capS_max, s->ecount(h),
+                                                s->hopprefix.as<uint4>(), s->W, s->dst[h].as<std::uint32_t>(),
+                                                s->capS[h]);
       count_launch();
       VK_LAUNCH_CHECK();
+      if (relabel_overlap) {
+        VK_CUDA(cudaEventRecord(s->join_ev, s->aux));
+        relabel_pending = true;
+      }
     }
     if (small) {
       run_compact_small(*s, false, 0, nmb, st);
@@ -1479,6 +1513,7 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
         count_launch();
       }
     }
+    if (relabel_pending) VK_CUDA(cudaStreamWaitEvent(st, s->join_ev, 0));  // the last hop's relabel
     count_launch();
     VK_LAUNCH_CHECK();
     VK_CUDA(cudaEventRecord(s->done, st));
