@@ -144,6 +144,12 @@ __global__ void __launch_bounds__(1024) k_prepare(const WaveDesc* __restrict__ d
   }
 }
 
+// Frontier bitmap insert: a 32-bit RED on the half of the 64-bit word that
+// holds v (little-endian halves), no return value.
+__device__ __forceinline__ void set_bit(unsigned long long* hb, std::uint32_t v) {
+  atomicOr(reinterpret_cast<unsigned*>(hb) + (v >> 5), 1u << (v & 31));
+}
+
 // Sparse partial Fisher-Yates, same draws as sampling.cpp:87-91: the value
 // at positions [0, f) lives in lo[], positions >= f displaced by a swap in the
 // (hp, hv) map (at most f entries); untouched positions read the CSR slice.
@@ -158,7 +164,7 @@ __device__ __forceinline__ void sample_one(const std::uint32_t* __restrict__ nbr
     for (std::uint32_t i = 0; i < deg; ++i) {
       const std::uint32_t u = __ldg(nbrs + i);
       out[i] = u;
-      atomicOr(hb + (u >> 6), 1ull << (u & 63));
+      set_bit(hb, u);
     }
     return;
   }
@@ -185,7 +191,7 @@ __device__ __forceinline__ void sample_one(const std::uint32_t* __restrict__ nbr
       }
     }
     out[i] = vj;  // scratch[i] after the swap
-    atomicOr(hb + (vj >> 6), 1ull << (vj & 63));
+    set_bit(hb, vj);
   }
 }
 
@@ -285,7 +291,7 @@ __device__ __forceinline__ void fy_registers(const std::uint32_t* __restrict__ n
         }
       }
       out[i] = vj;
-      atomicOr(hb + (vj >> 6), 1ull << (vj & 63));
+      set_bit(hb, vj);
     }
   }
 }
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
           for (int u = 0; u < 4; ++u)
             if (i0 + u < deg) {
               out[i0 + u] = t[u];
-              atomicOr(hb + (t[u] >> 6), 1ull << (t[u] & 63));
+              set_bit(hb, t[u]);
             }
         }
       } else if constexpr (FMAX > 0) {
@@ -407,7 +413,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
             }
           }
           out[i] = vj;  // scratch[i] after the swap (sampling.cpp:87-91)
-          atomicOr(hb + (vj >> 6), 1ull << (vj & 63));
+          set_bit(hb, vj);
         }
       }
     }
