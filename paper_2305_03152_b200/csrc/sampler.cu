@@ -1005,6 +1005,20 @@ constexpr int kIlp = 4;
 
 __device__ __forceinline__ void rank_range(const std::uint32_t* __restrict__ in, std::uint32_t* __restrict__ out,
                                            std::uint32_t cnt, const uint4* __restrict__ rk) {
+  if ((((std::uintptr_t)in | (std::uintptr_t)out) & 15) == 0) {
+    // 16 B-aligned lists: 4 consecutive ids per 128-bit load and store
+    const std::uint32_t n4 = cnt / 4;
+    const uint4* in4 = reinterpret_cast<const uint4*>(in);
+    uint4* out4 = reinterpret_cast<uint4*>(out);
+    const std::uint32_t stride = gridDim.x * blockDim.x;
+    for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+      const uint4 v = __ldg(in4 + i);
+      out4[i] = make_uint4(bit_rank(rk, v.x), bit_rank(rk, v.y), bit_rank(rk, v.z), bit_rank(rk, v.w));
+    }
+    for (std::uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride)
+      out[i] = bit_rank(rk, __ldg(in + i));
+    return;
+  }
   const std::uint32_t stride = gridDim.x * blockDim.x;
   for (std::uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < cnt; i0 += kIlp * stride) {
     std::uint32_t v[kIlp];
