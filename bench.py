@@ -1,11 +1,13 @@
 #!/usr/bin/env python
 """Sample+gather minibatches/s (+ VIP edges/s) on B200, BASELINE.json metric.
 
-One process per GPU (torchrun for N > 1). Workload (default `c3`, the
-ogbn-products-shaped config of BASELINE.json configs[2], the largest that
-fits one GPU): community power-law graph n=2,449,029, d=25 (m ~ 122.4M CSR
-slots), K=8 partitions (communities), 8% train, 100-dim fp32 features, VIP
-cache alpha=0.20, fanouts (15,10,5), batch 1024, SeedSpec{42}.
+One process per GPU (torchrun for N > 1). Default workload `c4`, BASELINE.json
+configs[3] (the largest configuration, and it fits one B200): the
+ogbn-papers100M-shaped community power-law graph n=111,059,956, d=15
+(m ~ 3.33B CSR slots), K=8 partitions (communities), 1.1% train, 128-dim fp16
+features, VIP cache alpha=0.32 (sweep 0-32%), fanouts (15,10,5), batch 1024,
+SeedSpec{42}. `--config c1|c2|c3` select the smaller configs, `c5` the
+VIP-analysis-only sweep.
 
 A "step" is one wave of `--wave` minibatches per GPU through the whole hot
 path: sampler (K5/K6 + MFG + relabel) then classify+gather (K9/K10). GPU g
@@ -13,14 +15,17 @@ owns partitions k = g (mod N) and processes their minibatches; rows of
 partitions owned by other GPUs are read over NVLink by the gather kernel
 (CUDA IPC mappings). Per-GPU work is fixed as N grows -> "scaling": "weak".
 
-`value`: inputs (seed ids) already resident in HBM. `e2e`: the same waves
-through the C ABI from pinned HOST seed buffers (H2D inside the timed region)
-with the per-minibatch tallies read back to the host. Both timed with CUDA
-events on the launching stream, max over ranks.
+`value`: inputs (seed ids) already resident in HBM. `e2e`: the same through
+the C ABI with the epoch schedule (train members once, each epoch's
+permutations on a host worker thread) produced inside the timed region,
+pinned HOST seed buffers copied H2D every wave and the per-minibatch tallies
+read back to the host. Both timed with CUDA events on the launching stream,
+max over ranks.
 
 `--impl reference` times the reference's own CPU implementation (the
-unmodified vipkit library compiled in oracle/_ref) on the same minibatches
-with all host threads.
+unmodified vipkit library compiled in oracle/_ref: epoch_minibatches +
+expand + classify, plus a labelled row-gather restatement) on the same config
+with all host threads; it never imports the product package.
 """
 from __future__ import annotations
 
@@ -236,13 +241,22 @@ def run_b200(args, cfg):
     # per wave: sampler start/end, gather start/end
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(W + 2 * S)]
 
+    # e2e: the schedule itself is produced inside the timed region
+    from paper_2305_03152_b200.dist import MinibatchStream
+    src = {"stream": None}
+
+    def fetch(i, host):
+        if host and src["stream"] is not None:
+            waves[i] = src["stream"].take(M)
+        return waves[i]
+
     def wave(i, host=False, pinned=None):
         # wave i runs on pipe i % P: sampler and gather of consecutive waves
         # overlap on separate streams (sampler is L2-latency bound, gather HBM bound)
         p = i % P
         st, sp = streams[p], samplers[p]
         sh_p = st.cuda_stream
-        wv = waves[i]
+        wv = fetch(i, host)
         refs = [(e, k, bi) for (e, k, bi, _) in wv]
         evs[i][0].record(st)
         if host:
@@ -260,7 +274,7 @@ def run_b200(args, cfg):
 
     def sample(i, host):
         sp = samplers[i % 2]
-        wv = waves[i]
+        wv = fetch(i, host)
         refs = [(e, k, bi) for (e, k, bi, _) in wv]
         evs[i][0].record(stream)
         if host:
@@ -291,7 +305,7 @@ def run_b200(args, cfg):
         hs = hi_stream.cuda_stream
         for i in range(lo, hi):
             sp = samplers[i % 2]
-            wv = waves[i]
+            wv = fetch(i, host)
             refs = [(e, k, bi) for (e, k, bi, _) in wv]
             if i - 2 >= lo:
                 hi_stream.wait_event(evs[i - 2][3])  # same sampler: its gather has read it
@@ -347,9 +361,11 @@ def run_b200(args, cfg):
     clk = clocks.stop()
     # e2e: host seeds (H2D inside the region) + tallies read back to the host
     pinned = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64).pin_memory()
+    src["stream"] = MinibatchStream(vk, roles, labels, mine, cfg["b"], SAMPLE_SEED)
     if world > 1:
         dist.barrier()
     e2e_ms = region(W + S, W + 2 * S, host=True, pinned=pinned)
+    src["stream"].close()
     ms, e2e_ms = max_over_ranks([ms, e2e_ms])
 
     # ---- roofline of the dominant kernel (gather) and of the sampler, from the timed waves
@@ -401,7 +417,8 @@ def run_b200(args, cfg):
     total_mb = sum(len(waves[i]) for i in range(W, W + S)) * world
     value = total_mb / (ms / 1e3)
     e2e_val = total_mb / (e2e_ms / 1e3)
-    h2d = int(sum(len(w[3]) * 4 for i in range(W + S, W + 2 * S) for w in waves[i]) / S)
+    # seeds plus the per-minibatch wave descriptors (WaveDesc, 80 B) every wave
+    h2d = int(sum(len(w[3]) * 4 + 80 for i in range(W + S, W + 2 * S) for w in waves[i]) / S)
     result = {
         "metric": "sample+gather minibatches/s", "value": value, "unit": "minibatches/s",
         "n_gpus": world, "steps": S, "warmup": W, "ms_per_step": ms / S, "higher_is_better": True,
@@ -462,7 +479,7 @@ def run_b200(args, cfg):
         result["alpha_sweep"] = {"scope": "one epoch, all partitions (vk_simulate)", "minibatches": mbs,
                                  "seconds": sim_s, "rows": sweep}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(cfg, off, tgt, labels, roles, plan, waves[W:W + S])
+        result["cpu_baseline"] = cpu_baseline(cfg, off, tgt, labels, roles, M)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -552,45 +569,105 @@ def run_vip_sweep(args, cfg):
 
 
 # -------------------------------------------------------------- CPU baseline
-def cpu_baseline(cfg, off, tgt, labels, roles, plan, waves, budget_s=12.0):
-    """The reference's own CPU path (oracle/_ref, unmodified vipkit) on a
-    bounded sample of the same minibatches: epoch_minibatches + expand +
-    classify (commsim.cpp:41-73), all host threads over independent
-    minibatches. Gather is not included (the reference has none)."""
+def capacity_all(cfg, max_deg):
+    """The sampler's per-minibatch all_vertices capacity (vk_sampler_create)."""
+    n, cap_prev, tot = cfg["n"], cfg["b"], cfg["b"]
+    for f in cfg["fanouts"]:
+        cap_prev = min(n, cap_prev * min(f, max(1, max_deg)))
+        tot += cap_prev
+    return min(n, tot)
+
+
+class CpuReference:
+    """The reference's own CPU path on this config (oracle/_ref = the
+    unmodified vipkit library; test infrastructure, used here only as the
+    measured baseline): the schedule comes from epoch_minibatches over a
+    PartitionMap built once (sampling.cpp:45-70, as for_each_expansion does,
+    commsim.cpp:38-52), each minibatch is expanded (sampling.cpp:94-128) and
+    classified (commsim.cpp:61-73), and its all_vertices rows are gathered from
+    the host feature table by a labelled restatement (the reference never
+    materialises features). Workers over independent minibatches
+    (expand is pure, sampling.cpp:82).
+
+    The cache plan is build_cache (policies.cpp:149-163) over rank_by_scores of
+    the out-degree: classify's cost does not depend on which rows are cached,
+    and the reference's own VIP propagate over 3.3 B slots x 8 partitions
+    would take ~10 min on the host."""
+
+    def __init__(self, cfg, off, tgt, labels, roles, threads, with_table=True):
+        import concurrent.futures as cf
+        from oracle import oracle as O
+        self.cfg, self.threads = cfg, threads
+        P, R = O.port(), O.ref()
+        self.R = R
+        t = time.time()
+        n, K = cfg["n"], cfg["K"]
+        self.G = O.CSR(n, off, tgt)
+        R.graph_symmetric(self.G, threads)
+        self.ctx = R.context(roles, labels, K)
+        deg = np.diff(off).astype(np.float64)
+        with cf.ThreadPoolExecutor(max_workers=min(K, threads)) as ex:
+            orders = list(ex.map(lambda k: R.rank_by_scores(labels, K, k, deg)[0], range(K)))
+        _, self.bits = R.build_cache(orders, cfg["alpha"], n)
+        del orders, deg
+        self.labels = labels
+        fp16 = cfg.get("dtype", 0) == 1
+        self.table = P.feature_table(FEATURE_SEED, cfg["dim"], n, fp16=fp16, threads=threads) if with_table else None
+        cap = capacity_all(cfg, int(np.diff(off).max()))
+        self.work = (np.empty((threads, cap, cfg["dim"]), np.float16 if fp16 else np.float32)
+                     if with_table else None)
+        self._epoch, self._buf, self._pos = 0, [], 0
+        log(f"[bench] reference setup (graph, plan, feature table) {time.time() - t:.1f}s")
+
+    def take(self, count):
+        """Next `count` (epoch, k, i, seeds) in minibatch_schedule order;
+        epochs are scheduled by the reference's epoch_minibatches on demand."""
+        cfg, out = self.cfg, []
+        while len(out) < count:
+            if self._pos == len(self._buf):
+                b, e = cfg["b"], self._epoch
+                per = {k: self.ctx.epoch(k, b, e, SAMPLE_SEED) for k in range(cfg["K"])}
+                nb = {k: (len(per[k]) + b - 1) // b for k in per}
+                self._buf = [(e, k, i, per[k][i * b:(i + 1) * b]) for i in range(max(nb.values()))
+                             for k in per if i < nb[k]]
+                self._pos, self._epoch = 0, e + 1
+            t = min(count - len(out), len(self._buf) - self._pos)
+            out.extend(self._buf[self._pos:self._pos + t])
+            self._pos += t
+        return out
+
+    def step(self, count, gather=True, threads=None):
+        """One timed step: schedule + expand + classify (+ gather) of `count` minibatches."""
+        t0 = time.perf_counter()
+        mbs = self.take(count)
+        self.R.bench_minibatches(self.G, mbs, self.cfg["fanouts"], SAMPLE_SEED, self.labels, self.bits,
+                                 self.table if gather else None, self.work if gather else None,
+                                 threads or self.threads)
+        return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, off, tgt, labels, roles, M, budget_s=20.0):
+    """cpu_baseline of the GPU arm (rank 0, N=1): the reference CPU path
+    (CpuReference) on a bounded sample of the same workload."""
     from oracle import oracle as O
     if not O.ref_available():
         return {"value": None, "unit": "minibatches/s", "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built"}
-    R = O.ref()
     threads = os.cpu_count() or 1
-    t = time.time()
-    from oracle.oracle import CSR
-    G = CSR(cfg["n"], off, tgt)
-    R._graph(G)
-    log(f"[bench] reference graph built in {time.time() - t:.1f}s")
-    mbs = [w for wv in waves for w in wv]
-    done, t0 = 0, time.time()
-    for (e, k, i, seeds) in mbs:
-        R.expand_classify_range(G, seeds, len(seeds), cfg["fanouts"], SAMPLE_SEED, e, k, 0, 1, labels,
-                                plan.member_bits[k], 1)
-        done += 1
-        if time.time() - t0 > budget_s / 4:
-            break
-    single = done / (time.time() - t0)
-    # threaded: independent minibatches of one partition-epoch cell
-    e, k = mbs[0][0], mbs[0][1]
-    perm = R.epoch_permutation(roles, labels, k, cfg["b"], e, SAMPLE_SEED, K=cfg["K"])
-    nb = (len(perm) + cfg["b"] - 1) // cfg["b"]
-    take = max(1, min(nb, int(single * threads * budget_s / 2)))
-    t0 = time.time()
-    R.expand_classify_range(G, perm, cfg["b"], cfg["fanouts"], SAMPLE_SEED, e, k, 0, take, labels,
-                            plan.member_bits[k], threads)
-    multi = take / (time.time() - t0)
-    R.release(G)
-    return {"value": multi, "unit": "minibatches/s", "cores": threads, "kind": "reference",
-            "single_thread_value": single,
-            "sample": f"{take} minibatches of (epoch {e}, partition {k}) expand+classify with {threads} "
-                      f"threads; {done} minibatches single-threaded; gather excluded (not in reference)"}
+    ref = CpuReference(cfg, off, tgt, labels, roles, threads)
+    per = max(threads, min(M, 64))
+    ref.step(per)  # warm (page-in of the feature table and graph)
+    t1 = ref.step(per)
+    steps = max(1, min(20, int(budget_s / 2 / max(t1, 1e-3))))
+    tt = sum(ref.step(per) for _ in range(steps))
+    no_gather = per / ref.step(per, gather=False)
+    single = 2 / ref.step(2, threads=1)
+    return {"value": steps * per / tt, "unit": "minibatches/s", "cores": threads, "kind": "reference",
+            "expand_classify_only": no_gather, "single_thread_value": single,
+            "sample": f"{steps} steps x {per} minibatches of the bench schedule: reference epoch_minibatches + "
+                      f"expand + classify (unmodified vipkit, oracle/_ref) + row gather restatement "
+                      f"(oracle/workload.c) on {threads} threads; cache plan = build_cache over a degree "
+                      f"ranking (classify cost is plan-independent)"}
 
 
 class _DevArray:
@@ -613,54 +690,44 @@ def distinct_rows(sampler, nmb, dev):
 
 
 def run_reference(args, cfg):
-    """--impl reference: the unmodified reference CPU path on the same config."""
+    """--impl reference: the unmodified reference CPU path (CpuReference) on
+    the same config, steps of --wave minibatches. Never imports the product
+    package: the graph comes from the oracle's restatement of the bench
+    generator (oracle/workload.c, pinned to the product's by tests), roles
+    from the reference's make_roles."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_2305_03152_b200 import vipkit as vk
-    K, M = cfg["K"], args.wave
-    threads = os.cpu_count() or 1
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    off, tgt, labels, roles = make_data(cfg, threads)
-    R = O.ref()
-    G = O.CSR(cfg["n"], off, tgt)
-    R._graph(G)
-    W, S = args.warmup, args.steps
-    n = cfg["n"]
-    # the reference's VIP for the cache plan (propagate, rank, build_cache)
-    R.set_threads(threads)
-    orders = []
-    for k in range(K):
-        _, tot = R.propagate(G, cfg["fanouts"], R.initial_probs(roles, labels, K, k, cfg["b"]))
-        orders.append(R.rank_by_scores(labels, K, k, tot)[0])
-    _, bits = R.build_cache(orders, cfg["alpha"], n)
-    # per-step minibatch count bounded so the whole run stays within minutes
-    # one minibatch per host thread per step (expand is pure; sampling.cpp:82)
-    per_step = max(1, min(M, int(os.environ.get("VIPKIT_REF_MB_PER_STEP", str(threads)))))
-    sched = schedule(vk, cfg, roles, labels, list(range(K)), (W + S) * per_step)
-    t_all = 0.0
-    for i in range(W + S):
-        t0 = time.time()
-        chunk = sched[i * per_step:(i + 1) * per_step]
-        import concurrent.futures as cf
-        with cf.ThreadPoolExecutor(max_workers=min(threads, len(chunk))) as ex:
-            list(ex.map(lambda w: R.expand_classify_range(
-                G, w[3], len(w[3]), cfg["fanouts"], SAMPLE_SEED, w[0], w[1], 0, 1, labels,
-                bits[w[1]], max(1, threads // len(chunk))), chunk))
-        if i >= W:
-            t_all += time.time() - t0
-    value = S * per_step / t_all
+    threads = os.cpu_count() or 1
+    t = time.time()
+    off, tgt, labels = O.port().synth_community_powerlaw(cfg["n"], cfg["d"], cfg["K"], cfg["p_in"], GRAPH_SEED,
+                                                         threads)
+    roles = O.ref().make_roles(cfg["n"], cfg["train"], 0.0, 0.0, ROLES_SEED)
+    log(f"[bench] reference arm: graph n={cfg['n']} m={len(tgt)} in {time.time() - t:.1f}s")
+    ref = CpuReference(cfg, off, tgt, labels, roles, threads)
+    M, W, S = args.wave, args.warmup, args.steps
+    for _ in range(W):
+        ref.step(M)
+    tt = sum(ref.step(M) for _ in range(S))
+    value = S * M / tt
+    no_gather = M / ref.step(M, gather=False)
     print(json.dumps({
         "impl": "reference", "metric": "sample+gather minibatches/s", "value": value,
         "unit": "minibatches/s", "n_gpus": args.gpus, "steps": S, "warmup": W,
-        "ms_per_step": t_all / S * 1e3, "higher_is_better": True, "scaling": "weak",
-        "config": {"workload": cfg["workload"], "minibatches_per_step": per_step},
+        "ms_per_step": tt / S * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32 ids / fp32 or fp16 rows",
+        "data": "synthetic (community power-law graph, counter-hashed feature rows)",
+        "config": {"workload": cfg["workload"], "n": cfg["n"], "m_slots": int(len(tgt)), "partitions": cfg["K"],
+                   "fanouts": list(cfg["fanouts"]), "batch": cfg["b"], "minibatches_per_step_per_gpu": M,
+                   "feature_dim": cfg["dim"], "alpha": cfg["alpha"]},
         "cpu_baseline": {"value": value, "unit": "minibatches/s", "cores": threads, "kind": "reference",
-                         "sample": f"{per_step} minibatches per step (expand+classify, unmodified vipkit), "
-                                   f"{threads} host threads; gather not in the reference"},
+                         "expand_classify_only": no_gather,
+                         "sample": f"{S} steps x {M} minibatches: reference epoch_minibatches + expand + "
+                                   f"classify + row gather restatement, {threads} host threads"},
         "e2e": {"value": value, "unit": "minibatches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -671,7 +738,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--alpha-sweep", action="store_true", help="also tally misses for cache sizes 0-32%%")
     ap.add_argument("--wave", type=int, default=None,
                     help="minibatches per step per GPU (default: the config's; 128 for c1-c3, 64 for c4)")

@@ -131,6 +131,17 @@ VK_API int vk_epoch_minibatches(uint64_t n, const uint8_t* roles, const uint32_t
                                 uint64_t global_seed, const uint32_t* seed_keys,
                                 uint32_t* out_perm, uint64_t* out_count);
 
+/* PartitionMap::train_members (graph.hpp:68, graph.cpp:106-111): the train
+ * vertices of partition k in ascending id order (out capacity n). */
+VK_API int vk_train_members(uint64_t n, const uint8_t* roles, const uint32_t* part_of, uint32_t k,
+                            uint32_t* out, uint64_t* out_count);
+/* The shuffle half of epoch_minibatches (sampling.cpp:54-63) over a train
+ * member list computed once (vk_train_members): out = the epoch-e
+ * permutation, identical to vk_epoch_minibatches' for seed_keys = NULL. out
+ * may alias train. Empty lists raise VK_ERR_SAMPLING (sampling.cpp:50-53). */
+VK_API int vk_epoch_shuffle(const uint32_t* train, uint64_t count, uint32_t k, uint64_t epoch,
+                            uint64_t global_seed, uint32_t* out);
+
 /* vipkit::BatchRef (sampling.hpp:33-37). */
 typedef struct vk_batch_ref {
   uint64_t epoch;

@@ -115,6 +115,10 @@ class Port:
         L.vp_graph_from_edges.argtypes = [c_u64, u32p, u32p, c_u64, c_int, C.POINTER(c_vp),
                                           C.POINTER(c_vp), C.POINTER(c_u64)]
         L.vp_free.argtypes = [c_vp]
+        L.vp_synth_community_powerlaw.argtypes = [c_u64, c_u64, c_u32, c_double, c_u64, C.c_uint,
+                                                  C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), c_vp]
+        L.vp_fill_features.argtypes = [c_u64, c_u32, c_int, c_u64, c_vp, C.c_uint]
+        L.vp_gather_rows.argtypes = [c_vp, c_u64, c_vp, c_u64, c_vp, C.c_uint]
         L.vp_stream_draws.argtypes = [c_u64, c_u64, c_u64, u64p]
         L.vp_make_roles.argtypes = [c_u64, c_double, c_double, c_double, c_u64, u8p]
         L.vp_epoch_minibatches.argtypes = [u8p, c_u64, u32p, c_u32, c_u64, c_u64, c_u64, u32p,
@@ -289,6 +293,40 @@ class Port:
         self.lib.vp_features(seed, D, int(fp16), ids, len(ids), out.ctypes.data)
         return out
 
+    # ---- workload (workload.c) ----
+    def synth_community_powerlaw(self, n, d, communities, p_in, seed, threads=0):
+        """The bench graph recipe (restated from the product generator):
+        (off u64[n+1], tgt u32[m], labels u32[n])."""
+        offp, tgtp, m = c_vp(), c_vp(), c_u64()
+        labels = np.zeros(n, np.uint32)
+        rc = self.lib.vp_synth_community_powerlaw(n, d, communities, p_in, seed, threads or (os.cpu_count() or 1),
+                                                  C.byref(offp), C.byref(tgtp), C.byref(m), labels.ctypes.data)
+        if rc != 0:
+            raise OracleError(rc, "bad generator parameters")
+        off = np.ctypeslib.as_array(C.cast(offp, C.POINTER(C.c_uint64)), shape=(n + 1,)).copy()
+        self.lib.vp_free(offp)
+        if m.value:
+            tgt = np.empty(m.value, np.uint32)
+            C.memmove(tgt.ctypes.data, tgtp, m.value * 4)
+        else:
+            tgt = np.zeros(0, np.uint32)
+        self.lib.vp_free(tgtp)
+        return off, tgt, labels
+
+    def feature_table(self, seed, D, n, fp16=False, threads=0):
+        out = np.empty((n, D), np.float16 if fp16 else np.float32)
+        self.lib.vp_fill_features(seed, D, int(fp16), n, out.ctypes.data, threads or (os.cpu_count() or 1))
+        return out
+
+    def gather_rows(self, table, ids, out=None, threads=0):
+        ids = _a32(ids)
+        rb = table.shape[1] * table.itemsize
+        if out is None:
+            out = np.empty((len(ids), table.shape[1]), table.dtype)
+        self.lib.vp_gather_rows(table.ctypes.data, rb, ids.ctypes.data, len(ids), out.ctypes.data,
+                                threads or (os.cpu_count() or 1))
+        return out
+
 
 def bitsets(cached, n):
     """CachePlan::member_bits layout (policies.hpp:55-60): K x ceil(n/64) u64."""
@@ -323,6 +361,14 @@ class Ref:
         L.ref_graph_generate.argtypes = [c_int, c_u64, c_u64, c_u64]
         L.ref_graph_from_edges.argtypes = [c_u64, u32p, u32p, c_u64, c_int]
         L.ref_graph_from_csr.argtypes = [c_u64, c_u64, u64p, u32p]
+        L.ref_graph_from_symmetric_csr.restype = c_vp
+        L.ref_graph_from_symmetric_csr.argtypes = [c_u64, c_u64, u64p, u32p, C.c_uint, c_int]
+        L.ref_ctx_create.restype = c_vp
+        L.ref_ctx_create.argtypes = [u8p, u32p, c_u64, c_u32]
+        L.ref_ctx_free.argtypes = [c_vp]
+        L.ref_ctx_epoch.argtypes = [c_vp, c_u32, c_u64, c_u64, c_u64, u32p, C.POINTER(c_u64)]
+        L.ref_bench_minibatches.argtypes = [c_vp, c_u32, u32p, u64p, u64p, u32p, c_u32, c_u64, u32p, c_vp,
+                                            c_u64, c_vp, c_u64, c_vp, c_u64, C.c_uint, u64p]
         L.ref_graph_load_vcsr.argtypes = [C.c_char_p]
         L.ref_graph_write_vcsr.argtypes = [c_vp, C.c_char_p]
         L.ref_graph_n.restype = c_u64
@@ -408,6 +454,55 @@ class Ref:
             h = (g, p)
             self._handles[id(g)] = h
         return h[1]
+
+    def graph_symmetric(self, g: CSR, threads=0, check=False):
+        """Reference Graph of an undirected canonical CSR (reverse = forward,
+        copied instead of transposed); registered like _graph."""
+        p = self._ptr(self.lib.ref_graph_from_symmetric_csr(g.n, g.m, _a64(g.off), _a32(g.tgt),
+                                                            threads or (os.cpu_count() or 1), int(check)))
+        self._handles[id(g)] = (g, p)
+        return p
+
+    def context(self, roles, labels, K):
+        """(VertexRoles, PartitionMap) built once; .epoch(k, b, e, seed) ->
+        the epoch_minibatches permutation (sampling.cpp:45-70)."""
+        lib, chk = self.lib, self._check
+        roles = np.ascontiguousarray(roles, np.uint8)
+        h = self._ptr(lib.ref_ctx_create(roles, _a32(labels), len(roles), K))
+        n = len(roles)
+
+        class _Ctx:
+            def epoch(self, k, b, e, seed):
+                out = np.zeros(n, np.uint32)
+                cnt = c_u64()
+                chk(lib.ref_ctx_epoch(h, k, b, e, seed, out, C.byref(cnt)))
+                return out[:cnt.value]
+
+            def __del__(self):
+                lib.ref_ctx_free(h)
+        return _Ctx()
+
+    def bench_minibatches(self, g: CSR, mbs, fanouts, seed, labels, cache_bits=None, table=None, work=None,
+                          threads=0):
+        """One CPU-arm step: mbs = [(epoch, k, i, seeds)]; reference expand +
+        classify (+ gather of all_vertices rows from `table` into `work`).
+        Returns tallies [nmb, 4] = (all, local, cache, miss)."""
+        nmb = len(mbs)
+        seeds = _a32(np.concatenate([np.asarray(w[3], np.uint32) for w in mbs]))
+        offs = np.zeros(nmb + 1, np.uint64)
+        offs[1:] = np.cumsum([len(w[3]) for w in mbs])
+        refs = np.array([[w[0], w[1], w[2]] for w in mbs], np.uint64).ravel()
+        f = _a32(fanouts)
+        bits = None if cache_bits is None else np.ascontiguousarray(cache_bits, np.uint64)
+        W = 0 if bits is None else bits.shape[-1]
+        rb = 0 if table is None else table.shape[1] * table.itemsize
+        cap = 0 if work is None else work.shape[1]
+        t = np.zeros(nmb * 4, np.uint64)
+        self._check(self.lib.ref_bench_minibatches(
+            self._graph(g), nmb, seeds, offs, refs, f, len(f), seed, _a32(labels),
+            None if bits is None else bits.ctypes.data, W, None if table is None else table.ctypes.data, rb,
+            None if work is None else work.ctypes.data, cap, threads or (os.cpu_count() or 1), t))
+        return t.reshape(nmb, 4)
 
     def release(self, g: CSR):
         h = self._handles.pop(id(g), None)

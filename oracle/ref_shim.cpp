@@ -3,11 +3,13 @@
 // extern "C" shim over the UNMODIFIED reference library compiled from
 // /root/reference/proj/src. It exists so the Python test-suite and bench.py's
 // CPU-baseline leg can call the real reference (vipkit::*) with plain arrays.
-// No reference logic is restated here: every entry point forwards to the
-// reference function named in its comment. The one loop that is not a single
-// call (ref_expand's MFG edge list) drives the reference's own
-// `SeedSpec::stream` + `sample_neighbors` exactly as `expand` does
-// (sampling.cpp:106-114), because the reference has no MFG output.
+// Every entry point forwards to the reference function named in its comment.
+// Three pieces are not single calls, and say so where they are defined:
+// ref_expand's MFG edge list drives the reference's own `SeedSpec::stream` +
+// `sample_neighbors` exactly as `expand` does (sampling.cpp:106-114), because
+// the reference has no MFG output; the CPU-arm drivers restate `classify`
+// (commsim.cpp:61-73, in an anonymous namespace there, so not callable) and
+// the row gather out[i] = X[all[i]] (not in the reference at all).
 #include <algorithm>
 #include <atomic>
 #include <thread>
@@ -150,6 +152,35 @@ void* ref_graph_from_csr(std::uint64_t n, std::uint64_t m, const std::uint64_t* 
   return rc == 0 ? out : nullptr;
 }
 
+// Undirected bench graphs (canonical symmetric CSR, sorted rows): the
+// transpose load_binary_csr builds (graph.cpp:587-595) is the forward CSR
+// itself, so the reverse side is a (threaded) copy instead of an O(m)
+// random scatter (150 s single-threaded at papers scale). check != 0 runs the
+// reference's check_invariants (graph.cpp:55-75) as well.
+void* ref_graph_from_symmetric_csr(std::uint64_t n, std::uint64_t m, const std::uint64_t* off,
+                                   const std::uint32_t* tgt, unsigned threads, int check) {
+  Graph* out = nullptr;
+  const int rc = guard([&] {
+    auto* g = new Graph();
+    g->fwd_offsets.assign(off, off + n + 1);
+    g->rev_offsets.assign(off, off + n + 1);
+    g->fwd_targets.resize(m);
+    g->rev_targets.resize(m);
+    const unsigned T = std::max(1u, threads);
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; ++t)
+      th.emplace_back([&, t] {
+        const std::uint64_t lo = m * t / T, hi = m * (t + 1) / T;
+        std::memcpy(g->fwd_targets.data() + lo, tgt + lo, (hi - lo) * 4);
+        std::memcpy(g->rev_targets.data() + lo, tgt + lo, (hi - lo) * 4);
+      });
+    for (auto& x : th) x.join();
+    if (check) g->check_invariants();
+    out = g;
+  });
+  return rc == 0 ? out : nullptr;
+}
+
 void* ref_graph_load_vcsr(const char* path) {
   Graph* out = nullptr;
   const int rc = guard([&] { out = new Graph(load_binary_csr(path)); });  // graph.cpp:565
@@ -193,6 +224,33 @@ int ref_partition_graph(void* g, const std::uint8_t* roles, std::uint64_t n, std
 }
 
 // ---- sampling ----
+// A VertexRoles + PartitionMap pair built once (as the reference's callers
+// do, commsim.cpp:45-52), so per-epoch schedules cost what
+// epoch_minibatches costs and not a PartitionMap rebuild.
+struct RefCtx {
+  VertexRoles roles;
+  PartitionMap part;
+};
+void* ref_ctx_create(const std::uint8_t* roles, const std::uint32_t* labels, std::uint64_t n, std::uint32_t K) {
+  RefCtx* out = nullptr;
+  const int rc = guard([&] { out = new RefCtx{make_roles_view(roles, n), make_part(labels, n, K)}; });
+  return rc == 0 ? out : nullptr;
+}
+void ref_ctx_free(void* c) { delete static_cast<RefCtx*>(c); }
+int ref_ctx_epoch(void* c, std::uint32_t k, std::uint64_t b, std::uint64_t epoch, std::uint64_t seed,
+                  std::uint32_t* out_perm, std::uint64_t* out_count) {
+  return guard([&] {
+    const RefCtx& x = *static_cast<RefCtx*>(c);
+    const auto batches = epoch_minibatches(x.roles, x.part, k, b, epoch, SeedSpec{seed});  // sampling.cpp:45
+    std::uint64_t pos = 0;
+    for (const auto& bt : batches) {
+      std::memcpy(out_perm + pos, bt.data(), bt.size() * 4);
+      pos += bt.size();
+    }
+    *out_count = pos;
+  });
+}
+
 // epoch_minibatches (sampling.cpp:45-70); batches are the consecutive
 // b-chunks of the returned permutation.
 int ref_epoch_minibatches(const std::uint8_t* roles, std::uint64_t n, const std::uint32_t* labels,
@@ -323,6 +381,66 @@ int ref_expand_classify_range(void* gp, const std::uint32_t* perm, std::uint64_t
     });
     for (std::uint64_t j = 0; j < nbatch; ++j)
       for (int c = 0; c < 4; ++c) tallies[c] += t[4 * j + c];
+  });
+}
+
+// bench.py's CPU arms, one call per step: minibatch j (its own BatchRef
+// refs[3j..3j+2] = epoch, partition, batch index, and its seeds) is expanded
+// by the reference (sampling.cpp:94-128) and classified as commsim.cpp:61-73
+// does (restated); with a feature table, its all_vertices rows are then
+// gathered (out[i] = X[all[i]], restated: the reference has no gather) into
+// the worker's slice of `work` (threads x cap rows). Workers take minibatches
+// dynamically. tallies: nmb x {all, local, cache, miss}.
+int ref_bench_minibatches(void* gp, std::uint32_t nmb, const std::uint32_t* seeds,
+                          const std::uint64_t* seed_off, const std::uint64_t* refs, const std::uint32_t* fan,
+                          std::uint32_t L, std::uint64_t seed, const std::uint32_t* labels,
+                          const std::uint64_t* cache_bits /* K x W, or null */, std::uint64_t W,
+                          const unsigned char* table, std::uint64_t row_bytes, unsigned char* work,
+                          std::uint64_t cap, unsigned threads, std::uint64_t* tallies) {
+  return guard([&] {
+    const Graph& g = *static_cast<Graph*>(gp);
+    const FanoutSpec fanouts = make_fanouts(fan, L);
+    const SeedSpec seeds_spec{seed};
+    std::atomic<std::uint32_t> next{0};
+    std::string err;
+    std::atomic<bool> failed{false};
+    auto worker = [&](unsigned w) {
+      try {
+        for (std::uint32_t j = next++; j < nmb; j = next++) {
+          const std::uint32_t k = (std::uint32_t)refs[3 * j + 1];
+          const auto nb = expand(g, std::span<const vertex_t>(seeds + seed_off[j], seed_off[j + 1] - seed_off[j]),
+                                 fanouts, seeds_spec, BatchRef{refs[3 * j], k, refs[3 * j + 2]});
+          std::uint64_t loc = 0, hit = 0, miss = 0;
+          const std::uint64_t* bits = cache_bits ? cache_bits + (std::uint64_t)k * W : nullptr;
+          for (vertex_t v : nb.all_vertices) {
+            if (labels[v] == k)
+              ++loc;
+            else if (bits && ((bits[v >> 6] >> (v & 63)) & 1u))
+              ++hit;
+            else
+              ++miss;
+          }
+          if (table) {
+            if (nb.all_vertices.size() > cap) throw shape_error("gather buffer too small");
+            unsigned char* out = work + (std::uint64_t)w * cap * row_bytes;
+            for (std::size_t i = 0; i < nb.all_vertices.size(); ++i)
+              std::memcpy(out + i * row_bytes, table + (std::uint64_t)nb.all_vertices[i] * row_bytes, row_bytes);
+          }
+          tallies[4 * j] = nb.all_vertices.size();
+          tallies[4 * j + 1] = loc;
+          tallies[4 * j + 2] = hit;
+          tallies[4 * j + 3] = miss;
+        }
+      } catch (const std::exception& e) {
+        if (!failed.exchange(true)) err = e.what();
+      }
+    };
+    const unsigned T = std::max(1u, std::min<unsigned>(threads, nmb));
+    std::vector<std::thread> th;
+    for (unsigned w = 1; w < T; ++w) th.emplace_back(worker, w);
+    worker(0);
+    for (auto& t : th) t.join();
+    if (failed) throw parameter_error(err);
   });
 }
 

@@ -127,6 +127,29 @@ int vk_stream_sync(vk_stream_t stream) {
 
 void vk_host_free(void* p) { std::free(p); }
 
+// graph.cpp:106-111
+int vk_train_members(uint64_t n, const uint8_t* roles, const uint32_t* part_of, uint32_t k, uint32_t* out,
+                     uint64_t* out_count) {
+  return guard([&] {
+    if (!roles || !part_of || !out || !out_count) raise(VK_ERR_PARAMETER, "null argument");
+    std::uint64_t T = 0;
+    for (std::uint64_t v = 0; v < n; ++v)
+      if (part_of[v] == k && roles[v] == 0) out[T++] = (std::uint32_t)v;
+    *out_count = T;
+  });
+}
+
+// sampling.cpp:54-63 over a precomputed train list
+int vk_epoch_shuffle(const uint32_t* train, uint64_t count, uint32_t k, uint64_t epoch, uint64_t global_seed,
+                     uint32_t* out) {
+  return guard([&] {
+    if ((!train && count) || !out) raise(VK_ERR_PARAMETER, "null argument");
+    if (count == 0) raise(VK_ERR_SAMPLING, "partition " + std::to_string(k) + " has no train vertices");
+    if (out != train) std::memcpy(out, train, count * 4);
+    vk::epoch_shuffle(out, count, k, epoch, global_seed);
+  });
+}
+
 // sampling.cpp:45-70 (+ train_members, graph.cpp:106-111).
 int vk_epoch_minibatches(uint64_t n, const uint8_t* roles, const uint32_t* part_of, uint32_t k,
                          uint64_t batch_size, uint64_t epoch, uint64_t global_seed, const uint32_t* seed_keys,

@@ -38,6 +38,7 @@ bool sampler_all_rank_dense(vk_sampler_s* s);
 std::uint64_t sampler_run_id(vk_sampler_s* s);
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out);
 cudaEvent_t sampler_done_event(vk_sampler_s* s);
+void sampler_add_reader(vk_sampler_s* s, cudaStream_t st);
 }  // namespace vk
 
 struct vk_plane_s {
@@ -73,6 +74,7 @@ struct vk_plane_s {
     vk::DevBuf ubits, uprefix, ulist, staging, scan_tmp;
     vk::DevBuf vbits;  // vertex-space union (word mark); cleared as consumed
     std::size_t scan_bytes = 0;
+    std::uint64_t stage_cap = 0;  // rows the staging buffer holds
     // vk_plane_prefetch: the exchange of sampler run `prefetched` was issued
     // on the aux stream and completes at `ready`
     std::uint64_t prefetched = ~0ull;
@@ -204,6 +206,7 @@ struct GatherParams {
   std::uint64_t row_bytes;
   std::uint32_t V;                   // vector elements per row
   std::uint32_t magic32;             // ceil(2^32 / V): row = umulhi(e, magic32) for e < 32*V
+  std::uint32_t magic_fix;           // 1 when V > 11585 (umulhi may overshoot by one; fix up)
   unsigned long long* counts;        // [nmb][4]
   // vertex-tile schedule: CTA b serves minibatch b % nmb, vertex tile b / nmb
   const uint4* all_rank;             // [nmb][W] {bits, rank prefix} of all_vertices
@@ -215,10 +218,22 @@ struct GatherParams {
   const unsigned long long* ubits;
   const std::uint32_t* uprefix;
   const char* staging;
+  std::uint32_t stage_cap;
   int idx_hint;    // VK_GATHER_IDX_HINT (see ld_u32_hint)
   int st_variant;  // VK_GATHER_ST: 0 .cs (evict-first), 1 plain, 2 L1::no_allocate
   int ld_variant;  // VK_GATHER_LD: 0 nc/no_allocate, 1 +L2 evict_last policy, 2 +evict_normal, 3 coherent
 };
+
+// Row of flattened element e (< 32 V) of a warp's 32 rows: umulhi with
+// ceil(2^32/V) is exact while V*V < 2^27 (V <= 11585); above that it can
+// overshoot by one, which the fix-up corrects.
+__device__ __forceinline__ std::uint32_t row_of(std::uint32_t e, std::uint32_t V, std::uint32_t magic,
+                                                std::uint32_t fix) {
+  if (V == 1) return e;
+  std::uint32_t row = __umulhi(e, magic);
+  if (fix) row -= (row * V > e) ? 1u : 0u;
+  return row;
+}
 
 // Owner partition of global row g: the last k with rstart[k] <= g (K+1
 // range starts, staged in shared memory when K <= kSmemParts).
@@ -407,7 +422,7 @@ __global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::
   __shared__ const T* s_src[8][32];
   __shared__ std::uint32_t s_rs[kSmemParts];
   const std::uint32_t* rs = stage_rstart(p, s_rs);
-  const std::uint32_t cnt = *count_ptr;
+  const std::uint32_t cnt = min(*count_ptr, p.stage_cap);
   const std::uint32_t V = p.V;
   const std::uint32_t magic = p.magic32;
   const std::uint64_t rowv = p.row_bytes / sizeof(T);
@@ -431,7 +446,7 @@ __global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::
       for (int u = 0; u < kUnroll; ++u) {
         const std::uint32_t e = e0 + 32 * u;
         if (e < total) {
-          const std::uint32_t row = V == 1 ? e : __umulhi(e, magic);
+          const std::uint32_t row = row_of(e, V, magic, p.magic_fix);
           val[u] = s_src[w][row][e - row * V];
         }
       }
@@ -507,7 +522,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
             const std::uint32_t wq = g >> 6;
             const std::uint32_t idx = __ldg(p.uprefix + wq) +
                                       (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (g & 63)) - 1ull));
-            src = reinterpret_cast<const T*>(p.staging) + (std::uint64_t)idx * rowv;
+            src = idx < p.stage_cap ? reinterpret_cast<const T*>(p.staging) + (std::uint64_t)idx * rowv
+                                    : owner_src;  // past the staging capacity: direct NVLink read
           } else if (MODE == 3) {
             src = owner_src;
           }
@@ -545,7 +561,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
       for (int u = 0; u < kUnroll; ++u) {
         const std::uint32_t e = e0 + 32 * u;
         if (e < total) {
-          const std::uint32_t row = V == 1 ? e : __umulhi(e, magic);
+          const std::uint32_t row = row_of(e, V, magic, p.magic_fix);
           const T* sp = s_src[w][row] + (e - row * V);
           if constexpr (STREAM_LD)
             val[u] = ld_stream(sp, p.ld_variant);
@@ -557,7 +573,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
       for (int u = 0; u < kUnroll; ++u) {
         const std::uint32_t e = e0 + 32 * u;
         if (e < total) {
-          const std::uint32_t row = V == 1 ? e : __umulhi(e, magic);
+          const std::uint32_t row = row_of(e, V, magic, p.magic_fix);
           st_stream(dst + (std::uint64_t)s_row[w][row] * V + (e - row * V), val[u], p.st_variant);
         }
       }
@@ -865,10 +881,11 @@ int vk_plane_destroy(vk_plane p) {
   return guard([&] {
     if (!p) return;
     DeviceGuard dg(p->device);
-    if (p->stream) cudaStreamSynchronize(p->stream);
+    // gathers on caller streams and prefetched exchanges may still read peer
+    // memory: drain the device before the IPC mappings go away
+    cudaDeviceSynchronize();
     for (auto& part : p->parts)
       if (part.peer) cudaIpcCloseMemHandle(part.peer);
-    if (p->aux) cudaStreamSynchronize(p->aux);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->aux) cudaStreamDestroy(p->aux);
     if (p->fork) cudaEventDestroy(p->fork);
@@ -1098,6 +1115,7 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
     gp.V = (std::uint32_t)(p->row_bytes / esz);
     if (gp.V >= (1u << 15)) raise(VK_ERR_UNSUPPORTED, "feature rows above 512 KiB are not supported");
     gp.magic32 = gp.V == 1 ? 0u : (std::uint32_t)((0xffffffffull / gp.V) + 1);  // ceil(2^32 / V)
+    gp.magic_fix = gp.V > 11585 ? 1u : 0u;
     sampler_all_rank(s, &gp.all_rank, &gp.W);
     gp.rmask = p->d_rmask.as<const unsigned long long* const>();
     static const int ld_variant = [] {
@@ -1203,6 +1221,7 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       gp.ubits = ss.ubits.as<unsigned long long>();
       gp.uprefix = ss.uprefix.as<std::uint32_t>();
       gp.staging = ss.staging.as<char>();
+      gp.stage_cap = (std::uint32_t)ss.stage_cap;
     }
     if (timing && have_prefetch) {
       VK_CUDA(cudaEventRecord(tev[1], xs));
@@ -1217,10 +1236,26 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
         if (b.bytes < bytes) b.alloc(bytes);
       };
       p->last_set = &ss;
+      // a superseded prefetch of this stage set may still be running on aux
+      if (ss.ready && xs != p->aux) VK_CUDA(cudaStreamWaitEvent(xs, ss.ready, 0));
+      ss.prefetched = ~0ull;
       ensure(ss.ubits, W * 8);
       ensure(ss.uprefix, (W + 1) * 4);
       ensure(ss.ulist, n * 4);
-      ensure(ss.staging, n * p->row_bytes);
+      // staging holds at most half a wave's row capacity (bounded by the rows
+      // owned by peers); distinct remote rows ranked past it are read from the
+      // owner over NVLink by the gather itself
+      {
+        std::uint64_t remote_rows = 0;
+        for (std::uint32_t k = 0; k < p->K; ++k)
+          if (p->parts[k].attached) remote_rows += p->rend[k] - p->rstart[k];
+        const std::uint64_t want = std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+            remote_rows, std::max<std::uint64_t>(1ull << 20, (std::uint64_t)nmb * gp.all_stride / 2)));
+        if (ss.stage_cap < want) {
+          ss.staging.alloc(want * p->row_bytes);
+          ss.stage_cap = want;
+        }
+      }
       if (!ss.scan_bytes) {
         VK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, ss.scan_bytes, ss.uprefix.as<std::uint32_t>(),
                                               ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), xs));
@@ -1281,9 +1316,11 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       gp.ubits = ss.ubits.as<unsigned long long>();
       gp.uprefix = ss.uprefix.as<std::uint32_t>();
       gp.staging = ss.staging.as<char>();
+      gp.stage_cap = (std::uint32_t)ss.stage_cap;
       if (prefetch_only) {
         if (!ss.ready) VK_CUDA(cudaEventCreateWithFlags(&ss.ready, cudaEventDisableTiming));
         VK_CUDA(cudaEventRecord(ss.ready, xs));
+        sampler_add_reader(s, xs);  // the exchange read the sampler's all-vertex lists
         ss.prefetched = run;
         if (timing) {
           for (auto& e : tev) VK_CUDA(cudaEventDestroy(e));
@@ -1363,6 +1400,7 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       VK_CUDA(cudaEventRecord(p->join, p->aux));
       VK_CUDA(cudaStreamWaitEvent(st, p->join, 0));
     }
+    sampler_add_reader(s, st);  // the next run of this sampler waits for this gather
     if (timing) {
       VK_CUDA(cudaEventRecord(tev[4], st));
       VK_CUDA(cudaEventSynchronize(tev[4]));

@@ -70,6 +70,10 @@ struct vk_sampler_s {
   std::uint32_t last_nmb = 0;
   std::vector<std::uint32_t> last_parts;
   cudaEvent_t done = nullptr;
+  // readers of the last run on other streams (a plane gather, its miss
+  // exchange on the plane's aux stream): the next run waits for them before
+  // it rewrites the workspace they read
+  std::vector<cudaEvent_t> readers, reader_pool;
   cudaStream_t stream = nullptr;
   cudaStream_t last_stream = nullptr;
   // seed_keys replay (sampling.hpp:46-56): per-vertex stream keys and a copy
@@ -1401,6 +1405,11 @@ int vk_sampler_destroy(vk_sampler s) {
     for (int k = 0; k < 2; ++k)
       if (s->staged[k]) cudaEventDestroy(s->staged[k]);
     if (s->done) cudaEventDestroy(s->done);
+    for (cudaEvent_t e : s->readers) {
+      cudaEventSynchronize(e);
+      cudaEventDestroy(e);
+    }
+    for (cudaEvent_t e : s->reader_pool) cudaEventDestroy(e);
     delete s;
   });
 }
@@ -1417,6 +1426,12 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
     // make sure the previous run on another stream has finished with the
     // shared workspace before it is rewritten
     if (s->last_stream && s->last_stream != st) VK_CUDA(cudaStreamSynchronize(s->last_stream));
+    // ... and that every reader of it on another stream is done
+    for (cudaEvent_t e : s->readers) {
+      VK_CUDA(cudaStreamWaitEvent(st, e, 0));
+      s->reader_pool.push_back(e);
+    }
+    s->readers.clear();
     const std::uint64_t b = s->cfg.batch_size;
     const std::uint64_t total = seed_offsets[nmb] - seed_offsets[0];
     for (std::uint32_t i = 0; i < nmb; ++i) {
@@ -1707,5 +1722,16 @@ bool sampler_all_rank_dense(vk_sampler_s* s) { return s->dense_all_rank; }
 std::uint64_t sampler_run_id(vk_sampler_s* s) { return s->runs; }
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out) { out = s->last_parts; }
 cudaEvent_t sampler_done_event(vk_sampler_s* s) { return s->done; }
+void sampler_add_reader(vk_sampler_s* s, cudaStream_t st) {
+  cudaEvent_t e;
+  if (s->reader_pool.empty()) {
+    VK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  } else {
+    e = s->reader_pool.back();
+    s->reader_pool.pop_back();
+  }
+  VK_CUDA(cudaEventRecord(e, st));
+  s->readers.push_back(e);
+}
 std::uint64_t sampler_capacity_all(vk_sampler_s* s) { return s->capAll; }
 }  // namespace vk

@@ -39,6 +39,46 @@ def minibatch_schedule(permutation: Callable[[int, int], Sequence[int]], parts: 
     return out[:count]
 
 
+class MinibatchStream:
+    """`minibatch_schedule`'s sequence produced incrementally, for loops that
+    time the schedule with the rest of the step: every partition's train
+    members are listed once (PartitionMap::train_members), and each epoch's
+    permutations (epoch_minibatches' shuffle, sampling.cpp:54-63) are computed
+    on a worker thread one epoch ahead of the consumer (the ctypes calls
+    release the GIL), so the host keeps queueing GPU work meanwhile."""
+
+    def __init__(self, vk, roles, part_of, parts: Sequence[int], b: int, seed: int, epoch: int = 0):
+        import concurrent.futures as cf
+        self._vk, self._parts, self._b, self._seed = vk, list(parts), b, seed
+        self._train = {k: vk.train_members(roles, part_of, k) for k in self._parts}
+        self._pool = cf.ThreadPoolExecutor(max_workers=1)
+        self._epoch = epoch
+        self._next = self._pool.submit(self._cells, epoch)
+        self._buf, self._pos = [], 0
+
+    def _cells(self, e):
+        per = {k: self._vk.epoch_shuffle(self._train[k], k, e, self._seed) for k in self._parts}
+        b = self._b
+        nb = {k: (len(per[k]) + b - 1) // b for k in self._parts}
+        return [(e, k, i, per[k][i * b:(i + 1) * b]) for i in range(max(nb.values()))
+                for k in self._parts if i < nb[k]]
+
+    def take(self, count: int) -> list:
+        out = []
+        while len(out) < count:
+            if self._pos == len(self._buf):
+                self._buf, self._pos = self._next.result(), 0
+                self._epoch += 1
+                self._next = self._pool.submit(self._cells, self._epoch)
+            t = min(count - len(out), len(self._buf) - self._pos)
+            out.extend(self._buf[self._pos:self._pos + t])
+            self._pos += t
+        return out
+
+    def close(self):
+        self._pool.shutdown(wait=True)
+
+
 def exchange_plane_handles(plane, owned: Sequence[int], group=None) -> dict:
     """Export owned partitions, all-gather the handles (any host backend, e.g.
     gloo) and attach every partition owned elsewhere. Returns {k: owner_rank}."""

@@ -108,6 +108,8 @@ def lib():
     L.vk_initial_probs.argtypes = [c_u64, u8p, u32p, c_u32, c_u64, f64p]
     L.vk_vip_propagate.argtypes = [c_vp, u32p, c_u32, c_u32, f64p, c_vp, f64p]
     L.vk_vip_propagate_device.argtypes = [c_vp, u32p, c_u32, c_u32, c_vp, c_vp, c_vp, c_vp]
+    L.vk_train_members.argtypes = [c_u64, u8p, u32p, c_u32, u32p, C.POINTER(c_u64)]
+    L.vk_epoch_shuffle.argtypes = [u32p, c_u64, c_u32, c_u64, c_u64, u32p]
     L.vk_epoch_minibatches.argtypes = [c_u64, u8p, u32p, c_u32, c_u64, c_u64, c_u64, c_vp, u32p,
                                        C.POINTER(c_u64)]
     L.vk_sampler_create.argtypes = [c_vp, C.POINTER(SamplerConfig), C.POINTER(c_vp)]
@@ -336,6 +338,23 @@ def epoch_permutation(roles, part_of, k, b, epoch, seed, seed_keys=None) -> np.n
     check(lib().vk_epoch_minibatches(len(roles), roles, _a32(part_of), k, b, epoch, seed,
                                      None if sk is None else sk.ctypes.data, out, C.byref(cnt)))
     return out[:cnt.value]
+
+
+def train_members(roles, part_of, k) -> np.ndarray:
+    """PartitionMap::train_members (graph.hpp:68): partition k's train ids, ascending."""
+    roles = np.ascontiguousarray(roles, np.uint8)
+    out = np.zeros(len(roles), np.uint32)
+    cnt = c_u64()
+    check(lib().vk_train_members(len(roles), roles, _a32(part_of), k, out, C.byref(cnt)))
+    return out[:cnt.value].copy()
+
+
+def epoch_shuffle(train, k, epoch, seed) -> np.ndarray:
+    """epoch_minibatches' permutation from a precomputed train list."""
+    train = _a32(train)
+    out = np.empty_like(train)
+    check(lib().vk_epoch_shuffle(train, len(train), k, epoch, seed, out))
+    return out
 
 
 def epoch_minibatches(roles, part_of, k, b, epoch, seed, seed_keys=None):

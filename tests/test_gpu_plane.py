@@ -238,3 +238,71 @@ def test_tma_gather_variant_parity():
                         os.path.join(root, "tests", "test_gpu_plane.py")],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def _gather_host(vk, plane, sampler, nmb, stream=0):
+    view = sampler.view()
+    rb = plane.row_bytes
+    out_ptr, cnt_ptr = C.c_void_p(), C.c_void_p()
+    vk.check(vk.lib().vk_device_alloc(0, nmb * view.all_stride * rb, C.byref(out_ptr)))
+    vk.check(vk.lib().vk_device_alloc(0, nmb * 32, C.byref(cnt_ptr)))
+    plane.gather(sampler, out_ptr.value, view.all_stride, cnt_ptr.value, stream=stream)
+    return out_ptr, cnt_ptr, view.all_stride
+
+
+def test_gather_wide_rows_exact_row_index(vk, port, golden):
+    """fp32 rows of 20001 features (V = 20001 4-byte vectors > 11585): the
+    warp's flattened element -> row mapping (umulhi with ceil(2^32/V)) needs
+    its fix-up there; rows must still be bit-exact."""
+    fx = golden("expand_grid.npz")
+    csr = csr_from(golden("graphs.npz"), "pa5000")
+    roles, labels = fx["roles"], fx["labels"]
+    dim = 20001
+    r = _pipeline(vk, port, csr, roles, labels, 4, [3, 2], 16, 0.2, 42, dim, 0, 77, 1)
+    for i, (e, k, bi) in enumerate(r["refs"]):
+        x = port.expand(csr, r["batches"][i], [3, 2], 42, e, k, bi)
+        exp = port.features(77, dim, x.all_vertices)
+        got = r["rows"][i].view(np.uint32).reshape(-1, dim)
+        np.testing.assert_array_equal(got, exp.view(np.uint32))
+
+
+def test_two_samplers_gather_on_separate_stream(vk, port, golden):
+    """Two samplers alternate on their own streams while every gather runs on
+    a third stream with no host synchronisation in between: run i+2 must not
+    rewrite the workspace gather i still reads."""
+    torch = pytest.importorskip("torch")
+    fx = golden("expand_grid.npz")
+    csr = csr_from(golden("graphs.npz"), "pa5000")
+    roles, labels = fx["roles"], fx["labels"]
+    K, b, fan, dim = 4, 64, [15, 10, 5], 64
+    n = csr.n
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    p0 = np.stack([vk.initial_probs(roles, labels, k, b) for k in range(K)])
+    totals = np.stack([s.total for s in vk.propagate(g, fan, p0, with_hops=False)])
+    plan = vk.build_cache([vk.rank_by_scores(labels, k, totals[k])[0] for k in range(K)], 0.2, n)
+    oon, ranges = vk.build_reorder(labels, K, totals)
+    plane = vk.FeaturePlane(n, K, dim, labels, oon, ranges)
+    for k in range(K):
+        plane.load_partition(k, plan.cached[k], feature_seed=5)
+    waves = []
+    for k in range(K):
+        perm = vk.epoch_permutation(roles, labels, k, b, 0, 42)
+        waves.append(([perm[i * b:(i + 1) * b] for i in range(2)], [(0, k, i) for i in range(2)]))
+    samplers = [vk.Sampler(g, fan, b, 2, 42) for _ in range(2)]
+    gs = torch.cuda.Stream()
+    outs = []
+    for w, (batches, refs) in enumerate(waves):
+        s = samplers[w % 2]
+        s.run(batches, refs)
+        outs.append(_gather_host(vk, plane, s, len(batches), stream=gs.cuda_stream))
+    gs.synchronize()
+    rb = plane.row_bytes
+    for w, (batches, refs) in enumerate(waves):
+        out_ptr, cnt_ptr, stride = outs[w]
+        for i, (e, k, bi) in enumerate(refs):
+            x = port.expand(csr, batches[i], fan, 42, e, k, bi)
+            buf = np.zeros(len(x.all_vertices) * rb, np.uint8)
+            vk.check(vk.lib().vk_memcpy(buf.ctypes.data, out_ptr.value + i * stride * rb, buf.nbytes, 2))
+            np.testing.assert_array_equal(buf.view(np.uint32), port.features(5, dim, x.all_vertices).view(np.uint32).ravel())
+        vk.lib().vk_device_free(out_ptr)
+        vk.lib().vk_device_free(cnt_ptr)
