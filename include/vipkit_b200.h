@@ -142,6 +142,15 @@ VK_API int vk_train_members(uint64_t n, const uint8_t* roles, const uint32_t* pa
 VK_API int vk_epoch_shuffle(const uint32_t* train, uint64_t count, uint32_t k, uint64_t epoch,
                             uint64_t global_seed, uint32_t* out);
 
+/* vipkit::sample_neighbors (sampling.hpp:54-56, sampling.cpp:72-92) for one
+ * vertex on the device: appends min(fanout, deg v) ids to out (capacity
+ * fanout); *stream_state is RngStream's counter, advanced by the draws as the
+ * reference's stream is. neighbor_keys (deg(v) host entries in CSR row order,
+ * the seed_keys of v's neighbours) or NULL: with keys the draws run over the
+ * row ordered by key (sampling.cpp:83-85). */
+VK_API int vk_graph_sample_neighbors(vk_graph g, uint32_t v, uint32_t fanout, uint64_t* stream_state,
+                                     const uint32_t* neighbor_keys, uint32_t* out, uint64_t* out_count);
+
 /* vipkit::BatchRef (sampling.hpp:33-37). */
 typedef struct vk_batch_ref {
   uint64_t epoch;
@@ -330,6 +339,20 @@ VK_API int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of
                        uint64_t global_seed, const uint32_t* seed_keys, const uint32_t* cached_ids,
                        const uint64_t* cached_offsets,
                        const uint64_t* takes, uint32_t num_plans, uint32_t wave, uint64_t* cells);
+/* vk_simulate for one plan (cached ids as above, takes = NULL) with the
+ * per-minibatch rows of SimulateOptions::batch_costs (commsim.hpp:42-51,
+ * commsim.cpp:104-118): batch_rows[i*7..] = {epoch, batch_index, partition,
+ * local - gpu, gpu, cache, miss} for the i-th minibatch in for_each_expansion
+ * order; gpu counts local vertices whose position in gpu_orderings[k]
+ * (gpu_ordering_sizes[k] ids) is below floor(gamma*size + 1e-9), 0 without
+ * orderings. *num_batches = the minibatch count (batch_rows may be NULL to
+ * query it; else capacity >= count or VK_ERR_SHAPE). */
+VK_API int vk_simulate_batches(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K,
+                               const uint32_t* fanouts, uint32_t num_hops, uint64_t batch_size, uint64_t epochs,
+                               uint64_t global_seed, const uint32_t* seed_keys, const uint32_t* cached_ids,
+                               const uint64_t* cached_offsets, const uint32_t* const* gpu_orderings,
+                               const uint64_t* gpu_ordering_sizes, double gamma, uint64_t* cells,
+                               uint64_t* batch_rows, uint64_t batch_rows_capacity, uint64_t* num_batches);
 /* The "oracle" policy's retrospective access counts (sweep pass 1,
  * commsim.cpp:155-166): counts[k*n + v] = minibatches of partition k over
  * `epochs` epochs (for_each_expansion order) whose all_vertices contain v. */
@@ -361,6 +384,29 @@ VK_API int vk_synth_community_powerlaw(uint64_t n, uint64_t d, uint32_t communit
 VK_API int vk_synth_roles(uint64_t n, double train, double valid, double test, uint64_t seed,
                           uint8_t* roles);
 VK_API void vk_host_free(void* p);
+
+/* ------------------------------------------------------------ file formats
+ * (csrc/io.cu) Text files: one decimal value per line, empty and '#' lines
+ * skipped, a line's leading digits are its value (std::from_chars), anything
+ * else VK_ERR_FORMAT naming file:line; unopenable files VK_ERR_IO.
+ * partition_from_file (graph.hpp:105, graph.cpp:461-484): exactly n labels,
+ * K == 0 infers max+1 (*K_out), then PartitionMap::from_labels' checks
+ * (label >= K: VK_ERR_FORMAT, empty partition: VK_ERR_PARTITION). */
+VK_API int vk_partition_from_file(const char* path, uint32_t K, uint64_t n, uint32_t* part_of,
+                                  uint32_t* K_out);
+/* write_partition_labels (graph.hpp:122, graph.cpp:624-628) */
+VK_API int vk_write_partition_labels(const char* path, const uint32_t* part_of, uint64_t n);
+/* load_roles (graph.hpp:119, graph.cpp:600-616): codes 0..3; *roles is
+ * allocated (vk_host_free). write_roles (graph.hpp:120, graph.cpp:618-622). */
+VK_API int vk_load_roles(const char* path, uint8_t** roles, uint64_t* n);
+VK_API int vk_write_roles(const char* path, const uint8_t* roles, uint64_t n);
+/* write_vip_binary / load_vip_binary (vip.hpp:58-59, vip.cpp:107-134): n
+ * little-endian f64 totals; *values allocated (vk_host_free). */
+VK_API int vk_write_vip_binary(const char* path, const double* total, uint64_t n);
+VK_API int vk_load_vip_binary(const char* path, double** values, uint64_t* n);
+/* write_binary_csr (graph.hpp:116, graph.cpp:553-563): the VCSR file
+ * vk_graph_load_vcsr reads. */
+VK_API int vk_write_vcsr(const char* path, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <limits>
 #include <initializer_list>
+#include <ostream>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -91,6 +92,8 @@ class RngStream {
     while (x >= limit) x = next_u64();
     return x % bound;
   }
+  /// The Weyl counter (the stream's whole state), for the device sample_neighbors.
+  std::uint64_t& state() { return counter_; }
 
  private:
   std::uint64_t counter_;
@@ -158,6 +161,15 @@ struct VertexRoles {
   std::vector<std::uint8_t> role;
   std::size_t size() const { return role.size(); }
   bool is_train(vertex_t v) const { return role[v] == static_cast<std::uint8_t>(Role::train); }
+  std::vector<vertex_t> train_vertices() const {  // graph.cpp:77-82
+    std::vector<vertex_t> out;
+    for (std::size_t v = 0; v < role.size(); ++v)
+      if (is_train(static_cast<vertex_t>(v))) out.push_back(static_cast<vertex_t>(v));
+    return out;
+  }
+  std::size_t train_count() const {
+    return static_cast<std::size_t>(std::count(role.begin(), role.end(), static_cast<std::uint8_t>(Role::train)));
+  }
 };
 
 struct PartitionMap {
@@ -181,6 +193,14 @@ struct PartitionMap {
       if (pm.members[k].empty()) throw partition_error("partition " + std::to_string(k) + " is empty");
     return pm;
   }
+  /// graph.hpp:68 (graph.cpp:106-111): partition k's train vertices, ascending.
+  std::vector<vertex_t> train_members(const VertexRoles& roles, std::uint32_t k) const {
+    std::vector<vertex_t> out(part_of.size());
+    std::uint64_t cnt = 0;
+    detail::check(vk_train_members(part_of.size(), roles.role.data(), part_of.data(), k, out.data(), &cnt));
+    out.resize(cnt);
+    return out;
+  }
 };
 
 /// load_binary_csr (graph.hpp:117): parsed on the host, validated and the
@@ -202,6 +222,35 @@ inline Graph load_binary_csr(const std::string& path, int device = 0) {
   detail::check(vk_graph_copy_reverse(h, g.rev_offsets.data(), g.rev_targets.data()));
   g.adopt(h);
   return g;
+}
+
+/// write_binary_csr (graph.hpp:116): the VCSR file load_binary_csr reads.
+inline void write_binary_csr(const Graph& g, const std::string& path) {
+  detail::check(vk_write_vcsr(path.c_str(), g.num_vertices(), g.num_edges(), g.fwd_offsets.data(),
+                              g.fwd_targets.data()));
+}
+
+/// partition_from_file (graph.hpp:105): n label lines; K == 0 infers max + 1.
+inline PartitionMap partition_from_file(const std::string& path, std::uint32_t K, std::size_t n) {
+  std::vector<std::uint32_t> labels(n);
+  std::uint32_t k_out = 0;
+  detail::check(vk_partition_from_file(path.c_str(), K, n, labels.data(), &k_out));
+  return PartitionMap::from_labels(std::move(labels), k_out);
+}
+inline void write_partition_labels(const PartitionMap& part, const std::string& path) {  // graph.hpp:122
+  detail::check(vk_write_partition_labels(path.c_str(), part.part_of.data(), part.part_of.size()));
+}
+inline VertexRoles load_roles(const std::string& path) {  // graph.hpp:119
+  std::uint8_t* r = nullptr;
+  std::uint64_t n = 0;
+  detail::check(vk_load_roles(path.c_str(), &r, &n));
+  VertexRoles roles;
+  roles.role.assign(r, r + n);
+  vk_host_free(r);
+  return roles;
+}
+inline void write_roles(const VertexRoles& roles, const std::string& path) {  // graph.hpp:120
+  detail::check(vk_write_roles(path.c_str(), roles.role.data(), roles.role.size()));
 }
 
 // ---- sampling.hpp:14-64 ------------------------------------------------------
@@ -328,6 +377,35 @@ inline ExpandedNeighborhood expand(const Graph& g, std::span<const vertex_t> bat
   return s.result(0);
 }
 
+/// vipkit::sample_neighbors (sampling.hpp:54-56): at most `fanout` of v's
+/// out-neighbours appended to `out`, drawn on the device from `stream`
+/// (advanced as the reference's is).
+inline void sample_neighbors(const Graph& g, vertex_t v, std::uint32_t fanout, RngStream& stream,
+                             std::vector<vertex_t>& out, const std::vector<vertex_t>* seed_keys = nullptr) {
+  if (v >= g.num_vertices()) throw range_error("vertex id out of range");
+  std::vector<std::uint32_t> keys;
+  if (seed_keys) {  // the keys of v's neighbours, in row order (argument marshalling)
+    if (seed_keys->size() != g.num_vertices()) throw shape_error("seed_keys length does not match vertex count");
+    for (vertex_t u : g.out_neighbors(v)) keys.push_back((*seed_keys)[u]);
+  }
+  const std::size_t base = out.size();
+  out.resize(base + std::min<std::uint64_t>(fanout, g.out_degree(v)));
+  std::uint64_t cnt = 0;
+  detail::check(vk_graph_sample_neighbors(g.handle(), v, fanout, &stream.state(), seed_keys ? keys.data() : nullptr,
+                                          out.data() + base, &cnt));
+  out.resize(base + cnt);
+}
+
+/// append_trace (sampling.hpp:67): epoch,partition,batch_index,vertex,hop rows.
+inline void append_trace(std::ostream& out, const BatchRef& ref, const ExpandedNeighborhood& nb) {
+  auto row = [&](vertex_t v, std::size_t hop) {
+    out << ref.epoch << ',' << ref.partition << ',' << ref.batch_index << ',' << v << ',' << hop << '\n';
+  };
+  for (vertex_t v : nb.batch) row(v, 0);
+  for (std::size_t h = 0; h < nb.frontier.size(); ++h)
+    for (vertex_t v : nb.frontier[h]) row(v, h + 1);
+}
+
 // ---- vip.hpp:15-46 -----------------------------------------------------------
 struct TransitionModel {
   enum class Kind { uniform_fanout };
@@ -386,6 +464,19 @@ inline VipScores propagate(const Graph& g, const TransitionModel& tm, std::vecto
   std::vector<std::vector<double>> v;
   v.push_back(std::move(p0));
   return std::move(propagate_all(g, tm, std::move(v), partition)[0]);
+}
+
+/// write_vip_binary / load_vip_binary (vip.hpp:58-59): n little-endian f64 totals.
+inline void write_vip_binary(const VipScores& scores, const std::string& path) {
+  detail::check(vk_write_vip_binary(path.c_str(), scores.total.data(), scores.total.size()));
+}
+inline std::vector<double> load_vip_binary(const std::string& path) {
+  double* v = nullptr;
+  std::uint64_t n = 0;
+  detail::check(vk_load_vip_binary(path.c_str(), &v, &n));
+  std::vector<double> out(v, v + n);
+  vk_host_free(v);
+  return out;
 }
 
 // ---- policies.hpp:16-64 -------------------------------------------------------
@@ -570,11 +661,25 @@ inline std::vector<CommReport> simulate_plans(const Graph& g, const VertexRoles&
 }
 }  // namespace detail
 
+struct SimulateOptions {  // commsim.hpp:42-51
+  std::ostream* trace = nullptr;        // sampling trace CSV rows
+  std::ostream* batch_costs = nullptr;  // per-batch class counts CSV rows
+  const std::vector<vertex_t>* seed_keys = nullptr;
+  // GPU-prefix split for batch-cost rows: per-partition orderings of local
+  // vertices plus the resident fraction. Empty = everything on CPU.
+  const std::vector<std::vector<vertex_t>>* gpu_orderings = nullptr;
+  double gamma = 0.0;
+};
+
 /// simulate (commsim.hpp:56-59) on the device: every minibatch of every
-/// partition for E epochs, classified against the plan.
+/// partition for E epochs, classified against the plan. SimulateOptions:
+/// seed_keys replays relabelled streams; batch_costs rows (per-minibatch
+/// class counts, the GPU-prefix split included) come from the device
+/// classification (vk_simulate_batches); trace rows are the device
+/// expansions' batch and frontiers, in for_each_expansion order.
 inline CommReport simulate(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
                            const FanoutSpec& fanouts, std::uint64_t b, std::uint64_t E, const SeedSpec& seeds,
-                           const CachePlan& plan, const std::vector<vertex_t>* seed_keys = nullptr) {
+                           const CachePlan& plan, const SimulateOptions& opts = {}) {
   if (plan.K != part.K) throw config_error("cache plan partition count differs from partition map");
   std::vector<vertex_t> ids;
   std::vector<std::uint64_t> offs{0};
@@ -582,8 +687,67 @@ inline CommReport simulate(const Graph& g, const VertexRoles& roles, const Parti
     ids.insert(ids.end(), c.begin(), c.end());
     offs.push_back(ids.size());
   }
-  return detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, nullptr, {plan.alpha},
-                                seed_keys)[0];
+  const std::vector<vertex_t>* sk = opts.seed_keys;
+  if (sk && sk->size() != g.num_vertices()) throw shape_error("seed_keys length does not match vertex count");
+  CommReport report;
+  if (!opts.batch_costs) {
+    report = detail::simulate_plans(g, roles, part, fanouts, b, E, seeds, ids, offs, nullptr, {plan.alpha}, sk)[0];
+  } else {
+    fanouts.validate();
+    if (opts.gpu_orderings && opts.gpu_orderings->size() != part.K)
+      throw shape_error("need one GPU ordering per partition");
+    std::vector<const std::uint32_t*> gp;
+    std::vector<std::uint64_t> gs;
+    if (opts.gpu_orderings)
+      for (const auto& o : *opts.gpu_orderings) {
+        gp.push_back(o.data());
+        gs.push_back(o.size());
+      }
+    std::uint64_t total = 0;
+    for (std::uint32_t k = 0; k < part.K; ++k) total += (part.train_members(roles, k).size() + b - 1) / (b ? b : 1);
+    total *= E;
+    std::vector<std::uint64_t> cells(E * part.K * 3), rows(std::max<std::uint64_t>(1, total) * 7);
+    std::uint64_t got = 0;
+    detail::check(vk_simulate_batches(g.handle(), roles.role.data(), part.part_of.data(), part.K,
+                                      fanouts.fanouts.data(), static_cast<std::uint32_t>(fanouts.hops()), b, E,
+                                      seeds.global_seed, sk ? sk->data() : nullptr, ids.empty() ? nullptr : ids.data(),
+                                      offs.data(), opts.gpu_orderings ? gp.data() : nullptr,
+                                      opts.gpu_orderings ? gs.data() : nullptr, opts.gamma, cells.data(), rows.data(),
+                                      total, &got));
+    report.alpha = plan.alpha;
+    report.fanout_label = fanouts.label();
+    report.epochs = E;
+    report.partitions = part.K;
+    report.cells.resize(E * part.K);
+    for (std::size_t c = 0; c < report.cells.size(); ++c)
+      report.cells[c] = {cells[3 * c], cells[3 * c + 1], cells[3 * c + 2]};
+    for (std::uint64_t i = 0; i < got; ++i) {
+      const std::uint64_t* r = rows.data() + 7 * i;
+      *opts.batch_costs << r[0] << ',' << r[1] << ',' << r[2] << ',' << r[3] << ',' << r[4] << ',' << r[5] << ','
+                        << r[6] << '\n';
+    }
+  }
+  if (opts.trace) {  // for_each_expansion (commsim.cpp:45-52) through the device sampler, one wave per cell
+    for (std::uint64_t e = 0; e < E; ++e)
+      for (std::uint32_t k = 0; k < part.K; ++k) {
+        const auto batches = epoch_minibatches(roles, part, k, b, e, seeds, sk);
+        for (std::size_t i0 = 0; i0 < batches.size(); i0 += 64) {
+          const std::size_t i1 = std::min(batches.size(), i0 + 64);
+          Sampler s(g, fanouts, b, static_cast<std::uint32_t>(i1 - i0), seeds);
+          if (sk) s.set_seed_keys(sk);
+          std::vector<std::span<const vertex_t>> bs;
+          std::vector<BatchRef> refs;
+          for (std::size_t i = i0; i < i1; ++i) {
+            bs.emplace_back(batches[i]);
+            refs.push_back(BatchRef{e, k, i});
+          }
+          s.run(bs, refs);
+          for (std::size_t i = i0; i < i1; ++i)
+            append_trace(*opts.trace, refs[i - i0], s.result(static_cast<std::uint32_t>(i - i0)));
+        }
+      }
+  }
+  return report;
 }
 
 /// The alpha axis of sweep (commsim.cpp:140-259) for one ranking policy:

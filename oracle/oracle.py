@@ -367,6 +367,16 @@ class Ref:
         L.ref_ctx_create.argtypes = [u8p, u32p, c_u64, c_u32]
         L.ref_ctx_free.argtypes = [c_vp]
         L.ref_ctx_epoch.argtypes = [c_vp, c_u32, c_u64, c_u64, c_u64, u32p, C.POINTER(c_u64)]
+        L.ref_sample_neighbors_state.argtypes = [c_vp, c_u32, c_u32, c_u64, c_vp, u32p, C.POINTER(c_u64),
+                                                 C.POINTER(c_u64)]
+        L.ref_write_partition_labels.argtypes = [u32p, c_u64, c_u32, C.c_char_p]
+        L.ref_partition_from_file.argtypes = [C.c_char_p, c_u32, c_u64, u32p, C.POINTER(c_u32)]
+        L.ref_write_roles.argtypes = [u8p, c_u64, C.c_char_p]
+        L.ref_load_roles.argtypes = [C.c_char_p, u8p, c_u64, C.POINTER(c_u64)]
+        L.ref_write_vip_binary.argtypes = [f64p, c_u64, C.c_char_p]
+        L.ref_load_vip_binary.argtypes = [C.c_char_p, f64p, c_u64, C.POINTER(c_u64)]
+        L.ref_simulate_streams.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, u32p, u64p,
+                                           C.c_char_p, C.c_char_p, c_vp, c_vp, c_double, u64p]
         L.ref_bench_minibatches.argtypes = [c_vp, c_u32, u32p, u64p, u64p, u32p, c_u32, c_u64, u32p, c_vp,
                                             c_u64, c_vp, c_u64, c_vp, c_u64, C.c_uint, u64p]
         L.ref_graph_load_vcsr.argtypes = [C.c_char_p]
@@ -462,6 +472,65 @@ class Ref:
                                                             threads or (os.cpu_count() or 1), int(check)))
         self._handles[id(g)] = (g, p)
         return p
+
+    def sample_neighbors(self, g: CSR, v, fanout, key, seed_keys=None):
+        """(ids, next draw of the stream afterwards)."""
+        out = np.zeros(max(1, fanout), np.uint32)
+        cnt, nxt = c_u64(), c_u64()
+        sk = None if seed_keys is None else _a32(seed_keys)
+        self._check(self.lib.ref_sample_neighbors_state(self._graph(g), v, fanout, key,
+                                                        None if sk is None else sk.ctypes.data, out,
+                                                        C.byref(cnt), C.byref(nxt)))
+        return out[:cnt.value].copy(), nxt.value
+
+    # ---- file formats (the reference's own readers / writers) ----
+    def write_partition_labels(self, labels, K, path):
+        labels = _a32(labels)
+        self._check(self.lib.ref_write_partition_labels(labels, len(labels), K, path.encode()))
+
+    def partition_from_file(self, path, K, n):
+        out = np.zeros(n, np.uint32)
+        k_out = c_u32()
+        self._check(self.lib.ref_partition_from_file(path.encode(), K, n, out, C.byref(k_out)))
+        return out, k_out.value
+
+    def write_roles(self, roles, path):
+        r = np.ascontiguousarray(roles, np.uint8)
+        self._check(self.lib.ref_write_roles(r, len(r), path.encode()))
+
+    def load_roles(self, path, cap=1 << 24):
+        out = np.zeros(cap, np.uint8)
+        n = c_u64()
+        self._check(self.lib.ref_load_roles(path.encode(), out, cap, C.byref(n)))
+        return out[:n.value].copy()
+
+    def write_vip_binary(self, total, path):
+        t = np.ascontiguousarray(total, np.float64)
+        self._check(self.lib.ref_write_vip_binary(t, len(t), path.encode()))
+
+    def load_vip_binary(self, path, cap=1 << 24):
+        out = np.zeros(cap, np.float64)
+        n = c_u64()
+        self._check(self.lib.ref_load_vip_binary(path.encode(), out, cap, C.byref(n)))
+        return out[:n.value].copy()
+
+    def simulate_streams(self, g: CSR, roles, labels, K, fanouts, b, E, seed, cached, trace_path=None,
+                         costs_path=None, orderings=None, gamma=0.0):
+        offs = np.zeros(K + 1, np.uint64)
+        offs[1:] = np.cumsum([len(c) for c in cached])
+        cat = _a32(np.concatenate([np.asarray(c, np.uint32) for c in cached]) if K else [])
+        cells = np.zeros(E * K * 3, np.uint64)
+        f = _a32(fanouts)
+        oc = oo = None
+        if orderings is not None:
+            oo = np.zeros(K + 1, np.uint64)
+            oo[1:] = np.cumsum([len(o) for o in orderings])
+            oc = _a32(np.concatenate([np.asarray(o, np.uint32) for o in orderings]))
+        self._check(self.lib.ref_simulate_streams(
+            self._graph(g), np.ascontiguousarray(roles, np.uint8), _a32(labels), K, f, len(f), b, E, seed, cat, offs,
+            None if trace_path is None else trace_path.encode(), None if costs_path is None else costs_path.encode(),
+            None if oc is None else oc.ctypes.data, None if oo is None else oo.ctypes.data, gamma, cells))
+        return cells.reshape(E, K, 3)
 
     def context(self, roles, labels, K):
         """(VertexRoles, PartitionMap) built once; .epoch(k, b, e, seed) ->

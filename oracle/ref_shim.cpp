@@ -16,6 +16,8 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <fstream>
+#include <iostream>
 #include <string>
 #include <vector>
 
@@ -34,6 +36,11 @@ using namespace vipkit;
 namespace {
 
 thread_local std::string g_err;
+
+// libstdc++ is linked statically into this .so: construct the standard
+// streams' locale state at load time so the reference's formatted ofstream
+// writers (write_roles, simulate's CSV streams) work when dlopen'ed.
+const std::ios_base::Init g_ios_init;
 
 // Same numbering as include/vipkit_b200.h (vk_status).
 int code_of(const std::exception& e) {
@@ -342,6 +349,59 @@ int ref_sample_neighbors(void* gp, std::uint32_t v, std::uint32_t fanout, std::u
   });
 }
 
+// sample_neighbors with the stream's final state and optional seed_keys.
+int ref_sample_neighbors_state(void* gp, std::uint32_t v, std::uint32_t fanout, std::uint64_t key,
+                               const std::uint32_t* seed_keys, std::uint32_t* out, std::uint64_t* out_count,
+                               std::uint64_t* next_draw) {
+  return guard([&] {
+    const Graph& g = *static_cast<Graph*>(gp);
+    RngStream s(key);
+    std::vector<vertex_t> o, keys;
+    if (seed_keys) keys.assign(seed_keys, seed_keys + g.num_vertices());
+    sample_neighbors(g, v, fanout, s, o, seed_keys ? &keys : nullptr);  // sampling.cpp:72-92
+    std::memcpy(out, o.data(), o.size() * 4);
+    *out_count = o.size();
+    *next_draw = s.next_u64();  // where the stream stands afterwards
+  });
+}
+
+// ---- file formats: the reference's own readers and writers ----
+int ref_write_partition_labels(const std::uint32_t* labels, std::uint64_t n, std::uint32_t K, const char* path) {
+  return guard([&] { write_partition_labels(make_part(labels, n, K), path); });  // graph.cpp:624
+}
+int ref_partition_from_file(const char* path, std::uint32_t K, std::uint64_t n, std::uint32_t* labels_out,
+                            std::uint32_t* K_out) {
+  return guard([&] {
+    const PartitionMap pm = partition_from_file(path, K, n);  // graph.cpp:461
+    std::memcpy(labels_out, pm.part_of.data(), n * 4);
+    *K_out = pm.K;
+  });
+}
+int ref_write_roles(const std::uint8_t* roles, std::uint64_t n, const char* path) {
+  return guard([&] { write_roles(make_roles_view(roles, n), path); });  // graph.cpp:618
+}
+int ref_load_roles(const char* path, std::uint8_t* out, std::uint64_t cap, std::uint64_t* n) {
+  return guard([&] {
+    const VertexRoles r = load_roles(path);  // graph.cpp:600
+    *n = r.role.size();
+    std::memcpy(out, r.role.data(), std::min<std::uint64_t>(cap, r.role.size()));
+  });
+}
+int ref_write_vip_binary(const double* total, std::uint64_t n, const char* path) {
+  return guard([&] {
+    VipScores s;
+    s.total.assign(total, total + n);
+    write_vip_binary(s, path);  // vip.cpp:107
+  });
+}
+int ref_load_vip_binary(const char* path, double* out, std::uint64_t cap, std::uint64_t* n) {
+  return guard([&] {
+    const auto v = load_vip_binary(path);  // vip.cpp:122
+    *n = v.size();
+    std::memcpy(out, v.data(), std::min<std::uint64_t>(cap, v.size()) * 8);
+  });
+}
+
 // Batched driver for the CPU baseline: expands minibatches [i0, i1) of one
 // (epoch, partition) cell with `threads` workers over independent minibatches
 // (expand is pure, sampling.cpp:82 thread_local scratch) and classifies each
@@ -513,6 +573,48 @@ int ref_build_cache(const std::uint32_t* orders, const std::uint64_t* order_offs
 
 // simulate (commsim.cpp:77-127) with a plan rebuilt from per-partition
 // cached id lists; cells_out is E*K*3 (local, cache, miss), epoch-major.
+// simulate with SimulateOptions' trace / batch_costs streams written to
+// files (commsim.cpp:104-118) and the optional GPU-prefix split.
+int ref_simulate_streams(void* gp, const std::uint8_t* roles, const std::uint32_t* labels, std::uint32_t K,
+                         const std::uint32_t* fan, std::uint32_t L, std::uint64_t b, std::uint64_t E,
+                         std::uint64_t seed, const std::uint32_t* cached, const std::uint64_t* cached_off,
+                         const char* trace_path, const char* costs_path, const std::uint32_t* orderings,
+                         const std::uint64_t* ordering_off, double gamma, std::uint64_t* cells_out) {
+  return guard([&] {
+    const Graph& g = *static_cast<Graph*>(gp);
+    const std::uint64_t n = g.num_vertices();
+    CachePlan plan = CachePlan::empty(K, n);
+    for (std::uint32_t k = 0; k < K; ++k)
+      for (std::uint64_t i = cached_off[k]; i < cached_off[k + 1]; ++i) {
+        plan.cached[k].push_back(cached[i]);
+        plan.member_bits[k][cached[i] >> 6] |= 1ull << (cached[i] & 63);
+      }
+    std::ofstream tr, bc;
+    SimulateOptions opts;
+    if (trace_path) {
+      tr.open(trace_path);
+      opts.trace = &tr;
+    }
+    if (costs_path) {
+      bc.open(costs_path);
+      opts.batch_costs = &bc;
+    }
+    std::vector<std::vector<vertex_t>> ords;
+    if (orderings) {
+      for (std::uint32_t k = 0; k < K; ++k) ords.emplace_back(orderings + ordering_off[k], orderings + ordering_off[k + 1]);
+      opts.gpu_orderings = &ords;
+      opts.gamma = gamma;
+    }
+    const CommReport r = simulate(g, make_roles_view(roles, n), make_part(labels, n, K), make_fanouts(fan, L), b, E,
+                                  SeedSpec{seed}, plan, opts);
+    for (std::size_t c = 0; c < r.cells.size(); ++c) {
+      cells_out[3 * c] = r.cells[c].local_hits;
+      cells_out[3 * c + 1] = r.cells[c].cache_hits;
+      cells_out[3 * c + 2] = r.cells[c].remote_misses;
+    }
+  });
+}
+
 int ref_simulate(void* gp, const std::uint8_t* roles, const std::uint32_t* labels, std::uint32_t K,
                  const std::uint32_t* fan, std::uint32_t L, std::uint64_t b, std::uint64_t E,
                  std::uint64_t seed, const std::uint32_t* cached, const std::uint64_t* cached_off,

@@ -1651,6 +1651,97 @@ int vk_sampler_copy_relabel(vk_sampler s, uint32_t mb, uint32_t hop, uint32_t* a
   });
 }
 
+// sample_neighbors (sampling.cpp:72-92) for one vertex, one device thread:
+// deg <= f copies the row in CSR order, else a partial Fisher-Yates over the
+// row (or over the row ordered by seed key, `sorted`) with the sparse
+// displaced-position map in global scratch; the caller's stream state is
+// advanced in place.
+__global__ void k_sample_vertex(const std::uint64_t* __restrict__ off, const std::uint32_t* __restrict__ tgt,
+                                const std::uint32_t* __restrict__ sorted, std::uint32_t v, std::uint32_t f,
+                                std::uint64_t* __restrict__ counter, std::uint32_t* __restrict__ out,
+                                std::uint32_t* __restrict__ cnt, std::uint32_t* __restrict__ hp,
+                                std::uint32_t* __restrict__ hv) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const std::uint64_t o0 = off[v];
+  const std::uint32_t deg = (std::uint32_t)(off[v + 1] - o0);
+  if (deg <= f) {
+    for (std::uint32_t i = 0; i < deg; ++i) out[i] = tgt[o0 + i];
+    *cnt = deg;
+    return;
+  }
+  const std::uint32_t* row = sorted ? sorted : tgt + o0;
+  Stream s(0);
+  s.counter = *counter;
+  // out[0..f) holds positions [0, f); positions >= f displaced by a swap in (hp, hv)
+  for (std::uint32_t i = 0; i < f; ++i) out[i] = row[i];
+  std::uint32_t nh = 0;
+  for (std::uint32_t i = 0; i < f; ++i) {
+    const std::uint32_t j = i + (std::uint32_t)s.next_below((std::uint64_t)(deg - i));
+    const std::uint32_t vi = out[i];
+    std::uint32_t vj;
+    if (j < f) {
+      vj = out[j];
+      out[j] = vi;
+    } else {
+      std::uint32_t c = 0;
+      while (c < nh && hp[c] != j) ++c;
+      if (c < nh) {
+        vj = hv[c];
+        hv[c] = vi;
+      } else {
+        vj = row[j];
+        hp[nh] = j;
+        hv[nh] = vi;
+        ++nh;
+      }
+    }
+    out[i] = vj;  // scratch[i] after the swap
+  }
+  *counter = s.counter;
+  *cnt = f;
+}
+
+int vk_graph_sample_neighbors(vk_graph g, uint32_t v, uint32_t fanout, uint64_t* stream_state,
+                              const uint32_t* neighbor_keys, uint32_t* out, uint64_t* out_count) {
+  return guard([&] {
+    if (!g || !stream_state || !out || !out_count) raise(VK_ERR_PARAMETER, "null argument");
+    if (v >= g->n) raise(VK_ERR_RANGE, "vertex id out of range");
+    DeviceGuard dg(g->device);
+    std::uint64_t o[2];
+    VK_CUDA(cudaMemcpy(o, g->d_off() + v, 16, cudaMemcpyDeviceToHost));
+    const std::uint64_t deg = o[1] - o[0];
+    const std::uint64_t take = std::min<std::uint64_t>(deg, fanout);
+    DevBuf d_out(std::max<std::uint64_t>(1, take) * 4), d_state(8), d_cnt(4),
+        d_hp(std::max<std::uint64_t>(1, take) * 4), d_hv(std::max<std::uint64_t>(1, take) * 4);
+    VK_CUDA(cudaMemcpy(d_state.p, stream_state, 8, cudaMemcpyHostToDevice));
+    DevBuf sorted;
+    if (neighbor_keys && deg > fanout) {
+      // the row ordered by the neighbours' seed keys (sampling.cpp:83-85):
+      // one radix sort of (key, neighbour) pairs
+      DevBuf k_in(deg * 4), k_out(deg * 4);
+      sorted.alloc(deg * 4);
+      VK_CUDA(cudaMemcpy(k_in.p, neighbor_keys, deg * 4, cudaMemcpyHostToDevice));
+      std::size_t tmp = 0;
+      VK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k_in.as<std::uint32_t>(), k_out.as<std::uint32_t>(),
+                                              g->d_tgt() + o[0], sorted.as<std::uint32_t>(), (std::int64_t)deg));
+      DevBuf tb(std::max<std::size_t>(tmp, 1));
+      VK_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, tmp, k_in.as<std::uint32_t>(), k_out.as<std::uint32_t>(),
+                                              g->d_tgt() + o[0], sorted.as<std::uint32_t>(), (std::int64_t)deg));
+      count_launch(4);
+    }
+    k_sample_vertex<<<1, 32>>>(g->d_off(), g->d_tgt(), sorted.p ? sorted.as<std::uint32_t>() : nullptr, v, fanout,
+                               d_state.as<std::uint64_t>(), d_out.as<std::uint32_t>(), d_cnt.as<std::uint32_t>(),
+                               d_hp.as<std::uint32_t>(), d_hv.as<std::uint32_t>());
+    count_launch();
+    VK_LAUNCH_CHECK();
+    std::uint32_t c = 0;
+    VK_CUDA(cudaMemcpy(&c, d_cnt.p, 4, cudaMemcpyDeviceToHost));
+    VK_CUDA(cudaMemcpy(out, d_out.p, (std::uint64_t)c * 4, cudaMemcpyDeviceToHost));
+    VK_CUDA(cudaMemcpy(stream_state, d_state.p, 8, cudaMemcpyDeviceToHost));
+    *out_count = c;
+  });
+}
+
 int vk_debug_stream_draws(int device, uint64_t key, uint64_t bound, uint64_t count, uint64_t* out) {
   return guard([&] {
     if (!out) raise(VK_ERR_PARAMETER, "null argument");

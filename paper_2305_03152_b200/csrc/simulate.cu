@@ -13,6 +13,7 @@
 // ranking prefixes build_cache produces, policies.cpp:149-163), so a vertex
 // at list position p is a hit for every plan with takes > p.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -54,17 +55,23 @@ __global__ void __launch_bounds__(256) k_classify_plans(const std::uint32_t* __r
                                                         const std::uint32_t* __restrict__ pos, std::uint64_t n,
                                                         const std::uint64_t* __restrict__ takes, std::uint32_t K,
                                                         std::uint32_t A, std::uint64_t cells_per_plan,
-                                                        unsigned long long* __restrict__ cells) {
-  __shared__ unsigned long long s_cnt[2 + kMaxPlans];
+                                                        unsigned long long* __restrict__ cells,
+                                                        unsigned long long* __restrict__ batch_cnt,
+                                                        std::uint64_t batch_base,
+                                                        const std::uint32_t* __restrict__ gpu_pos,
+                                                        const std::uint64_t* __restrict__ gpu_cut) {
+  __shared__ unsigned long long s_cnt[3 + kMaxPlans];
   const std::uint32_t mb = blockIdx.y;
   const std::uint32_t cell = cell_of[mb];
   const std::uint32_t k = cell % K;
-  for (std::uint32_t i = threadIdx.x; i < 2 + A; i += blockDim.x) s_cnt[i] = 0;
+  for (std::uint32_t i = threadIdx.x; i < 3 + A; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
   std::uint64_t tk[kMaxPlans];
 #pragma unroll
   for (std::uint32_t a = 0; a < kMaxPlans; ++a) tk[a] = a < A ? takes[a * K + k] : 0;
-  unsigned long long local = 0, remote = 0;
+  unsigned long long local = 0, remote = 0, gpu_local = 0;
+  const std::uint32_t* gp = gpu_pos ? gpu_pos + (std::uint64_t)k * n : nullptr;
+  const std::uint64_t cut = gpu_pos ? gpu_cut[k] : 0;
   unsigned hits[kMaxPlans];
 #pragma unroll
   for (std::uint32_t a = 0; a < kMaxPlans; ++a) hits[a] = 0;
@@ -75,6 +82,7 @@ __global__ void __launch_bounds__(256) k_classify_plans(const std::uint32_t* __r
     const std::uint32_t v = __ldg(av + r);
     if (__ldg(part_of + v) == k) {
       ++local;
+      if (gp && __ldg(gp + v) < cut) ++gpu_local;  // SimulateOptions GPU-prefix split
     } else {
       ++remote;
       const std::uint32_t p = __ldg(pk + v);
@@ -90,26 +98,35 @@ __global__ void __launch_bounds__(256) k_classify_plans(const std::uint32_t* __r
   };
   local = wsum(local);
   remote = wsum(remote);
+  gpu_local = wsum(gpu_local);
   const bool lead = (threadIdx.x & 31) == 0;
   if (lead) {
     atomicAdd(&s_cnt[0], local);
     atomicAdd(&s_cnt[1], remote);
+    atomicAdd(&s_cnt[2], gpu_local);
   }
 #pragma unroll
   for (std::uint32_t a = 0; a < kMaxPlans; ++a) {
     if (a < A) {
       const unsigned long long h = wsum(hits[a]);
-      if (lead) atomicAdd(&s_cnt[2 + a], h);
+      if (lead) atomicAdd(&s_cnt[3 + a], h);
     }
   }
   __syncthreads();
   if (threadIdx.x < A) {
     const std::uint32_t a = threadIdx.x;
     unsigned long long* cl = cells + a * cells_per_plan + (std::uint64_t)cell * 3;
-    const unsigned long long h = s_cnt[2 + a];
+    const unsigned long long h = s_cnt[3 + a];
     if (s_cnt[0]) atomicAdd(cl + 0, s_cnt[0]);
     if (h) atomicAdd(cl + 1, h);
     if (s_cnt[1] - h) atomicAdd(cl + 2, s_cnt[1] - h);
+  }
+  if (batch_cnt && threadIdx.x == 0) {  // per-minibatch rows of plan 0: local, gpu local, cache, miss
+    unsigned long long* bc = batch_cnt + (batch_base + mb) * 4;
+    atomicAdd(bc + 0, s_cnt[0]);
+    atomicAdd(bc + 1, s_cnt[2]);
+    atomicAdd(bc + 2, s_cnt[3]);
+    atomicAdd(bc + 3, s_cnt[1] - s_cnt[3]);
   }
 }
 
@@ -214,11 +231,19 @@ using namespace vk;
 
 extern "C" {
 
-int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, const uint32_t* fanouts,
-                uint32_t num_hops, uint64_t batch_size, uint64_t epochs, uint64_t global_seed,
-                const uint32_t* seed_keys, const uint32_t* cached_ids, const uint64_t* cached_offsets, const uint64_t* takes,
-                uint32_t num_plans, uint32_t wave, uint64_t* cells) {
-  return guard([&] {
+}  // extern "C"
+
+namespace {
+// vk_simulate / vk_simulate_batches: batch_rows (optional) receives one row
+// per minibatch in for_each_expansion order {epoch, batch_index, partition,
+// local - gpu, gpu, cache, miss} for plan 0 (commsim.cpp:104-118).
+void simulate_core(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, const uint32_t* fanouts,
+                   uint32_t num_hops, uint64_t batch_size, uint64_t epochs, uint64_t global_seed,
+                   const uint32_t* seed_keys, const uint32_t* cached_ids, const uint64_t* cached_offsets,
+                   const uint64_t* takes, uint32_t num_plans, uint32_t wave, uint64_t* cells,
+                   const uint32_t* const* gpu_orderings, const uint64_t* gpu_ordering_sizes, double gamma,
+                   uint64_t* batch_rows, uint64_t batch_rows_capacity, uint64_t* num_batches) {
+  {
     if (!g || !roles || !part_of || !fanouts || !cached_offsets || !cells) raise(VK_ERR_PARAMETER, "null argument");
     if (K == 0) raise(VK_ERR_PARAMETER, "need at least one partition");
     if (batch_size == 0) raise(VK_ERR_PARAMETER, "batch size must be >= 1");  // sampling.cpp:50-53
@@ -265,6 +290,51 @@ int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint3
     d_cells.alloc(std::max<std::uint64_t>(1, A * ncell * 3 * 8));
     VK_CUDA(cudaMemset(d_cells.p, 0, d_cells.bytes));
     d_cell_of.alloc(2 * M * 4);  // double-buffered: the host fills wave i+1 while wave i runs
+    // per-minibatch rows (SimulateOptions::batch_costs): the minibatch count
+    // in for_each order, device counters [total][4], refs kept on the host
+    DevBuf d_batch, d_gpu_pos, d_gpu_cut;
+    std::vector<std::uint64_t> batch_refs;  // epoch, batch_index, partition
+    if (batch_rows || num_batches) {
+      std::vector<std::uint64_t> T(K, 0);
+      for (std::uint64_t v = 0; v < n; ++v)
+        if (roles[v] == 0) ++T[part_of[v]];
+      std::uint64_t total = 0;
+      for (std::uint32_t k = 0; k < K; ++k) total += (T[k] + batch_size - 1) / batch_size;
+      total *= epochs;
+      if (num_batches) *num_batches = total;
+      if (batch_rows && batch_rows_capacity < total) raise(VK_ERR_SHAPE, "batch_rows capacity below the minibatch count");
+      if (batch_rows) {
+        d_batch.alloc(std::max<std::uint64_t>(1, total) * 4 * 8);
+        VK_CUDA(cudaMemset(d_batch.p, 0, d_batch.bytes));
+        batch_refs.reserve(total * 3);
+        for (std::uint64_t e = 0; e < epochs; ++e)  // for_each_expansion order (commsim.cpp:45-52)
+          for (std::uint32_t k = 0; k < K; ++k)
+            for (std::uint64_t i = 0; i * batch_size < T[k]; ++i) {
+              batch_refs.push_back(e);
+              batch_refs.push_back(i);
+              batch_refs.push_back(k);
+            }
+      }
+    }
+    if (batch_rows && gpu_orderings) {
+      // gpu_threshold_pos / gpu_cut of commsim.cpp:91-102
+      std::vector<std::uint32_t> pos((std::uint64_t)K * n, 0xffffffffu);
+      std::vector<std::uint64_t> cut(K);
+      for (std::uint32_t k = 0; k < K; ++k) {
+        const std::uint64_t sz = gpu_ordering_sizes[k];
+        for (std::uint64_t i = 0; i < sz; ++i) {
+          const std::uint32_t v = gpu_orderings[k][i];
+          if (v >= n) raise(VK_ERR_RANGE, "gpu ordering vertex out of range");
+          pos[(std::uint64_t)k * n + v] = (std::uint32_t)std::min<std::uint64_t>(i, 0xfffffffeu);
+        }
+        cut[k] = (std::uint64_t)std::floor(gamma * (double)sz + 1e-9);
+      }
+      d_gpu_pos.alloc(pos.size() * 4);
+      VK_CUDA(cudaMemcpy(d_gpu_pos.p, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice));
+      d_gpu_cut.alloc(K * 8);
+      VK_CUDA(cudaMemcpy(d_gpu_cut.p, cut.data(), K * 8, cudaMemcpyHostToDevice));
+    }
+    std::uint64_t batch_base = 0;
     VK_CUDA(cudaDeviceSynchronize());
     PinnedBuf cell_host;
     cell_host.ensure(2 * M * 4);
@@ -292,7 +362,11 @@ int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint3
                             1, std::min<std::uint64_t>(ceil_div(stride, 256 * 8), 64));
                         k_classify_plans<<<dim3(gx, nmb), 256, 0, st>>>(
                             all, stride, count, cd, d_part.as<std::uint32_t>(), d_pos.as<std::uint32_t>(), n,
-                            d_takes.as<std::uint64_t>(), K, A, ncell * 3, d_cells.as<unsigned long long>());
+                            d_takes.as<std::uint64_t>(), K, A, ncell * 3, d_cells.as<unsigned long long>(),
+                            d_batch.p ? d_batch.as<unsigned long long>() : nullptr, batch_base,
+                            d_gpu_pos.p ? d_gpu_pos.as<std::uint32_t>() : nullptr,
+                            d_gpu_cut.p ? d_gpu_cut.as<std::uint64_t>() : nullptr);
+                        batch_base += nmb;
                         count_launch();
                         VK_LAUNCH_CHECK();
                         VK_CUDA(cudaEventRecord(copied[parity], st));
@@ -301,6 +375,47 @@ int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint3
     std::vector<unsigned long long> host(A * ncell * 3);
     if (!host.empty()) VK_CUDA(cudaMemcpy(host.data(), d_cells.p, host.size() * 8, cudaMemcpyDeviceToHost));
     for (std::size_t i = 0; i < host.size(); ++i) cells[i] = host[i];
+    if (batch_rows) {
+      std::vector<unsigned long long> bc(batch_base * 4);
+      if (!bc.empty()) VK_CUDA(cudaMemcpy(bc.data(), d_batch.p, bc.size() * 8, cudaMemcpyDeviceToHost));
+      for (std::uint64_t i = 0; i < batch_base; ++i) {
+        std::uint64_t* r = batch_rows + i * 7;
+        r[0] = batch_refs[3 * i];
+        r[1] = batch_refs[3 * i + 1];
+        r[2] = batch_refs[3 * i + 2];
+        r[3] = bc[4 * i] - bc[4 * i + 1];
+        r[4] = bc[4 * i + 1];
+        r[5] = bc[4 * i + 2];
+        r[6] = bc[4 * i + 3];
+      }
+    }
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int vk_simulate(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K, const uint32_t* fanouts,
+                uint32_t num_hops, uint64_t batch_size, uint64_t epochs, uint64_t global_seed,
+                const uint32_t* seed_keys, const uint32_t* cached_ids, const uint64_t* cached_offsets, const uint64_t* takes,
+                uint32_t num_plans, uint32_t wave, uint64_t* cells) {
+  return guard([&] {
+    simulate_core(g, roles, part_of, K, fanouts, num_hops, batch_size, epochs, global_seed, seed_keys, cached_ids,
+                  cached_offsets, takes, num_plans, wave, cells, nullptr, nullptr, 0.0, nullptr, 0, nullptr);
+  });
+}
+
+int vk_simulate_batches(vk_graph g, const uint8_t* roles, const uint32_t* part_of, uint32_t K,
+                        const uint32_t* fanouts, uint32_t num_hops, uint64_t batch_size, uint64_t epochs,
+                        uint64_t global_seed, const uint32_t* seed_keys, const uint32_t* cached_ids,
+                        const uint64_t* cached_offsets, const uint32_t* const* gpu_orderings,
+                        const uint64_t* gpu_ordering_sizes, double gamma, uint64_t* cells, uint64_t* batch_rows,
+                        uint64_t batch_rows_capacity, uint64_t* num_batches) {
+  return guard([&] {
+    if (gpu_orderings && !gpu_ordering_sizes) raise(VK_ERR_PARAMETER, "null gpu ordering sizes");
+    simulate_core(g, roles, part_of, K, fanouts, num_hops, batch_size, epochs, global_seed, seed_keys, cached_ids,
+                  cached_offsets, nullptr, 1, 0, cells, gpu_orderings, gpu_ordering_sizes, gamma, batch_rows,
+                  batch_rows_capacity, num_batches);
   });
 }
 

@@ -150,6 +150,16 @@ def lib():
                                               C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), u32p]
     L.vk_debug_stream_draws.argtypes = [c_int, c_u64, c_u64, c_u64, u64p]
     L.vk_synth_roles.argtypes = [c_u64, c_double, c_double, c_double, c_u64, u8p]
+    L.vk_graph_sample_neighbors.argtypes = [c_vp, c_u32, c_u32, C.POINTER(c_u64), c_vp, u32p, C.POINTER(c_u64)]
+    L.vk_simulate_batches.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, c_vp, c_vp, u64p,
+                                      c_vp, c_vp, c_double, u64p, c_vp, c_u64, C.POINTER(c_u64)]
+    L.vk_partition_from_file.argtypes = [C.c_char_p, c_u32, c_u64, u32p, C.POINTER(c_u32)]
+    L.vk_write_partition_labels.argtypes = [C.c_char_p, u32p, c_u64]
+    L.vk_load_roles.argtypes = [C.c_char_p, C.POINTER(c_vp), C.POINTER(c_u64)]
+    L.vk_write_roles.argtypes = [C.c_char_p, u8p, c_u64]
+    L.vk_write_vip_binary.argtypes = [C.c_char_p, f64p, c_u64]
+    L.vk_load_vip_binary.argtypes = [C.c_char_p, C.POINTER(c_vp), C.POINTER(c_u64)]
+    L.vk_write_vcsr.argtypes = [C.c_char_p, c_u64, c_u64, u64p, u32p]
     _lib = L
     return L
 
@@ -631,6 +641,99 @@ def simulate(g: Graph, roles, part_of, K, fanouts, b, epochs, seed, cached, take
                             tk.ctypes.data if tk is not None else None, A, wave, cells))
     cells = cells.reshape(A, epochs, K, 3)
     return cells if takes is not None else cells[0]
+
+
+def simulate_batches(g: Graph, roles, part_of, K, fanouts, b, epochs, seed, cached, seed_keys=None,
+                     gpu_orderings=None, gamma=0.0):
+    """simulate with SimulateOptions::batch_costs (commsim.cpp:104-118) ->
+    (cells[E, K, 3], rows[B, 7]); row = (epoch, batch_index, partition,
+    local - gpu, gpu, cache, miss) in for_each_expansion order."""
+    part_of = _a32(part_of)
+    roles = np.ascontiguousarray(roles, np.uint8)
+    fan = _a32(fanouts)
+    offs = np.zeros(K + 1, np.uint64)
+    offs[1:] = np.cumsum([len(c) for c in cached])
+    ids = _a32(np.concatenate([np.asarray(c, np.uint32) for c in cached]) if K else [])
+    total = epochs * sum((len(train_members(roles, part_of, k)) + b - 1) // b for k in range(K))
+    rows = np.zeros(max(1, total) * 7, np.uint64)
+    cells = np.zeros(epochs * K * 3, np.uint64)
+    sk = None if seed_keys is None else _a32(seed_keys)
+    keep, ptrs, sizes = [], None, None
+    if gpu_orderings is not None:
+        keep = [_a32(o) for o in gpu_orderings]
+        ptrs = (c_vp * K)(*[o.ctypes.data for o in keep])
+        sizes = np.array([len(o) for o in keep], np.uint64)
+    got = c_u64()
+    check(lib().vk_simulate_batches(g.handle, roles, part_of, K, fan, len(fan), b, epochs, seed,
+                                    None if sk is None else sk.ctypes.data, ids.ctypes.data if ids.size else None,
+                                    offs, ptrs, None if sizes is None else sizes.ctypes.data, gamma, cells,
+                                    rows.ctypes.data, total, C.byref(got)))
+    return cells.reshape(epochs, K, 3), rows[:got.value * 7].reshape(-1, 7)
+
+
+def sample_neighbors(g: Graph, v, fanout, stream_state, seed_keys=None, offsets=None, targets=None):
+    """vipkit::sample_neighbors (sampling.hpp:54-56) on the device ->
+    (ids, advanced stream state). stream_state is RngStream's counter
+    (mix64(key) for a fresh stream). With seed_keys, the keys of v's
+    neighbours are marshalled from the host CSR (offsets, targets)."""
+    out = np.zeros(max(1, fanout), np.uint32)
+    cnt, st = c_u64(), c_u64(stream_state)
+    keys = None
+    if seed_keys is not None:
+        if offsets is None:
+            offsets, targets = g.forward()
+        keys = _a32(np.asarray(seed_keys, np.uint32)[targets[int(offsets[v]):int(offsets[v + 1])]])
+    check(lib().vk_graph_sample_neighbors(g.handle, v, fanout, C.byref(st), None if keys is None else keys.ctypes.data,
+                                          out, C.byref(cnt)))
+    return out[:cnt.value].copy(), st.value
+
+
+# ------------------------------------------------------------ file formats
+def partition_from_file(path, K, n):
+    """partition_from_file (graph.hpp:105) -> (part_of, K)."""
+    out = np.zeros(n, np.uint32)
+    k_out = c_u32()
+    check(lib().vk_partition_from_file(os.fsencode(path), K, n, out, C.byref(k_out)))
+    return out, k_out.value
+
+
+def write_partition_labels(part_of, path):
+    p = _a32(part_of)
+    check(lib().vk_write_partition_labels(os.fsencode(path), p, len(p)))
+
+
+def load_roles(path):
+    """load_roles (graph.hpp:119) -> u8 codes."""
+    ptr, n = c_vp(), c_u64()
+    check(lib().vk_load_roles(os.fsencode(path), C.byref(ptr), C.byref(n)))
+    out = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(max(1, n.value),))[:n.value].copy()
+    lib().vk_host_free(ptr)
+    return out
+
+
+def write_roles(roles, path):
+    r = np.ascontiguousarray(roles, np.uint8)
+    check(lib().vk_write_roles(os.fsencode(path), r, len(r)))
+
+
+def write_vip_binary(total, path):
+    """write_vip_binary (vip.hpp:58): n little-endian f64 totals."""
+    t = np.ascontiguousarray(total, np.float64)
+    check(lib().vk_write_vip_binary(os.fsencode(path), t, len(t)))
+
+
+def load_vip_binary(path):
+    ptr, n = c_vp(), c_u64()
+    check(lib().vk_load_vip_binary(os.fsencode(path), C.byref(ptr), C.byref(n)))
+    out = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(max(1, n.value),))[:n.value].copy()
+    lib().vk_host_free(ptr)
+    return out
+
+
+def write_binary_csr(offsets, targets, path):
+    """write_binary_csr (graph.hpp:116): the VCSR file Graph.load_vcsr reads."""
+    off, tgt = _a64(offsets), _a32(targets)
+    check(lib().vk_write_vcsr(os.fsencode(path), len(off) - 1, len(tgt), off, tgt))
 
 
 def access_counts(g: Graph, roles, part_of, K, fanouts, b, epochs, seed):

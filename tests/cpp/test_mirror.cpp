@@ -361,9 +361,11 @@ static void test_reorder_and_replay() {
     for (std::size_t i = 1; i < out.part.members[k].size(); ++i)
       CHECK(out.part.members[k][i] == out.part.members[k][i - 1] + 1);
   const SeedSpec seeds{2024};
+  SimulateOptions replay;
+  replay.seed_keys = &map.old_of_new;
   const CommReport before = simulate(g, roles, part, fan, 8, 3, seeds, CachePlan::empty(2, n));
   const CommReport after =
-      simulate(out.graph, out.roles, out.part, fan, 8, 3, seeds, CachePlan::empty(2, n), &map.old_of_new);
+      simulate(out.graph, out.roles, out.part, fan, 8, 3, seeds, CachePlan::empty(2, n), replay);
   CHECK(before.cells.size() == after.cells.size());
   for (std::size_t i = 0; i < before.cells.size(); ++i) {
     CHECK(before.cells[i].local_hits == after.cells[i].local_hits);
@@ -432,7 +434,51 @@ static void test_sweep_grid() {
   CHECK_THROWS_AS(sweep(g, roles, part, cfg), parameter_error);
 }
 
-int main() {
+// Reference-written inputs (driven by tests/test_gpu_boundary.py): load
+// dir/{graph.vcsr, labels.txt, roles.txt, vip0.bin} through the mirror's
+// readers, run simulate with SimulateOptions{trace, batch_costs,
+// gpu_orderings, gamma}, and write dir/mirror_{trace,costs}.csv for a
+// byte-for-byte comparison with the reference's own output; the VIP vector
+// is written back with write_vip_binary, and one sample_neighbors draw
+// sequence is printed.
+static int reference_files_mode(const std::string& dir) {
+  const Graph g = load_binary_csr(dir + "/graph.vcsr");
+  const PartitionMap part = partition_from_file(dir + "/labels.txt", 0, g.num_vertices());
+  const VertexRoles roles = load_roles(dir + "/roles.txt");
+  const std::vector<double> vip = load_vip_binary(dir + "/vip0.bin");
+  VipScores vs;
+  vs.total = vip;
+  write_vip_binary(vs, dir + "/mirror_vip0.bin");
+  std::vector<Ranking> rk;
+  for (std::uint32_t k = 0; k < part.K; ++k) rk.push_back(rank_by_scores(part, k, vip));
+  const CachePlan plan = build_cache(rk, 0.1, g.num_vertices());
+  std::vector<std::vector<vertex_t>> ords;
+  for (std::uint32_t k = 0; k < part.K; ++k) {
+    ords.push_back(part.members[k]);
+    std::reverse(ords.back().begin(), ords.back().end());
+  }
+  std::ofstream tr(dir + "/mirror_trace.csv"), bc(dir + "/mirror_costs.csv");
+  SimulateOptions opts;
+  opts.trace = &tr;
+  opts.batch_costs = &bc;
+  opts.gpu_orderings = &ords;
+  opts.gamma = 0.3;
+  const CommReport r = simulate(g, roles, part, FanoutSpec{{5, 3}}, 32, 2, SeedSpec{42}, plan, opts);
+  std::printf("cells");
+  for (const auto& c : r.cells) std::printf(" %llu %llu %llu", (unsigned long long)c.local_hits,
+                                            (unsigned long long)c.cache_hits, (unsigned long long)c.remote_misses);
+  std::printf("\ntrain_members0 %zu\n", part.train_members(roles, 0).size());
+  RngStream st(SeedSpec{7}.key({1, 2}));
+  std::vector<vertex_t> out;
+  sample_neighbors(g, 0, 4, st, out);
+  std::printf("sample0");
+  for (vertex_t v : out) std::printf(" %u", v);
+  std::printf("\nnext %llu\n", (unsigned long long)st.next_u64());
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc == 3 && std::string(argv[1]) == "--reference-files") return reference_files_mode(argv[2]);
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"initial probabilities", test_initial_probabilities},
       {"3-path hand values", test_three_path_hand_values},
