@@ -164,10 +164,16 @@ typedef struct vk_sampler_config {
   uint32_t fanouts[VK_MAX_HOPS];    /* FanoutSpec::fanouts (sampling.hpp:14-21) */
   uint64_t batch_size;              /* max seeds per minibatch (b) */
   uint32_t max_minibatches;         /* minibatches per wave (device batching) */
-  uint32_t flags;                   /* reserved, 0 */
+  uint32_t flags;                   /* VK_SAMPLER_* frontier representation, 0 = automatic */
   uint64_t global_seed;             /* SeedSpec::global_seed (rng.hpp:59) */
 } vk_sampler_config;
 
+/* Frontier representation (results are identical): dense = n-bit bitmaps per
+ * minibatch (graphs where a frontier covers a sizeable fraction of n), sparse
+ * = vertex-range buckets deduplicated in shared memory (papers-scale graphs).
+ * Automatic: sparse when n >= 16 x the per-minibatch vertex capacity. */
+#define VK_SAMPLER_FORCE_DENSE 1u
+#define VK_SAMPLER_FORCE_SPARSE 2u
 VK_API int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out);
 VK_API int vk_sampler_destroy(vk_sampler s);
 /* seed_keys replay (sampling.hpp:43-64, `seed_keys` of expand /

@@ -35,6 +35,7 @@ void sampler_internal(vk_sampler_s* s, const std::uint32_t** all, std::uint64_t*
 std::uint64_t sampler_desc_stride();
 void sampler_all_rank(vk_sampler_s* s, const uint4** rank, std::uint64_t* W);
 bool sampler_all_rank_dense(vk_sampler_s* s);
+const std::uint32_t* sampler_tile_base(vk_sampler_s* s, std::uint32_t* bucket_bits, std::uint32_t* nb);
 std::uint64_t sampler_run_id(vk_sampler_s* s);
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out);
 cudaEvent_t sampler_done_event(vk_sampler_s* s);
@@ -210,6 +211,10 @@ struct GatherParams {
   unsigned long long* counts;        // [nmb][4]
   // vertex-tile schedule: CTA b serves minibatch b % nmb, vertex tile b / nmb
   const uint4* all_rank;             // [nmb][W] {bits, rank prefix} of all_vertices
+  // sparse frontiers instead: rank of each all-level bucket's first vertex
+  // [nmb][tb_nb + 1]; a gather tile is tb_group consecutive buckets
+  const std::uint32_t* tile_base;
+  std::uint32_t tb_nb, tb_group;
   std::uint64_t W;
   std::uint32_t nmb, tiles, tile_words;
   // deduplicated remote rows: staged[rank of new_id[v] in the wave's remote
@@ -223,6 +228,24 @@ struct GatherParams {
   int st_variant;  // VK_GATHER_ST: 0 .cs (evict-first), 1 plain, 2 L1::no_allocate
   int ld_variant;  // VK_GATHER_LD: 0 nc/no_allocate, 1 +L2 evict_last policy, 2 +evict_normal, 3 coherent
 };
+
+// The all_vertices index range [lo, hi) of vertex tile `tile` of minibatch
+// mb: from the dense rank words at tile starts, or (sparse frontiers) from the
+// all-level bucket bases.
+__device__ __forceinline__ void tile_range(const GatherParams& p, std::uint32_t mb, std::uint32_t tile,
+                                           std::uint32_t cnt, std::uint32_t& lo, std::uint32_t& hi) {
+  if (p.tile_base) {
+    const std::uint32_t* tb = p.tile_base + (std::uint64_t)mb * (p.tb_nb + 1);
+    const std::uint32_t b0 = tile * p.tb_group;
+    lo = b0 < p.tb_nb ? tb[b0] : cnt;
+    hi = tb[min(b0 + p.tb_group, p.tb_nb)];
+    return;
+  }
+  const uint4* rk = p.all_rank + mb * p.W;
+  const std::uint64_t w0 = (std::uint64_t)tile * p.tile_words, w1 = w0 + p.tile_words;
+  lo = w0 < p.W ? rk[w0].z : cnt;
+  hi = w1 < p.W ? rk[w1].z : cnt;
+}
 
 // Row of flattened element e (< 32 V) of a warp's 32 rows: umulhi with
 // ceil(2^32/V) is exact while V*V < 2^27 (V <= 11585); above that it can
@@ -485,10 +508,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   const std::uint32_t tile = unit / p.nmb;
   const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
   const std::uint32_t cnt = p.all_count[mb];
-  const uint4* rk = p.all_rank + mb * p.W;
-  const std::uint64_t w0 = (std::uint64_t)tile * p.tile_words, w1 = w0 + p.tile_words;
-  const std::uint32_t lo = w0 < p.W ? rk[w0].z : cnt;
-  const std::uint32_t hi = w1 < p.W ? rk[w1].z : cnt;
+  std::uint32_t lo, hi;
+  tile_range(p, mb, tile, cnt, lo, hi);
   const std::uint32_t* all = p.all + mb * p.all_stride;
   const std::uint32_t* slot = p.slot[k];
   const std::uint32_t nl = p.nlocal[k];
@@ -633,10 +654,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) k_gather_tma(GatherParams p
     const std::uint32_t tile = unit / p.nmb;
     const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
     const std::uint32_t cnt = p.all_count[mb];
-    const uint4* rk = p.all_rank + mb * p.W;
-    const std::uint64_t w0 = (std::uint64_t)tile * p.tile_words, w1 = w0 + p.tile_words;
-    const std::uint32_t lo = w0 < p.W ? rk[w0].z : cnt;
-    const std::uint32_t hi = w1 < p.W ? rk[w1].z : cnt;
+    std::uint32_t lo, hi;
+    tile_range(p, mb, tile, cnt, lo, hi);
     const std::uint32_t* all = p.all + mb * p.all_stride;
     const std::uint32_t* slot = p.slot[k];
     const std::uint32_t nl = p.nlocal[k];
@@ -1157,6 +1176,16 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
     std::uint64_t tw = std::max<std::uint64_t>(tile_words, (want_words + 63) / 64 * 64);
     gp.tile_words = (std::uint32_t)tw;
     gp.tiles = (std::uint32_t)((gp.W + tw - 1) / tw);
+    {
+      std::uint32_t bbits = 0, nb = 0;
+      gp.tile_base = sampler_tile_base(s, &bbits, &nb);
+      if (gp.tile_base) {  // sparse frontiers: tiles of whole buckets, ~unit_rows rows each
+        const double rows_per_bucket = std::max(1.0, (double)gp.all_stride / (double)nb);
+        gp.tb_nb = nb;
+        gp.tb_group = (std::uint32_t)std::max(1.0, std::round(unit_rows / rows_per_bucket));
+        gp.tiles = (nb + gp.tb_group - 1) / gp.tb_group;
+      }
+    }
     const char* cap_env = std::getenv("VK_GATHER_CTAS_PER_SM");
     const std::uint64_t units = (std::uint64_t)gp.tiles * nmb;
     const int cap_per_sm = cap_env ? std::atoi(cap_env) : 0;

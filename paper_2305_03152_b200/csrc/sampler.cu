@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <type_traits>
 #include <cstring>
 #include <vector>
@@ -60,6 +61,14 @@ struct vk_sampler_s {
   // that costs no more than the id list itself (16 W <= 4 capAll): the plane
   // then derives the wave's remote-miss set from the bitmaps word by word
   bool dense_all_rank = false;
+  // sparse frontiers (frontier_sparse.cuh): bucket bits per level ([0] = all
+  // level, [h] = hop h), bucket workspaces sized for the largest level
+  bool sparse = false;
+  std::uint32_t bb[VK_MAX_HOPS + 1]{};
+  std::uint32_t nb_max = 0;
+  std::uint64_t pair_stride = 0;
+  vk::DevBuf bhist, bstart, bcursor, bstatus, pairs, tile_base;
+  std::uint32_t nbuckets(std::uint32_t level) const { return (std::uint32_t)((n + (1ull << bb[level]) - 1) >> bb[level]); }
   vk::DevBuf F[VK_MAX_HOPS + 1], allidx[VK_MAX_HOPS + 1], indptr[VK_MAX_HOPS + 1], dst[VK_MAX_HOPS + 1];
   vk::DevBuf counts;  // u32: fcount[(L+1)*M] | ecount[(L+1)*M] | allcount[M] | err[1]
   vk::DevBuf edges_tmp, all, hopbits, allbits, hopprefix, allprefix, status, tickets, desc, seed_stage;
@@ -121,7 +130,7 @@ __global__ void __launch_bounds__(1024) k_prepare(const WaveDesc* __restrict__ d
   const WaveDesc d = desc[mb];
   std::uint32_t* f0 = F0 + mb * capF0;
   std::uint32_t* ip = indptr1 + mb * (capF0 + 1);
-  unsigned long long* ab = allbits + mb * W;
+  unsigned long long* ab = allbits ? allbits + mb * W : nullptr;
   unsigned long long carry = 0;
   for (std::uint32_t base = 0; base < d.seed_count; base += blockDim.x) {
     const std::uint32_t i = base + threadIdx.x;
@@ -133,7 +142,7 @@ __global__ void __launch_bounds__(1024) k_prepare(const WaveDesc* __restrict__ d
         v = 0;
       }
       f0[i] = v;
-      atomicOr(ab + (v >> 6), 1ull << (v & 63));
+      if (ab) atomicOr(ab + (v >> 6), 1ull << (v & 63));
       c = min(f1, outdeg[v]);
     }
     unsigned long long tot;
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(1024) k_prepare(const WaveDesc* __restrict__ d
 // Frontier bitmap insert: a 32-bit RED on the half of the 64-bit word that
 // holds v (little-endian halves), no return value.
 __device__ __forceinline__ void set_bit(unsigned long long* hb, std::uint32_t v) {
-  atomicOr(reinterpret_cast<unsigned*>(hb) + (v >> 5), 1u << (v & 31));
+  if (hb) atomicOr(reinterpret_cast<unsigned*>(hb) + (v >> 5), 1u << (v & 31));  // null: sparse frontiers
 }
 
 // Sparse partial Fisher-Yates, same draws as sampling.cpp:87-91: the value
@@ -348,7 +357,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_smem(SampleParams p) 
   const std::uint32_t* fp = p.Fprev + mb * p.capFprev;
   const std::uint32_t* ip = p.indptr + mb * (p.capFprev + 1);
   std::uint32_t* ed = p.edges + mb * p.capS;
-  unsigned long long* hb = p.hopbits + mb * p.W;
+  unsigned long long* hb = p.hopbits ? p.hopbits + mb * p.W : nullptr;
   for (std::uint32_t j0 = jstart; j0 < cnt; j0 += jstride) {
     const std::uint32_t j = j0 + lane;
     const std::uint32_t base = ip[j0];
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
   const std::uint32_t* fp = p.Fprev + mb * p.capFprev;
   const std::uint32_t* ip = p.indptr + mb * (p.capFprev + 1);
   std::uint32_t* ed = p.edges + mb * p.capS;
-  unsigned long long* hb = p.hopbits + mb * p.W;
+  unsigned long long* hb = p.hopbits ? p.hopbits + mb * p.W : nullptr;
   for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x) {
     const std::uint32_t v = fp[j];
     Stream s(key_step(prefix, vertex_key(p, v)));
@@ -511,6 +520,12 @@ __device__ __forceinline__ unsigned long long capped_degree_sum(unsigned long lo
   }
   return dc;
 }
+
+}  // namespace
+}  // namespace vk
+#include "frontier_sparse.cuh"
+namespace vk {
+namespace {
 
 // Narrow tiles (<= 4 words/thread): words held in registers, fully unrolled.
 template <bool HAS_NEXT, bool OR_ALL, int WPT>
@@ -1084,7 +1099,7 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
   p.indptr = s.indptr[h].as<std::uint32_t>();
   p.edges = s.edges_buf(h);
   p.capS = s.capS_max;
-  p.hopbits = s.hopbits.as<unsigned long long>();
+  p.hopbits = s.sparse ? nullptr : s.hopbits.as<unsigned long long>();
   p.W = s.W;
   if constexpr (MAXF == 0) {
     // 5 FY slots per thread + a 32*f staging row per warp
@@ -1106,7 +1121,7 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
         k_sample_smem<0><<<grid, kSampleThreads, smem, st>>>(p);
     };
     p.tile_words = kSampleTileWords;
-    if (h >= 2) {
+    if (h >= 2 && !s.sparse) {
       p.rank_prev = s.hopprefix.as<uint4>();
       // ~512 sources per (tile, minibatch) CTA at full frontier capacity,
       // at least kSampleTileWords words (4096 vertices) per tile
@@ -1205,6 +1220,106 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   }
 }
 
+// Sparse frontiers: one level (hop h >= 1, or the all level for h == 0)
+// through hist -> scan -> scatter -> dedup (frontier_sparse.cuh).
+template <bool ALL, bool HN>
+void launch_dedup(const DedupParams& dp, std::uint32_t bb, unsigned grid, cudaStream_t st) {
+  const std::size_t smem = ((std::size_t)1 << (bb - 6)) * 12;
+  auto go = [&](auto kernel) {
+    static bool attr = false;
+    if (!attr) {
+      VK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8192 * 12)));
+      attr = true;
+    }
+    kernel<<<grid, kBktThreads, smem, st>>>(dp);
+  };
+  switch (bb) {
+    case 14: go(k_bucket_dedup<ALL, HN, 1>); break;
+    case 15: go(k_bucket_dedup<ALL, HN, 2>); break;
+    case 16: go(k_bucket_dedup<ALL, HN, 4>); break;
+    case 17: go(k_bucket_dedup<ALL, HN, 8>); break;
+    case 18: go(k_bucket_dedup<ALL, HN, 16>); break;
+    default: go(k_bucket_dedup<ALL, HN, 32>); break;
+  }
+}
+
+void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStream_t st) {
+  const bool all = h == 0;
+  BucketParams bp{};
+  std::uint64_t items_cap = 0;
+  if (!all) {
+    bp.ids = s.edges_buf(h);
+    bp.ids_stride = s.capS_max;
+    bp.count = s.ecount(h);
+    items_cap = s.capS[h];
+  } else {
+    bp.L = s.L;
+    for (std::uint32_t q = 0; q <= s.L; ++q) {
+      bp.F[q] = s.F[q].as<std::uint32_t>();
+      bp.capF[q] = s.capF[q];
+      bp.fcount[q] = s.fcount(q);
+      items_cap += s.capF[q];
+    }
+  }
+  bp.bb = s.bb[h];
+  bp.NB = s.nbuckets(h);
+  bp.hist = s.bhist.as<std::uint32_t>();
+  bp.bstart = s.bstart.as<std::uint32_t>();
+  bp.cursor = s.bcursor.as<std::uint32_t>();
+  bp.pairs = s.pairs.as<uint2>();
+  bp.pair_stride = s.pair_stride;
+  bp.status = s.bstatus.as<unsigned long long>();
+  // hist / scan / scatter re-use the same (chunk, minibatch) grid
+  const dim3 cgrid((unsigned)std::max<std::uint64_t>(1, ceil_div(items_cap, kChunkItems)), nmb);
+  k_bucket_hist<<<cgrid, kBktThreads, bp.NB * 4, st>>>(bp);
+  k_bucket_scan<<<nmb, kScanThreads, 0, st>>>(bp);
+  k_bucket_scatter<<<cgrid, kBktThreads, bp.NB * 8, st>>>(bp);
+  count_launch(3);
+  VK_LAUNCH_CHECK();
+  DedupParams dp{};
+  dp.bp = bp;
+  dp.ticket = s.tickets.as<unsigned>() + (all ? s.L : h - 1);
+  dp.nmb = nmb;
+  dp.outdeg = s.g->out_deg.as<std::uint32_t>();
+  const unsigned grid = (unsigned)((std::uint64_t)nmb * bp.NB);
+  if (all) {
+    dp.list = s.all.as<std::uint32_t>();
+    dp.cap_list = s.capAll;
+    dp.count = s.allcount();
+    for (std::uint32_t q = 0; q <= s.L; ++q) dp.allidx[q] = s.allidx[q].as<std::uint32_t>();
+    dp.tile_base = s.tile_base.as<std::uint32_t>();
+    launch_dedup<true, false>(dp, bp.bb, grid, st);
+  } else {
+    dp.list = s.F[h].as<std::uint32_t>();
+    dp.cap_list = s.capF[h];
+    dp.count = s.fcount(h);
+    dp.dst = s.dst[h].as<std::uint32_t>();
+    dp.dst_stride = s.capS[h];
+    if (h < s.L) {
+      dp.f_next = s.cfg.fanouts[h];
+      dp.indptr_next = s.indptr[h + 1].as<std::uint32_t>();
+      dp.ecount_next = s.ecount(h + 1);
+      launch_dedup<false, true>(dp, bp.bb, grid, st);
+    } else {
+      launch_dedup<false, false>(dp, bp.bb, grid, st);
+    }
+  }
+  count_launch();
+  VK_LAUNCH_CHECK();
+}
+
+// Bucket bits of a level with `items` items per minibatch at capacity: about
+// kBucketTarget items per bucket, 2^14..2^19 ids per bucket (shared bitmap
+// of 2..64 KB), at most kMaxBuckets buckets.
+constexpr double kBucketTarget = 1024.0;
+std::uint32_t bucket_bits(std::uint64_t n, std::uint64_t items) {
+  const double want = (double)n * kBucketTarget / (double)std::max<std::uint64_t>(1, items);
+  std::uint32_t bb = (std::uint32_t)std::lround(std::log2(std::max(1.0, want)));
+  bb = std::min<std::uint32_t>(19, std::max<std::uint32_t>(14, bb));
+  while (bb < 19 && ((n + (1ull << bb) - 1) >> bb) > kMaxBuckets) ++bb;
+  return bb;
+}
+
 void run_compact_small(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, cudaStream_t st) {
   SmallParams sp{};
   CompactParams& p = sp.c;
@@ -1294,7 +1409,18 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
         all += s->capF[h];
       }
       s->capAll = std::min<std::uint64_t>(s->n, all);
-      s->dense_all_rank = 4 * s->W <= s->capAll;
+      // frontier representation: buckets when a minibatch touches a small
+      // fraction of the vertices (papers scale), bitmaps otherwise
+      {
+        bool ok = L + 1 <= (1u << (32 - kTagLevelShift)) && s->n <= (1ull << 31);
+        for (std::uint32_t h = 0; h <= L; ++h) ok = ok && s->capF[h] < (1ull << kTagLevelShift);
+        const bool want = (cfg->flags & VK_SAMPLER_FORCE_SPARSE) ||
+                          (!(cfg->flags & VK_SAMPLER_FORCE_DENSE) && s->n >= 16 * s->capAll && s->n >= (1ull << 20));
+        s->sparse = ok && want;
+        if ((cfg->flags & VK_SAMPLER_FORCE_SPARSE) && !ok)
+          raise(VK_ERR_UNSUPPORTED, "sparse frontiers need per-level capacities below 2^28");
+      }
+      s->dense_all_rank = !s->sparse && 4 * s->W <= s->capAll;
       for (std::uint32_t h = 1; h <= L; ++h)
         if (s->capS[h] >= (1ull << 31))
           raise(VK_ERR_UNSUPPORTED, "per-minibatch edge capacity exceeds 2^31; lower batch size or fanouts");
@@ -1312,11 +1438,32 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       }
       s->edges_tmp.alloc(2 * M * s->capS_max * 4);
       s->all.alloc(M * s->capAll * 4);
-      s->hopbits.alloc(M * s->W * 8);
-      s->allbits.alloc(M * s->W * 8);
-      s->hopprefix.alloc(M * s->W * 16);  // RankWord {bits, prefix} per word
-      s->allprefix.alloc(M * s->W * 16);
-      s->status.alloc((std::uint64_t)(L + 1) * M * s->tiles * 8);
+      if (s->sparse) {
+        std::uint64_t all_items = 0;
+        for (std::uint32_t h = 0; h <= L; ++h) {
+          all_items += s->capF[h];
+          if (h >= 1) s->bb[h] = bucket_bits(s->n, s->capS[h]);
+        }
+        s->bb[0] = bucket_bits(s->n, all_items);
+        for (std::uint32_t h = 0; h <= L; ++h) s->nb_max = std::max(s->nb_max, s->nbuckets(h));
+        s->pair_stride = std::max(s->capS_max, all_items);
+        s->pairs.alloc(M * s->pair_stride * 8);
+        s->bhist.alloc(M * (s->nb_max + 1) * 4);
+        s->bstart.alloc(M * (s->nb_max + 1) * 4);
+        s->bcursor.alloc(M * s->nb_max * 4);
+        s->bstatus.alloc(M * s->nb_max * 8);
+        s->tile_base.alloc(M * (s->nbuckets(0) + 1) * 4);
+        VK_CUDA(cudaMemsetAsync(s->bhist.p, 0, s->bhist.bytes, nullptr));
+        VK_CUDA(cudaFuncSetAttribute(k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(kMaxBuckets * 8)));
+        s->status.alloc(8);
+      } else {
+        s->hopbits.alloc(M * s->W * 8);
+        s->allbits.alloc(M * s->W * 8);
+        s->hopprefix.alloc(M * s->W * 16);  // RankWord {bits, prefix} per word
+        s->allprefix.alloc(M * s->W * 16);
+        s->status.alloc((std::uint64_t)(L + 1) * M * s->tiles * 8);
+      }
       s->tickets.alloc((L + 1) * 4);
       s->counts.alloc(s->counts_words() * 4);
       s->desc.alloc(M * sizeof(WaveDesc));
@@ -1339,8 +1486,11 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       VK_CUDA(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking));
       VK_CUDA(cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming));
       VK_CUDA(cudaEventCreateWithFlags(&s->join_ev, cudaEventDisableTiming));
-      VK_CUDA(cudaMemsetAsync(s->hopbits.p, 0, s->hopbits.bytes, s->stream));
-      VK_CUDA(cudaMemsetAsync(s->allbits.p, 0, s->allbits.bytes, s->stream));
+      if (!s->sparse) {
+        VK_CUDA(cudaMemsetAsync(s->hopbits.p, 0, s->hopbits.bytes, s->stream));
+        VK_CUDA(cudaMemsetAsync(s->allbits.p, 0, s->allbits.bytes, s->stream));
+      }
+      VK_CUDA(cudaDeviceSynchronize());  // the legacy-stream bucket histogram clear
       VK_CUDA(cudaMemsetAsync(s->counts.p, 0, s->counts.bytes, s->stream));
       VK_CUDA(cudaStreamSynchronize(s->stream));
     } catch (...) {
@@ -1468,14 +1618,14 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
     }
     VK_CUDA(cudaEventRecord(s->staged[slot], st));
     s->staged_used[slot] = true;
-    VK_CUDA(cudaMemsetAsync(s->status.p, 0, s->status.bytes, st));
+    if (!s->sparse) VK_CUDA(cudaMemsetAsync(s->status.p, 0, s->status.bytes, st));
     VK_CUDA(cudaMemsetAsync(s->tickets.p, 0, s->tickets.bytes, st));
     VK_CUDA(cudaMemsetAsync(s->err(), 0, 4, st));
     const std::uint32_t* outdeg = g.out_deg.as<std::uint32_t>();
     k_prepare<<<nmb, 1024, 0, st>>>(s->desc.as<WaveDesc>(), dseeds, outdeg, s->n, s->cfg.fanouts[0],
                                     s->F[0].as<std::uint32_t>(), s->capF[0], s->fcount(0),
                                     s->indptr[1].as<std::uint32_t>(), s->ecount(1),
-                                    s->allbits.as<unsigned long long>(), s->W, s->err());
+                                    s->sparse ? nullptr : s->allbits.as<unsigned long long>(), s->W, s->err());
     count_launch();
     VK_LAUNCH_CHECK();
     // small graphs: per-minibatch CTAs compact with shared-memory bitmaps and
@@ -1484,7 +1634,7 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
       const char* e = std::getenv("VK_SAMPLER_SMALL");
       return !e || std::atoi(e) != 0;
     }();
-    const bool small = small_ok && s->W <= kSmallW;
+    const bool small = small_ok && !s->sparse && s->W <= kSmallW;
     static const bool relabel_overlap = [] {
       const char* e = std::getenv("VK_RELABEL_OVERLAP");
       return !e || std::atoi(e) != 0;
@@ -1502,6 +1652,10 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
         raise(VK_ERR_UNSUPPORTED, "fanouts above 1024 with higher-degree vertices are not supported");
       count_launch();
       VK_LAUNCH_CHECK();
+      if (s->sparse) {
+        run_bucket_level(*s, h, nmb, st);
+        continue;
+      }
       if (small) {
         run_compact_small(*s, true, h, nmb, st);
         count_launch();
@@ -1532,7 +1686,9 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
         relabel_pending = true;
       }
     }
-    if (small) {
+    if (s->sparse) {
+      run_bucket_level(*s, 0, nmb, st);
+    } else if (small) {
       run_compact_small(*s, false, 0, nmb, st);
       count_launch();
       VK_LAUNCH_CHECK();
@@ -1810,6 +1966,14 @@ void sampler_all_rank(vk_sampler_s* s, const uint4** rank, std::uint64_t* W) {
   *W = s->W;
 }
 bool sampler_all_rank_dense(vk_sampler_s* s) { return s->dense_all_rank; }
+// sparse frontiers: rank of every all-level bucket's first vertex per
+// minibatch ([nmb][NB + 1]) and the bucket width; nullptr for bitmaps
+const std::uint32_t* sampler_tile_base(vk_sampler_s* s, std::uint32_t* bucket_bits, std::uint32_t* nb) {
+  if (!s->sparse) return nullptr;
+  *bucket_bits = s->bb[0];
+  *nb = s->nbuckets(0);
+  return s->tile_base.as<std::uint32_t>();
+}
 std::uint64_t sampler_run_id(vk_sampler_s* s) { return s->runs; }
 void sampler_host_partitions(vk_sampler_s* s, std::vector<std::uint32_t>& out) { out = s->last_parts; }
 cudaEvent_t sampler_done_event(vk_sampler_s* s) { return s->done; }

@@ -387,10 +387,13 @@ class ExpandedNeighborhood:
 class Sampler:
     """Batched device sampler: one run = expand() of a wave of minibatches."""
 
-    def __init__(self, g: Graph, fanouts, batch_size, max_minibatches=1, seed=0):
+    FRONTIERS = {"auto": 0, "dense": 1, "sparse": 2}  # VK_SAMPLER_FORCE_*
+
+    def __init__(self, g: Graph, fanouts, batch_size, max_minibatches=1, seed=0, frontier="auto"):
         self.g = g
         f = _fan(fanouts)
         cfg = SamplerConfig()
+        cfg.flags = self.FRONTIERS[frontier]
         cfg.num_hops = len(f)
         for i, x in enumerate(f[:MAX_HOPS]):
             cfg.fanouts[i] = int(x)
