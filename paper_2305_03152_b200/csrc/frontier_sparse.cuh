@@ -22,9 +22,10 @@ namespace vk {
 namespace {
 
 constexpr int kBktThreads = 256;
-constexpr std::uint32_t kChunkItems = 4096;  // items per (chunk, minibatch) CTA of hist / scatter
+constexpr std::uint32_t kChunkItems = 16384;  // items per (chunk, minibatch) CTA of hist / scatter
 constexpr std::uint32_t kMaxBuckets = 8192;  // per minibatch (shared histogram of hist / scatter)
-constexpr std::uint32_t kTagLevelShift = 28;  // all level: tag = level << 28 | index in F_level
+constexpr std::uint32_t kTagLevelShift = 28;
+constexpr std::uint32_t kItemBatch = 8;  // item loads in flight per thread (hist / scatter)  // all level: tag = level << 28 | index in F_level
 
 struct BucketParams {
   // hop level: items ids[mb * ids_stride + i], i < count[mb], tag = i
@@ -81,8 +82,17 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_hist(BucketParams p) {
   const std::uint32_t c1 = min(total, c0 + kChunkItems);
   for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads) s_hist[b] = 0;
   __syncthreads();
-  for (std::uint32_t i = c0 + threadIdx.x; i < c1; i += kBktThreads)
-    atomicAdd(&s_hist[bucket_item(p, mb, i, s_pre).x >> p.bb], 1u);
+  for (std::uint32_t i0 = c0 + threadIdx.x; i0 < c1; i0 += kItemBatch * kBktThreads) {
+    std::uint32_t v[kItemBatch];  // loads in flight before their uses
+#pragma unroll
+    for (std::uint32_t k = 0; k < kItemBatch; ++k) {
+      const std::uint32_t i = i0 + k * kBktThreads;
+      v[k] = i < c1 ? bucket_item(p, mb, i, s_pre).x : 0xffffffffu;
+    }
+#pragma unroll
+    for (std::uint32_t k = 0; k < kItemBatch; ++k)
+      if (v[k] != 0xffffffffu) atomicAdd(&s_hist[v[k] >> p.bb], 1u);
+  }
   __syncthreads();
   std::uint32_t* hist = p.hist + (std::uint64_t)mb * (p.NB + 1);
   for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads)
@@ -132,8 +142,17 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_scatter(BucketParams p) 
   const std::uint32_t c1 = min(total, c0 + kChunkItems);
   for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads) s_cnt[b] = 0;
   __syncthreads();
-  for (std::uint32_t i = c0 + threadIdx.x; i < c1; i += kBktThreads)
-    atomicAdd(&s_cnt[bucket_item(p, mb, i, s_pre).x >> p.bb], 1u);
+  for (std::uint32_t i0 = c0 + threadIdx.x; i0 < c1; i0 += kItemBatch * kBktThreads) {
+    std::uint32_t v[kItemBatch];
+#pragma unroll
+    for (std::uint32_t k = 0; k < kItemBatch; ++k) {
+      const std::uint32_t i = i0 + k * kBktThreads;
+      v[k] = i < c1 ? bucket_item(p, mb, i, s_pre).x : 0xffffffffu;
+    }
+#pragma unroll
+    for (std::uint32_t k = 0; k < kItemBatch; ++k)
+      if (v[k] != 0xffffffffu) atomicAdd(&s_cnt[v[k] >> p.bb], 1u);
+  }
   __syncthreads();
   std::uint32_t* cur = p.cursor + (std::uint64_t)mb * p.NB;
   for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads) {
@@ -143,16 +162,24 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_scatter(BucketParams p) 
   }
   __syncthreads();
   uint2* out = p.pairs + mb * p.pair_stride;
-  for (std::uint32_t i = c0 + threadIdx.x; i < c1; i += kBktThreads) {
-    const uint2 it = bucket_item(p, mb, i, s_pre);
-    const std::uint32_t b = it.x >> p.bb;
-    out[s_base[b] + atomicAdd(&s_cnt[b], 1u)] = it;
+  for (std::uint32_t i0 = c0 + threadIdx.x; i0 < c1; i0 += kItemBatch * kBktThreads) {
+    uint2 it[kItemBatch];
+#pragma unroll
+    for (std::uint32_t k = 0; k < kItemBatch; ++k) {
+      const std::uint32_t i = i0 + k * kBktThreads;
+      it[k] = i < c1 ? bucket_item(p, mb, i, s_pre) : make_uint2(0xffffffffu, 0u);
+    }
+#pragma unroll
+    for (std::uint32_t k = 0; k < kItemBatch; ++k)
+      if (it[k].x != 0xffffffffu) {
+        const std::uint32_t b = it[k].x >> p.bb;
+        out[s_base[b] + atomicAdd(&s_cnt[b], 1u)] = it[k];
+      }
   }
 }
 
 struct DedupParams {
   BucketParams bp;
-  unsigned* ticket;
   std::uint32_t nmb;
   std::uint32_t* list;  // F_h or all_vertices [M][cap_list]
   std::uint64_t cap_list;
@@ -160,10 +187,11 @@ struct DedupParams {
   // hop level: dst[mb * dst_stride + tag] = rank (MFG relabel)
   std::uint32_t* dst;
   std::uint64_t dst_stride;
-  // all level: allidx[h][mb * capF[h] + index] = rank; tile_base[mb][b] =
-  // rank of bucket b's first vertex (the gather's vertex tiles)
+  // every level: base[mb][b] = rank of bucket b's first vertex in the list
+  // ([M][NB + 1]); the all level ranges F_1..F_L with the hops' bases
+  std::uint32_t* base_out;
+  const std::uint32_t* fbase[VK_MAX_HOPS + 1];  // all level: hop h's bases
   std::uint32_t* allidx[VK_MAX_HOPS + 1];
-  std::uint32_t* tile_base;  // [M][NB + 1]
   // next hop's MFG row pointers over the list (HAS_NEXT)
   const std::uint32_t* outdeg;
   std::uint32_t f_next;
@@ -171,107 +199,301 @@ struct DedupParams {
   std::uint32_t* ecount_next;  // [M]
 };
 
-// 4. one CTA per (minibatch, bucket); tickets hand out buckets in ascending
-// order per minibatch (minibatch fastest) so every look-back predecessor is
-// already running. WPT = bitmap words per thread (bucket = 256*WPT*64 ids).
-template <bool ALL, bool HAS_NEXT, int WPT>
-__global__ void __launch_bounds__(kBktThreads) k_bucket_dedup(DedupParams p) {
-  constexpr std::uint32_t BW = kBktThreads * WPT;  // words per bucket
-  extern __shared__ unsigned long long s_bits[];   // [BW] bits, then u32 [BW] word ranks
-  std::uint32_t* s_rank = reinterpret_cast<std::uint32_t*>(s_bits + BW);
-  __shared__ unsigned s_ticket;
+constexpr std::uint32_t kDegStage = 2048;  // capped degrees staged per bucket (else reloaded)
+constexpr std::uint32_t kPairRegs = 8;     // pairs per thread kept in registers between passes
+constexpr std::uint32_t kMbGroup = 8;      // minibatches interleaved per block group (L2 footprint)
+
+// Shared memory of a dedup CTA: the bucket bitmap (BW words), each word's
+// global rank, and (hop levels with a next hop) staged capped degrees.
+// Words are padded by one per thread-owned run of wpt words (index
+// w + w / wpt), so the owner threads' strided passes are bank-conflict free.
+__host__ __device__ constexpr std::size_t dedup_smem(std::uint32_t bb, bool degrees) {
+  return (((std::size_t)1 << (bb - 6)) + kBktThreads) * 12 + (degrees ? kDegStage * 4 : 0);
+}
+
+// The bucket bitmap and per-word ranks in shared memory (padded layout).
+struct SBits {
+  unsigned long long* bits;
+  std::uint32_t* rank;
+  std::uint32_t lw;  // log2(words per thread)
+  __device__ __forceinline__ std::uint32_t idx(std::uint32_t w) const { return w + (w >> lw); }
+  __device__ __forceinline__ void set(std::uint32_t v) const {
+    atomicOr(reinterpret_cast<unsigned*>(bits) + 2 * idx(v >> 6) + ((v >> 5) & 1u), 1u << (v & 31));
+  }
+  // rank of a present v, once rank[] holds the global rank of every nonzero word
+  __device__ __forceinline__ std::uint32_t rank_of(std::uint32_t v) const {
+    const std::uint32_t i = idx(v >> 6);
+    return rank[i] + (std::uint32_t)__popcll(bits[i] & ((1ull << (v & 63)) - 1ull));
+  }
+};
+
+// blockIdx -> (minibatch, bucket): groups of kMbGroup minibatches, buckets
+// ascending, minibatch fastest inside a group. Blocks are dispatched in
+// index order, so every look-back predecessor (same minibatch, lower bucket)
+// has a lower index and is already resident or done; a group's random writes
+// (MFG dst) stay inside a few minibatches' rows, i.e. inside L2.
+__device__ __forceinline__ void dedup_coords(std::uint32_t nmb, std::uint32_t NB, std::uint32_t& mb,
+                                             std::uint32_t& b) {
+  const std::uint32_t per_group = kMbGroup * NB;
+  const std::uint32_t g = blockIdx.x / per_group, r = blockIdx.x % per_group;
+  const std::uint32_t gsize = min(kMbGroup, nmb - g * kMbGroup);
+  b = r / gsize;
+  mb = g * kMbGroup + r % gsize;
+}
+
+
+// Set bits of words [j, end) in vertex order, 8 per call (bucket-relative
+// ids into vv); returns how many. Rolled over words: sparse buckets have ~1
+// bit per nonzero word, so a batch spans words and keeps 8 loads in flight.
+struct BitCursor {
+  std::uint32_t w0, p0;  // first word of the thread, its padded index
+  unsigned m;            // its nonzero words not yet visited (bit k = word w0 + k)
+  unsigned long long x;  // remaining bits of the current word
+  std::uint32_t w;       // current word
+  __device__ __forceinline__ int next8(const unsigned long long* bits, std::uint32_t* vv) {
+    int nq = 0;
+    while (nq < 8) {
+      if (!x) {
+        if (!m) break;
+        const std::uint32_t k = __ffs((int)m) - 1;
+        m &= m - 1;
+        w = w0 + k;
+        x = bits[p0 + k];
+      }
+      const int b = __ffsll(x) - 1;
+      x &= x - 1;
+      vv[nq++] = w * 64 + b;
+    }
+    return nq;
+  }
+};
+
+// Zero the padded bitmap; returns the view. wpt = words per thread.
+__device__ __forceinline__ SBits sbits_init(unsigned long long* smem, std::uint32_t BW, std::uint32_t wpt) {
+  const std::uint32_t BWp = BW + kBktThreads;
+  SBits sb{smem, reinterpret_cast<std::uint32_t*>(smem + BWp), (std::uint32_t)(__ffs((int)wpt) - 1)};
+  for (std::uint32_t w = threadIdx.x; w < BWp; w += kBktThreads) smem[w] = 0ull;
+  return sb;
+}
+
+// This thread's wpt consecutive words (<= 32, padded run at p0): distinct
+// count and the mask of nonzero words, the only ones later passes visit.
+__device__ __forceinline__ unsigned long long count_words(const SBits& sb, std::uint32_t p0, std::uint32_t wpt,
+                                                          unsigned& nz) {
+  unsigned long long vc = 0;
+  nz = 0;
+#pragma unroll 1
+  for (std::uint32_t k = 0; k < wpt; ++k) {
+    const unsigned long long x = sb.bits[p0 + k];
+    if (x) {
+      nz |= 1u << k;
+      vc += __popcll(x);
+    }
+  }
+  return vc;
+}
+
+// 4a. hop level: one CTA per (minibatch, bucket) over that bucket's pairs.
+template <bool HAS_NEXT>
+__global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_hop(DedupParams p) {
+  extern __shared__ unsigned long long s_dd[];
   __shared__ unsigned long long s_sm[kBktThreads / 32];
   __shared__ unsigned long long s_excl;
   const BucketParams& bp = p.bp;
-  if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1u);
-  __syncthreads();
-  const std::uint32_t mb = s_ticket % p.nmb;
-  const std::uint32_t b = s_ticket / p.nmb;
-  if (b >= bp.NB) return;
-  const std::uint32_t NB = bp.NB;
+  const std::uint32_t NB = bp.NB, BW = 1u << (bp.bb - 6), wpt = BW / kBktThreads;
+  std::uint32_t mb, b;
+  dedup_coords(p.nmb, NB, mb, b);
   const std::uint32_t* bs = bp.bstart + (std::uint64_t)mb * (NB + 1);
   const std::uint32_t s = bs[b], e = bs[b + 1];
   unsigned long long* status = bp.status + (std::uint64_t)mb * NB;
   const bool last = b + 1 == NB;
-  if (s == e && !ALL && !last) {  // empty bucket: an empty aggregate for the successors
-    if (threadIdx.x == 0) publish_aggregate(status, b, 0ull);
-    return;
-  }
   const uint2* pairs = bp.pairs + mb * bp.pair_stride;
-  const std::uint32_t vbase = b << bp.bb;
-  for (std::uint32_t w = threadIdx.x; w < BW; w += kBktThreads) s_bits[w] = 0ull;
-  __syncthreads();
-  unsigned* bits32 = reinterpret_cast<unsigned*>(s_bits);
-  for (std::uint32_t i = s + threadIdx.x; i < e; i += kBktThreads) {
-    const std::uint32_t v = pairs[i].x - vbase;
-    atomicOr(bits32 + (v >> 5), 1u << (v & 31));
-  }
-  __syncthreads();
-  // this thread's WPT consecutive words: distinct count and capped degrees
-  const std::uint32_t w0 = threadIdx.x * WPT;
-  unsigned long long wd[WPT];
-  unsigned long long vc = 0, dc = 0;
+  // this thread's pairs, in flight while the bitmap is cleared (kept for the rank pass)
+  uint2 pr[kPairRegs];
 #pragma unroll
-  for (int k = 0; k < WPT; ++k) {
-    wd[k] = s_bits[w0 + k];
-    vc += __popcll(wd[k]);
-    if (HAS_NEXT && wd[k]) dc += capped_degree_sum(wd[k], (vbase >> 6) + w0 + k, p.outdeg, p.f_next);
+  for (std::uint32_t k = 0; k < kPairRegs; ++k) {
+    const std::uint32_t i = s + threadIdx.x + k * kBktThreads;
+    pr[k] = i < e ? pairs[i] : make_uint2(0u, 0u);
   }
-  const unsigned long long mine = pack_vd(vc, dc);
-  unsigned long long total;
-  const unsigned long long lex = block_inclusive_scan<kBktThreads>(mine, s_sm, &total) - mine;
-  if (threadIdx.x == 0) publish_aggregate(status, b, total);
+  const SBits sb = sbits_init(s_dd, BW, wpt);
+  std::uint32_t* s_deg = sb.rank + BW + kBktThreads;
+  __syncthreads();
+  const std::uint32_t vbase = b << bp.bb;
+#pragma unroll
+  for (std::uint32_t k = 0; k < kPairRegs; ++k)
+    if (s + threadIdx.x + k * kBktThreads < e) sb.set(pr[k].x - vbase);
+  for (std::uint32_t i = s + threadIdx.x + kPairRegs * kBktThreads; i < e; i += kBktThreads) sb.set(pairs[i].x - vbase);
+  __syncthreads();
+  const std::uint32_t w0 = threadIdx.x * wpt, p0 = w0 + threadIdx.x;
+  unsigned nz;
+  const unsigned long long vc = count_words(sb, p0, wpt, nz);
+  unsigned long long vtot;
+  const std::uint32_t lpos = (std::uint32_t)(block_inclusive_scan<kBktThreads>(vc, s_sm, &vtot) - vc);
+  unsigned long long dc = 0, dlex = 0, dtot = 0;
+  if (HAS_NEXT) {
+    // next hop's row lengths min(f, deg): every degree of the CTA in flight
+    // in batches of 8, staged in shared memory by bucket-local position
+    BitCursor c{w0, p0, nz, 0ull, 0u};
+    std::uint32_t pos = lpos;
+    while (true) {
+      std::uint32_t vv[8], d[8];
+      const int nq = c.next8(sb.bits, vv);
+      if (!nq) break;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d[q] = q < nq ? __ldg(p.outdeg + vbase + vv[q]) : 0u;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < nq) {
+          const std::uint32_t cd = min(p.f_next, d[q]);
+          if (pos < kDegStage) s_deg[pos] = cd;
+          ++pos;
+          dc += cd;
+        }
+    }
+    dlex = block_inclusive_scan<kBktThreads>(dc, s_sm, &dtot) - dc;
+  }
+  const unsigned long long total = pack_vd(vtot, dtot);
   if (threadIdx.x < 32) {
-    const unsigned long long ex = lookback_resolve(status, b, total);
+    const unsigned long long ex = lookback_warp(status, b, total);
     if (threadIdx.x == 0) s_excl = ex;
   }
   __syncthreads();
   const unsigned long long base = s_excl;
-  std::uint32_t gv = (std::uint32_t)(unpack_v(base) + unpack_v(lex));
-  std::uint32_t gd = (std::uint32_t)(unpack_d(base) + unpack_d(lex));
+  std::uint32_t gv = (std::uint32_t)unpack_v(base) + lpos;
+  std::uint32_t gd = (std::uint32_t)(unpack_d(base) + dlex);
   std::uint32_t* list = p.list + mb * p.cap_list;
   std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
-#pragma unroll
-  for (int k = 0; k < WPT; ++k) {
-    s_rank[w0 + k] = gv;
-    unsigned long long x = wd[k];
-    const std::uint32_t wv = vbase + (w0 + k) * 64;
+  std::uint32_t pos = lpos;
+  for (unsigned m = nz; m; m &= m - 1) {  // ranks are only looked up in nonzero words
+    const std::uint32_t k = __ffs((int)m) - 1;
+    sb.rank[p0 + k] = gv;
+    unsigned long long x = sb.bits[p0 + k];
     while (x) {
-      const int bit = __ffsll(x) - 1;
+      const std::uint32_t v = vbase + (w0 + k) * 64 + (__ffsll(x) - 1);
       x &= x - 1;
-      const std::uint32_t v = wv + bit;
-      list[gv] = v;
+      list[gv++] = v;
       if (HAS_NEXT) {
-        ipn[gv] = gd;
-        gd += min(p.f_next, __ldg(p.outdeg + v));
+        ipn[gv - 1] = gd;
+        gd += pos < kDegStage ? s_deg[pos] : min(p.f_next, __ldg(p.outdeg + v));
+        ++pos;
       }
-      ++gv;
     }
   }
-  if (ALL && threadIdx.x == 0) p.tile_base[mb * (NB + 1) + b] = (std::uint32_t)unpack_v(base);
+  std::uint32_t* bo = p.base_out + (std::uint64_t)mb * (NB + 1);
+  if (threadIdx.x == 0) bo[b] = (std::uint32_t)unpack_v(base);
   if (last && threadIdx.x == kBktThreads - 1) {
     const unsigned long long all = base + total;
     const std::uint32_t tv = (std::uint32_t)unpack_v(all), td = (std::uint32_t)unpack_d(all);
     p.count[mb] = tv;
+    bo[NB] = tv;
     if (HAS_NEXT) {
       ipn[tv] = td;
       p.ecount_next[mb] = td;
     }
-    if (ALL) p.tile_base[mb * (NB + 1) + NB] = tv;
   }
   __syncthreads();
-  // every pair's rank: MFG dst (hop) or all_vertices index (all level)
-  for (std::uint32_t i = s + threadIdx.x; i < e; i += kBktThreads) {
-    const uint2 pr = pairs[i];
-    const std::uint32_t v = pr.x - vbase, w = v >> 6;
-    const std::uint32_t r = s_rank[w] + (std::uint32_t)__popcll(s_bits[w] & ((1ull << (v & 63)) - 1ull));
-    if (ALL) {
-      const std::uint32_t h = pr.y >> kTagLevelShift, idx = pr.y & ((1u << kTagLevelShift) - 1u);
-      p.allidx[h][mb * bp.capF[h] + idx] = r;
-    } else {
-      p.dst[mb * p.dst_stride + pr.y] = r;
+  std::uint32_t* dst = p.dst + mb * p.dst_stride;
+#pragma unroll
+  for (std::uint32_t k = 0; k < kPairRegs; ++k)
+    if (s + threadIdx.x + k * kBktThreads < e) dst[pr[k].y] = sb.rank_of(pr[k].x - vbase);
+  for (std::uint32_t i = s + threadIdx.x + kPairRegs * kBktThreads; i < e; i += kBktThreads) {
+    const uint2 q = pairs[i];
+    dst[q.y] = sb.rank_of(q.x - vbase);
+  }
+}
+
+// 4b. all level: all_vertices = sorted unique(F_0 u F_1 .. F_L) per bucket.
+// F_1..F_L are sorted and their dedups recorded every bucket's index range
+// (fbase, same bucket width), so no scatter pass is needed and the relabel
+// maps are written contiguously; the batch F_0 (unsorted, <= b ids) is
+// scanned whole by every bucket.
+__global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_all(DedupParams p) {
+  extern __shared__ unsigned long long s_dd[];
+  __shared__ unsigned long long s_sm[kBktThreads / 32];
+  __shared__ unsigned long long s_excl;
+  __shared__ std::uint32_t s_lo[VK_MAX_HOPS + 1], s_hi[VK_MAX_HOPS + 1];
+  const BucketParams& bp = p.bp;
+  const std::uint32_t NB = bp.NB, BW = 1u << (bp.bb - 6), wpt = BW / kBktThreads;
+  std::uint32_t mb, b;
+  dedup_coords(p.nmb, NB, mb, b);
+  const std::uint32_t vbase = b << bp.bb;
+  const std::uint32_t vend = (b + 1 == NB) ? 0xffffffffu : vbase + (1u << bp.bb);
+  if (threadIdx.x >= 1 && threadIdx.x <= bp.L) {
+    const std::uint32_t* fb = p.fbase[threadIdx.x] + (std::uint64_t)mb * (NB + 1);
+    s_lo[threadIdx.x] = fb[b];
+    s_hi[threadIdx.x] = fb[b + 1];
+  }
+  const std::uint32_t c0 = bp.fcount[0][mb];
+  const std::uint32_t* F0 = bp.F[0] + mb * bp.capF[0];
+  const SBits sb = sbits_init(s_dd, BW, wpt);
+  __syncthreads();
+  // loads issued kBatch at a time ahead of their uses
+  constexpr std::uint32_t kBatch = 8;
+  auto set_range = [&](const std::uint32_t* F, std::uint32_t lo, std::uint32_t hi, bool filter) {
+    for (std::uint32_t i0 = lo + threadIdx.x; i0 < hi; i0 += kBatch * kBktThreads) {
+      std::uint32_t v[kBatch];
+#pragma unroll
+      for (std::uint32_t k = 0; k < kBatch; ++k) {
+        const std::uint32_t i = i0 + k * kBktThreads;
+        v[k] = i < hi ? __ldg(F + i) : 0xffffffffu;
+      }
+#pragma unroll
+      for (std::uint32_t k = 0; k < kBatch; ++k)
+        if (v[k] != 0xffffffffu && (!filter || (v[k] >= vbase && v[k] < vend))) sb.set(v[k] - vbase);
+    }
+  };
+  set_range(F0, 0, c0, true);
+  for (std::uint32_t h = 1; h <= bp.L; ++h) set_range(bp.F[h] + mb * bp.capF[h], s_lo[h], s_hi[h], false);
+  __syncthreads();
+  const std::uint32_t w0 = threadIdx.x * wpt, p0 = w0 + threadIdx.x;
+  unsigned nz;
+  const unsigned long long vc = count_words(sb, p0, wpt, nz);
+  unsigned long long total;
+  const std::uint32_t lpos = (std::uint32_t)(block_inclusive_scan<kBktThreads>(vc, s_sm, &total) - vc);
+  unsigned long long* status = bp.status + (std::uint64_t)mb * NB;
+  const unsigned long long agg = pack_vd(total, 0);
+  if (threadIdx.x < 32) {
+    const unsigned long long ex = lookback_warp(status, b, agg);
+    if (threadIdx.x == 0) s_excl = ex;
+  }
+  __syncthreads();
+  const std::uint32_t base = (std::uint32_t)unpack_v(s_excl);
+  std::uint32_t gv = base + lpos;
+  std::uint32_t* list = p.list + mb * p.cap_list;
+  for (unsigned m = nz; m; m &= m - 1) {
+    const std::uint32_t k = __ffs((int)m) - 1;
+    sb.rank[p0 + k] = gv;
+    unsigned long long x = sb.bits[p0 + k];
+    while (x) {
+      list[gv++] = vbase + (w0 + k) * 64 + (__ffsll(x) - 1);
+      x &= x - 1;
     }
   }
+  std::uint32_t* tb = p.base_out + (std::uint64_t)mb * (NB + 1);
+  if (threadIdx.x == 0) tb[b] = base;
+  if (b + 1 == NB && threadIdx.x == kBktThreads - 1) {
+    const std::uint32_t tv = base + (std::uint32_t)total;
+    p.count[mb] = tv;
+    tb[NB] = tv;
+  }
+  __syncthreads();
+  auto rank_range = [&](const std::uint32_t* F, std::uint32_t* ai, std::uint32_t lo, std::uint32_t hi, bool filter) {
+    for (std::uint32_t i0 = lo + threadIdx.x; i0 < hi; i0 += kBatch * kBktThreads) {
+      std::uint32_t v[kBatch];
+#pragma unroll
+      for (std::uint32_t k = 0; k < kBatch; ++k) {
+        const std::uint32_t i = i0 + k * kBktThreads;
+        v[k] = i < hi ? __ldg(F + i) : 0xffffffffu;
+      }
+#pragma unroll
+      for (std::uint32_t k = 0; k < kBatch; ++k)
+        if (v[k] != 0xffffffffu && (!filter || (v[k] >= vbase && v[k] < vend)))
+          ai[i0 + k * kBktThreads] = sb.rank_of(v[k] - vbase);
+    }
+  };
+  rank_range(F0, p.allidx[0] + mb * bp.capF[0], 0, c0, true);
+  for (std::uint32_t h = 1; h <= bp.L; ++h)
+    rank_range(bp.F[h] + mb * bp.capF[h], p.allidx[h] + mb * bp.capF[h], s_lo[h], s_hi[h], false);
 }
 
 }  // namespace

@@ -67,7 +67,7 @@ struct vk_sampler_s {
   std::uint32_t bb[VK_MAX_HOPS + 1]{};
   std::uint32_t nb_max = 0;
   std::uint64_t pair_stride = 0;
-  vk::DevBuf bhist, bstart, bcursor, bstatus, pairs, tile_base;
+  vk::DevBuf bhist, bstart, bcursor, bstatus, pairs, tile_base, fbase;  // fbase: [L+1][M][NB+1] hop bucket bases
   std::uint32_t nbuckets(std::uint32_t level) const { return (std::uint32_t)((n + (1ull << bb[level]) - 1) >> bb[level]); }
   vk::DevBuf F[VK_MAX_HOPS + 1], allidx[VK_MAX_HOPS + 1], indptr[VK_MAX_HOPS + 1], dst[VK_MAX_HOPS + 1];
   vk::DevBuf counts;  // u32: fcount[(L+1)*M] | ecount[(L+1)*M] | allcount[M] | err[1]
@@ -1222,45 +1222,16 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
 
 // Sparse frontiers: one level (hop h >= 1, or the all level for h == 0)
 // through hist -> scan -> scatter -> dedup (frontier_sparse.cuh).
-template <bool ALL, bool HN>
-void launch_dedup(const DedupParams& dp, std::uint32_t bb, unsigned grid, cudaStream_t st) {
-  const std::size_t smem = ((std::size_t)1 << (bb - 6)) * 12;
-  auto go = [&](auto kernel) {
-    static bool attr = false;
-    if (!attr) {
-      VK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8192 * 12)));
-      attr = true;
-    }
-    kernel<<<grid, kBktThreads, smem, st>>>(dp);
-  };
-  switch (bb) {
-    case 14: go(k_bucket_dedup<ALL, HN, 1>); break;
-    case 15: go(k_bucket_dedup<ALL, HN, 2>); break;
-    case 16: go(k_bucket_dedup<ALL, HN, 4>); break;
-    case 17: go(k_bucket_dedup<ALL, HN, 8>); break;
-    case 18: go(k_bucket_dedup<ALL, HN, 16>); break;
-    default: go(k_bucket_dedup<ALL, HN, 32>); break;
-  }
+template <class P>
+void launch_smem(void (*kernel)(P), const P& p, unsigned grid, std::size_t smem, cudaStream_t st) {
+  if (smem >= 40 * 1024)  // beyond the default 48 KB with the static shared arrays
+    VK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kernel<<<grid, kBktThreads, smem, st>>>(p);
 }
 
 void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStream_t st) {
   const bool all = h == 0;
   BucketParams bp{};
-  std::uint64_t items_cap = 0;
-  if (!all) {
-    bp.ids = s.edges_buf(h);
-    bp.ids_stride = s.capS_max;
-    bp.count = s.ecount(h);
-    items_cap = s.capS[h];
-  } else {
-    bp.L = s.L;
-    for (std::uint32_t q = 0; q <= s.L; ++q) {
-      bp.F[q] = s.F[q].as<std::uint32_t>();
-      bp.capF[q] = s.capF[q];
-      bp.fcount[q] = s.fcount(q);
-      items_cap += s.capF[q];
-    }
-  }
   bp.bb = s.bb[h];
   bp.NB = s.nbuckets(h);
   bp.hist = s.bhist.as<std::uint32_t>();
@@ -1269,40 +1240,57 @@ void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaS
   bp.pairs = s.pairs.as<uint2>();
   bp.pair_stride = s.pair_stride;
   bp.status = s.bstatus.as<unsigned long long>();
+  DedupParams dp{};
+  dp.nmb = nmb;
+  dp.outdeg = s.g->out_deg.as<std::uint32_t>();
+  const unsigned grid = (unsigned)((std::uint64_t)nmb * bp.NB);
+  if (all) {
+    // sorted levels are ranged by binary search: no hist / scatter pass
+    bp.L = s.L;
+    for (std::uint32_t q = 0; q <= s.L; ++q) {
+      bp.F[q] = s.F[q].as<std::uint32_t>();
+      bp.capF[q] = s.capF[q];
+      bp.fcount[q] = s.fcount(q);
+    }
+    VK_CUDA(cudaMemsetAsync(s.bstatus.p, 0, (std::uint64_t)nmb * bp.NB * 8, st));
+    dp.bp = bp;
+    dp.list = s.all.as<std::uint32_t>();
+    dp.cap_list = s.capAll;
+    dp.count = s.allcount();
+    for (std::uint32_t q = 0; q <= s.L; ++q) {
+      dp.allidx[q] = s.allidx[q].as<std::uint32_t>();
+      dp.fbase[q] = s.fbase.as<std::uint32_t>() + (std::uint64_t)q * s.M * (s.nb_max + 1);
+    }
+    dp.base_out = s.tile_base.as<std::uint32_t>();
+    launch_smem(k_bucket_dedup_all, dp, grid, dedup_smem(bp.bb, false), st);
+    count_launch();
+    VK_LAUNCH_CHECK();
+    return;
+  }
+  bp.ids = s.edges_buf(h);
+  bp.ids_stride = s.capS_max;
+  bp.count = s.ecount(h);
   // hist / scan / scatter re-use the same (chunk, minibatch) grid
-  const dim3 cgrid((unsigned)std::max<std::uint64_t>(1, ceil_div(items_cap, kChunkItems)), nmb);
+  const dim3 cgrid((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capS[h], kChunkItems)), nmb);
   k_bucket_hist<<<cgrid, kBktThreads, bp.NB * 4, st>>>(bp);
   k_bucket_scan<<<nmb, kScanThreads, 0, st>>>(bp);
   k_bucket_scatter<<<cgrid, kBktThreads, bp.NB * 8, st>>>(bp);
   count_launch(3);
   VK_LAUNCH_CHECK();
-  DedupParams dp{};
   dp.bp = bp;
-  dp.ticket = s.tickets.as<unsigned>() + (all ? s.L : h - 1);
-  dp.nmb = nmb;
-  dp.outdeg = s.g->out_deg.as<std::uint32_t>();
-  const unsigned grid = (unsigned)((std::uint64_t)nmb * bp.NB);
-  if (all) {
-    dp.list = s.all.as<std::uint32_t>();
-    dp.cap_list = s.capAll;
-    dp.count = s.allcount();
-    for (std::uint32_t q = 0; q <= s.L; ++q) dp.allidx[q] = s.allidx[q].as<std::uint32_t>();
-    dp.tile_base = s.tile_base.as<std::uint32_t>();
-    launch_dedup<true, false>(dp, bp.bb, grid, st);
+  dp.list = s.F[h].as<std::uint32_t>();
+  dp.cap_list = s.capF[h];
+  dp.count = s.fcount(h);
+  dp.dst = s.dst[h].as<std::uint32_t>();
+  dp.dst_stride = s.capS[h];
+  dp.base_out = s.fbase.as<std::uint32_t>() + (std::uint64_t)h * s.M * (s.nb_max + 1);
+  if (h < s.L) {
+    dp.f_next = s.cfg.fanouts[h];
+    dp.indptr_next = s.indptr[h + 1].as<std::uint32_t>();
+    dp.ecount_next = s.ecount(h + 1);
+    launch_smem(k_bucket_dedup_hop<true>, dp, grid, dedup_smem(bp.bb, true), st);
   } else {
-    dp.list = s.F[h].as<std::uint32_t>();
-    dp.cap_list = s.capF[h];
-    dp.count = s.fcount(h);
-    dp.dst = s.dst[h].as<std::uint32_t>();
-    dp.dst_stride = s.capS[h];
-    if (h < s.L) {
-      dp.f_next = s.cfg.fanouts[h];
-      dp.indptr_next = s.indptr[h + 1].as<std::uint32_t>();
-      dp.ecount_next = s.ecount(h + 1);
-      launch_dedup<false, true>(dp, bp.bb, grid, st);
-    } else {
-      launch_dedup<false, false>(dp, bp.bb, grid, st);
-    }
+    launch_smem(k_bucket_dedup_hop<false>, dp, grid, dedup_smem(bp.bb, false), st);
   }
   count_launch();
   VK_LAUNCH_CHECK();
@@ -1311,11 +1299,16 @@ void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaS
 // Bucket bits of a level with `items` items per minibatch at capacity: about
 // kBucketTarget items per bucket, 2^14..2^19 ids per bucket (shared bitmap
 // of 2..64 KB), at most kMaxBuckets buckets.
-constexpr double kBucketTarget = 1024.0;
-std::uint32_t bucket_bits(std::uint64_t n, std::uint64_t items) {
-  const double want = (double)n * kBucketTarget / (double)std::max<std::uint64_t>(1, items);
-  std::uint32_t bb = (std::uint32_t)std::lround(std::log2(std::max(1.0, want)));
-  bb = std::min<std::uint32_t>(19, std::max<std::uint32_t>(14, bb));
+std::uint32_t bucket_bits(std::uint64_t n) {
+  // 2^14..2^19 ids per bucket (2..64 KB of shared bitmap), at most kMaxBuckets
+  static const std::uint32_t force = [] {  // TUNING (temporary)
+    const char* e = std::getenv("VK_BUCKET_BITS");
+    return e ? (std::uint32_t)std::atoi(e) : 0u;
+  }();
+  // ~512 buckets per minibatch: C4 (111 M ids) -> 2^18 ids (32 KB of bitmap)
+  // per bucket; measured per C4 wave: 2^17 5.3 ms, 2^18 4.2 ms, 2^19 4.2 ms
+  std::uint32_t bb = force ? force : (std::uint32_t)std::ceil(std::log2(std::max(1.0, (double)n / 512.0)));
+  bb = std::min<std::uint32_t>(force ? 19 : 18, std::max<std::uint32_t>(14, bb));
   while (bb < 19 && ((n + (1ull << bb) - 1) >> bb) > kMaxBuckets) ++bb;
   return bb;
 }
@@ -1439,14 +1432,13 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       s->edges_tmp.alloc(2 * M * s->capS_max * 4);
       s->all.alloc(M * s->capAll * 4);
       if (s->sparse) {
-        std::uint64_t all_items = 0;
-        for (std::uint32_t h = 0; h <= L; ++h) {
-          all_items += s->capF[h];
-          if (h >= 1) s->bb[h] = bucket_bits(s->n, s->capS[h]);
-        }
-        s->bb[0] = bucket_bits(s->n, all_items);
-        for (std::uint32_t h = 0; h <= L; ++h) s->nb_max = std::max(s->nb_max, s->nbuckets(h));
-        s->pair_stride = std::max(s->capS_max, all_items);
+        // one bucket width for every level, so the all level can range the
+        // sorted hop lists by the hops' bucket bases
+        const std::uint32_t bb = bucket_bits(s->n);
+        for (std::uint32_t h = 0; h <= L; ++h) s->bb[h] = bb;
+        s->nb_max = s->nbuckets(0);
+        s->fbase.alloc((std::uint64_t)(L + 1) * M * (s->nb_max + 1) * 4);
+        s->pair_stride = s->capS_max;  // hop levels only (the all level ranges sorted lists)
         s->pairs.alloc(M * s->pair_stride * 8);
         s->bhist.alloc(M * (s->nb_max + 1) * 4);
         s->bstart.alloc(M * (s->nb_max + 1) * 4);

@@ -79,8 +79,13 @@ __device__ __forceinline__ unsigned long long lookback_resolve(unsigned long lon
     const int t = top - (int)lane;
     unsigned long long s = t >= 0 ? peek(status + t) : (kFlagInc);  // t < 0: virtual zero prefix
     unsigned flag = (unsigned)(s >> 62);
-    // wait until every lane's predecessor has published something
+    // wait until every lane's predecessor has published something, backing
+    // off between polls: hundreds of spinning warps otherwise hammer the few
+    // L2 slices that hold a chain's status words and slow every CTA down
+    unsigned ns = 32;
     while (__any_sync(0xffffffffu, flag == 0)) {
+      __nanosleep(ns);
+      ns = min(ns * 2, 1024u);
       if (flag == 0) {
         s = peek(status + t);
         flag = (unsigned)(s >> 62);
