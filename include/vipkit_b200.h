@@ -48,7 +48,7 @@ typedef enum vk_status {
   VK_ERR_SHAPE = 8,       /* vipkit::shape_error      (error.hpp:32-34) */
   VK_ERR_IO = 9,          /* vipkit::io_error         (error.hpp:35-37) */
   VK_ERR_CUDA = 20,       /* CUDA runtime failure / no device */
-  VK_ERR_NCCL = 21,       /* NCCL failure */
+                          /* 21: unused (the exchange is CUDA IPC + NVLink, no NCCL) */
   VK_ERR_UNSUPPORTED = 22,
   VK_ERR_INTERNAL = 23
 } vk_status;

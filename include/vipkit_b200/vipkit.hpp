@@ -47,7 +47,7 @@ struct sampling_error : error { using error::error; };
 struct config_error : error { using error::error; };
 struct shape_error : error { using error::error; };
 struct io_error : error { using error::error; };
-struct device_error : error { using error::error; };  // CUDA / NCCL / unsupported (no reference twin)
+struct device_error : error { using error::error; };  // CUDA / unsupported (no reference twin)
 
 namespace detail {
 inline void check(int rc) {

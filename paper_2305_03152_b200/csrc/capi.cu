@@ -72,7 +72,6 @@ const char* vk_status_name(int s) {
     case VK_ERR_SHAPE: return "shape_error";
     case VK_ERR_IO: return "io_error";
     case VK_ERR_CUDA: return "cuda_error";
-    case VK_ERR_NCCL: return "nccl_error";
     case VK_ERR_UNSUPPORTED: return "unsupported";
     default: return "internal_error";
   }

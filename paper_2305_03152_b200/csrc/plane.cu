@@ -26,6 +26,7 @@
 
 #include "internal.cuh"
 #include "rng.cuh"
+#include "scan.cuh"
 
 struct vk_sampler_s;
 namespace vk {
@@ -66,15 +67,13 @@ struct vk_plane_s {
   vk::DevBuf d_base, d_slot, d_nlocal;  // K-entry tables for the gather kernel
   vk::DevBuf d_rmask;                   // [K] Part::rmask pointers (resident partitions)
   cudaStream_t stream = nullptr;
-  cudaStream_t aux = nullptr;  // remote-row gathers run here concurrently
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t aux = nullptr;  // prefetched miss exchanges (vk_plane_prefetch), high priority
   // per-wave deduplicated pull of remote rows (multi-GPU): union bitmap of
   // the wave's remote misses, its rank prefix, the distinct list, and the
   // local staging copy of those rows
   struct StageSet {
     vk::DevBuf ubits, uprefix, ulist, staging, scan_tmp;
     vk::DevBuf vbits;  // vertex-space union (word mark); cleared as consumed
-    std::size_t scan_bytes = 0;
     std::uint64_t stage_cap = 0;  // rows the staging buffer holds
     // vk_plane_prefetch: the exchange of sampler run `prefetched` was issued
     // on the aux stream and completes at `ready`
@@ -92,6 +91,15 @@ struct vk_plane_s {
 
 namespace vk {
 namespace {
+
+// In-place exclusive scan of n u32 (scan.cuh); `tmp` holds the look-back status.
+void exclusive_scan_u32(std::uint32_t* a, std::uint64_t n, DevBuf& tmp, cudaStream_t st) {
+  const std::uint64_t tiles = ceil_div(n, (std::uint64_t)kScanU32Threads * kScanU32Items);
+  if (tmp.bytes < tiles * 8) tmp.alloc(tiles * 8);
+  VK_CUDA(cudaMemsetAsync(tmp.p, 0, tiles * 8, st));
+  k_scan_u32<<<(unsigned)tiles, kScanU32Threads, 0, st>>>(a, n, tmp.as<unsigned long long>());
+  VK_LAUNCH_CHECK();
+}
 
 // Order-preserving u64 key of a double, descending: -0.0 == +0.0 as in the
 // reference comparator (policies.cpp:28).
@@ -207,14 +215,13 @@ struct GatherParams {
   std::uint64_t row_bytes;
   std::uint32_t V;                   // vector elements per row
   std::uint32_t magic32;             // ceil(2^32 / V): row = umulhi(e, magic32) for e < 32*V
-  std::uint32_t magic_fix;           // 1 when V > 11585 (umulhi may overshoot by one; fix up)
   unsigned long long* counts;        // [nmb][4]
   // vertex-tile schedule: CTA b serves minibatch b % nmb, vertex tile b / nmb
   const uint4* all_rank;             // [nmb][W] {bits, rank prefix} of all_vertices
   // sparse frontiers instead: rank of each all-level bucket's first vertex
   // [nmb][tb_nb + 1]; a gather tile is tb_group consecutive buckets
   const std::uint32_t* tile_base;
-  std::uint32_t tb_nb, tb_group;
+  std::uint32_t tb_nb, tb_group, tb_split;
   std::uint64_t W;
   std::uint32_t nmb, tiles, tile_words;
   // deduplicated remote rows: staged[rank of new_id[v] in the wave's remote
@@ -224,9 +231,6 @@ struct GatherParams {
   const std::uint32_t* uprefix;
   const char* staging;
   std::uint32_t stage_cap;
-  int idx_hint;    // VK_GATHER_IDX_HINT (see ld_u32_hint)
-  int st_variant;  // VK_GATHER_ST: 0 .cs (evict-first), 1 plain, 2 L1::no_allocate
-  int ld_variant;  // VK_GATHER_LD: 0 nc/no_allocate, 1 +L2 evict_last policy, 2 +evict_normal, 3 coherent
 };
 
 // The all_vertices index range [lo, hi) of vertex tile `tile` of minibatch
@@ -236,6 +240,13 @@ __device__ __forceinline__ void tile_range(const GatherParams& p, std::uint32_t 
                                            std::uint32_t cnt, std::uint32_t& lo, std::uint32_t& hi) {
   if (p.tile_base) {
     const std::uint32_t* tb = p.tile_base + (std::uint64_t)mb * (p.tb_nb + 1);
+    if (p.tb_split > 1) {  // part tile % split of bucket tile / split, by rows
+      const std::uint32_t b = tile / p.tb_split, part = tile % p.tb_split;
+      const std::uint32_t l = tb[b], h = tb[b + 1];
+      lo = l + (std::uint32_t)((std::uint64_t)(h - l) * part / p.tb_split);
+      hi = l + (std::uint32_t)((std::uint64_t)(h - l) * (part + 1) / p.tb_split);
+      return;
+    }
     const std::uint32_t b0 = tile * p.tb_group;
     lo = b0 < p.tb_nb ? tb[b0] : cnt;
     hi = tb[min(b0 + p.tb_group, p.tb_nb)];
@@ -246,6 +257,8 @@ __device__ __forceinline__ void tile_range(const GatherParams& p, std::uint32_t 
   lo = w0 < p.W ? rk[w0].z : cnt;
   hi = w1 < p.W ? rk[w1].z : cnt;
 }
+
+constexpr std::uint32_t kMagicExactV = 11585;  // largest V with V*V < 2^27
 
 // Row of flattened element e (< 32 V) of a warp's 32 rows: umulhi with
 // ceil(2^32/V) is exact while V*V < 2^27 (V <= 11585); above that it can
@@ -276,63 +289,61 @@ __device__ __forceinline__ const std::uint32_t* stage_rstart(const GatherParams&
   return sm;
 }
 
-// 4-byte index loads with an optional L2 policy (0 none, 1 evict_last,
-// 2 evict_first); VK_GATHER_IDX_HINT bit 0: the all-vertex list streamed
-// evict-first, bit 1: slot-map lookups kept evict-last.
-__device__ __forceinline__ std::uint32_t ld_u32_hint(const std::uint32_t* p, int hint) {
-  if (hint == 0) return __ldg(p);
-  std::uint64_t pol;
-  if (hint == 1)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  std::uint32_t r;
-  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
-  return r;
-}
-
-// Streaming 16/4/2-byte copies: the feature table is read through L1
-// (no_allocate) and the gathered rows are written evict-first so neither
-// evicts the graph / slot maps from L2.
+// Row copies move 16/4/2-byte vectors. Source rows are read through L1
+// without allocating and with an L2 evict_last policy (a row read for one
+// minibatch of the wave stays in L2 for the others; C3: 5.60 -> 5.23 ms);
+// gathered rows are written evict-first so they do not evict the graph and
+// slot maps from L2. Measured no better, and removed: plain / L1::no_allocate
+// stores, evict_normal loads, L2 hints on the index loads.
 template <class T>
-__device__ __forceinline__ T ld_stream(const T* p, int variant = 0) {
+__device__ __forceinline__ T ld_row(const T* p, std::uint64_t pol) {
   if constexpr (sizeof(T) == 16) {
     uint4 r;
-    if (variant == 1 || variant == 2) {
-      std::uint64_t pol;
-      if (variant == 1)
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-      else
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                   : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
-    }
-    else if (variant == 3)
-      asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    else
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
     return r;
   } else {
     return __ldg(p);
   }
 }
 template <class T>
-__device__ __forceinline__ void st_stream(T* p, const T& v, int variant = 0) {
-  if constexpr (sizeof(T) == 16) {
-    if (variant == 1)
-      asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                   : "memory");
-    else if (variant == 2)
-      asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-                   "r"(v.w)
-                   : "memory");
-    else
-      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                   : "memory");
-  } else {
+__device__ __forceinline__ void st_row(T* p, const T& v) {
+  if constexpr (sizeof(T) == 16)
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+  else
     __stcs(p, v);
+}
+__device__ __forceinline__ std::uint64_t evict_last_policy() {
+  std::uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Flat copy of a warp's group of `rows` rows (V vectors each) from the 32
+// source pointers in src[] to consecutive output rows: element e of the
+// group is vector e % V of row e / V, kUnroll independent loads in flight
+// per lane, fully coalesced stores. FIX: V > 11585 (see row_of).
+template <class T, int kUnroll, bool FIX>
+__device__ __forceinline__ void copy_group(const T* const* src, T* dst, std::uint32_t rows, std::uint32_t V,
+                                           std::uint32_t magic, std::uint64_t pol) {
+  const std::uint32_t total = rows * V;
+  for (std::uint32_t e0 = threadIdx.x & 31; e0 < total; e0 += 32 * kUnroll) {
+    T val[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const std::uint32_t e = e0 + 32 * u;
+      if (e < total) {
+        const std::uint32_t row = row_of(e, V, magic, FIX);
+        val[u] = ld_row(src[row] + (e - row * V), pol);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const std::uint32_t e = e0 + 32 * u;
+      if (e < total) st_row(dst + e, val[u]);
+    }
   }
 }
 
@@ -439,17 +450,16 @@ __global__ void k_emit_list(const unsigned long long* __restrict__ bits, const s
 // Step 2: one NVLink read per distinct remote row into the staging buffer
 // (warp per 32 rows, 128-bit copies); the gather then serves every
 // minibatch's remote misses from local HBM.
-template <class T, int kUnroll>
+template <class T, int kUnroll, bool FIX>
 __global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::uint32_t* __restrict__ list,
                                                      const std::uint32_t* __restrict__ count_ptr, T* __restrict__ staging) {
   __shared__ const T* s_src[8][32];
   __shared__ std::uint32_t s_rs[kSmemParts];
   const std::uint32_t* rs = stage_rstart(p, s_rs);
   const std::uint32_t cnt = min(*count_ptr, p.stage_cap);
-  const std::uint32_t V = p.V;
-  const std::uint32_t magic = p.magic32;
   const std::uint64_t rowv = p.row_bytes / sizeof(T);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const std::uint64_t pol = evict_last_policy();
   const std::uint32_t gw = blockIdx.x * (blockDim.x >> 5) + w, nw = gridDim.x * (blockDim.x >> 5);
   for (std::uint32_t r0 = gw * 32; r0 < cnt; r0 += nw * 32) {
     const std::uint32_t r = r0 + lane;
@@ -461,49 +471,28 @@ __global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::
     }
     s_src[w][lane] = src;
     __syncwarp();
-    const std::uint32_t total = min(32u, cnt - r0) * V;
-    T* dst = staging + (std::uint64_t)r0 * V;
-    for (std::uint32_t e0 = lane; e0 < total; e0 += 32 * kUnroll) {
-      T val[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const std::uint32_t e = e0 + 32 * u;
-        if (e < total) {
-          const std::uint32_t row = row_of(e, V, magic, p.magic_fix);
-          val[u] = s_src[w][row][e - row * V];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const std::uint32_t e = e0 + 32 * u;
-        if (e < total) dst[e] = val[u];
-      }
-    }
+    copy_group<T, kUnroll, FIX>(s_src[w], staging + (std::uint64_t)r0 * p.V, min(32u, cnt - r0), p.V, p.magic32, pol);
     __syncwarp();
   }
 }
 
-// MODE 0: every row (no peer partitions). MODE 1: rows served from this GPU
-// (local rows, cache rows, misses owned by a co-resident partition). MODE 2:
-// rows owned by a partition on another GPU, read over NVLink. With peers the
-// two run concurrently on two streams so HBM-bound local copies are not held
-// back by NVLink-latency-bound remote ones inside the same warp.
-template <class T, int kUnroll, int kMinBlocks, int MODE, bool STREAM_LD = true>
-__global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
+// STAGED false: every row is served from this GPU (no peer partitions);
+// true: the remote misses of the wave were pulled into the staging buffer by
+// the miss exchange and are read from there.
+template <class T, bool STAGED, bool FIX>
+__global__ void __launch_bounds__(256, sizeof(T) == 16 ? 4 : 1) k_gather(GatherParams p) {
+  constexpr int kUnroll = 8;
   __shared__ const T* s_src[8][32];
-  __shared__ std::uint32_t s_row[8][32];
   __shared__ unsigned sh[4][8];
   __shared__ std::uint32_t s_rs[kSmemParts];
   const std::uint32_t* rs = stage_rstart(p, s_rs);
-  // units are (vertex tile, minibatch) pairs, minibatch fastest; a capped
-  // grid (VK_GATHER_CTAS_PER_SM) walks them persistently so the gather can
-  // leave SM room for a concurrent sampler
-  for (std::uint32_t unit = blockIdx.x; unit < p.tiles * p.nmb; unit += gridDim.x) {
-  // Vertex-tile-major schedule, minibatch fastest: the CTAs resident at any
-  // moment serve the same vertex range for every minibatch of the wave, so a
-  // feature row needed by several minibatches is read from HBM once and hit
-  // in L2 by the others (all_vertices is sorted: a vertex range is a
-  // contiguous run of output rows).
+  const std::uint64_t pol = evict_last_policy();
+  // Units are (vertex tile, minibatch) pairs, vertex-tile-major with the
+  // minibatch fastest: the CTAs resident at any moment serve the same vertex
+  // range for every minibatch of the wave, so a feature row needed by several
+  // minibatches is read from HBM once and hit in L2 by the others
+  // (all_vertices is sorted: a vertex range is a contiguous run of output rows).
+  const std::uint32_t unit = blockIdx.x;
   const std::uint32_t mb = unit % p.nmb;
   const std::uint32_t tile = unit / p.nmb;
   const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
@@ -515,8 +504,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
   const std::uint32_t nl = p.nlocal[k];
   const T* store = reinterpret_cast<const T*>(p.base[k]);
   T* out = reinterpret_cast<T*>(p.out + mb * p.out_stride_bytes);
-  const std::uint32_t V = p.V;
-  const std::uint32_t magic = p.magic32;
   const std::uint64_t rowv = p.row_bytes / sizeof(T);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   unsigned c_local = 0, c_cache = 0, c_miss = 0, c_peer = 0;
@@ -524,81 +511,31 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
     const std::uint32_t r = r0 + lane;
     const T* src = nullptr;
     if (r < hi) {
-      const std::uint32_t v = ld_u32_hint(all + r, p.idx_hint & 1 ? 2 : 0);     // streamed once
-      const std::uint32_t s = ld_u32_hint(slot + v, p.idx_hint & 2 ? 1 : 0);    // reused by every row
-
+      // classify (commsim.cpp:61-73): slot map -> local / cache row of
+      // partition k, else the owner's row in global row order
+      const std::uint32_t v = __ldg(all + r);
+      const std::uint32_t s = __ldg(slot + v);
       if (s != VK_MISS) {
-        if (MODE != 2 && MODE != 4) {
-          src = store + (std::uint64_t)s * rowv;
-          (s < nl ? c_local : c_cache)++;
-        }
+        src = store + (std::uint64_t)s * rowv;
+        (s < nl ? c_local : c_cache)++;
       } else {
-        // miss: the owner's row in global row order (reorder position)
         const std::uint32_t g = __ldg(p.new_id + v);
         const std::uint32_t o = owner_of(rs, p.K, g);
-        const bool remote = p.peer_mask[o] != 0;
-        const T* owner_src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)(g - rs[o]) * rowv;
-        if (MODE == 3 || MODE == 4) {
-          if (remote) {  // pulled once per wave into the local staging buffer
-            const std::uint32_t wq = g >> 6;
-            const std::uint32_t idx = __ldg(p.uprefix + wq) +
-                                      (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (g & 63)) - 1ull));
-            src = idx < p.stage_cap ? reinterpret_cast<const T*>(p.staging) + (std::uint64_t)idx * rowv
-                                    : owner_src;  // past the staging capacity: direct NVLink read
-          } else if (MODE == 3) {
-            src = owner_src;
-          }
-          if (MODE == 3 || remote) {
-            ++c_miss;
-            c_peer += remote;
-          }
-        } else if ((MODE == 0) || (MODE == 1 && !remote) || (MODE == 2 && remote)) {
-          src = owner_src;
-          ++c_miss;
-          c_peer += remote;
+        src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)(g - rs[o]) * rowv;
+        ++c_miss;
+        if (STAGED && p.peer_mask[o]) {  // pulled once per wave into local staging
+          ++c_peer;
+          const std::uint32_t wq = g >> 6;
+          const std::uint32_t idx = __ldg(p.uprefix + wq) +
+                                    (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (g & 63)) - 1ull));
+          if (idx < p.stage_cap)  // else past the staging capacity: the direct NVLink read above
+            src = reinterpret_cast<const T*>(p.staging) + (std::uint64_t)idx * rowv;
         }
       }
     }
-    std::uint32_t rows;
-    if (MODE == 0 || MODE == 3) {
-      s_src[w][lane] = src;
-      s_row[w][lane] = lane;
-      rows = min(32u, hi - r0);
-    } else {  // compact this group's rows of the mode
-      const unsigned mask = __ballot_sync(0xffffffffu, src != nullptr);
-      const unsigned idx = __popc(mask & ((1u << lane) - 1u));
-      if (src) {
-        s_src[w][idx] = src;
-        s_row[w][idx] = lane;
-      }
-      rows = __popc(mask);
-    }
+    s_src[w][lane] = src;
     __syncwarp();
-    const std::uint32_t total = rows * V;
-    T* dst = out + (std::uint64_t)r0 * V;
-    for (std::uint32_t e0 = lane; e0 < total; e0 += 32 * kUnroll) {
-      T val[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const std::uint32_t e = e0 + 32 * u;
-        if (e < total) {
-          const std::uint32_t row = row_of(e, V, magic, p.magic_fix);
-          const T* sp = s_src[w][row] + (e - row * V);
-          if constexpr (STREAM_LD)
-            val[u] = ld_stream(sp, p.ld_variant);
-          else
-            val[u] = *sp;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const std::uint32_t e = e0 + 32 * u;
-        if (e < total) {
-          const std::uint32_t row = row_of(e, V, magic, p.magic_fix);
-          st_stream(dst + (std::uint64_t)s_row[w][row] * V + (e - row * V), val[u], p.st_variant);
-        }
-      }
-    }
+    copy_group<T, kUnroll, FIX>(s_src[w], out + (std::uint64_t)r0 * p.V, min(32u, hi - r0), p.V, p.magic32, pol);
     __syncwarp();
   }
   // block-reduce the class counts, one atomic per class per CTA
@@ -614,117 +551,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_gather(GatherParams p) {
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[threadIdx.x][w];
     if (t) atomicAdd(p.counts + mb * 4 + threadIdx.x, t);
   }
-  __syncthreads();
-  }
-}
-
-// Single-GPU gather on the Tensor Memory Accelerator's bulk-copy path
-// (VK_GATHER_TMA=1): per warp and group of 32 output rows, every lane issues
-// one cp.async.bulk of its source row (global -> the warp's shared buffer,
-// completion counted in bytes on an mbarrier), then one elected lane writes
-// the group's rows -- contiguous in the output -- with a single bulk store.
-// Rows must be 16 B multiples of at most 512 B.
-constexpr int kTmaWarps = 8;
-constexpr std::uint32_t kTmaMaxRow = 512;
-
-__device__ __forceinline__ std::uint32_t smem_u32(const void* ptr) {
-  return (std::uint32_t)__cvta_generic_to_shared(ptr);
-}
-
-__global__ void __launch_bounds__(kTmaWarps * 32, 1) k_gather_tma(GatherParams p) {
-  extern __shared__ __align__(128) unsigned char s_tma[];
-  __shared__ __align__(8) unsigned long long s_bar[kTmaWarps];
-  __shared__ unsigned sh[4][kTmaWarps];
-  __shared__ std::uint32_t s_rs[kSmemParts];
-  const std::uint32_t* rs = stage_rstart(p, s_rs);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const std::uint32_t rb = (std::uint32_t)p.row_bytes;
-  unsigned char* buf = s_tma + (std::size_t)w * 32 * rb;
-  const std::uint32_t bar = smem_u32(&s_bar[w]);
-  if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncwarp();
-  std::uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  std::uint32_t phase = 0;
-  for (std::uint32_t unit = blockIdx.x; unit < p.tiles * p.nmb; unit += gridDim.x) {
-    const std::uint32_t mb = unit % p.nmb;
-    const std::uint32_t tile = unit / p.nmb;
-    const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
-    const std::uint32_t cnt = p.all_count[mb];
-    std::uint32_t lo, hi;
-    tile_range(p, mb, tile, cnt, lo, hi);
-    const std::uint32_t* all = p.all + mb * p.all_stride;
-    const std::uint32_t* slot = p.slot[k];
-    const std::uint32_t nl = p.nlocal[k];
-    const char* store = p.base[k];
-    char* out = p.out + mb * p.out_stride_bytes;
-    unsigned c_local = 0, c_cache = 0, c_miss = 0;
-    for (std::uint32_t r0 = lo + w * 32; r0 < hi; r0 += kTmaWarps * 32) {
-      const std::uint32_t r = r0 + lane;
-      const std::uint32_t rows = min(32u, hi - r0);
-      const char* src = nullptr;
-      if (r < hi) {
-        const std::uint32_t v = __ldg(all + r);
-        const std::uint32_t s = __ldg(slot + v);
-        if (s != VK_MISS) {
-          src = store + (std::uint64_t)s * rb;
-          (s < nl ? c_local : c_cache)++;
-        } else {
-          const std::uint32_t g = __ldg(p.new_id + v);
-          const std::uint32_t o = owner_of(rs, p.K, g);
-          src = p.base[o] + (std::uint64_t)(g - rs[o]) * rb;
-          ++c_miss;
-        }
-      }
-      if (lane == 0) {
-        // the previous group's bulk store has finished reading the buffer
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * rb)
-                     : "memory");
-      }
-      __syncwarp();
-      if (r < hi)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
-            "%4;" ::"r"(smem_u32(buf + (std::size_t)lane * rb)),
-            "l"(src), "r"(rb), "r"(bar), "l"(pol)
-            : "memory");
-      // wait for this group's bytes
-      std::uint32_t done = 0;
-      while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.u32 %0, 1, 0, P;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(phase)
-            : "memory");
-      }
-      phase ^= 1u;
-      if (lane == 0) {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + (std::uint64_t)r0 * rb),
-                     "r"(smem_u32(buf)), "r"(rows * rb)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      __syncwarp();
-    }
-    unsigned vals[3] = {c_local, c_cache, c_miss};
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      unsigned x = __reduce_add_sync(0xffffffffu, vals[q]);
-      if (lane == 0) sh[q][w] = x;
-    }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-      unsigned long long t = 0;
-      for (int q = 0; q < kTmaWarps; ++q) t += sh[threadIdx.x][q];
-      if (t) atomicAdd(p.counts + mb * 4 + threadIdx.x, t);
-    }
-    __syncthreads();
-  }
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace
@@ -867,8 +693,6 @@ int vk_plane_create(int device, uint64_t n, uint32_t K, uint32_t dim, int dtype,
         VK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         VK_CUDA(cudaStreamCreateWithPriority(&p->aux, cudaStreamNonBlocking, hi));
       }
-      VK_CUDA(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
-      VK_CUDA(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
       p->part_of.alloc(n * 4);
       p->owner_row.alloc(n * 4);
       p->new_id.alloc(n * 4);
@@ -907,8 +731,6 @@ int vk_plane_destroy(vk_plane p) {
       if (part.peer) cudaIpcCloseMemHandle(part.peer);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->aux) cudaStreamDestroy(p->aux);
-    if (p->fork) cudaEventDestroy(p->fork);
-    if (p->join) cudaEventDestroy(p->join);
     delete p;
   });
 }
@@ -1134,111 +956,46 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
     gp.V = (std::uint32_t)(p->row_bytes / esz);
     if (gp.V >= (1u << 15)) raise(VK_ERR_UNSUPPORTED, "feature rows above 512 KiB are not supported");
     gp.magic32 = gp.V == 1 ? 0u : (std::uint32_t)((0xffffffffull / gp.V) + 1);  // ceil(2^32 / V)
-    gp.magic_fix = gp.V > 11585 ? 1u : 0u;
     sampler_all_rank(s, &gp.all_rank, &gp.W);
     gp.rmask = p->d_rmask.as<const unsigned long long* const>();
-    static const int ld_variant = [] {
-      // default evict_last: a row read for one minibatch of the wave stays in
-      // L2 for the others against the streaming (evict-first) output writes
-      // (C3, wave 128: gather 5.60 -> 5.23 ms)
-      const char* e = std::getenv("VK_GATHER_LD");
-      return e ? std::atoi(e) : 1;
-    }();
-    gp.ld_variant = ld_variant;
-    static const int st_variant = [] {
-      const char* e = std::getenv("VK_GATHER_ST");
-      return e ? std::atoi(e) : 0;
-    }();
-    gp.st_variant = st_variant;
-    static const int idx_hint = [] {
-      const char* e = std::getenv("VK_GATHER_IDX_HINT");
-      return e ? std::atoi(e) : 0;
-    }();
-    gp.idx_hint = idx_hint;
     gp.nmb = nmb;
-    static const std::uint32_t tile_words = [] {
-      const char* e = std::getenv("VK_GATHER_TILE_WORDS");
-      const std::uint32_t v = e ? (std::uint32_t)std::atoi(e) : kGatherTileWords;
-      return std::max<std::uint32_t>(64, (v + 63) / 64 * 64);  // rank words exist at multiples of 64
-    }();
-    // a few thousand output rows per (tile, minibatch) unit (the capacity
-    // over-estimates the density, ~1.8x at C3): sparse neighbourhoods take
-    // proportionally wider vertex tiles. C3: 4096-vertex tiles 5.35 ms,
-    // 16384-vertex tiles 5.08 ms; C1 keeps 4096 (VK_GATHER_UNIT_ROWS)
-    static const double unit_rows = [] {
-      const char* e = std::getenv("VK_GATHER_UNIT_ROWS");
-      return e ? std::atof(e) : 3584.0;
-    }();
+    // Gather tiles: a few thousand output rows per (tile, minibatch) unit.
+    // Dense rank words exist at multiples of 64 words; the capacity
+    // over-estimates the density (~1.8x at C3), so sparse neighbourhoods take
+    // proportionally wider tiles (C3: 4096-vertex tiles 5.35 ms, 16384 5.08
+    // ms), at most 2048 words: papers-scale waves have little row reuse
+    // across minibatches. Sparse frontiers: whole all-level buckets.
+    constexpr double kUnitRows = 3584.0;
     const double density = std::max(1e-9, (double)gp.all_stride / (double)p->n);
-    // ... at most 2048 words (131K vertices) per tile: papers-scale waves
-    // have little row reuse across minibatches and prefer narrower tiles
-    const std::uint64_t want_words = std::min<std::uint64_t>(2048, (std::uint64_t)(unit_rows / (64.0 * density)));
-    std::uint64_t tw = std::max<std::uint64_t>(tile_words, (want_words + 63) / 64 * 64);
+    const std::uint64_t want_words = std::min<std::uint64_t>(2048, (std::uint64_t)(kUnitRows / (64.0 * density)));
+    const std::uint64_t tw = std::max<std::uint64_t>(kGatherTileWords, (want_words + 63) / 64 * 64);
     gp.tile_words = (std::uint32_t)tw;
     gp.tiles = (std::uint32_t)((gp.W + tw - 1) / tw);
     {
       std::uint32_t bbits = 0, nb = 0;
       gp.tile_base = sampler_tile_base(s, &bbits, &nb);
-      if (gp.tile_base) {  // sparse frontiers: tiles of whole buckets, ~unit_rows rows each
+      if (gp.tile_base) {
+        // papers-scale neighbourhoods have little row reuse across the
+        // minibatches of a wave: ~1K-row units (C4: 2.2K-row buckets split in
+        // two, 4.58 ms vs 4.93 ms for 4.4K-row units of two buckets)
+        constexpr double kSparseUnitRows = 1024.0;
         const double rows_per_bucket = std::max(1.0, (double)gp.all_stride / (double)nb);
         gp.tb_nb = nb;
-        gp.tb_group = (std::uint32_t)std::max(1.0, std::round(unit_rows / rows_per_bucket));
-        gp.tiles = (nb + gp.tb_group - 1) / gp.tb_group;
+        if (rows_per_bucket > kSparseUnitRows) {
+          gp.tb_group = 1;
+          gp.tb_split = (std::uint32_t)std::min(64.0, std::round(rows_per_bucket / kSparseUnitRows));
+          gp.tiles = nb * gp.tb_split;
+        } else {
+          gp.tb_group = (std::uint32_t)std::max(1.0, std::round(kSparseUnitRows / rows_per_bucket));
+          gp.tb_split = 1;
+          gp.tiles = (nb + gp.tb_group - 1) / gp.tb_group;
+        }
       }
     }
-    const char* cap_env = std::getenv("VK_GATHER_CTAS_PER_SM");
     const std::uint64_t units = (std::uint64_t)gp.tiles * nmb;
-    const int cap_per_sm = cap_env ? std::atoi(cap_env) : 0;
-    const std::uint64_t cap = cap_per_sm > 0 ? (std::uint64_t)cap_per_sm * sm_count(p->device) : units;
-    dim3 grid((unsigned)std::max<std::uint64_t>(1, std::min(units, cap)));
-    // split local / remote rows into concurrent kernels (VK_GATHER_SPLIT=1);
-    // default: one kernel, each warp mixes HBM and NVLink rows
-    static const bool split = [] {
-      const char* e = std::getenv("VK_GATHER_SPLIT");
-      return e && std::atoi(e) != 0;
-    }();
-    bool any_peer = false;
-    for (const auto& q : p->parts) any_peer |= q.attached;
-    const bool peers = any_peer && split;
-    const bool staged = any_peer && !split;
-    // VK_GATHER_OVERLAP=1 runs the miss exchange on the aux stream alongside
-    // a gather of the locally served rows, then gathers the staged remote rows.
-    // Measured slower on 2 B200s (14.4K vs 17.7K mb/s on C3: the split costs a
-    // second compaction of the vertex list and the two passes contend for HBM),
-    // so the serial exchange -> single gather is the default.
-    static const bool overlap = [] {
-      const char* e = std::getenv("VK_GATHER_OVERLAP");
-      return e && std::atoi(e) != 0;
-    }();
-    cudaStream_t xs = st;  // exchange stream
-    if (staged && overlap) {
-      VK_CUDA(cudaEventRecord(p->fork, st));
-      VK_CUDA(cudaStreamWaitEvent(p->aux, p->fork, 0));
-      xs = p->aux;
-    }
-    // VK_GATHER_TIMING=1: per-phase event timing (synchronises each call;
-    // diagnostics only), summed and printed to stderr at exit
-    static const bool timing = [] {
-      const char* e = std::getenv("VK_GATHER_TIMING");
-      return e && std::atoi(e) != 0;
-    }();
-    static double t_acc[4] = {0, 0, 0, 0};  // mark, scan+emit, pull, gather
-    static long t_calls = 0;
-    cudaEvent_t tev[5];
-    if (timing) {
-      static bool reg = false;
-      if (!reg) {
-        reg = true;
-        std::atexit([] {
-          if (t_calls)
-            std::fprintf(stderr,
-                         "[vk gather timing] calls %ld  mark %.3f  scan+emit %.3f  pull %.3f  gather %.3f ms/call\n",
-                         t_calls, t_acc[0] / t_calls, t_acc[1] / t_calls, t_acc[2] / t_calls, t_acc[3] / t_calls);
-        });
-      }
-      for (auto& e : tev) VK_CUDA(cudaEventCreate(&e));
-      VK_CUDA(cudaEventRecord(tev[0], xs));
-    }
+    if (units >= (1ull << 31)) raise(VK_ERR_UNSUPPORTED, "too many gather tiles");
+    bool staged = false;
+    for (const auto& q : p->parts) staged |= q.attached;
     if (prefetch_only && !staged) return;  // nothing to exchange on one GPU
     auto& ss = p->stage_sets[static_cast<const void*>(s)];
     const std::uint64_t run = sampler_run_id(s);
@@ -1252,10 +1009,6 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       gp.staging = ss.staging.as<char>();
       gp.stage_cap = (std::uint32_t)ss.stage_cap;
     }
-    if (timing && have_prefetch) {
-      VK_CUDA(cudaEventRecord(tev[1], xs));
-      VK_CUDA(cudaEventRecord(tev[2], xs));
-    }
     if (staged && !have_prefetch) {
       // miss exchange: union of the wave's remote misses -> distinct list ->
       // one NVLink pull per distinct row into local staging -> the gather
@@ -1266,7 +1019,7 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       };
       p->last_set = &ss;
       // a superseded prefetch of this stage set may still be running on aux
-      if (ss.ready && xs != p->aux) VK_CUDA(cudaStreamWaitEvent(xs, ss.ready, 0));
+      if (ss.ready && st != p->aux) VK_CUDA(cudaStreamWaitEvent(st, ss.ready, 0));
       ss.prefetched = ~0ull;
       ensure(ss.ubits, W * 8);
       ensure(ss.uprefix, (W + 1) * 4);
@@ -1285,62 +1038,54 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
           ss.stage_cap = want;
         }
       }
-      if (!ss.scan_bytes) {
-        VK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, ss.scan_bytes, ss.uprefix.as<std::uint32_t>(),
-                                              ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), xs));
-        ss.scan_tmp.alloc(std::max<std::size_t>(ss.scan_bytes, 1));
-      }
-      VK_CUDA(cudaMemsetAsync(ss.ubits.p, 0, W * 8, xs));
-      VK_CUDA(cudaMemsetAsync(ss.uprefix.as<std::uint32_t>() + W, 0, 4, xs));
-      const unsigned gx = (unsigned)std::max<std::uint64_t>(
-          1, std::min<std::uint64_t>(ceil_div(gp.all_stride, 256), (std::uint64_t)sm_count(p->device) * 8 / nmb + 1));
-      static const bool word_mark = [] {
-        const char* e = std::getenv("VK_MARK_WORDS");
-        return !e || std::atoi(e) != 0;
-      }();
-      if (word_mark && sampler_all_rank_dense(s)) {
+      VK_CUDA(cudaMemsetAsync(ss.ubits.p, 0, W * 8, st));
+      VK_CUDA(cudaMemsetAsync(ss.uprefix.as<std::uint32_t>() + W, 0, 4, st));
+      if (sampler_all_rank_dense(s)) {
+        // word-parallel marking from the dense all-level rank words
         if (!ss.vbits.p) {
           ss.vbits.alloc(W * 8);
-          VK_CUDA(cudaMemsetAsync(ss.vbits.p, 0, W * 8, xs));
+          VK_CUDA(cudaMemsetAsync(ss.vbits.p, 0, W * 8, st));
         }
-        k_remote_union<<<dim3((unsigned)ceil_div(W, 256), (unsigned)ceil_div(nmb, kMarkChunk)), 256, 0, xs>>>(
+        k_remote_union<<<dim3((unsigned)ceil_div(W, 256), (unsigned)ceil_div(nmb, kMarkChunk)), 256, 0, st>>>(
             gp, ss.vbits.as<unsigned long long>());
-        k_remote_to_rows<<<grid_for(W, p->device), 256, 0, xs>>>(gp, ss.vbits.as<unsigned long long>(),
+        k_remote_to_rows<<<grid_for(W, p->device), 256, 0, st>>>(gp, ss.vbits.as<unsigned long long>(),
                                                                 ss.ubits.as<unsigned long long>());
-        count_launch();  // the second mark pass
-      } else
-        k_remote_mark<<<dim3(gx, nmb), 256, 0, xs>>>(gp, ss.ubits.as<unsigned long long>());
-      if (timing) VK_CUDA(cudaEventRecord(tev[1], xs));
-      k_word_popc<<<grid_for(W, p->device), 256, 0, xs>>>(ss.ubits.as<unsigned long long>(), W,
+        count_launch(2);
+      } else {
+        const unsigned gx = (unsigned)std::max<std::uint64_t>(
+            1, std::min<std::uint64_t>(ceil_div(gp.all_stride, 256), (std::uint64_t)sm_count(p->device) * 8 / nmb + 1));
+        k_remote_mark<<<dim3(gx, nmb), 256, 0, st>>>(gp, ss.ubits.as<unsigned long long>());
+        count_launch();
+      }
+      k_word_popc<<<grid_for(W, p->device), 256, 0, st>>>(ss.ubits.as<unsigned long long>(), W,
                                                           ss.uprefix.as<std::uint32_t>());
-      std::size_t tb = ss.scan_bytes;
-      VK_CUDA(cub::DeviceScan::ExclusiveSum(ss.scan_tmp.p, tb, ss.uprefix.as<std::uint32_t>(),
-                                            ss.uprefix.as<std::uint32_t>(), (std::int64_t)(W + 1), xs));
-      k_emit_list<<<grid_for(W, p->device), 256, 0, xs>>>(ss.ubits.as<unsigned long long>(),
+      exclusive_scan_u32(ss.uprefix.as<std::uint32_t>(), W + 1, ss.scan_tmp, st);
+      k_emit_list<<<grid_for(W, p->device), 256, 0, st>>>(ss.ubits.as<unsigned long long>(),
                                                           ss.uprefix.as<std::uint32_t>(), W,
                                                           ss.ulist.as<std::uint32_t>());
-      if (timing) VK_CUDA(cudaEventRecord(tev[2], xs));
-      // NVLink-bound: a few CTAs per SM keep enough bytes in flight and leave
-      // room for the concurrent local gather
-      static const unsigned pull_per_sm = [] {
-        const char* e = std::getenv("VK_PULL_CTAS_PER_SM");
-        return e && std::atoi(e) > 0 ? (unsigned)std::atoi(e) : 0u;
-      }();
-      // prefetched exchanges share the SMs with a running gather: 2 CTAs/SM
-      const unsigned pg =
-          (unsigned)sm_count(p->device) * (pull_per_sm ? pull_per_sm : ((overlap || prefetch_only) ? 2 : 8));
-      if (pv16)
-        k_remote_pull<uint4, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
-                                                     ss.uprefix.as<std::uint32_t>() + W, ss.staging.as<uint4>());
-      else if (pv4)
-        k_remote_pull<std::uint32_t, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
-                                                             ss.uprefix.as<std::uint32_t>() + W,
-                                                             ss.staging.as<std::uint32_t>());
+      // NVLink-bound: a prefetched exchange shares the SMs with a running
+      // gather (2 CTAs/SM, on the high-priority aux stream); inline, 8 CTAs/SM
+      const unsigned pg = (unsigned)sm_count(p->device) * (prefetch_only ? 2 : 8);
+      GatherParams pp = gp;  // staged rows are plain rows: the pull's vector width follows the row size
+      auto pull = [&](auto tag, std::uint32_t esz) {
+        using T = decltype(tag);
+        pp.V = (std::uint32_t)(p->row_bytes / esz);
+        pp.magic32 = pp.V == 1 ? 0u : (std::uint32_t)((0xffffffffull / pp.V) + 1);
+        pp.stage_cap = (std::uint32_t)ss.stage_cap;
+        if (pp.V > kMagicExactV)
+          k_remote_pull<T, 8, true><<<pg, 256, 0, st>>>(pp, ss.ulist.as<std::uint32_t>(),
+                                                        ss.uprefix.as<std::uint32_t>() + W, ss.staging.as<T>());
+        else
+          k_remote_pull<T, 8, false><<<pg, 256, 0, st>>>(pp, ss.ulist.as<std::uint32_t>(),
+                                                         ss.uprefix.as<std::uint32_t>() + W, ss.staging.as<T>());
+      };
+      if (p->row_bytes % 16 == 0)
+        pull(uint4{}, 16);
+      else if (p->row_bytes % 4 == 0)
+        pull(std::uint32_t{}, 4);
       else
-        k_remote_pull<std::uint16_t, 8><<<pg, 256, 0, xs>>>(gp, ss.ulist.as<std::uint32_t>(),
-                                                             ss.uprefix.as<std::uint32_t>() + W,
-                                                             ss.staging.as<std::uint16_t>());
-      count_launch(6);  // mark, popc, scan (2 cub kernels), emit, pull
+        pull(std::uint16_t{}, 2);
+      count_launch(3);
       VK_LAUNCH_CHECK();
       gp.ubits = ss.ubits.as<unsigned long long>();
       gp.uprefix = ss.uprefix.as<std::uint32_t>();
@@ -1348,99 +1093,30 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
       gp.stage_cap = (std::uint32_t)ss.stage_cap;
       if (prefetch_only) {
         if (!ss.ready) VK_CUDA(cudaEventCreateWithFlags(&ss.ready, cudaEventDisableTiming));
-        VK_CUDA(cudaEventRecord(ss.ready, xs));
-        sampler_add_reader(s, xs);  // the exchange read the sampler's all-vertex lists
+        VK_CUDA(cudaEventRecord(ss.ready, st));
+        sampler_add_reader(s, st);  // the exchange read the sampler's all-vertex lists
         ss.prefetched = run;
-        if (timing) {
-          for (auto& e : tev) VK_CUDA(cudaEventDestroy(e));
-        }
         return;
       }
     }
-    // VK_GATHER_CFG: (unroll, min CTAs/SM) 0 (8,4) 1 (16,2) 2 (4,8) 3 (8,2);
-    // C3: 5.05 / 6.73 / 5.62 / 6.62 ms, so (8,4) is the default
-    static const int gcfg = [] {
-      const char* e = std::getenv("VK_GATHER_CFG");
-      return e ? std::atoi(e) : 0;
-    }();
-    static const bool tma_env = [] {
-      const char* e = std::getenv("VK_GATHER_TMA");
-      return e && std::atoi(e) != 0;
-    }();
-    const bool use_tma = tma_env && v16 && p->row_bytes <= kTmaMaxRow;
-    auto launch = [&](int mode, cudaStream_t where) {
-      if (v16) {
-        if (mode == 4) k_gather<uint4, 8, 4, 4><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 3) k_gather<uint4, 8, 4, 3><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 0 && use_tma) {
-          static bool attr = false;
-          if (!attr) {
-            VK_CUDA(cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(kTmaWarps * 32 * kTmaMaxRow)));
-            attr = true;
-          }
-          const unsigned tgrid = (unsigned)std::min<std::uint64_t>(units, (std::uint64_t)sm_count(p->device) * 2);
-          k_gather_tma<<<tgrid, kTmaWarps * 32, (std::size_t)kTmaWarps * 32 * p->row_bytes, where>>>(gp);
-        }
-        else if (mode == 0 && gcfg == 1) k_gather<uint4, 16, 2, 0><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 0 && gcfg == 2) k_gather<uint4, 4, 8, 0><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 0 && gcfg == 3) k_gather<uint4, 8, 2, 0><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 0) k_gather<uint4, 8, 4, 0><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 1) k_gather<uint4, 8, 4, 1><<<grid, 256, 0, where>>>(gp);
-        else k_gather<uint4, 16, 2, 2, false><<<grid, 256, 0, where>>>(gp);  // peer rows: plain LDG
-      } else if (v4) {
-        if (mode == 4) k_gather<std::uint32_t, 8, 1, 4><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 3) k_gather<std::uint32_t, 8, 1, 3><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 0) k_gather<std::uint32_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 1) k_gather<std::uint32_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
-        else k_gather<std::uint32_t, 8, 1, 2><<<grid, 256, 0, where>>>(gp);
-      } else {
-        if (mode == 4) k_gather<std::uint16_t, 8, 1, 4><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 3) k_gather<std::uint16_t, 8, 1, 3><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 0) k_gather<std::uint16_t, 8, 1, 0><<<grid, 256, 0, where>>>(gp);
-        else if (mode == 1) k_gather<std::uint16_t, 8, 1, 1><<<grid, 256, 0, where>>>(gp);
-        else k_gather<std::uint16_t, 8, 1, 2><<<grid, 256, 0, where>>>(gp);
-      }
-      count_launch();
-      VK_LAUNCH_CHECK();
+    const dim3 grid((unsigned)std::max<std::uint64_t>(1, units));
+    auto launch = [&](auto tag) {
+      using T = decltype(tag);
+      const bool fix = gp.V > kMagicExactV;
+      if (staged)
+        fix ? k_gather<T, true, true><<<grid, 256, 0, st>>>(gp) : k_gather<T, true, false><<<grid, 256, 0, st>>>(gp);
+      else
+        fix ? k_gather<T, false, true><<<grid, 256, 0, st>>>(gp) : k_gather<T, false, false><<<grid, 256, 0, st>>>(gp);
     };
-    if (timing) {
-      if (!staged) {
-        VK_CUDA(cudaEventRecord(tev[1], xs));
-        VK_CUDA(cudaEventRecord(tev[2], xs));
-      }
-      VK_CUDA(cudaEventRecord(tev[3], xs));
-    }
-    if (staged && overlap) {
-      launch(1, st);  // local + cache + co-resident rows while the pull runs
-      VK_CUDA(cudaEventRecord(p->join, p->aux));
-      VK_CUDA(cudaStreamWaitEvent(st, p->join, 0));
-      launch(4, st);  // remote rows from staging
-    } else if (staged) {
-      launch(3, st);
-    } else if (!peers) {
-      launch(0, st);
-    } else {
-      // fork: remote (NVLink) rows on the plane's auxiliary stream, local rows on st
-      VK_CUDA(cudaEventRecord(p->fork, st));
-      VK_CUDA(cudaStreamWaitEvent(p->aux, p->fork, 0));
-      launch(2, p->aux);
-      launch(1, st);
-      VK_CUDA(cudaEventRecord(p->join, p->aux));
-      VK_CUDA(cudaStreamWaitEvent(st, p->join, 0));
-    }
+    if (v16)
+      launch(uint4{});
+    else if (v4)
+      launch(std::uint32_t{});
+    else
+      launch(std::uint16_t{});
+    count_launch();
+    VK_LAUNCH_CHECK();
     sampler_add_reader(s, st);  // the next run of this sampler waits for this gather
-    if (timing) {
-      VK_CUDA(cudaEventRecord(tev[4], st));
-      VK_CUDA(cudaEventSynchronize(tev[4]));
-      for (int i = 0; i < 4; ++i) {
-        float ms = 0;
-        VK_CUDA(cudaEventElapsedTime(&ms, tev[i], tev[i + 1]));
-        t_acc[i] += ms;
-      }
-      ++t_calls;
-      for (auto& e : tev) VK_CUDA(cudaEventDestroy(e));
-    }
   }
 }
 

@@ -1125,10 +1125,7 @@ void launch_sample(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaStre
       p.rank_prev = s.hopprefix.as<uint4>();
       // ~512 sources per (tile, minibatch) CTA at full frontier capacity,
       // at least kSampleTileWords words (4096 vertices) per tile
-      static const std::uint64_t tile_sources = [] {
-        const char* e = std::getenv("VK_SAMPLE_TILE_SOURCES");
-        return (std::uint64_t)(e && std::atoi(e) > 0 ? std::atoi(e) : 512);
-      }();
+      constexpr std::uint64_t tile_sources = 512;  // 256 / 1024 measured flat
       const std::uint64_t want_tiles = std::max<std::uint64_t>(1, p.capFprev / tile_sources);
       std::uint64_t tw = std::max<std::uint64_t>(kSampleTileWords, (s.W + want_tiles - 1) / want_tiles);
       tw = (tw + kRankStride - 1) / kRankStride * kRankStride;  // tile starts carry rank words
@@ -1177,11 +1174,7 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
   const std::uint64_t min_ctas = (std::uint64_t)sm_count(s.g->device) * 8;
   auto ctas = [&](int w) { return (std::uint64_t)nmb * ((s.W + (std::uint64_t)kCompactThreads * w - 1) /
                                                          ((std::uint64_t)kCompactThreads * w)); };
-  static const int max_wpt = [] {
-    const char* e = std::getenv("VK_COMPACT_MAX_WPT");
-    const int v = e ? std::atoi(e) : 16;
-    return v >= 32 ? 32 : 16;
-  }();
+  constexpr int max_wpt = 16;  // 32 measured no faster
   while (wpt < max_wpt && (double)kCompactThreads * (wpt * 2) * 64.0 * density <= (double)kStage &&
          ctas(wpt * 2) >= min_ctas)
     wpt *= 2;
@@ -1300,15 +1293,11 @@ void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaS
 // kBucketTarget items per bucket, 2^14..2^19 ids per bucket (shared bitmap
 // of 2..64 KB), at most kMaxBuckets buckets.
 std::uint32_t bucket_bits(std::uint64_t n) {
-  // 2^14..2^19 ids per bucket (2..64 KB of shared bitmap), at most kMaxBuckets
-  static const std::uint32_t force = [] {  // TUNING (temporary)
-    const char* e = std::getenv("VK_BUCKET_BITS");
-    return e ? (std::uint32_t)std::atoi(e) : 0u;
-  }();
-  // ~512 buckets per minibatch: C4 (111 M ids) -> 2^18 ids (32 KB of bitmap)
-  // per bucket; measured per C4 wave: 2^17 5.3 ms, 2^18 4.2 ms, 2^19 4.2 ms
-  std::uint32_t bb = force ? force : (std::uint32_t)std::ceil(std::log2(std::max(1.0, (double)n / 512.0)));
-  bb = std::min<std::uint32_t>(force ? 19 : 18, std::max<std::uint32_t>(14, bb));
+  // 2^14..2^19 ids per bucket (2..64 KB of shared bitmap), at most
+  // kMaxBuckets; ~512 buckets per minibatch: C4 (111 M ids) -> 2^18 ids per
+  // bucket (measured per C4 wave of 64: 2^17 5.3 ms, 2^18 4.2 ms, 2^19 4.2 ms)
+  std::uint32_t bb = (std::uint32_t)std::ceil(std::log2(std::max(1.0, (double)n / 512.0)));
+  bb = std::min<std::uint32_t>(18, std::max<std::uint32_t>(14, bb));
   while (bb < 19 && ((n + (1ull << bb) - 1) >> bb) > kMaxBuckets) ++bb;
   return bb;
 }
@@ -1621,16 +1610,10 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
     count_launch();
     VK_LAUNCH_CHECK();
     // small graphs: per-minibatch CTAs compact with shared-memory bitmaps and
-    // fuse the relabels (VK_SAMPLER_SMALL=0 forces the general path)
-    static const bool small_ok = [] {
-      const char* e = std::getenv("VK_SAMPLER_SMALL");
-      return !e || std::atoi(e) != 0;
-    }();
-    const bool small = small_ok && !s->sparse && s->W <= kSmallW;
-    static const bool relabel_overlap = [] {
-      const char* e = std::getenv("VK_RELABEL_OVERLAP");
-      return !e || std::atoi(e) != 0;
-    }();
+    // fuse the relabels (C1: 65 K -> 71 K minibatches/s)
+    const bool small = !s->sparse && s->W <= kSmallW;
+    // the MFG relabel of hop h overlaps the sampling of hop h+1 on aux
+    constexpr bool relabel_overlap = true;
     bool relabel_pending = false;  // a relabel is running on aux (join before the next compaction)
     for (std::uint32_t h = 1; h <= s->L; ++h) {
       const std::uint32_t f = s->cfg.fanouts[h - 1];

@@ -117,4 +117,36 @@ __device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* 
   return lookback_resolve(status, tile, aggregate);
 }
 
+// In-place exclusive scan of n u32 values (the last output is the total of
+// all earlier inputs): one pass, 2048 values per CTA, decoupled look-back
+// across CTAs in blockIdx order. Totals must stay below 2^31.
+constexpr int kScanU32Threads = 256, kScanU32Items = 8;
+static __global__ void __launch_bounds__(kScanU32Threads) k_scan_u32(std::uint32_t* __restrict__ a, std::uint64_t n,
+                                                            unsigned long long* __restrict__ status) {
+  __shared__ unsigned long long s_sm[kScanU32Threads / 32];
+  __shared__ unsigned long long s_excl;
+  const std::uint64_t base = ((std::uint64_t)blockIdx.x * kScanU32Threads + threadIdx.x) * kScanU32Items;
+  std::uint32_t x[kScanU32Items];
+  unsigned long long sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanU32Items; ++k) {
+    x[k] = base + k < n ? a[base + k] : 0u;
+    sum += x[k];
+  }
+  unsigned long long total;
+  const unsigned long long lex = block_inclusive_scan<kScanU32Threads>(sum, s_sm, &total) - sum;
+  if (threadIdx.x < 32) {
+    const unsigned long long ex = lookback_warp(status, blockIdx.x, pack_vd(total, 0));
+    if (threadIdx.x == 0) s_excl = ex;
+  }
+  __syncthreads();
+  unsigned long long run = unpack_v(s_excl) + lex;
+#pragma unroll
+  for (int k = 0; k < kScanU32Items; ++k)
+    if (base + k < n) {
+      a[base + k] = (std::uint32_t)run;
+      run += x[k];
+    }
+}
+
 }  // namespace vk

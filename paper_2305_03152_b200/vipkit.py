@@ -41,13 +41,12 @@ class ConfigError(VipkitError): code = 7         # noqa: E701
 class ShapeError(VipkitError): code = 8          # noqa: E701
 class IOError_(VipkitError): code = 9            # noqa: E701
 class CudaError(VipkitError): code = 20          # noqa: E701
-class NcclError(VipkitError): code = 21          # noqa: E701
 class UnsupportedError(VipkitError): code = 22   # noqa: E701
 
 
 _BY_CODE = {c.code: c for c in (ParseError, RangeError, ParameterError, FormatError,
                                 PartitionError, SamplingError, ConfigError, ShapeError,
-                                IOError_, CudaError, NcclError, UnsupportedError)}
+                                IOError_, CudaError, UnsupportedError)}
 
 # ------------------------------------------------------------------ library
 _lib = None

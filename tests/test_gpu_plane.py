@@ -226,20 +226,6 @@ def test_baseline_rankings_vs_reference(vk, ref, golden, graph, directed):
         vk.rank_wpr(g, roles, labels, K, 0, 2, 0)
 
 
-def test_tma_gather_variant_parity():
-    """The opt-in TMA bulk-copy gather (VK_GATHER_TMA=1, read once per
-    process) passes the same row/tally parity tests in a fresh process."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, VK_GATHER_TMA="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "gather_rows",
-                        os.path.join(root, "tests", "test_gpu_plane.py")],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-
-
 def _gather_host(vk, plane, sampler, nmb, stream=0):
     view = sampler.view()
     rb = plane.row_bytes
