@@ -115,8 +115,10 @@ def test_c3_wave_sample_and_gather(vk, port, c3):
 
 def test_sparse_graph_wide_tile_compaction(vk, port):
     """8 M vertices, batch 64: every hop's expected density is far below one
-    id per 64-bit word, so the compaction takes its wide-tile (16 words per
-    thread, nonzero-word) path; bit-exact against the oracle."""
+    id per 64-bit word. The dense (bitmap) representation, forced here, takes
+    its wide-tile compaction (16 words per thread, nonzero-word) path; the
+    automatic choice for this shape is the sparse (bucket) one, and both are
+    bit-exact against the oracle and identical to each other."""
     n = 8_000_000
     off, tgt, labels = vk.synth_community_powerlaw(n, 3, 4, 0.8, 11, 0)
     roles = vk.synth_roles(n, 0.01, 0, 0, 5)
@@ -129,13 +131,20 @@ def test_sparse_graph_wide_tile_compaction(vk, port):
         for i in range(M // 4):
             batches.append(perm[i * b:(i + 1) * b])
             refs.append((2, k, i))
-    s = vk.Sampler(g, fan, b, M, seed)
+    s = vk.Sampler(g, fan, b, M, seed, frontier="dense")
+    auto = vk.Sampler(g, fan, b, M, seed)
     for rep in range(2):  # the second run checks the workspace was left clean
         s.run(batches, refs)
+        auto.run(batches, refs)
         rng = np.random.default_rng(rep)
         for i in range(M):
             r = s.result(i)
             assert_invariants(r, off, tgt, fan, rng)
+            q = auto.result(i)
+            np.testing.assert_array_equal(q.all_vertices, r.all_vertices)
+            for h in range(len(fan)):
+                np.testing.assert_array_equal(q.mfg_dst[h], r.mfg_dst[h])
+                np.testing.assert_array_equal(q.all_index[h + 1], r.all_index[h + 1])
             if i % 23 == 0:
                 e, k, bi = refs[i]
                 assert_bit_exact(r, port.expand(csr, batches[i], fan, seed, e, k, bi), len(fan))
