@@ -134,6 +134,25 @@ class Clocks:
                 "sm_max_mhz": self.max_sm, "reasons": reasons, "samples": len(self.samples)}
 
 
+def nvlink_counters(device):
+    """NVLink data bytes (tx, rx) this GPU has moved, from the NVML
+    throughput counters (KiB, all links), or None where unavailable."""
+    try:
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(device)
+        vals = N.nvmlDeviceGetFieldValues(h, [N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                              N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                return None
+            out.append(int(v.value.ullVal) * 1024)
+        return tuple(out)
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def make_data(cfg, threads):
     from paper_2305_03152_b200 import vipkit as vk
     t = time.time()
@@ -285,17 +304,21 @@ def run_b200(args, cfg):
 
     def waves_prefetch(lo, hi, host, pinned):
         # main: S(i+1) G(i) S(i+2) G(i+1) ...; aux: the NVLink exchange of
-        # wave i+1 (issued after S(i+1)) runs during the HBM-bound G(i)
+        # wave i+1, issued after S(i+1) (runs during the HBM-bound G(i)) or,
+        # --prefetch-order gather, after G(i) (runs during S(i+2))
         sample(lo, host)
         plane.prefetch(samplers[lo % 2])
         for i in range(lo, hi):
             sp = samplers[i % 2]
             if i + 1 < hi:
                 sample(i + 1, host)
-                plane.prefetch(samplers[(i + 1) % 2])
+                if args.prefetch_order == "sample":
+                    plane.prefetch(samplers[(i + 1) % 2])
             evs[i][2].record(stream)
             plane.gather(sp, outs[0].data_ptr(), cap_all, hist_tally[i].data_ptr(), stream=sh)
             evs[i][3].record(stream)
+            if i + 1 < hi and args.prefetch_order == "gather":
+                plane.prefetch_after(samplers[(i + 1) % 2], sh)
             sp.snapshot_counts(hist_counts[i].data_ptr(), stream=sh)
             if pinned is not None:
                 with torch.cuda.stream(stream):
@@ -355,9 +378,11 @@ def run_b200(args, cfg):
         dist.barrier()
     clocks = Clocks(dev)
     clocks.start()
+    nvl0 = nvlink_counters(dev) if world > 1 else None
     l0 = vk.launch_count()
     ms = region(W, W + S)
     launches = vk.launch_count() - l0
+    nvl1 = nvlink_counters(dev) if world > 1 else None
     clk = clocks.stop()
     # e2e: host seeds (H2D inside the region) + tallies read back to the host
     pinned = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64).pin_memory()
@@ -425,7 +450,8 @@ def run_b200(args, cfg):
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 ids / fp32 rows / fp64 VIP",
         "data": "synthetic (community power-law graph, counter-hashed feature rows)",
         "config": {"workload": cfg["workload"], "n": n, "m_slots": m, "partitions": K, "pipes": P,
-                   "exchange_prefetch": bool(prefetch), "schedule": args.sched,
+                   "exchange_prefetch": bool(prefetch), "prefetch_order": args.prefetch_order,
+                   "schedule": args.sched,
                    "fanouts": list(cfg["fanouts"]), "batch": cfg["b"], "minibatches_per_step_per_gpu": M,
                    "feature_dim": cfg["dim"], "row_bytes": rb, "alpha": cfg["alpha"],
                    "partitions_per_gpu": len(mine), "l2": "inputs larger than L2 (graph "
@@ -453,6 +479,14 @@ def run_b200(args, cfg):
         pulled = plane.pulled_rows()
         result["nvlink"] = {"rows_pulled_last_wave": pulled, "bytes_pulled_last_wave": pulled * rb,
                             "rows_requested_last_wave": int(tally[W + 2 * S - 1, :len(waves[W + 2 * S - 1]), 3].sum())}
+        if nvl0 and nvl1:
+            # hardware counters over the timed region (this rank's GPU, all
+            # links): rx = rows this GPU pulled, tx = rows peers pulled from it
+            tx, rx = (nvl1[0] - nvl0[0]) / S, (nvl1[1] - nvl0[1]) / S
+            result["nvlink"].update({"hw_rx_bytes_per_wave": rx, "hw_tx_bytes_per_wave": tx,
+                                     "hw_rx_gbs": rx / (ms / S / 1e3) / 1e9,
+                                     "peak_gbs_per_direction": 900.0,
+                                     "source": "NVML NVLINK_THROUGHPUT_DATA_{TX,RX} around the timed region"})
     if cfg.get("alpha_sweep") and rank == 0:
         # vipkit::simulate over one full epoch of every partition on the device
         # (vk_simulate): one expansion pass scored against every
@@ -745,13 +779,19 @@ def main():
     ap.add_argument("--pipes", type=int, default=1, help="overlapped sampler+gather pipelines (streams)")
     ap.add_argument("--prefetch", default="auto", choices=["auto", "0", "1"],
                     help="overlap the multi-GPU miss exchange with the next wave's sampling (auto: on for N>1)")
+    ap.add_argument("--prefetch-order", default="sample", choices=["sample", "gather"],
+                    help="issue wave i+1's exchange after its sampling (overlaps gather i) or after gather i "
+                         "(overlaps the sampling of wave i+2)")
     ap.add_argument("--sched", default="serial", choices=["serial", "overlap"],
                     help="overlap: sample wave i+1 on a high-priority stream while wave i gathers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--alpha", type=float, default=None, help="override the config's VIP cache fraction")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = dict(CONFIGS[args.config])
+    if args.alpha is not None:
+        cfg["alpha"] = args.alpha
     if args.wave is None:
         args.wave = cfg.get("wave", 32)
     if args.alpha_sweep and "alpha_sweep" not in cfg:

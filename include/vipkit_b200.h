@@ -320,6 +320,11 @@ VK_API int vk_plane_row_bytes(vk_plane p, uint64_t* row_bytes);
  * vk_plane_gather of that run waits for it instead of exchanging again.
  * No-op without attached peer partitions. */
 VK_API int vk_plane_prefetch(vk_plane p, vk_sampler s);
+/* vk_plane_prefetch ordered after the work queued so far on `after` as well
+ * (e.g. the gather of the previous wave), so the NVLink pull overlaps the
+ * next wave's latency-bound sampling instead of contending with an
+ * HBM-bound gather. */
+VK_API int vk_plane_prefetch_after(vk_plane p, vk_sampler s, vk_stream_t after);
 /* Distinct remote rows the last multi-GPU gather pulled over NVLink (the
  * wave's deduplicated miss exchange); synchronises the device. */
 VK_API int vk_plane_pulled_rows(vk_plane p, uint64_t* rows);

@@ -68,6 +68,7 @@ struct vk_plane_s {
   vk::DevBuf d_rmask;                   // [K] Part::rmask pointers (resident partitions)
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // prefetched miss exchanges (vk_plane_prefetch), high priority
+  cudaEvent_t after_ev = nullptr;  // vk_plane_prefetch_after ordering
   // per-wave deduplicated pull of remote rows (multi-GPU): union bitmap of
   // the wave's remote misses, its rank prefix, the distinct list, and the
   // local staging copy of those rows
@@ -258,7 +259,8 @@ __device__ __forceinline__ void tile_range(const GatherParams& p, std::uint32_t 
   hi = w1 < p.W ? rk[w1].z : cnt;
 }
 
-constexpr std::uint32_t kMagicExactV = 11585;  // largest V with V*V < 2^27
+constexpr std::uint32_t kMagicExactV = 11585;
+constexpr unsigned kPullCtasPrefetch = 2;  // pull CTAs per SM beside a running gather  // largest V with V*V < 2^27
 
 // Row of flattened element e (< 32 V) of a warp's 32 rows: umulhi with
 // ceil(2^32/V) is exact while V*V < 2^27 (V <= 11585); above that it can
@@ -315,6 +317,31 @@ __device__ __forceinline__ void st_row(T* p, const T& v) {
   else
     __stcs(p, v);
 }
+// Plain coherent loads for rows that live on a peer GPU (read over NVLink
+// through a CUDA IPC mapping): the non-coherent / cache-hinted path above
+// measured ~40x slower there.
+template <class T>
+__device__ __forceinline__ T ld_peer(const T* p) {
+  if constexpr (sizeof(T) == 16) {
+    uint4 r;
+    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+  } else if constexpr (sizeof(T) == 4) {
+    std::uint32_t r;
+    asm volatile("ld.global.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+  } else {
+    std::uint16_t r;
+    asm volatile("ld.global.u16 %0, [%1];" : "=h"(r) : "l"(p));
+    return r;
+  }
+}
+// Source pointers of peer rows carry tag bit 0 (rows are >= 2-byte aligned).
+template <class T>
+__device__ __forceinline__ const T* tag_peer(const T* p) {
+  return reinterpret_cast<const T*>(reinterpret_cast<std::uintptr_t>(p) | 1u);
+}
+
 __device__ __forceinline__ std::uint64_t evict_last_policy() {
   std::uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -336,7 +363,9 @@ __device__ __forceinline__ void copy_group(const T* const* src, T* dst, std::uin
       const std::uint32_t e = e0 + 32 * u;
       if (e < total) {
         const std::uint32_t row = row_of(e, V, magic, FIX);
-        val[u] = ld_row(src[row] + (e - row * V), pol);
+        const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(src[row]);
+        const T* sp = reinterpret_cast<const T*>(a & ~std::uintptr_t(1)) + (e - row * V);
+        val[u] = (a & 1u) ? ld_peer(sp) : ld_row(sp, pol);
       }
     }
 #pragma unroll
@@ -467,7 +496,7 @@ __global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::
     if (r < cnt) {
       const std::uint32_t g = __ldg(list + r);  // global row order
       const std::uint32_t o = owner_of(rs, p.K, g);
-      src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)(g - rs[o]) * rowv;
+      src = tag_peer(reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)(g - rs[o]) * rowv);  // NVLink
     }
     s_src[w][lane] = src;
     __syncwarp();
@@ -476,9 +505,10 @@ __global__ void __launch_bounds__(256) k_remote_pull(GatherParams p, const std::
   }
 }
 
-// STAGED false: every row is served from this GPU (no peer partitions);
-// true: the remote misses of the wave were pulled into the staging buffer by
-// the miss exchange and are read from there.
+// STAGED false: every row is read where it lives -- local HBM, or a peer
+// GPU's store over NVLink (CUDA IPC mapping) for remote misses; true: the
+// remote misses of the wave were pulled into the staging buffer by the
+// deduplicating miss exchange and are read from there.
 template <class T, bool STAGED, bool FIX>
 __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 4 : 1) k_gather(GatherParams p) {
   constexpr int kUnroll = 8;
@@ -523,8 +553,11 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 4 : 1) k_gather(GatherP
         const std::uint32_t o = owner_of(rs, p.K, g);
         src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)(g - rs[o]) * rowv;
         ++c_miss;
-        if (STAGED && p.peer_mask[o]) {  // pulled once per wave into local staging
+        if (p.peer_mask[o]) {  // owned by a partition on another GPU
           ++c_peer;
+          src = tag_peer(src);  // read over NVLink unless staged below
+        }
+        if (STAGED && p.peer_mask[o]) {  // pulled once per wave into local staging
           const std::uint32_t wq = g >> 6;
           const std::uint32_t idx = __ldg(p.uprefix + wq) +
                                     (std::uint32_t)__popcll(__ldg(p.ubits + wq) & ((1ull << (g & 63)) - 1ull));
@@ -692,6 +725,7 @@ int vk_plane_create(int device, uint64_t n, uint32_t K, uint32_t dim, int dtype,
         int lo = 0, hi = 0;
         VK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         VK_CUDA(cudaStreamCreateWithPriority(&p->aux, cudaStreamNonBlocking, hi));
+        VK_CUDA(cudaEventCreateWithFlags(&p->after_ev, cudaEventDisableTiming));
       }
       p->part_of.alloc(n * 4);
       p->owner_row.alloc(n * 4);
@@ -731,6 +765,7 @@ int vk_plane_destroy(vk_plane p) {
       if (part.peer) cudaIpcCloseMemHandle(part.peer);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->aux) cudaStreamDestroy(p->aux);
+    if (p->after_ev) cudaEventDestroy(p->after_ev);
     delete p;
   });
 }
@@ -996,7 +1031,12 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
     if (units >= (1ull << 31)) raise(VK_ERR_UNSUPPORTED, "too many gather tiles");
     bool staged = false;
     for (const auto& q : p->parts) staged |= q.attached;
-    if (prefetch_only && !staged) return;  // nothing to exchange on one GPU
+    // With peers, the wave's remote misses are always exchanged (deduplicated,
+    // pulled in ascending owner-row order) before the gather: even where the
+    // dedup gains little (C4 at N=2: 11.0 M requests, 9.9 M distinct rows),
+    // reading remote rows in random order straight from the gather measured
+    // ~40x slower (199 ms per C4 wave) than the sorted pull.
+    if (prefetch_only && !staged) return;  // nothing to exchange
     auto& ss = p->stage_sets[static_cast<const void*>(s)];
     const std::uint64_t run = sampler_run_id(s);
     const bool have_prefetch = staged && !prefetch_only && ss.prefetched == run;
@@ -1065,7 +1105,7 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
                                                           ss.ulist.as<std::uint32_t>());
       // NVLink-bound: a prefetched exchange shares the SMs with a running
       // gather (2 CTAs/SM, on the high-priority aux stream); inline, 8 CTAs/SM
-      const unsigned pg = (unsigned)sm_count(p->device) * (prefetch_only ? 2 : 8);
+      const unsigned pg = (unsigned)sm_count(p->device) * (prefetch_only ? kPullCtasPrefetch : 8);
       GatherParams pp = gp;  // staged rows are plain rows: the pull's vector width follows the row size
       auto pull = [&](auto tag, std::uint32_t esz) {
         using T = decltype(tag);
@@ -1131,6 +1171,18 @@ int vk_plane_gather(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride
 
 int vk_plane_prefetch(vk_plane p, vk_sampler s) {
   return guard([&] { gather_impl(p, s, nullptr, 0, nullptr, nullptr, true); });
+}
+
+int vk_plane_prefetch_after(vk_plane p, vk_sampler s, vk_stream_t after) {
+  return guard([&] {
+    if (!p) raise(VK_ERR_PARAMETER, "null plane");
+    if (after) {
+      DeviceGuard dg(p->device);
+      VK_CUDA(cudaEventRecord(p->after_ev, static_cast<cudaStream_t>(after)));
+      VK_CUDA(cudaStreamWaitEvent(p->aux, p->after_ev, 0));
+    }
+    gather_impl(p, s, nullptr, 0, nullptr, nullptr, true);
+  });
 }
 
 }  // extern "C"

@@ -141,6 +141,7 @@ def lib():
     L.vk_plane_row_bytes.argtypes = [c_vp, C.POINTER(c_u64)]
     L.vk_plane_pulled_rows.argtypes = [c_vp, C.POINTER(c_u64)]
     L.vk_plane_prefetch.argtypes = [c_vp, c_vp]
+    L.vk_plane_prefetch_after.argtypes = [c_vp, c_vp, c_vp]
     L.vk_simulate.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, c_vp, c_vp, u64p,
                               c_vp, c_u32, c_u32, u64p]
     L.vk_empirical_vip.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u64, u32p, c_u32, c_u64, c_u64, f64p]
@@ -830,6 +831,11 @@ class FeaturePlane:
         """Issue the multi-GPU miss exchange of the sampler's last run now
         (vk_plane_prefetch); no-op on a single GPU."""
         check(lib().vk_plane_prefetch(self._h, sampler.handle))
+
+    def prefetch_after(self, sampler: Sampler, stream):
+        """vk_plane_prefetch_after: the exchange also waits for the work
+        queued so far on `stream` (a cudaStream_t)."""
+        check(lib().vk_plane_prefetch_after(self._h, sampler.handle, stream))
 
     def pulled_rows(self) -> int:
         """Distinct remote rows pulled over NVLink by the last gather."""
