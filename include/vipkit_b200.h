@@ -391,6 +391,12 @@ VK_API int vk_synth_community_powerlaw(uint64_t n, uint64_t d, uint32_t communit
                                        double p_in, uint64_t seed, unsigned threads,
                                        uint64_t** offsets, uint32_t** targets, uint64_t* m,
                                        uint32_t* labels);
+/* ... with the popularity skew as a parameter: the target is the member of
+ * popularity rank floor(size * U^skew) (skew 2 above; larger concentrates
+ * the edges on fewer, bigger hubs). */
+VK_API int vk_synth_community_powerlaw_skew(uint64_t n, uint64_t d, uint32_t communities, double p_in,
+                                            double skew, uint64_t seed, unsigned threads, uint64_t** offsets,
+                                            uint32_t** targets, uint64_t* m_out, uint32_t* labels);
 /* vipkit::make_roles (graph.hpp:93-94, graph.cpp:247-268). */
 VK_API int vk_synth_roles(uint64_t n, double train, double valid, double test, uint64_t seed,
                           uint8_t* roles);

@@ -117,6 +117,8 @@ class Port:
         L.vp_free.argtypes = [c_vp]
         L.vp_synth_community_powerlaw.argtypes = [c_u64, c_u64, c_u32, c_double, c_u64, C.c_uint,
                                                   C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), c_vp]
+        L.vp_synth_community_powerlaw_skew.argtypes = [c_u64, c_u64, c_u32, c_double, c_double, c_u64, C.c_uint,
+                                                       C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), c_vp]
         L.vp_fill_features.argtypes = [c_u64, c_u32, c_int, c_u64, c_vp, C.c_uint]
         L.vp_gather_rows.argtypes = [c_vp, c_u64, c_vp, c_u64, c_vp, C.c_uint]
         L.vp_stream_draws.argtypes = [c_u64, c_u64, c_u64, u64p]
@@ -294,13 +296,14 @@ class Port:
         return out
 
     # ---- workload (workload.c) ----
-    def synth_community_powerlaw(self, n, d, communities, p_in, seed, threads=0):
+    def synth_community_powerlaw(self, n, d, communities, p_in, seed, threads=0, skew=2.0):
         """The bench graph recipe (restated from the product generator):
         (off u64[n+1], tgt u32[m], labels u32[n])."""
         offp, tgtp, m = c_vp(), c_vp(), c_u64()
         labels = np.zeros(n, np.uint32)
-        rc = self.lib.vp_synth_community_powerlaw(n, d, communities, p_in, seed, threads or (os.cpu_count() or 1),
-                                                  C.byref(offp), C.byref(tgtp), C.byref(m), labels.ctypes.data)
+        rc = self.lib.vp_synth_community_powerlaw_skew(n, d, communities, p_in, skew, seed,
+                                                       threads or (os.cpu_count() or 1), C.byref(offp),
+                                                       C.byref(tgtp), C.byref(m), labels.ctypes.data)
         if rc != 0:
             raise OracleError(rc, "bad generator parameters")
         off = np.ctypeslib.as_array(C.cast(offp, C.POINTER(C.c_uint64)), shape=(n + 1,)).copy()

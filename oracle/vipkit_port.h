@@ -87,6 +87,9 @@ void vp_features(uint64_t seed, uint32_t D, int fp16, const uint32_t* ids, uint6
 int vp_synth_community_powerlaw(uint64_t n, uint64_t d, uint32_t C, double p_in, uint64_t seed,
                                 unsigned threads, uint64_t** off_out, uint32_t** tgt_out,
                                 uint64_t* m_out, uint32_t* labels);
+int vp_synth_community_powerlaw_skew(uint64_t n, uint64_t d, uint32_t C, double p_in, double skew, uint64_t seed,
+                                     unsigned threads, uint64_t** off_out, uint32_t** tgt_out,
+                                     uint64_t* m_out, uint32_t* labels);
 void vp_fill_features(uint64_t seed, uint32_t D, int fp16, uint64_t n, void* out, unsigned threads);
 void vp_gather_rows(const void* table, uint64_t row_bytes, const uint32_t* ids, uint64_t count, void* out,
                     unsigned threads);

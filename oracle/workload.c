@@ -9,7 +9,7 @@
  *    product: vk_synth_community_powerlaw in csrc/capi.cu). The output is the
  *    canonical CSR of Graph::from_edges (graph.cpp:33-53: symmetrised,
  *    self-loops dropped, rows sorted and deduplicated), so it is identical for
- *    any thread count; tests/test_oracle_workload.py pins it to the product's.
+ *    any thread count; tests/test_bench_arms.py pins it to the product's.
  *  - vp_fill_features / vp_gather_rows: the counter-hashed feature table
  *     and the CPU row gather out[i] = X[ids[i]] the GPU gather is
  *    measured against (the reference never materialises features,
@@ -21,6 +21,7 @@
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <math.h>
 #include <string.h>
 
 #include "vipkit_port.h"
@@ -56,7 +57,7 @@ static void parallel_rows(unsigned T, uint64_t n, range_fn fn, void* ctx) {
 typedef struct {
   uint64_t n, d, base_key;
   uint32_t C;
-  double p_in;
+  double p_in, skew;
   uint32_t *rank_to_vertex, *vertex_to_rank;
   uint32_t* deg;     /* pass 1 (atomic) */
   uint64_t* off;     /* raw multigraph offsets */
@@ -76,7 +77,7 @@ static uint32_t comm_of_rank(const gen_ctx* g, uint64_t r) {
 }
 /* stub (u, j): own stream key (0xA1, 3, u, j); target community = own with
  * probability p_in else uniform; target = member of popularity rank
- * floor(size * U^2) */
+ * floor(size * U^skew) */
 static uint32_t stub(const gen_ctx* g, uint64_t u, uint64_t j) {
   vp_stream s;
   vp_stream_init(&s, key_step(key_step(g->base_key, u), j));
@@ -85,7 +86,7 @@ static uint32_t stub(const gen_ctx* g, uint64_t u, uint64_t j) {
   const uint32_t c = a < g->p_in ? cu : (uint32_t)vp_next_below(&s, g->C);
   const uint64_t lo = cstart(g, c), size = cstart(g, c + 1) - lo;
   const double x = vp_next_double(&s);
-  uint64_t r = (uint64_t)((double)size * x * x);
+  uint64_t r = (uint64_t)((double)size * (g->skew == 2.0 ? x * x : pow(x, g->skew)));
   if (r >= size) r = size - 1;
   return g->rank_to_vertex[lo + r];
 }
@@ -145,6 +146,13 @@ static void pass_copy(void* p, uint64_t lo, uint64_t hi) {
 int vp_synth_community_powerlaw(uint64_t n, uint64_t d, uint32_t C, double p_in, uint64_t seed,
                                 unsigned threads, uint64_t** off_out, uint32_t** tgt_out,
                                 uint64_t* m_out, uint32_t* labels) {
+  return vp_synth_community_powerlaw_skew(n, d, C, p_in, 2.0, seed, threads, off_out, tgt_out, m_out, labels);
+}
+
+int vp_synth_community_powerlaw_skew(uint64_t n, uint64_t d, uint32_t C, double p_in, double skew, uint64_t seed,
+                                     unsigned threads, uint64_t** off_out, uint32_t** tgt_out,
+                                     uint64_t* m_out, uint32_t* labels) {
+  if (!(skew >= 1.0 && skew <= 64.0)) return VP_PARAMETER;
   if (n < 2 || n > (1ull << 32) || d < 1 || C < 1 || C > n || !(p_in >= 0.0 && p_in <= 1.0))
     return VP_PARAMETER;
   gen_ctx g = {0};
@@ -152,6 +160,7 @@ int vp_synth_community_powerlaw(uint64_t n, uint64_t d, uint32_t C, double p_in,
   g.d = d;
   g.C = C;
   g.p_in = p_in;
+  g.skew = skew;
   g.base_key = key_step(key_step(seed, 0xA1), 3);
   /* vertex placement: one seeded Fisher-Yates, stream (0xA1, 4) */
   g.rank_to_vertex = malloc(n * 4);

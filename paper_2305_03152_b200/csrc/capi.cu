@@ -246,7 +246,15 @@ void parallel_rows(unsigned T, std::uint64_t n, F&& fn) {
 extern "C" int vk_synth_community_powerlaw(uint64_t n, uint64_t d, uint32_t communities, double p_in,
                                            uint64_t seed, unsigned threads, uint64_t** offsets,
                                            uint32_t** targets, uint64_t* m_out, uint32_t* labels) {
+  return vk_synth_community_powerlaw_skew(n, d, communities, p_in, 2.0, seed, threads, offsets, targets, m_out,
+                                          labels);
+}
+
+extern "C" int vk_synth_community_powerlaw_skew(uint64_t n, uint64_t d, uint32_t communities, double p_in,
+                                                double skew, uint64_t seed, unsigned threads, uint64_t** offsets,
+                                                uint32_t** targets, uint64_t* m_out, uint32_t* labels) {
   return guard([&] {
+    if (!(skew >= 1.0 && skew <= 64.0)) raise(VK_ERR_PARAMETER, "skew must lie in [1, 64]");
     if (!offsets || !targets || !m_out) raise(VK_ERR_PARAMETER, "null argument");
     if (n < 2 || n > (1ull << 32)) raise(VK_ERR_RANGE, "vertex count out of range");
     if (d < 1) raise(VK_ERR_PARAMETER, "edges-per-vertex must be >= 1");
@@ -272,7 +280,7 @@ extern "C" int vk_synth_community_powerlaw(uint64_t n, uint64_t d, uint32_t comm
       const std::uint32_t c = a < p_in ? cu : (std::uint32_t)s.next_below(C);
       const std::uint64_t lo = cstart(c), size = cstart(c + 1) - lo;
       const double x = (double)(s.next_u64() >> 11) * 0x1.0p-53;
-      std::uint64_t r = (std::uint64_t)((double)size * x * x);
+      std::uint64_t r = (std::uint64_t)((double)size * (skew == 2.0 ? x * x : std::pow(x, skew)));
       if (r >= size) r = size - 1;
       return perm.rank_to_vertex[lo + r];
     };

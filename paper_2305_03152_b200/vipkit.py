@@ -146,6 +146,8 @@ def lib():
                               c_vp, c_u32, c_u32, u64p]
     L.vk_empirical_vip.argtypes = [c_vp, u8p, u32p, c_u32, c_u32, c_u64, u32p, c_u32, c_u64, c_u64, f64p]
     L.vk_access_counts.argtypes = [c_vp, u8p, u32p, c_u32, u32p, c_u32, c_u64, c_u64, c_u64, f64p]
+    L.vk_synth_community_powerlaw_skew.argtypes = [c_u64, c_u64, c_u32, c_double, c_double, c_u64, C.c_uint,
+                                                   C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), u32p]
     L.vk_synth_community_powerlaw.argtypes = [c_u64, c_u64, c_u32, c_double, c_u64, C.c_uint,
                                               C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_u64), u32p]
     L.vk_debug_stream_draws.argtypes = [c_int, c_u64, c_u64, c_u64, u64p]
@@ -856,12 +858,12 @@ class FeaturePlane:
 
 
 # --------------------------------------------------------- synthetic data
-def synth_community_powerlaw(n, d, communities, p_in=0.8, seed=7, threads=0):
+def synth_community_powerlaw(n, d, communities, p_in=0.8, seed=7, threads=0, skew=2.0):
     """Community-structured power-law graph -> (offsets u64, targets u32, labels u32)."""
     po, pt, m = c_vp(), c_vp(), c_u64()
     labels = np.zeros(n, np.uint32)
-    check(lib().vk_synth_community_powerlaw(n, d, communities, p_in, seed, threads, C.byref(po),
-                                            C.byref(pt), C.byref(m), labels))
+    check(lib().vk_synth_community_powerlaw_skew(n, d, communities, p_in, skew, seed, threads, C.byref(po),
+                                                 C.byref(pt), C.byref(m), labels))
     try:
         off = np.ctypeslib.as_array(C.cast(po, C.POINTER(c_u64)), shape=(n + 1,)).copy()
         tgt = (np.ctypeslib.as_array(C.cast(pt, C.POINTER(C.c_uint32)), shape=(m.value,)).copy()
