@@ -153,13 +153,61 @@ def nvlink_counters(device):
         return None
 
 
-def make_data(cfg, threads):
+def make_data(cfg, threads, world=1, rank=0):
+    """The config's graph, labels and roles. With several ranks on one host,
+    rank 0 generates the graph once (all host threads) and shares it through
+    /dev/shm (the other ranks map it read-only: one copy in the page cache
+    instead of one generation peak and one 14 GB copy per rank -- 8 C4 ranks
+    would otherwise exhaust host memory); without room there, ranks generate
+    one after another."""
     from paper_2305_03152_b200 import vipkit as vk
     t = time.time()
-    off, tgt, labels = vk.synth_community_powerlaw(cfg["n"], cfg["d"], cfg["K"], cfg["p_in"], GRAPH_SEED,
-                                                   threads)
-    roles = vk.synth_roles(cfg["n"], cfg["train"], 0.0, 0.0, ROLES_SEED)
-    log(f"[bench] graph n={cfg['n']} m={len(tgt)} generated in {time.time() - t:.1f}s")
+    n = cfg["n"]
+
+    def generate(th):
+        return vk.synth_community_powerlaw(n, cfg["d"], cfg["K"], cfg["p_in"], GRAPH_SEED, th,
+                                           skew=cfg.get("skew", 2.0))
+
+    if world == 1:
+        off, tgt, labels = generate(threads)
+    else:
+        import torch.distributed as dist
+        base = f"/dev/shm/vk_bench_{cfg['n']}_{cfg['d']}_{cfg['K']}_{os.environ.get('MASTER_PORT', '0')}"
+        ok = np.zeros(1, np.int64)
+        if rank == 0:
+            off, tgt, labels = generate(os.cpu_count() or threads)
+            try:
+                for name, a in (("off", off), ("tgt", tgt), ("lab", labels)):
+                    a.tofile(f"{base}.{name}.tmp")
+                    os.replace(f"{base}.{name}.tmp", f"{base}.{name}")
+                ok[0] = len(tgt)
+            except OSError as e:
+                log(f"[bench] /dev/shm share failed ({e}); ranks generate in turn")
+                for name in ("off", "tgt", "lab"):
+                    for suffix in ("", ".tmp"):
+                        try:
+                            os.remove(f"{base}.{name}{suffix}")
+                        except OSError:
+                            pass
+        t_ok = __import__("torch").from_numpy(ok)
+        dist.broadcast(t_ok, 0)
+        m = int(t_ok[0])
+        if rank != 0:
+            if m:
+                off = np.memmap(f"{base}.off", np.uint64, "r", shape=(n + 1,))
+                tgt = np.memmap(f"{base}.tgt", np.uint32, "r", shape=(m,))
+                labels = np.fromfile(f"{base}.lab", np.uint32)
+            else:
+                for r in range(1, world):  # one generation at a time
+                    if r == rank:
+                        off, tgt, labels = generate(threads)
+                    dist.barrier()
+        dist.barrier()
+        if rank == 0 and m:
+            for name in ("off", "tgt", "lab"):  # unlinked now, mapped pages stay valid
+                os.remove(f"{base}.{name}")
+    roles = vk.synth_roles(n, cfg["train"], 0.0, 0.0, ROLES_SEED)
+    log(f"[bench] graph n={n} m={len(tgt)} ready in {time.time() - t:.1f}s")
     return off, tgt, labels, roles
 
 
@@ -188,15 +236,18 @@ def run_b200(args, cfg):
     dev = local
     K, M, L = cfg["K"], args.wave, len(cfg["fanouts"])
     nthreads = max(1, (os.cpu_count() or 8) // world)
-    off, tgt, labels, roles = make_data(cfg, nthreads)
+    off, tgt, labels, roles = make_data(cfg, nthreads, world, rank)
     n, m = cfg["n"], len(tgt)
     g = vk.Graph.from_csr(off, tgt, undirected=True, device=dev)
+    if world > 1:  # the host CSR is only needed again by the N=1 CPU baseline
+        off = tgt = None
     stream = torch.cuda.Stream(device=dev)
     sh = stream.cuda_stream
 
     # ---- VIP analysis for all K partitions in one multi-column pass (timed)
     p0 = np.stack([vk.initial_probs(roles, labels, k, cfg["b"]) for k in range(K)])
     p0_d = torch.from_numpy(p0).to(f"cuda:{dev}")
+    del p0  # K x n f64 on every rank: keep host memory for N ranks per box
     tot_d = torch.empty((K, n), dtype=torch.float64, device=f"cuda:{dev}")
     with torch.cuda.stream(stream):
         vk.propagate_device(g, cfg["fanouts"], K, p0_d.data_ptr(), None, tot_d.data_ptr(), sh)  # warm
@@ -537,10 +588,10 @@ def run_vip_sweep(args, cfg):
     if world > 1:
         dist.init_process_group("gloo")
     K = cfg["K"]
-    off, tgt, labels, roles = make_data(cfg, max(1, (os.cpu_count() or 8) // world))
+    off, tgt, labels, roles = make_data(cfg, max(1, (os.cpu_count() or 8) // world), world, rank)
     n, m = cfg["n"], len(tgt)
     g = vk.Graph.from_csr(off, tgt, undirected=True, device=local)
-    del tgt
+    off = tgt = None
     mine = [k for k in range(K) if k % world == rank]
     p0 = np.stack([vk.initial_probs(roles, labels, k, cfg["b"]) for k in mine])
     stream = torch.cuda.Stream(device=local)

@@ -15,8 +15,10 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 
 
 def main():
-    raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    # base units (bytes, ns, ...) for every row: with auto units each row may
+    # pick its own scale while the header carries only the first row's
+    raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")
