@@ -22,17 +22,17 @@ namespace vk {
 namespace {
 
 constexpr int kBktThreads = 256;
-constexpr std::uint32_t kChunkItems = 16384;  // items per (chunk, minibatch) CTA of hist / scatter
+constexpr std::uint32_t kHistItems = 16384;    // items per (chunk, minibatch) CTA of the histogram
+constexpr std::uint32_t kScatterItems = 4096;  // ... of the scatter (16 per thread, held in registers)
 constexpr std::uint32_t kMaxBuckets = 8192;  // per minibatch (shared histogram of hist / scatter)
-constexpr std::uint32_t kTagLevelShift = 28;
-constexpr std::uint32_t kItemBatch = 8;  // item loads in flight per thread (hist / scatter)  // all level: tag = level << 28 | index in F_level
+constexpr std::uint32_t kItemBatch = 8;  // item loads in flight per thread (hist)
 
 struct BucketParams {
-  // hop level: items ids[mb * ids_stride + i], i < count[mb], tag = i
+  // hop level: items ids[mb * ids_stride + i], i < count[mb], tag = i (MFG position)
   const std::uint32_t* ids;
   std::uint64_t ids_stride;
   const std::uint32_t* count;
-  // all level (ids == nullptr): F_0..F_L, tag = level << 28 | index
+  // all level: the sorted lists F_1..F_L and the batch F_0 (k_bucket_dedup_all)
   std::uint32_t L;
   const std::uint32_t* F[VK_MAX_HOPS + 1];
   std::uint64_t capF[VK_MAX_HOPS + 1];
@@ -41,45 +41,20 @@ struct BucketParams {
   std::uint32_t* hist;      // [M][NB + 1], zero between levels
   std::uint32_t* bstart;    // [M][NB + 1] pair offset of every bucket
   std::uint32_t* cursor;    // [M][NB]
-  uint2* pairs;             // [M][pair_stride] {id, tag}
+  uint2* pairs;             // [M][pair_stride] {id, MFG position}
   std::uint64_t pair_stride;
   unsigned long long* status;  // [M][NB] look-back of the dedup (reset by the scan)
 };
 
-// The i-th item of minibatch mb (all level: `pre` = level starts).
-__device__ __forceinline__ uint2 bucket_item(const BucketParams& p, std::uint32_t mb, std::uint32_t i,
-                                             const std::uint32_t* pre) {
-  if (p.ids) return make_uint2(__ldg(p.ids + mb * p.ids_stride + i), i);
-  std::uint32_t h = 0;
-  while (i >= pre[h + 1]) ++h;
-  const std::uint32_t idx = i - pre[h];
-  return make_uint2(__ldg(p.F[h] + mb * p.capF[h] + idx), (h << kTagLevelShift) | idx);
-}
-
-// Item count of minibatch mb; all level: level starts into pre[0..L+1].
-__device__ __forceinline__ std::uint32_t bucket_items(const BucketParams& p, std::uint32_t mb, std::uint32_t* pre) {
-  if (p.ids) return p.count[mb];
-  if (threadIdx.x == 0) {
-    std::uint32_t a = 0;
-    for (std::uint32_t h = 0; h <= p.L; ++h) {
-      pre[h] = a;
-      a += p.fcount[h][mb];
-    }
-    pre[p.L + 1] = a;
-  }
-  __syncthreads();
-  return pre[p.L + 1];
-}
-
 // 1. per-bucket item counts; shared histogram per (chunk, minibatch) CTA
 __global__ void __launch_bounds__(kBktThreads) k_bucket_hist(BucketParams p) {
   extern __shared__ std::uint32_t s_hist[];
-  __shared__ std::uint32_t s_pre[VK_MAX_HOPS + 2];
   const std::uint32_t mb = blockIdx.y;
-  const std::uint32_t total = bucket_items(p, mb, s_pre);
-  const std::uint32_t c0 = blockIdx.x * kChunkItems;
+  const std::uint32_t total = p.count[mb];
+  const std::uint32_t c0 = blockIdx.x * kHistItems;
   if (c0 >= total) return;
-  const std::uint32_t c1 = min(total, c0 + kChunkItems);
+  const std::uint32_t c1 = min(total, c0 + kHistItems);
+  const std::uint32_t* ids = p.ids + mb * p.ids_stride;
   for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads) s_hist[b] = 0;
   __syncthreads();
   for (std::uint32_t i0 = c0 + threadIdx.x; i0 < c1; i0 += kItemBatch * kBktThreads) {
@@ -87,7 +62,7 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_hist(BucketParams p) {
 #pragma unroll
     for (std::uint32_t k = 0; k < kItemBatch; ++k) {
       const std::uint32_t i = i0 + k * kBktThreads;
-      v[k] = i < c1 ? bucket_item(p, mb, i, s_pre).x : 0xffffffffu;
+      v[k] = i < c1 ? __ldg(ids + i) : 0xffffffffu;
     }
 #pragma unroll
     for (std::uint32_t k = 0; k < kItemBatch; ++k)
@@ -127,32 +102,32 @@ __global__ void __launch_bounds__(kScanThreads) k_bucket_scan(BucketParams p) {
   if (threadIdx.x == 0) bs[NB] = (std::uint32_t)total;
 }
 
-// 3. (id, tag) pairs into bucket order: the CTA reserves one range per
-// bucket it touches (one global atomic per bucket), then places its items
-// with shared cursors. Order inside a bucket is irrelevant (set semantics).
+// 3. (id, MFG position) pairs into bucket order: the CTA's kScatterItems
+// items stay in registers between its count and place passes; it reserves
+// one range per bucket it touches (one global atomic per bucket), then places
+// its items with shared cursors. Order inside a bucket is irrelevant (set
+// semantics).
 __global__ void __launch_bounds__(kBktThreads) k_bucket_scatter(BucketParams p) {
+  constexpr std::uint32_t kPer = kScatterItems / kBktThreads;
   extern __shared__ std::uint32_t s_dyn[];
   std::uint32_t* s_cnt = s_dyn;          // [NB]
   std::uint32_t* s_base = s_dyn + p.NB;  // [NB]
-  __shared__ std::uint32_t s_pre[VK_MAX_HOPS + 2];
   const std::uint32_t mb = blockIdx.y;
-  const std::uint32_t total = bucket_items(p, mb, s_pre);
-  const std::uint32_t c0 = blockIdx.x * kChunkItems;
+  const std::uint32_t total = p.count[mb];
+  const std::uint32_t c0 = blockIdx.x * kScatterItems;
   if (c0 >= total) return;
-  const std::uint32_t c1 = min(total, c0 + kChunkItems);
+  const std::uint32_t* ids = p.ids + mb * p.ids_stride;
+  std::uint32_t v[kPer];
+#pragma unroll
+  for (std::uint32_t k = 0; k < kPer; ++k) {
+    const std::uint32_t i = c0 + threadIdx.x + k * kBktThreads;
+    v[k] = i < total ? __ldg(ids + i) : 0xffffffffu;
+  }
   for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads) s_cnt[b] = 0;
   __syncthreads();
-  for (std::uint32_t i0 = c0 + threadIdx.x; i0 < c1; i0 += kItemBatch * kBktThreads) {
-    std::uint32_t v[kItemBatch];
 #pragma unroll
-    for (std::uint32_t k = 0; k < kItemBatch; ++k) {
-      const std::uint32_t i = i0 + k * kBktThreads;
-      v[k] = i < c1 ? bucket_item(p, mb, i, s_pre).x : 0xffffffffu;
-    }
-#pragma unroll
-    for (std::uint32_t k = 0; k < kItemBatch; ++k)
-      if (v[k] != 0xffffffffu) atomicAdd(&s_cnt[v[k] >> p.bb], 1u);
-  }
+  for (std::uint32_t k = 0; k < kPer; ++k)
+    if (v[k] != 0xffffffffu) atomicAdd(&s_cnt[v[k] >> p.bb], 1u);
   __syncthreads();
   std::uint32_t* cur = p.cursor + (std::uint64_t)mb * p.NB;
   for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads) {
@@ -162,20 +137,12 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_scatter(BucketParams p) 
   }
   __syncthreads();
   uint2* out = p.pairs + mb * p.pair_stride;
-  for (std::uint32_t i0 = c0 + threadIdx.x; i0 < c1; i0 += kItemBatch * kBktThreads) {
-    uint2 it[kItemBatch];
 #pragma unroll
-    for (std::uint32_t k = 0; k < kItemBatch; ++k) {
-      const std::uint32_t i = i0 + k * kBktThreads;
-      it[k] = i < c1 ? bucket_item(p, mb, i, s_pre) : make_uint2(0xffffffffu, 0u);
+  for (std::uint32_t k = 0; k < kPer; ++k)
+    if (v[k] != 0xffffffffu) {
+      const std::uint32_t b = v[k] >> p.bb;
+      out[s_base[b] + atomicAdd(&s_cnt[b], 1u)] = make_uint2(v[k], c0 + threadIdx.x + k * kBktThreads);
     }
-#pragma unroll
-    for (std::uint32_t k = 0; k < kItemBatch; ++k)
-      if (it[k].x != 0xffffffffu) {
-        const std::uint32_t b = it[k].x >> p.bb;
-        out[s_base[b] + atomicAdd(&s_cnt[b], 1u)] = it[k];
-      }
-  }
 }
 
 struct DedupParams {
@@ -199,7 +166,7 @@ struct DedupParams {
   std::uint32_t* ecount_next;  // [M]
 };
 
-constexpr std::uint32_t kDegStage = 2048;  // capped degrees staged per bucket (else reloaded)
+constexpr std::uint32_t kDegStage = 1024;  // capped degrees staged per bucket (else reloaded)
 constexpr std::uint32_t kPairRegs = 8;     // pairs per thread kept in registers between passes
 constexpr std::uint32_t kMbGroup = 8;      // minibatches interleaved per block group (L2 footprint)
 
@@ -232,19 +199,22 @@ struct SBits {
 // index order, so every look-back predecessor (same minibatch, lower bucket)
 // has a lower index and is already resident or done; a group's random writes
 // (MFG dst) stay inside a few minibatches' rows, i.e. inside L2.
-__device__ __forceinline__ void dedup_coords(std::uint32_t nmb, std::uint32_t NB, std::uint32_t& mb,
+__device__ __forceinline__ bool dedup_coords(std::uint32_t nmb, std::uint32_t NB, std::uint32_t& mb,
                                              std::uint32_t& b) {
-  const std::uint32_t per_group = kMbGroup * NB;
-  const std::uint32_t g = blockIdx.x / per_group, r = blockIdx.x % per_group;
+  // grid (kMbGroup * NB, ceil(nmb / kMbGroup)); the last group may be partial,
+  // its surplus blocks exit
+  const std::uint32_t g = blockIdx.y;
   const std::uint32_t gsize = min(kMbGroup, nmb - g * kMbGroup);
-  b = r / gsize;
-  mb = g * kMbGroup + r % gsize;
+  if (gsize == kMbGroup) {
+    b = blockIdx.x / kMbGroup;
+    mb = g * kMbGroup + blockIdx.x % kMbGroup;
+  } else {
+    b = blockIdx.x / gsize;
+    mb = g * kMbGroup + blockIdx.x % gsize;
+  }
+  return b < NB;
 }
 
-
-// Set bits of words [j, end) in vertex order, 8 per call (bucket-relative
-// ids into vv); returns how many. Rolled over words: sparse buckets have ~1
-// bit per nonzero word, so a batch spans words and keeps 8 loads in flight.
 struct BitCursor {
   std::uint32_t w0, p0;  // first word of the thread, its padded index
   unsigned m;            // its nonzero words not yet visited (bit k = word w0 + k)
@@ -295,14 +265,14 @@ __device__ __forceinline__ unsigned long long count_words(const SBits& sb, std::
 
 // 4a. hop level: one CTA per (minibatch, bucket) over that bucket's pairs.
 template <bool HAS_NEXT>
-__global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_hop(DedupParams p) {
+__global__ void __launch_bounds__(kBktThreads, 4) k_bucket_dedup_hop(DedupParams p) {
   extern __shared__ unsigned long long s_dd[];
   __shared__ unsigned long long s_sm[kBktThreads / 32];
   __shared__ unsigned long long s_excl;
   const BucketParams& bp = p.bp;
   const std::uint32_t NB = bp.NB, BW = 1u << (bp.bb - 6), wpt = BW / kBktThreads;
   std::uint32_t mb, b;
-  dedup_coords(p.nmb, NB, mb, b);
+  if (!dedup_coords(p.nmb, NB, mb, b)) return;
   const std::uint32_t* bs = bp.bstart + (std::uint64_t)mb * (NB + 1);
   const std::uint32_t s = bs[b], e = bs[b + 1];
   unsigned long long* status = bp.status + (std::uint64_t)mb * NB;
@@ -404,9 +374,9 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_hop(DedupParams p)
 
 // 4b. all level: all_vertices = sorted unique(F_0 u F_1 .. F_L) per bucket.
 // F_1..F_L are sorted and their dedups recorded every bucket's index range
-// (fbase, same bucket width), so no scatter pass is needed and the relabel
-// maps are written contiguously; the batch F_0 (unsorted, <= b ids) is
-// scanned whole by every bucket.
+// (fbase, same bucket width), so they need no scatter pass and the relabel
+// maps are written contiguously; only the batch F_0 (unsorted) goes through
+// hist / scan / scatter first.
 __global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_all(DedupParams p) {
   extern __shared__ unsigned long long s_dd[];
   __shared__ unsigned long long s_sm[kBktThreads / 32];
@@ -415,7 +385,7 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_all(DedupParams p)
   const BucketParams& bp = p.bp;
   const std::uint32_t NB = bp.NB, BW = 1u << (bp.bb - 6), wpt = BW / kBktThreads;
   std::uint32_t mb, b;
-  dedup_coords(p.nmb, NB, mb, b);
+  if (!dedup_coords(p.nmb, NB, mb, b)) return;
   const std::uint32_t vbase = b << bp.bb;
   const std::uint32_t vend = (b + 1 == NB) ? 0xffffffffu : vbase + (1u << bp.bb);
   if (threadIdx.x >= 1 && threadIdx.x <= bp.L) {
@@ -423,8 +393,11 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_all(DedupParams p)
     s_lo[threadIdx.x] = fb[b];
     s_hi[threadIdx.x] = fb[b + 1];
   }
-  const std::uint32_t c0 = bp.fcount[0][mb];
-  const std::uint32_t* F0 = bp.F[0] + mb * bp.capF[0];
+  // the batch F_0 (unsorted) was bucketed by the hop machinery: pairs
+  // {id, index in F_0} of this bucket
+  const std::uint32_t* bs = bp.bstart + (std::uint64_t)mb * (NB + 1);
+  const std::uint32_t s0 = bs[b], e0 = bs[b + 1];
+  const uint2* pairs = bp.pairs + mb * bp.pair_stride;
   const SBits sb = sbits_init(s_dd, BW, wpt);
   __syncthreads();
   // loads issued kBatch at a time ahead of their uses
@@ -442,7 +415,7 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_all(DedupParams p)
         if (v[k] != 0xffffffffu && (!filter || (v[k] >= vbase && v[k] < vend))) sb.set(v[k] - vbase);
     }
   };
-  set_range(F0, 0, c0, true);
+  for (std::uint32_t i = s0 + threadIdx.x; i < e0; i += kBktThreads) sb.set(pairs[i].x - vbase);
   for (std::uint32_t h = 1; h <= bp.L; ++h) set_range(bp.F[h] + mb * bp.capF[h], s_lo[h], s_hi[h], false);
   __syncthreads();
   const std::uint32_t w0 = threadIdx.x * wpt, p0 = w0 + threadIdx.x;
@@ -491,7 +464,11 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_all(DedupParams p)
           ai[i0 + k * kBktThreads] = sb.rank_of(v[k] - vbase);
     }
   };
-  rank_range(F0, p.allidx[0] + mb * bp.capF[0], 0, c0, true);
+  std::uint32_t* ai0 = p.allidx[0] + mb * bp.capF[0];
+  for (std::uint32_t i = s0 + threadIdx.x; i < e0; i += kBktThreads) {
+    const uint2 q = pairs[i];
+    ai0[q.y] = sb.rank_of(q.x - vbase);
+  }
   for (std::uint32_t h = 1; h <= bp.L; ++h)
     rank_range(bp.F[h] + mb * bp.capF[h], p.allidx[h] + mb * bp.capF[h], s_lo[h], s_hi[h], false);
 }

@@ -1216,7 +1216,7 @@ void run_compact(vk_sampler_s& s, bool hop, std::uint32_t h, std::uint32_t nmb, 
 // Sparse frontiers: one level (hop h >= 1, or the all level for h == 0)
 // through hist -> scan -> scatter -> dedup (frontier_sparse.cuh).
 template <class P>
-void launch_smem(void (*kernel)(P), const P& p, unsigned grid, std::size_t smem, cudaStream_t st) {
+void launch_smem(void (*kernel)(P), const P& p, dim3 grid, std::size_t smem, cudaStream_t st) {
   if (smem >= 40 * 1024)  // beyond the default 48 KB with the static shared arrays
     VK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kernel<<<grid, kBktThreads, smem, st>>>(p);
@@ -1236,16 +1236,27 @@ void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaS
   DedupParams dp{};
   dp.nmb = nmb;
   dp.outdeg = s.g->out_deg.as<std::uint32_t>();
-  const unsigned grid = (unsigned)((std::uint64_t)nmb * bp.NB);
+  // dedup grid: groups of kMbGroup minibatches (y), buckets ascending with
+  // the minibatch fastest inside a group (x); blocks run in index order
+  const dim3 grid(kMbGroup * bp.NB, (unsigned)ceil_div(nmb, kMbGroup));
   if (all) {
-    // sorted levels are ranged by binary search: no hist / scatter pass
+    // the sorted levels are ranged by the hops' bucket bases; the batch F_0
+    // is bucketed like a hop's draws (its scan also resets the look-back)
     bp.L = s.L;
     for (std::uint32_t q = 0; q <= s.L; ++q) {
       bp.F[q] = s.F[q].as<std::uint32_t>();
       bp.capF[q] = s.capF[q];
       bp.fcount[q] = s.fcount(q);
     }
-    VK_CUDA(cudaMemsetAsync(s.bstatus.p, 0, (std::uint64_t)nmb * bp.NB * 8, st));
+    bp.ids = s.F[0].as<std::uint32_t>();
+    bp.ids_stride = s.capF[0];
+    bp.count = s.fcount(0);
+    k_bucket_hist<<<dim3((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capF[0], kHistItems)), nmb), kBktThreads,
+                    bp.NB * 4, st>>>(bp);
+    k_bucket_scan<<<nmb, kScanThreads, 0, st>>>(bp);
+    k_bucket_scatter<<<dim3((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capF[0], kScatterItems)), nmb),
+                       kBktThreads, bp.NB * 8, st>>>(bp);
+    count_launch(3);
     dp.bp = bp;
     dp.list = s.all.as<std::uint32_t>();
     dp.cap_list = s.capAll;
@@ -1263,11 +1274,11 @@ void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaS
   bp.ids = s.edges_buf(h);
   bp.ids_stride = s.capS_max;
   bp.count = s.ecount(h);
-  // hist / scan / scatter re-use the same (chunk, minibatch) grid
-  const dim3 cgrid((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capS[h], kChunkItems)), nmb);
-  k_bucket_hist<<<cgrid, kBktThreads, bp.NB * 4, st>>>(bp);
+  k_bucket_hist<<<dim3((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capS[h], kHistItems)), nmb), kBktThreads,
+                  bp.NB * 4, st>>>(bp);
   k_bucket_scan<<<nmb, kScanThreads, 0, st>>>(bp);
-  k_bucket_scatter<<<cgrid, kBktThreads, bp.NB * 8, st>>>(bp);
+  k_bucket_scatter<<<dim3((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capS[h], kScatterItems)), nmb),
+                     kBktThreads, bp.NB * 8, st>>>(bp);
   count_launch(3);
   VK_LAUNCH_CHECK();
   dp.bp = bp;
@@ -1394,13 +1405,12 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
       // frontier representation: buckets when a minibatch touches a small
       // fraction of the vertices (papers scale), bitmaps otherwise
       {
-        bool ok = L + 1 <= (1u << (32 - kTagLevelShift)) && s->n <= (1ull << 31);
-        for (std::uint32_t h = 0; h <= L; ++h) ok = ok && s->capF[h] < (1ull << kTagLevelShift);
+        const bool ok = s->n <= (1ull << 31);  // ids and look-back counts fit 31 bits
         const bool want = (cfg->flags & VK_SAMPLER_FORCE_SPARSE) ||
                           (!(cfg->flags & VK_SAMPLER_FORCE_DENSE) && s->n >= 16 * s->capAll && s->n >= (1ull << 20));
         s->sparse = ok && want;
         if ((cfg->flags & VK_SAMPLER_FORCE_SPARSE) && !ok)
-          raise(VK_ERR_UNSUPPORTED, "sparse frontiers need per-level capacities below 2^28");
+          raise(VK_ERR_UNSUPPORTED, "sparse frontiers need fewer than 2^31 vertices");
       }
       s->dense_all_rank = !s->sparse && 4 * s->W <= s->capAll;
       for (std::uint32_t h = 1; h <= L; ++h)
