@@ -36,7 +36,7 @@ struct vk_graph_s {
   cudaStream_t stream = nullptr;
   // VIP workspace, grown on demand and kept across calls (no allocation on
   // the timed path).
-  vk::DevBuf vip_lm_a, vip_lm_b, vip_partial, vip_flag;
+  vk::DevBuf vip_lm_a, vip_lm_b, vip_partial, vip_flag, vip_active;
   bool vip_last_f32 = false;  // storage width used by the last propagate (diagnostics)
 
   const std::uint64_t* d_off() const { return fwd_off.as<std::uint64_t>(); }

@@ -61,6 +61,10 @@ struct HopParams {
   std::uint32_t L;
   double f_next;                 // fanout of hop h+1 (as double)
   int write_hop;
+  // active sources of this hop (bit v: some column of lm[v] is nonzero), or
+  // null: a sparse hop (hop 1: only the train vertices) skips the random lm
+  // gathers of inactive sources -- their terms are exactly zero
+  const std::uint32_t* active;
 };
 
 template <class LM>
@@ -189,13 +193,17 @@ __device__ __forceinline__ void lane_sum(const HopParams& p, std::uint64_t a, st
     std::uint32_t v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = i + k * G < b ? __ldg(p.tgt + i + k * G) : 0u;
+    bool on[4];  // in range and active (the activity bitmap is small enough to stay in L2)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      on[k] = i + k * G < b && (!p.active || ((__ldg(p.active + (v[k] >> 5)) >> (v[k] & 31)) & 1u));
     if constexpr (sizeof(LM) == 4) {
       // float storage: the 4 terms of a batch are added in float (error
       // ~2e-7 relative, bounded whatever the degree) and converted once
       float x[4][C];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (i + k * G < b) {
+        if (on[k]) {
           load_lm_f<C>(p.lm, v[k], x[k]);
         } else {
 #pragma unroll
@@ -208,7 +216,7 @@ __device__ __forceinline__ void lane_sum(const HopParams& p, std::uint64_t a, st
       double x[4][C];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (i + k * G < b) {
+        if (on[k]) {
           load_lm<C, LM>(p.lm, v[k], x[k]);
         } else {
 #pragma unroll
@@ -364,6 +372,32 @@ __global__ void k_hoist_p0(const double* __restrict__ p0, std::uint64_t n, std::
   }
 }
 
+// Activity bitmap of a hop's hoisted terms: bit v = some column of lm[v] is
+// nonzero; counts the active vertices.
+template <int C, class LM>
+__global__ void k_lm_active(const void* __restrict__ lmv, std::uint64_t n, std::uint32_t* __restrict__ bits,
+                            unsigned long long* __restrict__ count) {
+  const LM* lm = static_cast<const LM*>(lmv);
+  unsigned long long cnt = 0;
+  const std::uint64_t words = (n + 31) / 32;
+  for (std::uint64_t w = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; w < words;
+       w += (std::uint64_t)gridDim.x * blockDim.x) {
+    std::uint32_t m = 0;
+    for (int b = 0; b < 32; ++b) {
+      const std::uint64_t v = w * 32 + b;
+      if (v >= n) break;
+      bool on = false;
+#pragma unroll
+      for (int c = 0; c < C; ++c) on |= lm[v * C + c] != (LM)0;
+      m |= (std::uint32_t)on << b;
+    }
+    bits[w] = m;
+    cnt += __popc(m);
+  }
+  cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(count, cnt);
+}
+
 unsigned grid_cap(int device, std::uint64_t work, unsigned block) {
   const std::uint64_t g = (work + block - 1) / block;
   const std::uint64_t cap = (std::uint64_t)sm_count(device) * (2048 / block) * 4;
@@ -389,8 +423,30 @@ void run_columns(vk_graph_s& g, const std::uint32_t* fan, std::uint32_t L, const
   VK_LAUNCH_CHECK();
   const auto& so = g.sched_offsets;  // [6 classes + split-rows meta]
   const std::uint32_t* rows = g.sched_rows.as<std::uint32_t>();
+  // source activity: while a hop's active sources are a minority (hop 1 =
+  // the partitions' train vertices), its pull skips the inactive ones' lm
+  // gathers; once a hop is mostly active the check stops (activity only
+  // spreads hop by hop)
+  const std::uint64_t words = (n + 31) / 32;
+  if (g.vip_active.bytes < words * 4 + 16) g.vip_active.alloc(words * 4 + 16);
+  std::uint32_t* act = g.vip_active.as<std::uint32_t>();
+  unsigned long long* act_cnt = reinterpret_cast<unsigned long long*>(act + ((words + 1) & ~1ull));
+  bool track = true;
+  auto activity = [&](const void* lmh) -> const std::uint32_t* {
+    if (!track) return nullptr;
+    VK_CUDA(cudaMemsetAsync(act_cnt, 0, 8, st));
+    k_lm_active<C, LM><<<grid_cap(g.device, words, 256), 256, 0, st>>>(lmh, n, act, act_cnt);
+    count_launch();
+    VK_LAUNCH_CHECK();
+    unsigned long long c = 0;
+    VK_CUDA(cudaMemcpyAsync(&c, act_cnt, 8, cudaMemcpyDeviceToHost, st));
+    VK_CUDA(cudaStreamSynchronize(st));
+    track = c * 2 < n;
+    return track ? act : nullptr;
+  };
   for (std::uint32_t h = 1; h <= L; ++h) {
     HopParams p;
+    p.active = activity(lm);
     p.off = g.rev_off;
     p.tgt = g.rev_tgt;
     p.outdeg = g.out_deg.as<std::uint32_t>();
