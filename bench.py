@@ -437,7 +437,8 @@ def run_b200(args, cfg):
     clk = clocks.stop()
     # e2e: host seeds (H2D inside the region) + tallies read back to the host
     pinned = torch.zeros((W + 2 * S, M, 4), dtype=torch.int64).pin_memory()
-    src["stream"] = MinibatchStream(vk, roles, labels, mine, cfg["b"], SAMPLE_SEED)
+    # steady state: the schedule worker runs one epoch ahead of the waves
+    src["stream"] = MinibatchStream(vk, roles, labels, mine, cfg["b"], SAMPLE_SEED).ready()
     if world > 1:
         dist.barrier()
     e2e_ms = region(W + S, W + 2 * S, host=True, pinned=pinned)

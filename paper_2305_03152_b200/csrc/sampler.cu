@@ -72,9 +72,12 @@ struct vk_sampler_s {
   vk::DevBuf F[VK_MAX_HOPS + 1], allidx[VK_MAX_HOPS + 1], indptr[VK_MAX_HOPS + 1], dst[VK_MAX_HOPS + 1];
   vk::DevBuf counts;  // u32: fcount[(L+1)*M] | ecount[(L+1)*M] | allcount[M] | err[1]
   vk::DevBuf edges_tmp, all, hopbits, allbits, hopprefix, allprefix, status, tickets, desc, seed_stage;
-  vk::PinnedBuf desc_host[2], seed_host[2];
-  cudaEvent_t staged[2] = {nullptr, nullptr};
-  bool staged_used[2] = {false, false};
+  // pinned staging ring for host seeds / wave descriptors: the host may run
+  // kStageSlots - 1 waves ahead of the device
+  static constexpr int kStageSlots = 4;
+  vk::PinnedBuf desc_host[kStageSlots], seed_host[kStageSlots];
+  cudaEvent_t staged[kStageSlots] = {};
+  bool staged_used[kStageSlots] = {};
   int slot = 0;
   std::uint32_t last_nmb = 0;
   std::vector<std::uint32_t> last_parts;
@@ -1467,7 +1470,7 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
                                    kCompactThreads * 17 * 8));
       VK_CUDA(cudaFuncSetAttribute(k_sample_smem<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    6 * 32 * kSampleThreads * 4));
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < vk_sampler_s::kStageSlots; ++k) {
         s->desc_host[k].ensure(M * sizeof(WaveDesc));
         s->seed_host[k].ensure(M * cfg->batch_size * 4);
         VK_CUDA(cudaEventCreateWithFlags(&s->staged[k], cudaEventDisableTiming));
@@ -1543,7 +1546,7 @@ int vk_sampler_destroy(vk_sampler s) {
     if (s->aux) cudaStreamDestroy(s->aux);
     if (s->fork_ev) cudaEventDestroy(s->fork_ev);
     if (s->join_ev) cudaEventDestroy(s->join_ev);
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < vk_sampler_s::kStageSlots; ++k)
       if (s->staged[k]) cudaEventDestroy(s->staged[k]);
     if (s->done) cudaEventDestroy(s->done);
     for (cudaEvent_t e : s->readers) {
@@ -1580,10 +1583,10 @@ int vk_sampler_run(vk_sampler s, uint32_t nmb, const vk_batch_ref* refs, const u
       if (c == 0) raise(VK_ERR_SAMPLING, "cannot expand an empty batch");  // sampling.cpp:97
       if (c > b) raise(VK_ERR_PARAMETER, "minibatch larger than the sampler's batch_size");
     }
-    // double-buffered pinned staging: only wait for the H2D copy issued two
+    // ring of pinned staging slots: only wait for the H2D copy issued kStageSlots
     // waves ago, so the host can queue the next wave while this one runs
     const int slot = s->slot;
-    s->slot ^= 1;
+    s->slot = (s->slot + 1) % vk_sampler_s::kStageSlots;
     if (s->staged_used[slot]) VK_CUDA(cudaEventSynchronize(s->staged[slot]));
     WaveDesc* d = s->desc_host[slot].as<WaveDesc>();
     for (std::uint32_t i = 0; i < nmb; ++i) {

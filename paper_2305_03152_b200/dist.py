@@ -63,6 +63,12 @@ class MinibatchStream:
         return [(e, k, i, per[k][i * b:(i + 1) * b]) for i in range(max(nb.values()))
                 for k in self._parts if i < nb[k]]
 
+    def ready(self):
+        """Block until the first epoch's schedule exists (steady state: the
+        worker stays one epoch ahead of the consumer)."""
+        self._next.result()
+        return self
+
     def take(self, count: int) -> list:
         out = []
         while len(out) < count:
