@@ -473,5 +473,106 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_all(DedupParams p)
     rank_range(bp.F[h] + mb * bp.capF[h], p.allidx[h] + mb * bp.capF[h], s_lo[h], s_hi[h], false);
 }
 
+// 4c. Small hop levels (at most kSmallLevel drawn ids per minibatch, e.g. C4's
+// hop 1 with 15,360): one 1024-thread CTA per minibatch sorts the (id, MFG
+// position) pairs in shared memory (bitonic), so no histogram / scatter pass
+// and ~400 near-empty buckets per minibatch become one CTA. Same outputs as
+// k_bucket_dedup_hop: sorted distinct F_h, next-hop row pointers, MFG dst,
+// and the bucket bases the all level ranges F_h with.
+constexpr std::uint32_t kSmallLevel = 16384;
+constexpr int kSmallLevelThreads = 1024;
+
+template <bool HAS_NEXT>
+__global__ void __launch_bounds__(kSmallLevelThreads) k_small_level(DedupParams p) {
+  constexpr std::uint32_t kPer = kSmallLevel / kSmallLevelThreads;  // 16 per thread
+  extern __shared__ unsigned long long s_key[];                    // [kSmallLevel] id << 32 | position
+  __shared__ unsigned long long s_sm[kSmallLevelThreads / 32];
+  const BucketParams& bp = p.bp;
+  const std::uint32_t mb = blockIdx.x;
+  const std::uint32_t cnt = bp.count[mb];
+  const std::uint32_t* ids = bp.ids + mb * bp.ids_stride;
+  std::uint32_t P = 2;
+  while (P < cnt) P <<= 1;
+  for (std::uint32_t i = threadIdx.x; i < P; i += kSmallLevelThreads)
+    s_key[i] = i < cnt ? ((unsigned long long)__ldg(ids + i) << 32) | i : ~0ull;
+  __syncthreads();
+  // bitonic sort of P keys, ascending
+  for (std::uint32_t k = 2; k <= P; k <<= 1)
+    for (std::uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (std::uint32_t t = threadIdx.x; t < P / 2; t += kSmallLevelThreads) {
+        const std::uint32_t i = 2 * t - (t & (j - 1));  // first of the pair (i, i + j)
+        const unsigned long long a = s_key[i], c = s_key[i + j];
+        const bool up = (i & k) == 0;
+        if ((a > c) == up) {
+          s_key[i] = c;
+          s_key[i + j] = a;
+        }
+      }
+      __syncthreads();
+    }
+  // ranks: thread t owns sorted positions [t*kPer, (t+1)*kPer)
+  const std::uint32_t i0 = threadIdx.x * kPer;
+  unsigned long long uc = 0;
+#pragma unroll
+  for (std::uint32_t q = 0; q < kPer; ++q) {
+    const std::uint32_t i = i0 + q;
+    if (i < cnt && (i == 0 || (s_key[i] >> 32) != (s_key[i - 1] >> 32))) ++uc;
+  }
+  unsigned long long utot;
+  const std::uint32_t ubase = (std::uint32_t)(block_inclusive_scan<kSmallLevelThreads>(uc, s_sm, &utot) - uc);
+  std::uint32_t deg[kPer];
+  unsigned long long dc = 0;
+  if (HAS_NEXT) {
+#pragma unroll
+    for (std::uint32_t q = 0; q < kPer; ++q) {
+      const std::uint32_t i = i0 + q;
+      const bool first = i < cnt && (i == 0 || (s_key[i] >> 32) != (s_key[i - 1] >> 32));
+      deg[q] = first ? min(p.f_next, __ldg(p.outdeg + (std::uint32_t)(s_key[i] >> 32))) : 0u;
+    }
+#pragma unroll
+    for (std::uint32_t q = 0; q < kPer; ++q) dc += deg[q];
+  }
+  unsigned long long dtot = 0;
+  const std::uint32_t dbase =
+      HAS_NEXT ? (std::uint32_t)(block_inclusive_scan<kSmallLevelThreads>(dc, s_sm, &dtot) - dc) : 0u;
+  std::uint32_t* list = p.list + mb * p.cap_list;
+  std::uint32_t* ipn = HAS_NEXT ? p.indptr_next + mb * (p.cap_list + 1) : nullptr;
+  std::uint32_t* dst = p.dst + mb * p.dst_stride;
+  std::uint32_t* bo = p.base_out + (std::uint64_t)mb * (bp.NB + 1);
+  // r = distinct ids started so far: a run start takes rank r, a repeat
+  // (possibly continuing a run an earlier thread started) rank r - 1
+  std::uint32_t r = ubase, d = dbase;
+#pragma unroll
+  for (std::uint32_t q = 0; q < kPer; ++q) {
+    const std::uint32_t i = i0 + q;
+    if (i >= cnt) break;
+    const std::uint32_t v = (std::uint32_t)(s_key[i] >> 32);
+    const bool first = i == 0 || (s_key[i - 1] >> 32) != v;
+    if (first) {
+      list[r] = v;
+      if (HAS_NEXT) {
+        ipn[r] = d;
+        d += deg[q];
+      }
+      // bucket bases: buckets (previous id's bucket, this bucket] start here
+      const std::uint32_t bcur = v >> bp.bb;
+      const std::uint32_t bprev = i == 0 ? 0u : (std::uint32_t)(s_key[i - 1] >> 32 >> bp.bb) + 1u;
+      for (std::uint32_t bb_ = (i == 0 ? 0u : bprev); bb_ <= bcur; ++bb_) bo[bb_] = r;
+      ++r;
+    }
+    dst[(std::uint32_t)s_key[i]] = r - 1;
+  }
+  if (threadIdx.x == kSmallLevelThreads - 1) {
+    const std::uint32_t U = (std::uint32_t)utot;
+    const std::uint32_t blast = cnt ? (std::uint32_t)(s_key[cnt - 1] >> 32 >> bp.bb) + 1u : 0u;
+    for (std::uint32_t bb_ = blast; bb_ <= bp.NB; ++bb_) bo[bb_] = U;
+    p.count[mb] = U;
+    if (HAS_NEXT) {
+      ipn[U] = (std::uint32_t)dtot;
+      p.ecount_next[mb] = (std::uint32_t)dtot;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace vk

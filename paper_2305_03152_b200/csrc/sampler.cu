@@ -1277,6 +1277,31 @@ void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaS
   bp.ids = s.edges_buf(h);
   bp.ids_stride = s.capS_max;
   bp.count = s.ecount(h);
+  if (s.capS[h] <= kSmallLevel) {  // one sorting CTA per minibatch
+    dp.bp = bp;
+    dp.list = s.F[h].as<std::uint32_t>();
+    dp.cap_list = s.capF[h];
+    dp.count = s.fcount(h);
+    dp.dst = s.dst[h].as<std::uint32_t>();
+    dp.dst_stride = s.capS[h];
+    dp.base_out = s.fbase.as<std::uint32_t>() + (std::uint64_t)h * s.M * (s.nb_max + 1);
+    const std::size_t smem = (std::size_t)kSmallLevel * 8;
+    auto go = [&](void (*kernel)(DedupParams)) {
+      VK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kernel<<<nmb, kSmallLevelThreads, smem, st>>>(dp);
+    };
+    if (h < s.L) {
+      dp.f_next = s.cfg.fanouts[h];
+      dp.indptr_next = s.indptr[h + 1].as<std::uint32_t>();
+      dp.ecount_next = s.ecount(h + 1);
+      go(k_small_level<true>);
+    } else {
+      go(k_small_level<false>);
+    }
+    count_launch();
+    VK_LAUNCH_CHECK();
+    return;
+  }
   k_bucket_hist<<<dim3((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capS[h], kHistItems)), nmb), kBktThreads,
                   bp.NB * 4, st>>>(bp);
   k_bucket_scan<<<nmb, kScanThreads, 0, st>>>(bp);

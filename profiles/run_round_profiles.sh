@@ -3,7 +3,7 @@
 # timed waves and ncu --set full captures of the top kernels.
 cd ${GRAFT_REPO_ROOT:-.}
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
-K='k_bucket|k_sample|k_prepare|k_gather|k_compact|k_relabel|k_allidx'
+K='k_bucket|k_small|k_sample|k_prepare|k_gather|k_compact|k_relabel|k_allidx'
 timeout 600 ncu --metrics $M --clock-control none -k regex:"$K" -c 60 --csv --log-file gpurun_out/r02_launches_c4.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r02_launches_c4.log 2>&1
 timeout 600 ncu --metrics $M --clock-control none -k regex:"$K" -c 60 --csv --log-file gpurun_out/r02_launches_c3.csv \
