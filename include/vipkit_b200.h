@@ -114,6 +114,10 @@ VK_API int vk_initial_probs(uint64_t n, const uint8_t* roles, const uint32_t* pa
  * vectors at once (e.g. all K partitions: one pass over the reverse CSR
  * serves every column). p0: ncols x n (column c = vector c, contiguous).
  * hop_out: ncols x L x n or NULL; total_out: ncols x n. Host buffers. */
+/* Storage width of the hoisted log terms between hops (process-wide): 0 =
+ * automatic (double while n x columns x 8 B fits 64 MB, else float with a
+ * guarded fallback to double), 32 or 64 to force one (tests). */
+VK_API int vk_vip_force_storage(int bits);
 VK_API int vk_vip_propagate(vk_graph g, const uint32_t* fanouts, uint32_t num_hops,
                             uint32_t ncols, const double* p0, double* hop_out, double* total_out);
 /* Same on device buffers, asynchronous on `stream`. */

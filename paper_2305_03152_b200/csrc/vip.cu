@@ -20,6 +20,7 @@
 // reverse CSR. `C` columns (partitions) are propagated together: one index
 // stream serves C probability vectors (the lm gather fetches C contiguous
 // doubles).
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <type_traits>
@@ -31,6 +32,7 @@ namespace vk {
 namespace {
 
 constexpr double kFlushBelow = 1e-300;  // vip.cpp:16
+std::atomic<int> g_lm_force{0};  // 0 automatic, 32 / 64 forced storage width of the hoisted terms
 constexpr int kMaxHops = VK_MAX_HOPS;
 
 // In-degree classes: [0] G=4 deg<=12, [1] G=8 <=48, [2] G=16 <=160,
@@ -601,8 +603,7 @@ void propagate_device(vk_graph_s& g, const std::uint32_t* fanouts, std::uint32_t
   // every output stay double; the float relative error (6e-8 per term, all
   // terms one sign) is far inside the 1e-5 contract. A nonzero term below
   // FLT_MIN sets a flag and the propagation is redone with double storage.
-  const char* force_env = std::getenv("VK_VIP_LM");  // "64" / "32" force the storage width
-  const int force = force_env ? std::atoi(force_env) : 0;
+  const int force = g_lm_force.load(std::memory_order_relaxed);  // vk_vip_force_storage
   const bool use_f32 = force == 32 || (force != 64 && n * 8ull * cmax > kLmDoubleBudget);
   auto pass = [&](bool f32) {
     VK_CUDA(cudaMemsetAsync(bad.p, 0, 2 * sizeof(unsigned), st));
@@ -648,6 +649,13 @@ int vk_initial_probs(uint64_t n, const uint8_t* roles, const uint32_t* part_of, 
     if (T == 0) raise(VK_ERR_SAMPLING, "partition " + std::to_string(k) + " has no train vertices");
     const double p = std::min(1.0, (double)batch_size / (double)T);
     for (std::uint64_t v = 0; v < n; ++v) p0_out[v] = (part_of[v] == k && roles[v] == 0) ? p : 0.0;
+  });
+}
+
+int vk_vip_force_storage(int bits) {
+  return guard([&] {
+    if (bits != 0 && bits != 32 && bits != 64) raise(VK_ERR_PARAMETER, "storage width must be 0, 32 or 64");
+    g_lm_force.store(bits, std::memory_order_relaxed);
   });
 }
 

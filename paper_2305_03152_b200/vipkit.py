@@ -106,6 +106,7 @@ def lib():
     L.vk_graph_apply_reorder.argtypes = [c_vp, u32p, C.POINTER(c_vp)]
     L.vk_initial_probs.argtypes = [c_u64, u8p, u32p, c_u32, c_u64, f64p]
     L.vk_vip_propagate.argtypes = [c_vp, u32p, c_u32, c_u32, f64p, c_vp, f64p]
+    L.vk_vip_force_storage.argtypes = [c_int]
     L.vk_vip_propagate_device.argtypes = [c_vp, u32p, c_u32, c_u32, c_vp, c_vp, c_vp, c_vp]
     L.vk_train_members.argtypes = [c_u64, u8p, u32p, c_u32, u32p, C.POINTER(c_u64)]
     L.vk_epoch_shuffle.argtypes = [u32p, c_u64, c_u32, c_u64, c_u64, u32p]
@@ -332,6 +333,11 @@ def propagate(g: Graph, fanouts, p0, partition: int = 0, with_hops: bool = True)
     res = [VipScores(partition + c if p.ndim > 1 else partition, cols[c],
                      None if hop is None else hop[c], total[c]) for c in range(nc)]
     return res if p.ndim > 1 else res[0]
+
+
+def vip_force_storage(bits):
+    """vk_vip_force_storage: 0 automatic, 32 / 64 force the hoisted-term width."""
+    check(lib().vk_vip_force_storage(bits))
 
 
 def propagate_device(g: Graph, fanouts, ncols, p0_ptr, hop_ptr, total_ptr, stream=0):

@@ -11,5 +11,5 @@ timeout 600 ncu --metrics $M --clock-control none -k regex:"$K" -c 60 --csv --lo
 # full captures: C4 gather + sampler kernels of one steady-state wave (skip warm-up wave 0)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$K" --launch-skip 20 -c 20 \
   -o gpurun_out/r02_ncu_full_c4 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/r02_ncu_full_c4.log 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:"k_gather" --launch-skip 4 -c 1 \
+timeout 600 ncu --set full --clock-control none --kernel-name-base function -k regex:'^k_gather$' --launch-skip 4 -c 1 \
   -o gpurun_out/r02_ncu_full_c3_gather python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/r02_ncu_full_c3.log 2>&1

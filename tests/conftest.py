@@ -58,3 +58,11 @@ def csr_from(golden_graphs, name):
     g = golden_graphs
     return CSR(len(g[name + "_off"]) - 1, g[name + "_off"], g[name + "_tgt"], g[name + "_roff"],
                g[name + "_rtgt"])
+
+
+@pytest.fixture
+def float_storage(vk):
+    """Force the VIP hoisted terms into float storage for one test."""
+    vk.vip_force_storage(32)
+    yield
+    vk.vip_force_storage(0)

@@ -48,11 +48,10 @@ def test_vip_c3_float_storage_8_columns_vs_reference(vk, ref):
     ref.release(csr)
 
 
-def test_vip_float_storage_split_rows_vs_reference(vk, ref, port, monkeypatch):
+def test_vip_float_storage_split_rows_vs_reference(vk, ref, port, float_storage):
     """Rows with in-degree > 32768 take the chunked (split) reduction; in
     float storage (forced: this graph is below the automatic threshold) with
     8 columns, against the reference."""
-    monkeypatch.setenv("VK_VIP_LM", "32")
     n = 150_000
     rng = np.random.default_rng(3)
     # three hubs adjacent to almost everything, plus a sparse random part

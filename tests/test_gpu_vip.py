@@ -127,10 +127,9 @@ def test_errors(vk, golden):
         vk.Graph.from_csr(np.array([0, 1, 1], np.uint64), np.array([0], np.uint32), validate=True)
 
 
-def test_float_lm_storage_within_tolerance(vk, port, monkeypatch):
+def test_float_lm_storage_within_tolerance(vk, port, float_storage):
     """Large graphs store the hoisted log terms in float; forced
     here on C1: still within 1e-5 relative, 0/1 cases exact."""
-    monkeypatch.setenv("VK_VIP_LM", "32")
     csr = port.generate("pa", 100000, 10, 7)
     roles = port.make_roles(csr.n, 0.1, 0, 0, 3)
     labels = (np.arange(csr.n) % 4).astype(np.uint32)
@@ -144,10 +143,9 @@ def test_float_lm_storage_within_tolerance(vk, port, monkeypatch):
         assert np.all((tot == 0) == (res[k].total == 0))
 
 
-def test_float_lm_storage_falls_back_for_subnormal_terms(vk, port, monkeypatch):
+def test_float_lm_storage_falls_back_for_subnormal_terms(vk, port, float_storage):
     """A nonzero w*p below FLT_MIN would lose relative accuracy in float
     storage: the library detects it and redoes the pass in double."""
-    monkeypatch.setenv("VK_VIP_LM", "32")
     csr = port.generate("pa", 2000, 4, 3)
     p0 = np.zeros(csr.n)
     p0[:50] = 1e-200
