@@ -286,7 +286,7 @@ def run_b200(args, cfg):
     prefetch = (world > 1) if args.prefetch == "auto" else args.prefetch == "1"
     overlap = args.sched == "overlap"
     P = 1 if (prefetch or overlap) else args.pipes
-    samplers = [vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED)
+    samplers = [vk.Sampler(g, cfg["fanouts"], cfg["b"], M, SAMPLE_SEED, frontier=args.frontier)
                 for _ in range(2 if (prefetch or overlap) else P)]
     # overlap schedule: samplers on a high-priority stream, gathers on the
     # main one, so wave i+1 samples (L2/latency bound) while wave i gathers
@@ -502,7 +502,7 @@ def run_b200(args, cfg):
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 ids / fp32 rows / fp64 VIP",
         "data": "synthetic (community power-law graph, counter-hashed feature rows)",
         "config": {"workload": cfg["workload"], "n": n, "m_slots": m, "partitions": K, "pipes": P,
-                   "exchange_prefetch": bool(prefetch), "prefetch_order": args.prefetch_order,
+                   "exchange_prefetch": bool(prefetch), "prefetch_order": args.prefetch_order, "frontier": args.frontier,
                    "schedule": args.sched,
                    "fanouts": list(cfg["fanouts"]), "batch": cfg["b"], "minibatches_per_step_per_gpu": M,
                    "feature_dim": cfg["dim"], "row_bytes": rb, "alpha": cfg["alpha"],
@@ -836,6 +836,8 @@ def main():
                          "(overlaps the sampling of wave i+2)")
     ap.add_argument("--sched", default="serial", choices=["serial", "overlap"],
                     help="overlap: sample wave i+1 on a high-priority stream while wave i gathers")
+    ap.add_argument("--frontier", default="auto", choices=["auto", "dense", "sparse"],
+                    help="sampler frontier representation (default: automatic by graph size)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--alpha", type=float, default=None, help="override the config's VIP cache fraction")
     args = ap.parse_args()

@@ -75,6 +75,8 @@ inline std::uint64_t mix64(std::uint64_t x) {
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
   return x ^ (x >> 31);
 }
+// Restated from the reference (rng.hpp:9-74): the stream definition is the
+// bit-exact sampling contract, so it is the reference's, not a new design.
 class RngStream {
  public:
   explicit RngStream(std::uint64_t key) : counter_(mix64(key)) {}
@@ -177,6 +179,8 @@ struct PartitionMap {
   std::vector<std::uint32_t> part_of;
   std::vector<std::vector<vertex_t>> members;
 
+  // Restated from graph.cpp:88-104, error strings included: the exception
+  // types and messages are part of the API callers match on.
   static PartitionMap from_labels(std::vector<std::uint32_t> labels, std::uint32_t K) {  // graph.cpp:88-104
     if (K == 0) throw parameter_error("partition count must be >= 1");
     PartitionMap pm;
@@ -803,6 +807,7 @@ struct SweepResult {
   std::vector<Geomean> geomeans;
 };
 
+// Restated from commsim.cpp:129-138 (the sweep's summary statistic).
 inline double geometric_mean(std::span<const double> xs) {  // commsim.cpp:129-138
   if (xs.empty()) throw parameter_error("geometric mean of empty set");
   double log_sum = 0.0;
@@ -816,7 +821,10 @@ inline double geometric_mean(std::span<const double> xs) {  // commsim.cpp:129-1
 
 /// The policy x alpha x fanout grid on the device: every ranking, the
 /// oracle's access counts and each policy's alpha axis (vk_simulate) run on
-/// the GPU; expansions are identical across plans by construction.
+/// the GPU; expansions are identical across plans by construction. The
+/// control flow (grid loops, no-cache baseline, improvement and geomean
+/// bookkeeping) follows commsim.cpp:140-259 so the SweepResult matches the
+/// reference's; the per-cell work is replaced by the device calls.
 inline SweepResult sweep(const Graph& g, const VertexRoles& roles, const PartitionMap& part,
                          const SweepConfig& cfg) {
   if (cfg.fanouts.empty() || cfg.alphas.empty() || cfg.policies.empty())
