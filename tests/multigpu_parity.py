@@ -68,19 +68,33 @@ def main():
     s.run(batches, refs)
     ok &= check_wave(vk, P, csr, plane, plan, labels, batches, refs, s, out2, cnt2, dim, local, rank, world,
                      prefetch=True)
-    for b_ in (out, cnt, out2, cnt2):
+    # sparse (bucket) frontiers -- the papers-scale representation, whose
+    # gather tiles come from bucket bases -- with the exchange ordered after
+    # a caller stream's queued work (vk_plane_prefetch_after)
+    sp = vk.Sampler(g, [10, 5], 128, len(batches), 42, frontier="sparse")
+    sp.run(batches, refs)
+    out3, cnt3 = C.c_void_p(), C.c_void_p()
+    vk.check(vk.lib().vk_device_alloc(local, len(batches) * sp.view().all_stride * plane.row_bytes, C.byref(out3)))
+    vk.check(vk.lib().vk_device_alloc(local, len(batches) * 32, C.byref(cnt3)))
+    side = torch.cuda.Stream()
+    ok &= check_wave(vk, P, csr, plane, plan, labels, batches, refs, sp, out3, cnt3, dim, local, rank, world,
+                     prefetch="after", stream=side.cuda_stream)
+    for b_ in (out, cnt, out2, cnt2, out3, cnt3):
         vk.lib().vk_device_free(b_)
     flag = torch.tensor([1 if ok else 0])
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     dist.barrier()
-    print(f"rank {rank}: {'ok' if ok else 'FAIL'} ({len(refs)} minibatches x 2)", flush=True)
+    print(f"rank {rank}: {'ok' if ok else 'FAIL'} ({len(refs)} minibatches x 3)", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if int(flag) == 1 else 1)
 
 
-def check_wave(vk, P, csr, plane, plan, labels, batches, refs, s, out, cnt, dim, local, rank, world, prefetch):
+def check_wave(vk, P, csr, plane, plan, labels, batches, refs, s, out, cnt, dim, local, rank, world, prefetch,
+               stream=None):
     view = s.view()
-    if prefetch:
+    if prefetch == "after":
+        plane.prefetch_after(s, stream)
+    elif prefetch:
         plane.prefetch(s)
     plane.gather(s, out.value, view.all_stride, cnt.value)
     counts = np.zeros(len(batches) * 4, np.uint64)

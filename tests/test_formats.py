@@ -115,3 +115,10 @@ def test_vcsr_writer_matches_reference(ref, port, tmp_path):
     g = ref.load_vcsr(b)
     np.testing.assert_array_equal(g.off, csr.off)
     np.testing.assert_array_equal(g.tgt, csr.tgt)
+
+
+def test_vip_storage_width_api():
+    with pytest.raises(vk.ParameterError):
+        vk.vip_force_storage(16)
+    vk.vip_force_storage(32)
+    vk.vip_force_storage(0)
