@@ -838,6 +838,8 @@ def main():
                     help="overlap: sample wave i+1 on a high-priority stream while wave i gathers")
     ap.add_argument("--frontier", default="auto", choices=["auto", "dense", "sparse"],
                     help="sampler frontier representation (default: automatic by graph size)")
+    ap.add_argument("--vip-storage", type=int, default=0, choices=[0, 32, 64],
+                    help="VIP hoisted-term storage width (0: automatic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--alpha", type=float, default=None, help="override the config's VIP cache fraction")
     args = ap.parse_args()
@@ -850,6 +852,9 @@ def main():
         args.wave = cfg.get("wave", 32)
     if args.alpha_sweep and "alpha_sweep" not in cfg:
         cfg["alpha_sweep"] = (0.0, 0.04, 0.08, 0.16, 0.32)
+    if args.vip_storage and args.impl != "reference":
+        from paper_2305_03152_b200 import vipkit as vk
+        vk.vip_force_storage(args.vip_storage)
     if args.config == "c5" and args.impl != "reference":
         run_vip_sweep(args, cfg)
         return
