@@ -282,8 +282,9 @@ VK_API int vk_build_reorder(int device, uint64_t n, uint32_t K, const uint32_t* 
  * The VIP-ordered feature store (north-star (3); no reference code: features
  * are never materialised there). For each partition k resident
  * on this device: local rows = members of k in build_reorder order, then
- * cache rows = the CachePlan prefix of ranking k (policies.cpp:149-163), and a
- * slot map u32[n] (local row / cache row / VK_MISS). Rows are `dim` values
+ * cache rows = the CachePlan prefix of ranking k (policies.cpp:149-163) in
+ * ascending vertex id, and a cache index (membership bits + rank per 64 ids).
+ * Rows are `dim` values
  * of dtype VK_F32 or VK_F16. Partitions owned by another GPU are attached by
  * CUDA IPC and read over NVLink inside the gather kernel. */
 #define VK_F32 0

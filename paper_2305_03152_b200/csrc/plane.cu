@@ -7,8 +7,10 @@
 //  * vk_build_reorder    = build_reorder (reorder.cpp:11-34): two stable sorts
 //    (score desc within partition, then partition id).
 //  * feature plane       = the north-star's VIP-ordered store: per resident
-//    partition k, local rows in build_reorder order then cache rows in ranking
-//    order (CachePlan prefix, policies.cpp:149-163), plus slot map u32[n].
+//    partition k, local rows in build_reorder order then the cache rows (the
+//    CachePlan prefix, policies.cpp:149-163) in ascending vertex id, plus a
+//    cache index of one 16-byte word per 64 vertex ids (membership bits and
+//    the cache rank of the word's first member).
 //  * vk_plane_gather     = classify (commsim.cpp:61-73) + row gather for a
 //    whole wave: 128-bit loads/stores, flattened over (row, 16-byte chunk) so
 //    every lane moves data and writes are fully coalesced; misses read the
@@ -57,14 +59,14 @@ struct vk_plane_s {
   struct Part {
     bool resident = false, attached = false;
     vk::DevBuf store;  // (n_local + n_cache) rows
-    vk::DevBuf slot;   // u32 [n]
+    vk::DevBuf cword;  // uint4 [W]: {member bits lo, hi, cache rank of the word's first member, 0}
     std::uint64_t n_local = 0, n_cache = 0;
     std::vector<std::uint64_t> cache_bits;  // CachePlan::member_bits[k]
     void* peer = nullptr;                   // IPC-mapped local rows of a remote partition
     vk::DevBuf rmask;  // [W] bit v: v is neither local nor cached here and its owner is on a peer GPU
   };
   std::vector<Part> parts;
-  vk::DevBuf d_base, d_slot, d_nlocal;  // K-entry tables for the gather kernel
+  vk::DevBuf d_base, d_cword, d_nlocal;  // K-entry tables for the gather kernel
   vk::DevBuf d_rmask;                   // [K] Part::rmask pointers (resident partitions)
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // prefetched miss exchanges (vk_plane_prefetch), high priority
@@ -186,11 +188,19 @@ __global__ void k_synth_rows(const std::uint32_t* __restrict__ ids, std::uint64_
   }
 }
 
-__global__ void k_fill_slots(const std::uint32_t* __restrict__ ids, std::uint64_t count, std::uint32_t base,
-                             std::uint32_t* __restrict__ slot) {
-  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < count;
-       i += (std::uint64_t)gridDim.x * blockDim.x)
-    slot[ids[i]] = base + (std::uint32_t)i;
+// Cache row of v in partition k's store (after its n_local local rows), from
+// the cache index: cache rows are stored in ascending vertex id, so the row
+// is the word's first-member rank plus the members below v in the word. A
+// gather tile covers a contiguous vertex range, so its index words (and the
+// new_id entries every row reads) are shared by all the wave's minibatches
+// and stay in L2 -- unlike a u32 slot map per partition, whose entries for a
+// minibatch's rows are scattered sectors (C4: ~1.5 GB of DRAM reads a wave).
+__device__ __forceinline__ bool cache_rank(const uint4* __restrict__ cw, std::uint32_t v, std::uint32_t& rank) {
+  const uint4 c = __ldg(cw + (v >> 6));
+  const unsigned long long bits = ((unsigned long long)c.y << 32) | c.x;
+  const unsigned long long below = bits & ((1ull << (v & 63)) - 1ull);
+  rank = c.z + (std::uint32_t)__popcll(below);
+  return (bits >> (v & 63)) & 1ull;
 }
 
 // ---- classify + gather ----
@@ -202,7 +212,7 @@ struct GatherParams {
   const char* desc;          // WaveDesc array; partition at desc + mb*desc_stride
   std::uint64_t desc_stride;
   const char* const* base;   // [K] local-row base of each partition (local or peer)
-  const std::uint32_t* const* slot;  // [K] slot map (resident partitions)
+  const uint4* const* cword;         // [K] cache index (resident partitions)
   const std::uint32_t* nlocal;       // [K]
   const std::uint32_t* part_of;
   const std::uint32_t* owner_row;
@@ -259,8 +269,8 @@ __device__ __forceinline__ void tile_range(const GatherParams& p, std::uint32_t 
   hi = w1 < p.W ? rk[w1].z : cnt;
 }
 
-constexpr std::uint32_t kMagicExactV = 11585;
-constexpr unsigned kPullCtasPrefetch = 2;  // pull CTAs per SM beside a running gather  // largest V with V*V < 2^27
+constexpr std::uint32_t kMagicExactV = 11585;  // largest V with V*V < 2^27
+constexpr unsigned kPullCtasPrefetch = 2;  // pull CTAs per SM beside a running gather
 
 // Row of flattened element e (< 32 V) of a warp's 32 rows: umulhi with
 // ceil(2^32/V) is exact while V*V < 2^27 (V <= 11585); above that it can
@@ -295,7 +305,7 @@ __device__ __forceinline__ const std::uint32_t* stage_rstart(const GatherParams&
 // without allocating and with an L2 evict_last policy (a row read for one
 // minibatch of the wave stays in L2 for the others; C3: 5.60 -> 5.23 ms);
 // gathered rows are written evict-first so they do not evict the graph and
-// slot maps from L2. Measured no better, and removed: plain / L1::no_allocate
+// cache index from L2. Measured no better, and removed: plain / L1::no_allocate
 // stores, evict_normal loads, L2 hints on the index loads.
 template <class T>
 __device__ __forceinline__ T ld_row(const T* p, std::uint64_t pol) {
@@ -377,7 +387,7 @@ __device__ __forceinline__ void copy_group(const T* const* src, T* dst, std::uin
 }
 
 // One warp per group of 32 consecutive output rows: lanes first resolve the
-// 32 source rows in parallel (classify: slot map -> local / cache row, or the
+// 32 source rows in parallel (classify: local row, cache row, or the
 // owner partition's row, local HBM or a peer GPU over NVLink), then the warp
 // copies the group as one flat, fully coalesced range of 32*V vectors with
 // kUnroll independent loads in flight per lane.
@@ -391,13 +401,13 @@ __global__ void __launch_bounds__(256) k_remote_mark(GatherParams p, unsigned lo
   const std::uint32_t k = *reinterpret_cast<const std::uint32_t*>(p.desc + mb * p.desc_stride);
   const std::uint32_t cnt = p.all_count[mb];
   const std::uint32_t* all = p.all + mb * p.all_stride;
-  const std::uint32_t* slot = p.slot[k];
+  const uint4* cw = p.cword[k];
   for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < cnt; r += gridDim.x * blockDim.x) {
     const std::uint32_t v = __ldg(all + r);
-    if (__ldg(slot + v) == VK_MISS) {
-      const std::uint32_t g = __ldg(p.new_id + v);
-      if (p.peer_mask[owner_of(rs, p.K, g)]) atomicOr(ubits + (g >> 6), 1ull << (g & 63));
-    }
+    const std::uint32_t g = __ldg(p.new_id + v);
+    std::uint32_t cr;
+    // owner on a peer GPU (so not k, which is resident) and not cached for k
+    if (p.peer_mask[owner_of(rs, p.K, g)] && !cache_rank(cw, v, cr)) atomicOr(ubits + (g >> 6), 1ull << (g & 63));
   }
 }
 
@@ -406,7 +416,7 @@ __global__ void __launch_bounds__(256) k_remote_mark(GatherParams p, unsigned lo
 // all-vertex bits masked by each minibatch partition's remote-miss mask into
 // a vertex-space union; (b) per union word, set each vertex's bit in global
 // row order and clear the word for the next wave. Reads M*W*16 B of rank
-// words instead of every row's id, slot and new_id.
+// words instead of every row's id, new_id and cache word.
 constexpr std::uint32_t kMarkChunk = 8;
 __global__ void __launch_bounds__(256) k_remote_union(GatherParams p, unsigned long long* __restrict__ vbits) {
   const std::uint64_t w = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
@@ -440,16 +450,19 @@ __global__ void __launch_bounds__(256) k_remote_to_rows(const GatherParams p, un
   }
 }
 
-__global__ void k_remote_miss_mask(const std::uint32_t* __restrict__ slot, const std::uint32_t* __restrict__ part_of,
+__global__ void k_remote_miss_mask(const uint4* __restrict__ cword, const std::uint32_t* __restrict__ part_of,
                                    const unsigned char* __restrict__ peer_mask, std::uint64_t n,
                                    unsigned long long* __restrict__ out) {
   const std::uint64_t W = (n + 63) / 64;
   for (std::uint64_t w = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; w < W;
        w += (std::uint64_t)gridDim.x * blockDim.x) {
+    const uint4 c = cword[w];
+    const unsigned long long cached = ((unsigned long long)c.y << 32) | c.x;
     unsigned long long m = 0;
     for (int b = 0; b < 64; ++b) {
       const std::uint64_t v = w * 64 + b;
-      if (v < n && slot[v] == VK_MISS && peer_mask[part_of[v]]) m |= 1ull << b;
+      // owner on a peer GPU (never the resident partition itself), not cached
+      if (v < n && peer_mask[part_of[v]] && !((cached >> b) & 1ull)) m |= 1ull << b;
     }
     out[w] = m;
   }
@@ -530,8 +543,8 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 4 : 1) k_gather(GatherP
   std::uint32_t lo, hi;
   tile_range(p, mb, tile, cnt, lo, hi);
   const std::uint32_t* all = p.all + mb * p.all_stride;
-  const std::uint32_t* slot = p.slot[k];
-  const std::uint32_t nl = p.nlocal[k];
+  const uint4* cw = p.cword[k];
+  const std::uint32_t nl = p.nlocal[k], rk = rs[k];
   const T* store = reinterpret_cast<const T*>(p.base[k]);
   T* out = reinterpret_cast<T*>(p.out + mb * p.out_stride_bytes);
   const std::uint64_t rowv = p.row_bytes / sizeof(T);
@@ -541,16 +554,20 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 4 : 1) k_gather(GatherP
     const std::uint32_t r = r0 + lane;
     const T* src = nullptr;
     if (r < hi) {
-      // classify (commsim.cpp:61-73): slot map -> local / cache row of
-      // partition k, else the owner's row in global row order
+      // classify (commsim.cpp:61-73): the owner of global row g = new_id[v]
+      // is k -> local row; else cached for k -> cache row; else the owner's
+      // row in global row order
       const std::uint32_t v = __ldg(all + r);
-      const std::uint32_t s = __ldg(slot + v);
-      if (s != VK_MISS) {
-        src = store + (std::uint64_t)s * rowv;
-        (s < nl ? c_local : c_cache)++;
+      const std::uint32_t g = __ldg(p.new_id + v);
+      const std::uint32_t o = owner_of(rs, p.K, g);
+      std::uint32_t cr;
+      if (o == k) {
+        src = store + (std::uint64_t)(g - rk) * rowv;
+        ++c_local;
+      } else if (cache_rank(cw, v, cr)) {
+        src = store + (std::uint64_t)(nl + cr) * rowv;
+        ++c_cache;
       } else {
-        const std::uint32_t g = __ldg(p.new_id + v);
-        const std::uint32_t o = owner_of(rs, p.K, g);
         src = reinterpret_cast<const T*>(p.base[o]) + (std::uint64_t)(g - rs[o]) * rowv;
         ++c_miss;
         if (p.peer_mask[o]) {  // owned by a partition on another GPU
@@ -740,10 +757,10 @@ int vk_plane_create(int device, uint64_t n, uint32_t K, uint32_t dim, int dtype,
       VK_CUDA(cudaMemcpyAsync(p->new_id.p, nid.data(), n * 4, cudaMemcpyHostToDevice, p->stream));
       VK_CUDA(cudaMemcpyAsync(p->d_rstart.p, rst.data(), (K + 1) * 4, cudaMemcpyHostToDevice, p->stream));
       p->d_base.alloc(K * sizeof(void*));
-      p->d_slot.alloc(K * sizeof(void*));
+      p->d_cword.alloc(K * sizeof(void*));
       p->d_nlocal.alloc(K * 4 + K);  // u32 nlocal[K] then u8 peer_mask[K]
       VK_CUDA(cudaMemsetAsync(p->d_base.p, 0, p->d_base.bytes, p->stream));
-      VK_CUDA(cudaMemsetAsync(p->d_slot.p, 0, p->d_slot.bytes, p->stream));
+      VK_CUDA(cudaMemsetAsync(p->d_cword.p, 0, p->d_cword.bytes, p->stream));
       VK_CUDA(cudaMemsetAsync(p->d_nlocal.p, 0, p->d_nlocal.bytes, p->stream));
       VK_CUDA(cudaStreamSynchronize(p->stream));
     } catch (...) {
@@ -773,13 +790,13 @@ int vk_plane_destroy(vk_plane p) {
 namespace {
 
 void publish_tables(vk_plane_s& p) {
-  std::vector<const void*> base(p.K, nullptr), slot(p.K, nullptr);
+  std::vector<const void*> base(p.K, nullptr), cword(p.K, nullptr);
   std::vector<unsigned char> nl(p.K * 4 + p.K, 0);
   for (std::uint32_t k = 0; k < p.K; ++k) {
     const auto& q = p.parts[k];
     if (q.resident) {
       base[k] = q.store.p;
-      slot[k] = q.slot.p;
+      cword[k] = q.cword.p;
       const std::uint32_t x = (std::uint32_t)q.n_local;
       std::memcpy(nl.data() + 4 * k, &x, 4);
     } else if (q.attached) {
@@ -788,7 +805,7 @@ void publish_tables(vk_plane_s& p) {
     }
   }
   VK_CUDA(cudaMemcpyAsync(p.d_base.p, base.data(), p.K * sizeof(void*), cudaMemcpyHostToDevice, p.stream));
-  VK_CUDA(cudaMemcpyAsync(p.d_slot.p, slot.data(), p.K * sizeof(void*), cudaMemcpyHostToDevice, p.stream));
+  VK_CUDA(cudaMemcpyAsync(p.d_cword.p, cword.data(), p.K * sizeof(void*), cudaMemcpyHostToDevice, p.stream));
   VK_CUDA(cudaMemcpyAsync(p.d_nlocal.p, nl.data(), nl.size(), cudaMemcpyHostToDevice, p.stream));
   std::vector<const void*> rm(p.K, nullptr);
   const std::uint64_t W = (p.n + 63) / 64;
@@ -797,7 +814,7 @@ void publish_tables(vk_plane_s& p) {
     if (!q.resident) continue;
     if (!q.rmask.p) q.rmask.alloc(W * 8);
     k_remote_miss_mask<<<grid_for(W, p.device), 256, 0, p.stream>>>(
-        q.slot.as<std::uint32_t>(), p.part_of.as<std::uint32_t>(), p.d_nlocal.as<unsigned char>() + 4 * p.K, p.n,
+        q.cword.as<uint4>(), p.part_of.as<std::uint32_t>(), p.d_nlocal.as<unsigned char>() + 4 * p.K, p.n,
         q.rmask.as<unsigned long long>());
     VK_LAUNCH_CHECK();
     rm[k] = q.rmask.p;
@@ -832,21 +849,30 @@ int vk_plane_load_partition(vk_plane p, uint32_t k, const uint32_t* cache_ids, u
     }
     const std::uint64_t rows = nl + n_cache;
     if (rows >= VK_MISS) raise(VK_ERR_UNSUPPORTED, "too many rows in one partition store");
+    // store rows: local rows in global row order, then the cached vertices
+    // in ascending id (the cache index below ranks them by word)
     std::vector<std::uint32_t> ids(rows);
     std::memcpy(ids.data(), p->old_of_new.data() + p->rstart[k], nl * 4);
-    if (n_cache) std::memcpy(ids.data() + nl, cache_ids, n_cache * 4);
+    {
+      std::uint64_t r = nl;
+      for (std::uint64_t w = 0; w < bits.size(); ++w)
+        for (std::uint64_t x = bits[w]; x; x &= x - 1) ids[r++] = (std::uint32_t)(w * 64 + __builtin_ctzll(x));
+    }
+    const std::uint64_t W = bits.size();
+    std::vector<std::uint32_t> cw(W * 4, 0u);
+    std::uint32_t crank = 0;
+    for (std::uint64_t w = 0; w < W; ++w) {
+      cw[4 * w] = (std::uint32_t)bits[w];
+      cw[4 * w + 1] = (std::uint32_t)(bits[w] >> 32);
+      cw[4 * w + 2] = crank;
+      crank += (std::uint32_t)__builtin_popcountll(bits[w]);
+    }
     q.store.alloc(std::max<std::uint64_t>(rows, 1) * p->row_bytes);
-    q.slot.alloc(n * 4);
+    q.cword.alloc(std::max<std::uint64_t>(W, 1) * 16);
     DevBuf dids(std::max<std::uint64_t>(rows, 1) * 4);
     cudaStream_t st = p->stream;
     VK_CUDA(cudaMemcpyAsync(dids.p, ids.data(), rows * 4, cudaMemcpyHostToDevice, st));
-    VK_CUDA(cudaMemsetAsync(q.slot.p, 0xFF, n * 4, st));
-    if (rows) {
-      k_fill_slots<<<grid_for(rows, p->device), 256, 0, st>>>(dids.as<std::uint32_t>(), rows, 0,
-                                                             q.slot.as<std::uint32_t>());
-      count_launch();
-      VK_LAUNCH_CHECK();
-    }
+    VK_CUDA(cudaMemcpyAsync(q.cword.p, cw.data(), W * 16, cudaMemcpyHostToDevice, st));
     if (features) {
       // stage the selected rows on the host, one H2D copy
       std::vector<unsigned char> rowsbuf(rows * p->row_bytes);
@@ -970,7 +996,7 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
     gp.desc = reinterpret_cast<const char*>(parts);
     gp.desc_stride = sampler_desc_stride();
     gp.base = reinterpret_cast<const char* const*>(p->d_base.p);
-    gp.slot = reinterpret_cast<const std::uint32_t* const*>(p->d_slot.p);
+    gp.cword = reinterpret_cast<const uint4* const*>(p->d_cword.p);
     gp.nlocal = p->d_nlocal.as<std::uint32_t>();
     gp.peer_mask = p->d_nlocal.as<unsigned char>() + 4 * p->K;
     gp.part_of = p->part_of.as<std::uint32_t>();
@@ -1105,7 +1131,8 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
                                                           ss.ulist.as<std::uint32_t>());
       // NVLink-bound: a prefetched exchange shares the SMs with a running
       // gather (2 CTAs/SM, on the high-priority aux stream); inline, 8 CTAs/SM
-      const unsigned pg = (unsigned)sm_count(p->device) * (prefetch_only ? kPullCtasPrefetch : 8);
+      unsigned pg = (unsigned)sm_count(p->device) * (prefetch_only ? kPullCtasPrefetch : 8);
+      if (const char* e = getenv("VK_PULL_CTAS_EXPERIMENT")) pg = (unsigned)atoi(e);
       GatherParams pp = gp;  // staged rows are plain rows: the pull's vector width follows the row size
       auto pull = [&](auto tag, std::uint32_t esz) {
         using T = decltype(tag);
