@@ -103,46 +103,68 @@ __global__ void __launch_bounds__(kScanThreads) k_bucket_scan(BucketParams p) {
 }
 
 // 3. (id, MFG position) pairs into bucket order: the CTA's kScatterItems
-// items stay in registers between its count and place passes; it reserves
-// one range per bucket it touches (one global atomic per bucket), then places
-// its items with shared cursors. Order inside a bucket is irrelevant (set
-// semantics).
+// items stay in registers with their rank inside their bucket (one shared
+// atomic each); a block scan of the bucket counts sorts them by bucket in
+// shared memory, the CTA reserves one range per bucket it touches (one global
+// atomic per bucket), and the sorted pairs are written out so consecutive
+// threads store consecutive addresses of a bucket's range (coalesced runs
+// instead of one scattered 8-byte store per item). Order inside a bucket is
+// irrelevant (set semantics).
+constexpr std::size_t scatter_smem(std::uint32_t NB) {
+  return ((std::size_t)3 * NB + 1) / 2 * 8 + (std::size_t)kScatterItems * 8;
+}
 __global__ void __launch_bounds__(kBktThreads) k_bucket_scatter(BucketParams p) {
   constexpr std::uint32_t kPer = kScatterItems / kBktThreads;
-  extern __shared__ std::uint32_t s_dyn[];
-  std::uint32_t* s_cnt = s_dyn;          // [NB]
-  std::uint32_t* s_base = s_dyn + p.NB;  // [NB]
+  extern __shared__ unsigned long long s_dyn8[];
+  __shared__ unsigned long long s_sm[kBktThreads / 32];
+  const std::uint32_t NB = p.NB;
+  std::uint32_t* s_cnt = reinterpret_cast<std::uint32_t*>(s_dyn8);  // [NB]
+  std::uint32_t* s_base = s_cnt + NB;                                // [NB] reserved global offset
+  std::uint32_t* s_off = s_base + NB;                                // [NB] CTA-local bucket offset
+  uint2* s_stage = reinterpret_cast<uint2*>(s_dyn8 + (3 * NB + 1) / 2);  // [kScatterItems]
   const std::uint32_t mb = blockIdx.y;
   const std::uint32_t total = p.count[mb];
   const std::uint32_t c0 = blockIdx.x * kScatterItems;
   if (c0 >= total) return;
+  const std::uint32_t nloc = min(kScatterItems, total - c0);
   const std::uint32_t* ids = p.ids + mb * p.ids_stride;
-  std::uint32_t v[kPer];
+  std::uint32_t v[kPer], lr[kPer];
 #pragma unroll
   for (std::uint32_t k = 0; k < kPer; ++k) {
     const std::uint32_t i = c0 + threadIdx.x + k * kBktThreads;
     v[k] = i < total ? __ldg(ids + i) : 0xffffffffu;
   }
-  for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads) s_cnt[b] = 0;
+  for (std::uint32_t b = threadIdx.x; b < NB; b += kBktThreads) s_cnt[b] = 0;
   __syncthreads();
 #pragma unroll
   for (std::uint32_t k = 0; k < kPer; ++k)
-    if (v[k] != 0xffffffffu) atomicAdd(&s_cnt[v[k] >> p.bb], 1u);
+    if (v[k] != 0xffffffffu) lr[k] = atomicAdd(&s_cnt[v[k] >> p.bb], 1u);
   __syncthreads();
-  std::uint32_t* cur = p.cursor + (std::uint64_t)mb * p.NB;
-  for (std::uint32_t b = threadIdx.x; b < p.NB; b += kBktThreads) {
-    const std::uint32_t c = s_cnt[b];
-    if (c) s_base[b] = atomicAdd(cur + b, c);
-    s_cnt[b] = 0;
+  {
+    const std::uint32_t per = (NB + kBktThreads - 1) / kBktThreads;
+    const std::uint32_t b0 = min(NB, threadIdx.x * per), b1 = min(NB, b0 + per);
+    unsigned long long mine = 0, tot;
+    for (std::uint32_t b = b0; b < b1; ++b) mine += s_cnt[b];
+    std::uint32_t run = (std::uint32_t)(block_inclusive_scan<kBktThreads>(mine, s_sm, &tot) - mine);
+    std::uint32_t* cur = p.cursor + (std::uint64_t)mb * NB;
+    for (std::uint32_t b = b0; b < b1; ++b) {
+      const std::uint32_t c = s_cnt[b];
+      s_off[b] = run;
+      run += c;
+      if (c) s_base[b] = atomicAdd(cur + b, c);
+    }
   }
   __syncthreads();
-  uint2* out = p.pairs + mb * p.pair_stride;
 #pragma unroll
   for (std::uint32_t k = 0; k < kPer; ++k)
-    if (v[k] != 0xffffffffu) {
-      const std::uint32_t b = v[k] >> p.bb;
-      out[s_base[b] + atomicAdd(&s_cnt[b], 1u)] = make_uint2(v[k], c0 + threadIdx.x + k * kBktThreads);
-    }
+    if (v[k] != 0xffffffffu) s_stage[s_off[v[k] >> p.bb] + lr[k]] = make_uint2(v[k], c0 + threadIdx.x + k * kBktThreads);
+  __syncthreads();
+  uint2* out = p.pairs + mb * p.pair_stride;
+  for (std::uint32_t i = threadIdx.x; i < nloc; i += kBktThreads) {
+    const uint2 q = s_stage[i];
+    const std::uint32_t b = q.x >> p.bb;
+    out[s_base[b] + (i - s_off[b])] = q;
+  }
 }
 
 struct DedupParams {

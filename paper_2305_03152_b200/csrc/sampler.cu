@@ -1258,7 +1258,7 @@ void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaS
                     bp.NB * 4, st>>>(bp);
     k_bucket_scan<<<nmb, kScanThreads, 0, st>>>(bp);
     k_bucket_scatter<<<dim3((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capF[0], kScatterItems)), nmb),
-                       kBktThreads, bp.NB * 8, st>>>(bp);
+                       kBktThreads, scatter_smem(bp.NB), st>>>(bp);
     count_launch(3);
     dp.bp = bp;
     dp.list = s.all.as<std::uint32_t>();
@@ -1306,7 +1306,7 @@ void run_bucket_level(vk_sampler_s& s, std::uint32_t h, std::uint32_t nmb, cudaS
                   bp.NB * 4, st>>>(bp);
   k_bucket_scan<<<nmb, kScanThreads, 0, st>>>(bp);
   k_bucket_scatter<<<dim3((unsigned)std::max<std::uint64_t>(1, ceil_div(s.capS[h], kScatterItems)), nmb),
-                     kBktThreads, bp.NB * 8, st>>>(bp);
+                     kBktThreads, scatter_smem(bp.NB), st>>>(bp);
   count_launch(3);
   VK_LAUNCH_CHECK();
   dp.bp = bp;
@@ -1474,7 +1474,7 @@ int vk_sampler_create(vk_graph g, const vk_sampler_config* cfg, vk_sampler* out)
         s->tile_base.alloc(M * (s->nbuckets(0) + 1) * 4);
         VK_CUDA(cudaMemsetAsync(s->bhist.p, 0, s->bhist.bytes, nullptr));
         VK_CUDA(cudaFuncSetAttribute(k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(kMaxBuckets * 8)));
+                                     (int)scatter_smem(kMaxBuckets)));
         s->status.alloc(8);
       } else {
         s->hopbits.alloc(M * s->W * 8);
