@@ -497,8 +497,12 @@ __global__ void __launch_bounds__(kBktThreads) k_bucket_dedup_all(DedupParams p)
 
 // 4c. Small hop levels (at most kSmallLevel drawn ids per minibatch, e.g. C4's
 // hop 1 with 15,360): one 1024-thread CTA per minibatch sorts the (id, MFG
-// position) pairs in shared memory (bitonic), so no histogram / scatter pass
-// and ~400 near-empty buckets per minibatch become one CTA. Same outputs as
+// position) pairs (bitonic network over kSmallLevel keys, padded with ~0), so
+// no histogram / scatter pass and ~400 near-empty buckets per minibatch become
+// one CTA. Thread t holds keys t*16 .. t*16+15 in registers: compare-exchange
+// distances below 16 stay in the thread, 16..256 go through warp shuffles,
+// and only distances >= 512 (15 of the network's 105 stages) through shared
+// memory, laid out [q][t] so every access is conflict-free. Same outputs as
 // k_bucket_dedup_hop: sorted distinct F_h, next-hop row pointers, MFG dst,
 // and the bucket bases the all level ranges F_h with.
 constexpr std::uint32_t kSmallLevel = 16384;
@@ -507,38 +511,74 @@ constexpr int kSmallLevelThreads = 1024;
 template <bool HAS_NEXT>
 __global__ void __launch_bounds__(kSmallLevelThreads) k_small_level(DedupParams p) {
   constexpr std::uint32_t kPer = kSmallLevel / kSmallLevelThreads;  // 16 per thread
-  extern __shared__ unsigned long long s_key[];                    // [kSmallLevel] id << 32 | position
+  constexpr std::uint32_t T = kSmallLevelThreads;
+  extern __shared__ unsigned long long s_key[];  // [kPer][T]: key i = t*kPer + q at q*T + t
   __shared__ unsigned long long s_sm[kSmallLevelThreads / 32];
   const BucketParams& bp = p.bp;
   const std::uint32_t mb = blockIdx.x;
   const std::uint32_t cnt = bp.count[mb];
   const std::uint32_t* ids = bp.ids + mb * bp.ids_stride;
-  std::uint32_t P = 2;
-  while (P < cnt) P <<= 1;
-  for (std::uint32_t i = threadIdx.x; i < P; i += kSmallLevelThreads)
-    s_key[i] = i < cnt ? ((unsigned long long)__ldg(ids + i) << 32) | i : ~0ull;
-  __syncthreads();
-  // bitonic sort of P keys, ascending
-  for (std::uint32_t k = 2; k <= P; k <<= 1)
-    for (std::uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (std::uint32_t t = threadIdx.x; t < P / 2; t += kSmallLevelThreads) {
-        const std::uint32_t i = 2 * t - (t & (j - 1));  // first of the pair (i, i + j)
-        const unsigned long long a = s_key[i], c = s_key[i + j];
-        const bool up = (i & k) == 0;
-        if ((a > c) == up) {
-          s_key[i] = c;
-          s_key[i + j] = a;
-        }
+  const std::uint32_t t = threadIdx.x;
+  unsigned long long key[kPer];  // id << 32 | position
+#pragma unroll
+  for (std::uint32_t q = 0; q < kPer; ++q) {
+    const std::uint32_t i = t * kPer + q;
+    key[q] = i < cnt ? ((unsigned long long)__ldg(ids + i) << 32) | i : ~0ull;
+  }
+  // element i keeps min(a, partner) iff (i is the lower of the pair) == (its
+  // k-block ascends)
+  auto cx = [](unsigned long long a, unsigned long long b, bool keep_min) {
+    return keep_min ? (a < b ? a : b) : (a < b ? b : a);
+  };
+  for (std::uint32_t k = 2; k <= kSmallLevel; k <<= 1) {
+    std::uint32_t j = k >> 1;
+    for (; j >= kPer * 32; j >>= 1) {  // partner in another warp: shared memory
+      const std::uint32_t m = j / kPer;
+#pragma unroll
+      for (std::uint32_t q = 0; q < kPer; ++q) s_key[q * T + t] = key[q];
+      __syncthreads();
+#pragma unroll
+      for (std::uint32_t q = 0; q < kPer; ++q) {
+        const std::uint32_t i = t * kPer + q;
+        key[q] = cx(key[q], s_key[q * T + (t ^ m)], ((i & j) == 0) == ((i & k) == 0));
       }
       __syncthreads();
     }
+    for (; j >= kPer; j >>= 1) {  // partner in another lane of the warp
+      const std::uint32_t m = j / kPer;
+#pragma unroll
+      for (std::uint32_t q = 0; q < kPer; ++q) {
+        const std::uint32_t i = t * kPer + q;
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, key[q], m);
+        key[q] = cx(key[q], b, ((i & j) == 0) == ((i & k) == 0));
+      }
+    }
+#pragma unroll
+    for (std::uint32_t jj = kPer / 2; jj > 0; jj >>= 1) {  // partner in this thread
+      if (jj > j) continue;
+#pragma unroll
+      for (std::uint32_t q = 0; q < kPer; ++q)
+        if ((q & jj) == 0) {
+          const bool up = ((t * kPer + q) & k) == 0;
+          const unsigned long long a = key[q], b = key[q | jj];
+          if ((a > b) == up) {
+            key[q] = b;
+            key[q | jj] = a;
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (std::uint32_t q = 0; q < kPer; ++q) s_key[q * T + t] = key[q];
+  __syncthreads();
+  auto key_at = [&](std::uint32_t i) { return s_key[(i % kPer) * T + i / kPer]; };
   // ranks: thread t owns sorted positions [t*kPer, (t+1)*kPer)
   const std::uint32_t i0 = threadIdx.x * kPer;
   unsigned long long uc = 0;
 #pragma unroll
   for (std::uint32_t q = 0; q < kPer; ++q) {
     const std::uint32_t i = i0 + q;
-    if (i < cnt && (i == 0 || (s_key[i] >> 32) != (s_key[i - 1] >> 32))) ++uc;
+    if (i < cnt && (i == 0 || (key_at(i) >> 32) != (key_at(i - 1) >> 32))) ++uc;
   }
   unsigned long long utot;
   const std::uint32_t ubase = (std::uint32_t)(block_inclusive_scan<kSmallLevelThreads>(uc, s_sm, &utot) - uc);
@@ -548,8 +588,8 @@ __global__ void __launch_bounds__(kSmallLevelThreads) k_small_level(DedupParams 
 #pragma unroll
     for (std::uint32_t q = 0; q < kPer; ++q) {
       const std::uint32_t i = i0 + q;
-      const bool first = i < cnt && (i == 0 || (s_key[i] >> 32) != (s_key[i - 1] >> 32));
-      deg[q] = first ? min(p.f_next, __ldg(p.outdeg + (std::uint32_t)(s_key[i] >> 32))) : 0u;
+      const bool first = i < cnt && (i == 0 || (key_at(i) >> 32) != (key_at(i - 1) >> 32));
+      deg[q] = first ? min(p.f_next, __ldg(p.outdeg + (std::uint32_t)(key_at(i) >> 32))) : 0u;
     }
 #pragma unroll
     for (std::uint32_t q = 0; q < kPer; ++q) dc += deg[q];
@@ -568,8 +608,8 @@ __global__ void __launch_bounds__(kSmallLevelThreads) k_small_level(DedupParams 
   for (std::uint32_t q = 0; q < kPer; ++q) {
     const std::uint32_t i = i0 + q;
     if (i >= cnt) break;
-    const std::uint32_t v = (std::uint32_t)(s_key[i] >> 32);
-    const bool first = i == 0 || (s_key[i - 1] >> 32) != v;
+    const std::uint32_t v = (std::uint32_t)(key_at(i) >> 32);
+    const bool first = i == 0 || (key_at(i - 1) >> 32) != v;
     if (first) {
       list[r] = v;
       if (HAS_NEXT) {
@@ -578,15 +618,15 @@ __global__ void __launch_bounds__(kSmallLevelThreads) k_small_level(DedupParams 
       }
       // bucket bases: buckets (previous id's bucket, this bucket] start here
       const std::uint32_t bcur = v >> bp.bb;
-      const std::uint32_t bprev = i == 0 ? 0u : (std::uint32_t)(s_key[i - 1] >> 32 >> bp.bb) + 1u;
+      const std::uint32_t bprev = i == 0 ? 0u : (std::uint32_t)(key_at(i - 1) >> 32 >> bp.bb) + 1u;
       for (std::uint32_t bb_ = (i == 0 ? 0u : bprev); bb_ <= bcur; ++bb_) bo[bb_] = r;
       ++r;
     }
-    dst[(std::uint32_t)s_key[i]] = r - 1;
+    dst[(std::uint32_t)key_at(i)] = r - 1;
   }
   if (threadIdx.x == kSmallLevelThreads - 1) {
     const std::uint32_t U = (std::uint32_t)utot;
-    const std::uint32_t blast = cnt ? (std::uint32_t)(s_key[cnt - 1] >> 32 >> bp.bb) + 1u : 0u;
+    const std::uint32_t blast = cnt ? (std::uint32_t)(key_at(cnt - 1) >> 32 >> bp.bb) + 1u : 0u;
     for (std::uint32_t bb_ = blast; bb_ <= bp.NB; ++bb_) bo[bb_] = U;
     p.count[mb] = U;
     if (HAS_NEXT) {
