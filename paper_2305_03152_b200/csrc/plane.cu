@@ -1131,8 +1131,7 @@ void gather_impl(vk_plane p, vk_sampler s, void* out_dev, uint64_t out_stride_ro
                                                           ss.ulist.as<std::uint32_t>());
       // NVLink-bound: a prefetched exchange shares the SMs with a running
       // gather (2 CTAs/SM, on the high-priority aux stream); inline, 8 CTAs/SM
-      unsigned pg = (unsigned)sm_count(p->device) * (prefetch_only ? kPullCtasPrefetch : 8);
-      if (const char* e = getenv("VK_PULL_CTAS_EXPERIMENT")) pg = (unsigned)atoi(e);
+      const unsigned pg = (unsigned)sm_count(p->device) * (prefetch_only ? kPullCtasPrefetch : 8);
       GatherParams pp = gp;  // staged rows are plain rows: the pull's vector width follows the row size
       auto pull = [&](auto tag, std::uint32_t esz) {
         using T = decltype(tag);
