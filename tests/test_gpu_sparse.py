@@ -115,3 +115,42 @@ def test_sparse_equals_dense_and_gather(vk, port):
         np.testing.assert_array_equal(rowd[i], rows_[i])
         exp = port.features(3, 64, a.all_vertices, fp16=True)
         np.testing.assert_array_equal(rows_[i].view(np.uint16), exp.view(np.uint16).ravel())
+
+
+@pytest.mark.parametrize("frontier", ["sparse", "dense"])
+def test_isolated_seeds_empty_frontiers(vk, port, frontier):
+    """Seeds without neighbours (empty F_1 and every later hop for that
+    minibatch), hubs beside them, and a graph spanning several buckets: both
+    representations equal the oracle, including the empty levels."""
+    from oracle.oracle import CSR
+    n = 600000
+    rng = np.random.default_rng(11)
+    # vertices >= 300000 are isolated; the rest form a sparse random graph
+    # with a few hubs
+    src = rng.integers(0, 300000, 900000).astype(np.uint32)
+    dst = rng.integers(0, 300000, 900000).astype(np.uint32)
+    hubs = rng.integers(0, 300000, 5).astype(np.uint32)
+    src = np.concatenate([src, np.repeat(hubs, 4000)])
+    dst = np.concatenate([dst, rng.integers(0, 300000, 20000).astype(np.uint32)])
+    keep = src != dst
+    u = np.concatenate([src[keep], dst[keep]])
+    v = np.concatenate([dst[keep], src[keep]])
+    key = np.unique(u.astype(np.uint64) << 32 | v)
+    u, v = (key >> 32).astype(np.uint32), (key & 0xffffffff).astype(np.uint32)
+    off = np.zeros(n + 1, np.uint64)
+    np.add.at(off, u.astype(np.int64) + 1, 1)
+    off = np.cumsum(off).astype(np.uint64)
+    csr = CSR(n, off, v)
+    g = vk.Graph.from_csr(csr.off, csr.tgt, undirected=True)
+    fan = [10, 5, 3]
+    batches = [np.arange(300000, 300100, dtype=np.uint32),          # isolated only
+               np.concatenate([hubs, np.arange(300000, 300050, dtype=np.uint32)]),
+               rng.integers(0, 300000, 200).astype(np.uint32),
+               np.array([599999], np.uint32)]                         # last vertex, isolated
+    refs = [(0, 0, i) for i in range(len(batches))]
+    s = vk.Sampler(g, fan, 200, len(batches), 77, frontier=frontier)
+    s.run(batches, refs)
+    for i, bt in enumerate(batches):
+        x = port.expand(csr, bt, fan, 77, 0, 0, i)
+        assert_same(s.result(i), 3, x.frontier, x.all_vertices, x.indptr, x.edges)
+    assert len(port.expand(csr, batches[0], fan, 77, 0, 0, 0).frontier[0]) == 0
