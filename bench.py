@@ -65,7 +65,7 @@ CONFIGS = {
 CONFIGS["c4"] = dict(workload="C4 ogbn-papers100M-shaped 111M nodes / 3.3B CSR slots, 128-d fp16, "
                               "8 partitions, fanout (15,10,5), batch 1024, VIP cache 32% (sweep 0-32%)",
                      n=111_059_956, d=15, K=8, p_in=0.8, train=0.011, dim=128, dtype=1, alpha=0.32,
-                     fanouts=(15, 10, 5), b=1024, wave=64, alpha_sweep=(0.0, 0.04, 0.08, 0.16, 0.32))
+                     fanouts=(15, 10, 5), b=1024, wave=128, alpha_sweep=(0.0, 0.04, 0.08, 0.16, 0.32))
 CONFIGS["c5"] = dict(workload="C5 VIP analysis on ogbn-papers100M-shaped 111M nodes / 3.3B CSR slots, "
                               "8 partitions, fanout sweep", n=111_059_956, d=15, K=8, p_in=0.8, train=0.011,
                      b=1024, fanouts=(15, 10, 5),
